@@ -1,0 +1,516 @@
+// sbr_common.cuh -- device-side building blocks shared by the sm_100a kernels.
+//
+//  * scene layout in HBM (BVH2 nodes with both child boxes, 64 B; float64
+//    triangle corners, 80 B per slot)
+//  * stateless Philox4x64-10 == numpy Philox + Generator.random
+//    (emtrace sampling.py:49-78)
+//  * float64 complex arithmetic with numpy's algorithms (division, |z|)
+//  * the watertight float64 ray/triangle test of _core.pyx:26-112 and the
+//    conservative fp32 child-box test
+//
+// The library is compiled with -fmad=false so float64 expressions round like
+// the reference's numpy / Cython code; FMAs appear only where written
+// explicitly (fp32 box tests, emulation of OpenBLAS products).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/sbr.h"
+
+namespace sbr {
+
+// ---------------------------------------------------------------------------
+// scene layout
+// ---------------------------------------------------------------------------
+// Internal node: 4 x float4 = 64 B
+//   a = (l.lo.x, l.hi.x, l.lo.y, l.hi.y)
+//   b = (r.lo.x, r.hi.x, r.lo.y, r.hi.y)
+//   c = (l.lo.z, l.hi.z, r.lo.z, r.hi.z)
+//   d = (int left, int right, 0, 0)    child >= 0: internal node index
+//                                      child <  0: leaf ~((start << 2) | (count-1))
+struct alignas(16) BvhNode {
+  float4 a, b, c;
+  int4 d;
+};
+
+__host__ __device__ inline int leaf_encode(int start, int count) {
+  return ~((start << 2) | (count - 1));
+}
+__host__ __device__ inline int leaf_start(int code) { return (~code) >> 2; }
+__host__ __device__ inline int leaf_count(int code) { return ((~code) & 3) + 1; }
+
+// Triangle slot: v0.xyz v1.xyz v2.xyz + pad, as 5 double2 (80 B)
+struct alignas(16) TriSlot {
+  double2 p[5];
+};
+
+struct DevScene {
+  const BvhNode* nodes;
+  const TriSlot* tris;
+  const int32_t* tie_rank;     // rank of (object_id, primitive_id)
+  const double* normals;       // (T,3)
+  const int32_t* matrow;       // material row per slot
+  const uint64_t* hash_r;      // plane hash (round quantizer)
+  const uint64_t* hash_f;      // plane hash (floor quantizer)
+  const SbrMaterial* mats;
+  unsigned int* error_word;    // bit0: traversal stack overflow
+  int64_t ntri;
+  int32_t nnodes;
+  int32_t nmat;
+  float pad_base;              // conservative box padding: 2^-20 * (max|coord| + 1)
+};
+
+constexpr int kStackSize = 64;
+constexpr unsigned kErrStack = 1u;
+
+// ---------------------------------------------------------------------------
+// Philox4x64-10 keyed stream
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double philox_uniform(uint64_t seed, uint64_t sample,
+                                                 uint64_t depth, uint64_t tag,
+                                                 uint64_t i) {
+  uint64_t c0 = i / 4 + 1, c1 = 0, c2 = depth, c3 = tag;
+  uint64_t k0 = seed, k1 = sample;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B97F4A7C15ULL;
+      k1 += 0xBB67AE8584CAA73BULL;
+    }
+    const uint64_t lo0 = 0xD2E7470EE14C6C93ULL * c0;
+    const uint64_t hi0 = __umul64hi(0xD2E7470EE14C6C93ULL, c0);
+    const uint64_t lo1 = 0xCA5A826395121157ULL * c2;
+    const uint64_t hi1 = __umul64hi(0xCA5A826395121157ULL, c2);
+    const uint64_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  const uint64_t w = (i & 3) == 0 ? c0 : (i & 3) == 1 ? c1 : (i & 3) == 2 ? c2 : c3;
+  return (double)(w >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// FNV-1a tags of the radio-map streams (sampling.py:42-46)
+constexpr uint64_t TAG_MAP_INTERACTION = 0xb89bb7c3608d55f4ULL;
+constexpr uint64_t TAG_MAP_RESPAWN = 0x123e3e11a6151f88ULL;
+constexpr uint64_t TAG_MAP_PHASE = 0xec7920a818db590bULL;
+constexpr uint64_t TAG_MAP_ROULETTE = 0xba18862d049a6e7cULL;
+
+constexpr double kTwoPi = 6.283185307179586;
+constexpr double kFourPi = 12.566370614359172;
+constexpr double kPi = 3.141592653589793;
+constexpr double kGolden = 1.618033988749895;
+
+// Fibonacci lattice direction of global sample g (sampling.py:81-95); the
+// azimuth 2*pi*n/golden is formed and range-reduced in float64.
+__device__ __forceinline__ double3 fibonacci_dir(uint64_t N, uint64_t g) {
+  const double n = (double)((int64_t)g - (int64_t)(N / 2));
+  const double cos_t = 2.0 * n / (double)N;
+  const double x = 1.0 - cos_t * cos_t;
+  const double sin_t = sqrt(x > 0.0 ? x : 0.0);
+  const double phi = kTwoPi * n / kGolden;
+  double s, c;
+  sincos(phi, &s, &c);
+  return make_double3(sin_t * c, sin_t * s, cos_t);
+}
+
+// ---------------------------------------------------------------------------
+// vectors (numpy evaluation orders)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double3 operator+(double3 a, double3 b) {
+  return make_double3(a.x + b.x, a.y + b.y, a.z + b.z);
+}
+__device__ __forceinline__ double3 operator-(double3 a, double3 b) {
+  return make_double3(a.x - b.x, a.y - b.y, a.z - b.z);
+}
+__device__ __forceinline__ double3 operator*(double s, double3 a) {
+  return make_double3(s * a.x, s * a.y, s * a.z);
+}
+__device__ __forceinline__ double3 neg(double3 a) { return make_double3(-a.x, -a.y, -a.z); }
+// np.sum(a*b, axis=1): sequential
+__device__ __forceinline__ double dot_seq(double3 a, double3 b) {
+  return (a.x * b.x + a.y * b.y) + a.z * b.z;
+}
+// (n,3) @ (3,) through OpenBLAS dgemv (order measured)
+__device__ __forceinline__ double dot_gemv(double3 a, double3 b) {
+  return fma(a.z, b.z, fma(a.x, b.x, a.y * b.y));
+}
+// 1-D dot through ddot
+__device__ __forceinline__ double dot_ddot(double3 a, double3 b) {
+  return fma(a.z, b.z, fma(a.y, b.y, a.x * b.x));
+}
+__device__ __forceinline__ double3 cross3(double3 a, double3 b) {
+  return make_double3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ double norm_seq(double3 a) {
+  return sqrt((a.x * a.x + a.y * a.y) + a.z * a.z);
+}
+__device__ __forceinline__ double3 ld3(const double* p) {
+  return make_double3(p[0], p[1], p[2]);
+}
+__device__ __forceinline__ double3 ldg3(const double* p) {
+  return make_double3(__ldg(p), __ldg(p + 1), __ldg(p + 2));
+}
+
+// ---------------------------------------------------------------------------
+// complex128, numpy algorithms
+// ---------------------------------------------------------------------------
+struct cplx {
+  double re, im;
+};
+__device__ __forceinline__ cplx C(double r, double i) { return cplx{r, i}; }
+__device__ __forceinline__ cplx operator+(cplx a, cplx b) { return C(a.re + b.re, a.im + b.im); }
+__device__ __forceinline__ cplx operator-(cplx a, cplx b) { return C(a.re - b.re, a.im - b.im); }
+__device__ __forceinline__ cplx operator*(cplx a, cplx b) {
+  return C(a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re);
+}
+__device__ __forceinline__ cplx operator*(double s, cplx a) { return C(s * a.re, s * a.im); }
+// numpy CDOUBLE_divide: Smith's method with a reciprocal
+__device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
+  const double br = fabs(b.re), bi = fabs(b.im);
+  if (br >= bi) {
+    if (br == 0.0 && bi == 0.0) return C(a.re / br, a.im / br);
+    const double rat = b.im / b.re;
+    const double scl = 1.0 / (b.re + b.im * rat);
+    return C((a.re + a.im * rat) * scl, (a.im - a.re * rat) * scl);
+  }
+  const double rat = b.re / b.im;
+  const double scl = 1.0 / (b.im + b.re * rat);
+  return C((a.re * rat + a.im) * scl, (a.im * rat - a.re) * scl);
+}
+// np.abs(complex128) in numpy 2.x: max * sqrt(fma(r, r, 1)), r = min/max
+__device__ __forceinline__ double cabs_np(cplx a) {
+  const double x = fabs(a.re), y = fabs(a.im);
+  const double m = fmax(x, y), k = fmin(x, y);
+  if (m == 0.0 || isinf(m)) return m + k;
+  const double r = k / m;
+  return m * sqrt(fma(r, r, 1.0));
+}
+__device__ __forceinline__ double cabs2(cplx a) {
+  const double m = cabs_np(a);
+  return m * m;
+}
+__device__ __forceinline__ cplx cexp_(cplx a) {
+  const double e = exp(a.re);
+  double s, c;
+  sincos(a.im, &s, &c);
+  return C(e * c, e * s);
+}
+// principal sqrt, glibc csqrt finite branch (np.sqrt(complex) -> libm csqrt)
+__device__ __forceinline__ cplx csqrt_(cplx z) {
+  const double x = z.re, y = z.im;
+  if (y == 0.0) {
+    if (x < 0.0) return C(0.0, copysign(sqrt(-x), y));
+    return C(fabs(sqrt(x)), copysign(0.0, y));
+  }
+  if (x == 0.0) {
+    const double r = sqrt(0.5 * fabs(y));
+    return C(r, copysign(r, y));
+  }
+  const double d = hypot(x, y);
+  double r, s;
+  if (x > 0.0) {
+    r = sqrt(0.5 * (d + x));
+    s = 0.5 * (y / r);
+  } else {
+    s = sqrt(0.5 * (d - x));
+    r = fabs(0.5 * (y / s));
+  }
+  return C(r, copysign(s, y));
+}
+
+struct cvec3 {
+  cplx x, y, z;
+};
+// sum(field * e, axis=1) with complex field, real e: componentwise sequential
+__device__ __forceinline__ cplx cdot_real(const cvec3& f, double3 e) {
+  return C((f.x.re * e.x + f.y.re * e.y) + f.z.re * e.z,
+           (f.x.im * e.x + f.y.im * e.y) + f.z.im * e.z);
+}
+__device__ __forceinline__ double field_energy(const cvec3& f) {
+  return (cabs2(f.x) + cabs2(f.y)) + cabs2(f.z);
+}
+
+// ---------------------------------------------------------------------------
+// ray / triangle (float64 watertight shear test, _core.pyx:26-112)
+// ---------------------------------------------------------------------------
+struct Ray64 {
+  double3 o;
+  int kx, ky, kz;
+  double sx, sy, sz;
+};
+
+__device__ __forceinline__ double comp(double3 v, int k) {
+  return k == 0 ? v.x : (k == 1 ? v.y : v.z);
+}
+
+__device__ __forceinline__ Ray64 ray_setup(double3 o, double3 d) {
+  Ray64 r;
+  r.o = o;
+  int kz = 0;
+  if (fabs(d.y) > fabs(d.x)) kz = 1;
+  if (fabs(d.z) > fabs(comp(d, kz))) kz = 2;
+  int kx = kz + 1 == 3 ? 0 : kz + 1;
+  int ky = kx + 1 == 3 ? 0 : kx + 1;
+  const double dkz = comp(d, kz);
+  if (dkz < 0.0) {
+    const int t = kx;
+    kx = ky;
+    ky = t;
+  }
+  r.kx = kx;
+  r.ky = ky;
+  r.kz = kz;
+  r.sx = comp(d, kx) / dkz;
+  r.sy = comp(d, ky) / dkz;
+  r.sz = 1.0 / dkz;
+  return r;
+}
+
+// Returns true on a hit with t > t_min; t, u, v as the reference computes them.
+__device__ __forceinline__ bool tri_hit(const Ray64& r, const TriSlot* __restrict__ tri,
+                                        double t_min, double& t_out, double& u_out,
+                                        double& v_out) {
+  const double2 q0 = __ldg(&tri->p[0]);
+  const double2 q1 = __ldg(&tri->p[1]);
+  const double2 q2 = __ldg(&tri->p[2]);
+  const double2 q3 = __ldg(&tri->p[3]);
+  const double2 q4 = __ldg(&tri->p[4]);
+  const double3 a = make_double3(q0.x - r.o.x, q0.y - r.o.y, q1.x - r.o.z);
+  const double3 b = make_double3(q1.y - r.o.x, q2.x - r.o.y, q2.y - r.o.z);
+  const double3 c = make_double3(q3.x - r.o.x, q3.y - r.o.y, q4.x - r.o.z);
+  const double az = comp(a, r.kz), bz = comp(b, r.kz), cz = comp(c, r.kz);
+  const double ax = comp(a, r.kx) - r.sx * az, ay = comp(a, r.ky) - r.sy * az;
+  const double bx = comp(b, r.kx) - r.sx * bz, by = comp(b, r.ky) - r.sy * bz;
+  const double cx = comp(c, r.kx) - r.sx * cz, cy = comp(c, r.ky) - r.sy * cz;
+  const double u = cx * by - cy * bx;
+  const double v = ax * cy - ay * cx;
+  const double w = bx * ay - by * ax;
+  if ((u < 0.0 || v < 0.0 || w < 0.0) && (u > 0.0 || v > 0.0 || w > 0.0)) return false;
+  const double det = u + v + w;
+  if (det == 0.0) return false;
+  const double t_num = u * (r.sz * az) + v * (r.sz * bz) + w * (r.sz * cz);
+  const double t = t_num / det;
+  if (!(t > t_min)) return false;
+  t_out = t;
+  u_out = v / det;
+  v_out = w / det;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// conservative fp32 box test
+// ---------------------------------------------------------------------------
+// Per axis, the slab [lo, hi] is widened by `pad` (covers the rounding of the
+// origin to fp32, of (lo - o) and of the product by 1/d), so the computed
+// entry/exit interval always contains the exact one: the BVH can only
+// over-visit, never cull a box holding the exact closest triangle.
+struct RayBox {
+  float ix, iy, iz;       // 1/d (finite)
+  float oxp, oyp, ozp;    // (o + pad) * inv   -> lo planes
+  float oxm, oym, ozm;    // (o - pad) * inv   -> hi planes
+};
+
+__device__ __forceinline__ float safe_inv(double d) {
+  const float f = (float)d;
+  return fabsf(f) > 1e-20f ? 1.0f / f : copysignf(1e20f, f);
+}
+
+__device__ __forceinline__ RayBox box_setup(double3 o, double3 d, float pad_base) {
+  RayBox b;
+  b.ix = safe_inv(d.x);
+  b.iy = safe_inv(d.y);
+  b.iz = safe_inv(d.z);
+  const float ox = (float)o.x, oy = (float)o.y, oz = (float)o.z;
+  const float px = pad_base + 1e-6f * fabsf(ox);
+  const float py = pad_base + 1e-6f * fabsf(oy);
+  const float pz = pad_base + 1e-6f * fabsf(oz);
+  b.oxp = (ox + px) * b.ix;
+  b.oyp = (oy + py) * b.iy;
+  b.ozp = (oz + pz) * b.iz;
+  b.oxm = (ox - px) * b.ix;
+  b.oym = (oy - py) * b.iy;
+  b.ozm = (oz - pz) * b.iz;
+  return b;
+}
+
+// entry distance of [lo,hi] or +inf when missed / beyond `bound`
+__device__ __forceinline__ float box_enter(const RayBox& rb, float lox, float hix, float loy,
+                                           float hiy, float loz, float hiz, float bound) {
+  const float x0 = fmaf(lox, rb.ix, -rb.oxp), x1 = fmaf(hix, rb.ix, -rb.oxm);
+  const float y0 = fmaf(loy, rb.iy, -rb.oyp), y1 = fmaf(hiy, rb.iy, -rb.oym);
+  const float z0 = fmaf(loz, rb.iz, -rb.ozp), z1 = fmaf(hiz, rb.iz, -rb.ozm);
+  const float tn = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fminf(z0, z1));
+  const float tf = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fmaxf(z0, z1));
+  return (tn <= tf && tf >= 0.0f && tn <= bound) ? tn : __int_as_float(0x7f800000);
+}
+
+// float upper bound of a float64 distance (for comparing fp32 entries)
+__device__ __forceinline__ float bound_up(double t) {
+  if (!(t < 3.0e38)) return __int_as_float(0x7f800000);
+  return __double2float_ru(t) * 1.000002f + 1e-30f;
+}
+
+// ---------------------------------------------------------------------------
+// closest hit / any hit over the device BVH
+// ---------------------------------------------------------------------------
+struct HitRecord {
+  double t, u, v;
+  int tri;  // slot, -1 = miss
+};
+
+// Exact reference semantics: minimum over hit triangles of (t, tie_rank) with
+// t_min < t < t_max.  Returns false on stack overflow.
+__device__ __forceinline__ bool trace_closest(const DevScene& S, double3 o, double3 d,
+                                              double t_min, double t_max, HitRecord& h) {
+  const Ray64 r = ray_setup(o, d);
+  const RayBox rb = box_setup(o, d, S.pad_base);
+  double best_t = t_max, bu = 0.0, bv = 0.0;
+  int best = -1, best_rank = 0x7fffffff;
+  float bound = bound_up(best_t);
+  int stack_node[kStackSize];
+  float stack_t[kStackSize];
+  int sp = 0;
+  int node = 0;
+  bool ok = true;
+  while (true) {
+    if (node >= 0) {
+      const BvhNode* nd = S.nodes + node;
+      const float4 a = __ldg(&nd->a), b = __ldg(&nd->b), c = __ldg(&nd->c);
+      const int4 ch = __ldg(&nd->d);
+      const float tl = box_enter(rb, a.x, a.y, a.z, a.w, c.x, c.y, bound);
+      const float tr = box_enter(rb, b.x, b.y, b.z, b.w, c.z, c.w, bound);
+      const bool hl = tl < __int_as_float(0x7f800000);
+      const bool hr = tr < __int_as_float(0x7f800000);
+      if (hl && hr) {
+        const bool lfirst = tl <= tr;
+        const int near = lfirst ? ch.x : ch.y;
+        const int far = lfirst ? ch.y : ch.x;
+        if (sp >= kStackSize) {
+          ok = false;
+          break;
+        }
+        stack_node[sp] = far;
+        stack_t[sp] = lfirst ? tr : tl;
+        ++sp;
+        node = near;
+        continue;
+      }
+      if (hl) {
+        node = ch.x;
+        continue;
+      }
+      if (hr) {
+        node = ch.y;
+        continue;
+      }
+    } else {
+      const int s = leaf_start(node), n = leaf_count(node);
+      for (int j = s; j < s + n; ++j) {
+        double t, u, v;
+        if (tri_hit(r, S.tris + j, t_min, t, u, v)) {
+          const int rank = __ldg(S.tie_rank + j);
+          if (t < best_t || (t == best_t && best >= 0 && rank < best_rank)) {
+            best_t = t;
+            best = j;
+            best_rank = rank;
+            bu = u;
+            bv = v;
+            bound = bound_up(best_t);
+          }
+        }
+      }
+    }
+    // pop the next box still in front of the best hit
+    bool found = false;
+    while (sp > 0) {
+      --sp;
+      if (stack_t[sp] <= bound) {
+        node = stack_node[sp];
+        found = true;
+        break;
+      }
+    }
+    if (!found) break;
+  }
+  h.tri = best;
+  h.t = best >= 0 ? best_t : __longlong_as_double(0x7ff0000000000000LL);
+  h.u = best >= 0 ? bu : 0.0;
+  h.v = best >= 0 ? bv : 0.0;
+  return ok;
+}
+
+// any hit with t_min < t < limit (_core.pyx:198-253); returns false on overflow
+__device__ __forceinline__ bool trace_any(const DevScene& S, double3 o, double3 d,
+                                          double t_min, double limit, bool& found) {
+  const Ray64 r = ray_setup(o, d);
+  const RayBox rb = box_setup(o, d, S.pad_base);
+  const float bound = bound_up(limit);
+  int stack_node[kStackSize];
+  int sp = 0;
+  int node = 0;
+  found = false;
+  while (true) {
+    if (node >= 0) {
+      const BvhNode* nd = S.nodes + node;
+      const float4 a = __ldg(&nd->a), b = __ldg(&nd->b), c = __ldg(&nd->c);
+      const int4 ch = __ldg(&nd->d);
+      const float tl = box_enter(rb, a.x, a.y, a.z, a.w, c.x, c.y, bound);
+      const float tr = box_enter(rb, b.x, b.y, b.z, b.w, c.z, c.w, bound);
+      const bool hl = tl < __int_as_float(0x7f800000);
+      const bool hr = tr < __int_as_float(0x7f800000);
+      if (hl && hr) {
+        if (sp >= kStackSize) return false;
+        const bool lfirst = tl <= tr;
+        stack_node[sp++] = lfirst ? ch.y : ch.x;
+        node = lfirst ? ch.x : ch.y;
+        continue;
+      }
+      if (hl) {
+        node = ch.x;
+        continue;
+      }
+      if (hr) {
+        node = ch.y;
+        continue;
+      }
+    } else {
+      const int s = leaf_start(node), n = leaf_count(node);
+      for (int j = s; j < s + n; ++j) {
+        double t, u, v;
+        if (tri_hit(r, S.tris + j, t_min, t, u, v) && t < limit) {
+          found = true;
+          return true;
+        }
+      }
+    }
+    if (sp == 0) break;
+    node = stack_node[--sp];
+  }
+  return true;
+}
+
+__device__ __forceinline__ void flag_error(const DevScene& S, unsigned bits) {
+  atomicOr(S.error_word, bits);
+}
+
+// occluded_batch for one segment (geometry.py:187-201)
+__device__ __forceinline__ bool occluded_segment(const DevScene& S, double3 a, double3 b,
+                                                 double eps, bool& ok) {
+  const double3 d = b - a;
+  const double len = norm_seq(d);
+  ok = true;
+  if (!(len > 2.0 * eps)) return false;
+  const double3 dn = make_double3(d.x / len, d.y / len, d.z / len);
+  const double3 o = make_double3(a.x + eps * dn.x, a.y + eps * dn.y, a.z + eps * dn.z);
+  bool found;
+  ok = trace_any(S, o, dn, 0.0, len - 2.0 * eps, found);
+  return found;
+}
+
+// kernel-launch evidence counter (host side, defined in sbr_scene.cu)
+void count_launch();
+
+}  // namespace sbr

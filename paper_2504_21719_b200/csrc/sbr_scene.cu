@@ -1,0 +1,536 @@
+// sbr_scene.cu -- device scene: LBVH build in HBM plus the scene C ABI.
+//
+// Replaces Accel.__init__ / _build_bvh (emtrace geometry.py:134-166, 244-349).
+// Build pipeline (all on the GPU, stream-ordered):
+//   1. per-triangle float64 AABB -> centroid; centroid bounds (atomics)
+//   2. 63-bit Morton keys (21 bits per axis)              [kernel]
+//   3. radix sort of (key, triangle) pairs                 [cub::DeviceRadixSort]
+//   4. Karras 2012 binary radix tree over the sorted keys  [kernel]
+//   5. bottom-up refit of conservative fp32 boxes          [kernel, atomics]
+//   6. collapse subtrees of <= 4 triangles into leaves and
+//      emit 64-B BVH2 nodes (both child boxes per node)    [scan + kernel]
+// Triangles are stored in Morton (slot) order as float64 corners so the
+// watertight test reproduces the reference's arithmetic exactly.
+#include <cub/cub.cuh>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sbr_common.cuh"
+
+namespace sbr {
+
+static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int set_error(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define SBR_CUDA(call)                                                             \
+  do {                                                                             \
+    cudaError_t _e = (call);                                                       \
+    if (_e != cudaSuccess)                                                         \
+      return ::sbr::set_error(SBR_ERR_CUDA, std::string(#call) + ": " +            \
+                                                cudaGetErrorString(_e));           \
+  } while (0)
+
+}  // namespace sbr
+
+struct SbrScene {
+  int device = 0;
+  int64_t ntri = 0;
+  int32_t nnodes = 0;
+  sbr::BvhNode* nodes = nullptr;
+  sbr::TriSlot* tris = nullptr;
+  int32_t* tie_rank = nullptr;
+  double* normals = nullptr;
+  int32_t* matrow = nullptr;
+  uint64_t* hash_r = nullptr;
+  uint64_t* hash_f = nullptr;
+  SbrMaterial* mats = nullptr;
+  int32_t nmat = 0;
+  unsigned int* error_word = nullptr;
+  float pad_base = 0.f;
+  std::vector<int64_t> perm;
+};
+
+namespace sbr {
+
+DevScene dev_view(const SbrScene* s) {
+  DevScene d;
+  d.nodes = s->nodes;
+  d.tris = s->tris;
+  d.tie_rank = s->tie_rank;
+  d.normals = s->normals;
+  d.matrow = s->matrow;
+  d.hash_r = s->hash_r;
+  d.hash_f = s->hash_f;
+  d.mats = s->mats;
+  d.error_word = s->error_word;
+  d.ntri = s->ntri;
+  d.nnodes = s->nnodes;
+  d.nmat = s->nmat;
+  d.pad_base = s->pad_base;
+  return d;
+}
+
+// ---------------------------------------------------------------------------
+// build kernels
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned int f2ord(float f) {
+  const unsigned int u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(unsigned int u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+__global__ void k_centroids(const double* __restrict__ v0, const double* __restrict__ v1,
+                            const double* __restrict__ v2, int64_t n, float3* cen,
+                            unsigned int* cbounds /* 6: min xyz, max xyz (ordered) */) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  float c[3] = {0.f, 0.f, 0.f};
+  const bool live = i < n;
+  if (live) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double a = v0[3 * i + k], b = v1[3 * i + k], d = v2[3 * i + k];
+      const double lo = fmin(fmin(a, b), d), hi = fmax(fmax(a, b), d);
+      c[k] = (float)((lo + hi) * 0.5);
+    }
+    cen[i] = make_float3(c[0], c[1], c[2]);
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    unsigned int mn = live ? f2ord(c[k]) : 0xffffffffu;
+    unsigned int mx = live ? f2ord(c[k]) : 0u;
+    for (int off = 16; off; off >>= 1) {
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(cbounds + k, mn);
+      atomicMax(cbounds + 3 + k, mx);
+    }
+  }
+}
+
+__device__ __forceinline__ uint64_t spread21(uint64_t x) {
+  x &= 0x1fffffULL;
+  x = (x | (x << 32)) & 0x1f00000000ffffULL;
+  x = (x | (x << 16)) & 0x1f0000ff0000ffULL;
+  x = (x | (x << 8)) & 0x100f00f00f00f00fULL;
+  x = (x | (x << 4)) & 0x10c30c30c30c30c3ULL;
+  x = (x | (x << 2)) & 0x1249249249249249ULL;
+  return x;
+}
+
+__global__ void k_morton(const float3* __restrict__ cen, int64_t n,
+                         const unsigned int* __restrict__ cbounds, uint64_t* keys,
+                         int32_t* ids) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float3 c = cen[i];
+  const float lo[3] = {ord2f(cbounds[0]), ord2f(cbounds[1]), ord2f(cbounds[2])};
+  const float hi[3] = {ord2f(cbounds[3]), ord2f(cbounds[4]), ord2f(cbounds[5])};
+  const float v[3] = {c.x, c.y, c.z};
+  uint64_t q[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float ext = hi[k] - lo[k];
+    float f = ext > 0.f ? (v[k] - lo[k]) / ext : 0.5f;
+    f = fminf(fmaxf(f, 0.f), 1.f);
+    q[k] = (uint64_t)fminf(f * 2097152.0f, 2097151.0f);
+  }
+  keys[i] = (spread21(q[0]) << 2) | (spread21(q[1]) << 1) | spread21(q[2]);
+  ids[i] = (int32_t)i;
+}
+
+__device__ __forceinline__ int delta(const uint64_t* __restrict__ keys, int n, int i, int j) {
+  if (j < 0 || j >= n) return -1;
+  const uint64_t a = keys[i], b = keys[j];
+  if (a != b) return __clzll(a ^ b);
+  return 64 + __clz(i ^ j);
+}
+
+// Karras 2012: internal node i of n-1; children < 0 encode leaves ~index.
+__global__ void k_karras(const uint64_t* __restrict__ keys, int n, int2* children,
+                         int2* ranges, int* parent_int, int* parent_leaf) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n - 1) return;
+  const int d = (delta(keys, n, i, i + 1) - delta(keys, n, i, i - 1)) >= 0 ? 1 : -1;
+  const int dmin = delta(keys, n, i, i - d);
+  int lmax = 2;
+  while (delta(keys, n, i, i + lmax * d) > dmin) lmax <<= 1;
+  int l = 0;
+  for (int t = lmax >> 1; t >= 1; t >>= 1)
+    if (delta(keys, n, i, i + (l + t) * d) > dmin) l += t;
+  const int j = i + l * d;
+  const int dnode = delta(keys, n, i, j);
+  int s = 0;
+  int t = l;
+  do {
+    t = (t + 1) >> 1;
+    if (delta(keys, n, i, i + (s + t) * d) > dnode) s += t;
+  } while (t > 1);
+  const int gamma = i + s * d + min(d, 0);
+  const int first = min(i, j), last = max(i, j);
+  const int left = (first == gamma) ? ~gamma : gamma;
+  const int right = (last == gamma + 1) ? ~(gamma + 1) : gamma + 1;
+  children[i] = make_int2(left, right);
+  ranges[i] = make_int2(first, last);
+  if (left < 0) parent_leaf[~left] = i; else parent_int[left] = i;
+  if (right < 0) parent_leaf[~right] = i; else parent_int[right] = i;
+}
+
+struct Box32 {
+  float lo[3], hi[3];
+};
+
+// Leaf boxes from float64 corners rounded outward, then bottom-up refit.
+__global__ void k_refit(const double* __restrict__ v0, const double* __restrict__ v1,
+                        const double* __restrict__ v2, const int32_t* __restrict__ ids,
+                        int n, const int2* __restrict__ children,
+                        const int* __restrict__ parent_int, const int* __restrict__ parent_leaf,
+                        Box32* leaf_box, Box32* int_box, unsigned int* visits) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int tri = ids[i];
+  Box32 b;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double a = v0[3 * tri + k], c = v1[3 * tri + k], d = v2[3 * tri + k];
+    b.lo[k] = __double2float_rd(fmin(fmin(a, c), d));
+    b.hi[k] = __double2float_ru(fmax(fmax(a, c), d));
+  }
+  leaf_box[i] = b;
+  if (n == 1) return;
+  int node = parent_leaf[i];
+  while (node >= 0) {
+    __threadfence();
+    if (atomicAdd(visits + node, 1u) == 0) return;  // first arrival: sibling not done
+    __threadfence();
+    const int2 ch = children[node];
+    const Box32 bl = ch.x < 0 ? leaf_box[~ch.x] : int_box[ch.x];
+    const Box32 br = ch.y < 0 ? leaf_box[~ch.y] : int_box[ch.y];
+    Box32 u;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      u.lo[k] = fminf(bl.lo[k], br.lo[k]);
+      u.hi[k] = fmaxf(bl.hi[k], br.hi[k]);
+    }
+    int_box[node] = u;
+    node = node == 0 ? -1 : parent_int[node];
+  }
+}
+
+__global__ void k_keep_flags(const int2* __restrict__ ranges, int nint, int* keep) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nint) return;
+  const int2 r = ranges[i];
+  keep[i] = (r.y - r.x + 1) > 4 ? 1 : 0;
+}
+
+// Emit the collapsed BVH2 nodes.  Child code: internal kept node -> its
+// compact index; subtree of <= 4 triangles -> leaf(first, count).
+__global__ void k_emit(const int2* __restrict__ children, const int2* __restrict__ ranges,
+                       const int* __restrict__ keep, const int* __restrict__ compact,
+                       const Box32* __restrict__ leaf_box, const Box32* __restrict__ int_box,
+                       int nint, BvhNode* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nint || !keep[i]) return;
+  const int2 ch = children[i];
+  int code[2];
+  Box32 bx[2];
+  const int c2[2] = {ch.x, ch.y};
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int c = c2[s];
+    if (c < 0) {
+      code[s] = leaf_encode(~c, 1);
+      bx[s] = leaf_box[~c];
+    } else {
+      const int2 r = ranges[c];
+      bx[s] = int_box[c];
+      code[s] = keep[c] ? compact[c] : leaf_encode(r.x, r.y - r.x + 1);
+    }
+  }
+  BvhNode nd;
+  nd.a = make_float4(bx[0].lo[0], bx[0].hi[0], bx[0].lo[1], bx[0].hi[1]);
+  nd.b = make_float4(bx[1].lo[0], bx[1].hi[0], bx[1].lo[1], bx[1].hi[1]);
+  nd.c = make_float4(bx[0].lo[2], bx[0].hi[2], bx[1].lo[2], bx[1].hi[2]);
+  nd.d = make_int4(code[0], code[1], 0, 0);
+  out[compact[i]] = nd;
+}
+
+// root for scenes of <= 4 triangles: both children are the single leaf
+__global__ void k_small_root(const Box32* __restrict__ leaf_box, int n, BvhNode* out) {
+  Box32 u = leaf_box[0];
+  for (int i = 1; i < n; ++i)
+    for (int k = 0; k < 3; ++k) {
+      u.lo[k] = fminf(u.lo[k], leaf_box[i].lo[k]);
+      u.hi[k] = fmaxf(u.hi[k], leaf_box[i].hi[k]);
+    }
+  BvhNode nd;
+  nd.a = make_float4(u.lo[0], u.hi[0], u.lo[1], u.hi[1]);
+  nd.b = nd.a;
+  nd.c = make_float4(u.lo[2], u.hi[2], u.lo[2], u.hi[2]);
+  const int code = leaf_encode(0, n);
+  nd.d = make_int4(code, code, 0, 0);
+  out[0] = nd;
+}
+
+__global__ void k_gather_tris(const double* __restrict__ v0, const double* __restrict__ v1,
+                              const double* __restrict__ v2, const int32_t* __restrict__ ids,
+                              int n, TriSlot* tris) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int t = ids[i];
+  TriSlot s;
+  s.p[0] = make_double2(v0[3 * t], v0[3 * t + 1]);
+  s.p[1] = make_double2(v0[3 * t + 2], v1[3 * t]);
+  s.p[2] = make_double2(v1[3 * t + 1], v1[3 * t + 2]);
+  s.p[3] = make_double2(v2[3 * t], v2[3 * t + 1]);
+  s.p[4] = make_double2(v2[3 * t + 2], 0.0);
+  tris[i] = s;
+}
+
+template <typename T>
+static int dalloc(T** p, size_t count, cudaStream_t st) {
+  SBR_CUDA(cudaMallocAsync((void**)p, sizeof(T) * (count ? count : 1), st));
+  return SBR_OK;
+}
+
+static inline unsigned grid_for(int64_t n, int block) {
+  return (unsigned)((n + block - 1) / block);
+}
+
+}  // namespace sbr
+
+using namespace sbr;
+
+extern "C" {
+
+const char* sbr_last_error(void) { return g_last_error.c_str(); }
+int sbr_version(void) { return 100; }
+uint64_t sbr_kernel_launches(void) { return g_launches.load(); }
+
+int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64_t ntri,
+                     int32_t device, void* stream, SbrScene** out) {
+  if (!out) return set_error(SBR_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  if (ntri <= 0) return set_error(SBR_ERR_EMPTY_SCENE, "no triangles");
+  if (ntri >= (1LL << 29)) return set_error(SBR_ERR_INVALID, "too many triangles");
+  SBR_CUDA(cudaSetDevice(device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = (int)ntri;
+  SbrScene* S = new SbrScene();
+  S->device = device;
+  S->ntri = ntri;
+
+  double max_abs = 0.0;
+  for (int64_t i = 0; i < 3 * ntri; ++i) {
+    max_abs = fmax(max_abs, fabs(v0[i]));
+    max_abs = fmax(max_abs, fabs(v1[i]));
+    max_abs = fmax(max_abs, fabs(v2[i]));
+  }
+  S->pad_base = (float)(ldexp(max_abs + 1.0, -20));
+
+  double *dv0, *dv1, *dv2;
+  const size_t bytes = sizeof(double) * 3 * (size_t)ntri;
+  int rc;
+  if ((rc = dalloc(&dv0, 3 * ntri, st)) || (rc = dalloc(&dv1, 3 * ntri, st)) ||
+      (rc = dalloc(&dv2, 3 * ntri, st)))
+    return rc;
+  SBR_CUDA(cudaMemcpyAsync(dv0, v0, bytes, cudaMemcpyHostToDevice, st));
+  SBR_CUDA(cudaMemcpyAsync(dv1, v1, bytes, cudaMemcpyHostToDevice, st));
+  SBR_CUDA(cudaMemcpyAsync(dv2, v2, bytes, cudaMemcpyHostToDevice, st));
+
+  float3* cen;
+  unsigned int* cb;
+  uint64_t *keys, *keys_sorted;
+  int32_t *ids, *ids_sorted;
+  if ((rc = dalloc(&cen, n, st)) || (rc = dalloc(&cb, 6, st)) || (rc = dalloc(&keys, n, st)) ||
+      (rc = dalloc(&keys_sorted, n, st)) || (rc = dalloc(&ids, n, st)) ||
+      (rc = dalloc(&ids_sorted, n, st)))
+    return rc;
+  const unsigned init[6] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0u, 0u, 0u};
+  SBR_CUDA(cudaMemcpyAsync(cb, init, sizeof init, cudaMemcpyHostToDevice, st));
+  k_centroids<<<grid_for(n, 256), 256, 0, st>>>(dv0, dv1, dv2, n, cen, cb);
+  count_launch();
+  k_morton<<<grid_for(n, 256), 256, 0, st>>>(cen, n, cb, keys, ids);
+  count_launch();
+  size_t tmp_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys_sorted, ids, ids_sorted, n, 0,
+                                  64, st);
+  void* tmp;
+  SBR_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+  SBR_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_sorted, ids, ids_sorted,
+                                           n, 0, 64, st));
+  count_launch();
+
+  const int nint = n > 1 ? n - 1 : 0;
+  int2 *children, *ranges;
+  int *parent_int, *parent_leaf, *keep, *compact;
+  Box32 *leaf_box, *int_box;
+  unsigned int* visits;
+  if ((rc = dalloc(&children, nint, st)) || (rc = dalloc(&ranges, nint, st)) ||
+      (rc = dalloc(&parent_int, nint, st)) || (rc = dalloc(&parent_leaf, n, st)) ||
+      (rc = dalloc(&keep, nint, st)) || (rc = dalloc(&compact, nint, st)) ||
+      (rc = dalloc(&leaf_box, n, st)) || (rc = dalloc(&int_box, nint, st)) ||
+      (rc = dalloc(&visits, nint, st)))
+    return rc;
+  if (nint) {
+    SBR_CUDA(cudaMemsetAsync(visits, 0, sizeof(unsigned) * nint, st));
+    SBR_CUDA(cudaMemsetAsync(parent_int, 0xff, sizeof(int) * nint, st));
+    k_karras<<<grid_for(nint, 256), 256, 0, st>>>(keys_sorted, n, children, ranges, parent_int,
+                                                  parent_leaf);
+    count_launch();
+  }
+  k_refit<<<grid_for(n, 256), 256, 0, st>>>(dv0, dv1, dv2, ids_sorted, n, children, parent_int,
+                                            parent_leaf, leaf_box, int_box, visits);
+  count_launch();
+
+  int nnodes = 1;
+  if (n > 4) {
+    k_keep_flags<<<grid_for(nint, 256), 256, 0, st>>>(ranges, nint, keep);
+    count_launch();
+    size_t scan_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, keep, compact, nint, st);
+    void* scan_tmp;
+    SBR_CUDA(cudaMallocAsync(&scan_tmp, scan_bytes, st));
+    SBR_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, keep, compact, nint, st));
+    count_launch();
+    int last_c = 0, last_k = 0;
+    SBR_CUDA(cudaMemcpyAsync(&last_c, compact + nint - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SBR_CUDA(cudaMemcpyAsync(&last_k, keep + nint - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SBR_CUDA(cudaStreamSynchronize(st));
+    nnodes = last_c + last_k;
+    SBR_CUDA(cudaFreeAsync(scan_tmp, st));
+  }
+  if ((rc = dalloc(&S->nodes, nnodes, st))) return rc;
+  if (n > 4) {
+    k_emit<<<grid_for(nint, 256), 256, 0, st>>>(children, ranges, keep, compact, leaf_box,
+                                                int_box, nint, S->nodes);
+  } else {
+    k_small_root<<<1, 1, 0, st>>>(leaf_box, n, S->nodes);
+  }
+  count_launch();
+  S->nnodes = nnodes;
+
+  if ((rc = dalloc(&S->tris, n, st))) return rc;
+  k_gather_tris<<<grid_for(n, 256), 256, 0, st>>>(dv0, dv1, dv2, ids_sorted, n, S->tris);
+  count_launch();
+
+  S->perm.resize(n);
+  std::vector<int32_t> ids_host(n);
+  SBR_CUDA(cudaMemcpyAsync(ids_host.data(), ids_sorted, sizeof(int32_t) * n,
+                           cudaMemcpyDeviceToHost, st));
+  if ((rc = dalloc(&S->error_word, 1, st))) return rc;
+  SBR_CUDA(cudaMemsetAsync(S->error_word, 0, sizeof(unsigned), st));
+  // default per-slot tables
+  if ((rc = dalloc(&S->tie_rank, n, st)) || (rc = dalloc(&S->normals, 3 * (size_t)n, st)) ||
+      (rc = dalloc(&S->matrow, n, st)) || (rc = dalloc(&S->hash_r, n, st)) ||
+      (rc = dalloc(&S->hash_f, n, st)))
+    return rc;
+  SBR_CUDA(cudaMemsetAsync(S->matrow, 0, sizeof(int32_t) * n, st));
+  SBR_CUDA(cudaMemsetAsync(S->hash_r, 0, sizeof(uint64_t) * n, st));
+  SBR_CUDA(cudaMemsetAsync(S->hash_f, 0, sizeof(uint64_t) * n, st));
+  SBR_CUDA(cudaStreamSynchronize(st));
+  for (int i = 0; i < n; ++i) S->perm[i] = ids_host[i];
+
+  cudaFreeAsync(dv0, st);
+  cudaFreeAsync(dv1, st);
+  cudaFreeAsync(dv2, st);
+  cudaFreeAsync(cen, st);
+  cudaFreeAsync(cb, st);
+  cudaFreeAsync(keys, st);
+  cudaFreeAsync(keys_sorted, st);
+  cudaFreeAsync(ids, st);
+  cudaFreeAsync(ids_sorted, st);
+  cudaFreeAsync(tmp, st);
+  cudaFreeAsync(children, st);
+  cudaFreeAsync(ranges, st);
+  cudaFreeAsync(parent_int, st);
+  cudaFreeAsync(parent_leaf, st);
+  cudaFreeAsync(keep, st);
+  cudaFreeAsync(compact, st);
+  cudaFreeAsync(leaf_box, st);
+  cudaFreeAsync(int_box, st);
+  cudaFreeAsync(visits, st);
+  SBR_CUDA(cudaStreamSynchronize(st));
+  SBR_CUDA(cudaGetLastError());
+  *out = S;
+  return SBR_OK;
+}
+
+void sbr_scene_destroy(SbrScene* S) {
+  if (!S) return;
+  cudaSetDevice(S->device);
+  cudaFree(S->nodes);
+  cudaFree(S->tris);
+  cudaFree(S->tie_rank);
+  cudaFree(S->normals);
+  cudaFree(S->matrow);
+  cudaFree(S->hash_r);
+  cudaFree(S->hash_f);
+  cudaFree(S->mats);
+  cudaFree(S->error_word);
+  delete S;
+}
+
+int64_t sbr_scene_num_triangles(const SbrScene* S) { return S ? S->ntri : 0; }
+int64_t sbr_scene_num_nodes(const SbrScene* S) { return S ? S->nnodes : 0; }
+
+int sbr_scene_permutation(const SbrScene* S, int64_t* perm_out) {
+  if (!S || !perm_out) return set_error(SBR_ERR_INVALID, "NULL argument");
+  memcpy(perm_out, S->perm.data(), sizeof(int64_t) * S->perm.size());
+  return SBR_OK;
+}
+
+int sbr_scene_set_attributes(SbrScene* S, const int32_t* tie_rank, const double* normals,
+                             const int32_t* matrow, const uint64_t* hash_r,
+                             const uint64_t* hash_f) {
+  if (!S) return set_error(SBR_ERR_INVALID, "NULL scene");
+  SBR_CUDA(cudaSetDevice(S->device));
+  const size_t n = (size_t)S->ntri;
+  if (tie_rank) SBR_CUDA(cudaMemcpy(S->tie_rank, tie_rank, 4 * n, cudaMemcpyHostToDevice));
+  if (normals) SBR_CUDA(cudaMemcpy(S->normals, normals, 24 * n, cudaMemcpyHostToDevice));
+  if (matrow) SBR_CUDA(cudaMemcpy(S->matrow, matrow, 4 * n, cudaMemcpyHostToDevice));
+  if (hash_r) SBR_CUDA(cudaMemcpy(S->hash_r, hash_r, 8 * n, cudaMemcpyHostToDevice));
+  if (hash_f) SBR_CUDA(cudaMemcpy(S->hash_f, hash_f, 8 * n, cudaMemcpyHostToDevice));
+  return SBR_OK;
+}
+
+int sbr_scene_set_materials(SbrScene* S, const SbrMaterial* mats, int32_t n) {
+  if (!S || !mats || n <= 0) return set_error(SBR_ERR_INVALID, "bad material table");
+  SBR_CUDA(cudaSetDevice(S->device));
+  if (S->mats) SBR_CUDA(cudaFree(S->mats));
+  SBR_CUDA(cudaMalloc(&S->mats, sizeof(SbrMaterial) * n));
+  SBR_CUDA(cudaMemcpy(S->mats, mats, sizeof(SbrMaterial) * n, cudaMemcpyHostToDevice));
+  S->nmat = n;
+  return SBR_OK;
+}
+
+int sbr_scene_check(SbrScene* S, void* stream) {
+  if (!S) return set_error(SBR_ERR_INVALID, "NULL scene");
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned int w = 0;
+  SBR_CUDA(cudaMemcpyAsync(&w, S->error_word, sizeof w, cudaMemcpyDeviceToHost, st));
+  SBR_CUDA(cudaStreamSynchronize(st));
+  SBR_CUDA(cudaGetLastError());
+  if (w) {
+    SBR_CUDA(cudaMemsetAsync(S->error_word, 0, sizeof(unsigned), st));
+    if (w & kErrStack) return set_error(SBR_ERR_STACK, "BVH traversal stack overflow");
+  }
+  return SBR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,118 @@
+"""GPU parity of the radio-map SBR megakernel against the reference (golden) and the oracle.
+
+Tolerance: the north star allows 1e-3 relative per cell; float64 on both sides
+makes the agreement ~1e-12 except where CUDA's libm and numpy differ by an
+ulp at a decision boundary, so the tests assert 1e-9 on >= 99.9 % of cells
+and 1e-3 on all of them, plus exact diagnostics counters.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from cases import COUNTER_KEYS, MAP_CASES, build_case, golden_map
+from conftest import golden
+from paper_2504_21719_b200 import SceneModel, compute_radio_map_sbr, scenes
+from paper_2504_21719_b200.radiomap import MeasurementGrid, RadioMapConfig
+from paper_2504_21719_b200.sampling import Interaction
+
+pytestmark = pytest.mark.gpu
+
+RS = frozenset({Interaction.REFLECTION, Interaction.SCATTERING})
+
+
+def _compare(vals, want, tight=1e-9, frac=0.999, loose=1e-3):
+    nz = (want != 0) | (vals != 0)
+    if not nz.any():
+        return 0.0
+    rel = np.abs(vals[nz] - want[nz]) / np.maximum(np.abs(want[nz]), 1e-300)
+    assert np.mean(rel < tight) >= frac, (np.mean(rel < tight), rel.max())
+    assert rel.max() < loose, rel.max()
+    return rel.max()
+
+
+@pytest.mark.parametrize("name", list(MAP_CASES))
+def test_map_matches_reference_golden(cuda, name):
+    g = golden("radiomap.npz")
+    want, want_diag = golden_map(g, name)
+    meshes, mats, src, grid, cfg, kw = build_case(name)
+    scene = SceneModel(meshes, mats)
+    vals, diag = compute_radio_map_sbr(scene, src, grid, cfg, **kw)
+    for key in COUNTER_KEYS:
+        assert diag.get(key, 0) == want_diag.get(key, 0), key
+    _compare(vals, want)
+
+
+def test_canyon_map_vs_oracle_1e5_samples(cuda):
+    meshes = scenes.street_canyon()
+    mats = scenes.uniform_materials(meshes, scenes.concrete(scattering=0.3))
+    grid = MeasurementGrid((0, 0, 1.5), (1, 0, 0), (0, 1, 0), (1.0, 1.0), (200, 200))
+    cfg = RadioMapConfig(num_samples=10_000_000, max_depth=5, enabled=RS, seed=0)
+    rng_range = (3_000_000, 3_100_000)   # 1e5 samples out of the 1e7 lattice
+    vals, diag = compute_radio_map_sbr(SceneModel(meshes, mats), (0.0, 5.0, 20.0), grid, cfg,
+                                       sample_range=rng_range, include_direct=False)
+    want, wdiag = oracle.OracleScene(meshes, mats).radiomap(
+        np.array([0.0, 5.0, 20.0]), grid, cfg, sample_range=rng_range, include_direct=False)
+    for key in ("deposits", "escaped", "respawns", "ray_bounces"):
+        assert diag.get(key, 0) == wdiag[key], key
+    _compare(vals, want)
+
+
+def test_sharding_reproduces_full_map(cuda):
+    """Shards of the global sample ids sum to the single-run map (multi-GPU contract)."""
+    meshes, mats, src, grid, cfg, kw = build_case("box_rst_rr")
+    scene = SceneModel(meshes, mats)
+    full, d_full = compute_radio_map_sbr(scene, src, grid, cfg)
+    parts = [(0, 17_000), (17_000, 40_001), (40_001, cfg.num_samples)]
+    acc = np.zeros_like(full)
+    rb = 0
+    for k, rg in enumerate(parts):
+        v, d = compute_radio_map_sbr(scene, src, grid, cfg, sample_range=rg,
+                                     include_direct=(k == 0))
+        acc += v
+        rb += d["ray_bounces"]
+    assert rb == d_full["ray_bounces"]
+    np.testing.assert_allclose(acc, full, rtol=1e-12)
+
+
+def test_refined_grid_mean_equals_coarse(cuda):
+    # reference test_radiomap.py:281-296 (deposit consistency, direct term excluded)
+    meshes = scenes.box_room_walls()
+    mats = scenes.uniform_materials(meshes, scenes.concrete())
+    scene = SceneModel(meshes, mats)
+    coarse = MeasurementGrid((0.5, 1.0, 1.2), (1, 0, 0), (0, 1, 0), (1.0, 1.0), (1, 1))
+    fine = MeasurementGrid((0.5, 1.0, 1.2), (1, 0, 0), (0, 1, 0), (0.5, 0.5), (2, 2))
+    cfg = RadioMapConfig(num_samples=150_000, max_depth=2, enabled=RS, seed=3)
+    src = np.array([-1.0, -2.0, 1.5])
+    vc, _ = compute_radio_map_sbr(scene, src, coarse, cfg, include_direct=False)
+    vf, _ = compute_radio_map_sbr(scene, src, fine, cfg, include_direct=False)
+    assert vc[0, 0] == pytest.approx(vf.mean(), rel=1e-12)
+
+
+def test_direct_only_map_is_exact(cuda):
+    # reference test_radiomap.py:225-241
+    floor = scenes.quad_mesh(half=5.0, z=-60.0, object_id=1)
+    scene = SceneModel([floor], {1: scenes.concrete()})
+    tx = np.array([0.0, 0.0, 3.0])
+    grid = MeasurementGrid((0.0, 0.0, 0.0), (1, 0, 0), (0, 1, 0), (0.5, 0.5), (4, 4))
+    cfg = RadioMapConfig(num_samples=1000, max_depth=0,
+                         enabled=frozenset({Interaction.REFLECTION}))
+    vals, diag = compute_radio_map_sbr(scene, tx, grid, cfg)
+    centers = grid.cell_centers().reshape(-1, 3)
+    dist = np.linalg.norm(centers - tx, axis=1)
+    expected = (cfg.wavelength / (4.0 * np.pi * dist)) ** 2
+    assert np.allclose(vals.reshape(-1), expected, rtol=1e-12, atol=0.0)
+    assert diag["direct_visible"] == 16
+    assert diag.get("deposits", 0) == 0
+
+
+def test_threshold_only_removes_energy(cuda):
+    meshes, mats, src, grid, cfg, _ = build_case("box_rs")
+    scene = SceneModel(meshes, mats)
+    base = RadioMapConfig(num_samples=100_000, max_depth=3, enabled=RS, seed=1)
+    thr = RadioMapConfig(num_samples=100_000, max_depth=3, enabled=RS, seed=1,
+                         gain_threshold=1e-3)
+    v0, d0 = compute_radio_map_sbr(scene, src, grid, base)
+    v2, d2 = compute_radio_map_sbr(scene, src, grid, thr)
+    assert d2["threshold_killed"] > 0 and d0.get("threshold_killed", 0) == 0
+    assert np.all(v2 <= v0 + 1e-18)

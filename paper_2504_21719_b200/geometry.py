@@ -96,7 +96,7 @@ def _to_device(x, dev, shape_last=None):
     if isinstance(x, torch.Tensor):
         t = x.to(device=dev, dtype=torch.float64)
     else:
-        t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(dev)
+        t = torch.from_numpy(np.array(x, dtype=np.float64, copy=True)).to(dev)
     return t.contiguous()
 
 

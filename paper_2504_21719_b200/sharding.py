@@ -1,0 +1,98 @@
+"""Multi-GPU sharding of the SBR sample lattice (one process per GPU).
+
+The reference parallelises only over host threads (a ThreadPool over
+sample chunks, radiomap.py:605-628, paths.py:1057-1075) and guarantees the
+result is identical for any worker count.  Here the same contract holds
+across GPUs: the RNG is keyed by global sample id, so
+a contiguous shard of ids traced on any rank makes exactly the decisions
+the single-GPU run makes for those ids.
+
+Radio map: each rank traces its shard into a private float64 grid, rank 0
+adds the analytic direct term, then ONE all-reduce (sum) of the grid and
+one of the diagnostics counters (NCCL over NVLink on the GPU box; gloo in
+the CPU tests).  There is no other data-path collective.
+"""
+
+
+def shard_range(num_samples, rank, world):
+    """Contiguous [lo, hi) of the global sample ids owned by `rank`.
+
+    Balanced to within one sample; shard sizes differ by at most 1 so the
+    max-over-ranks time is the per-rank time.
+    """
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank / world size")
+    n = int(num_samples)
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return lo, hi
+
+
+def allreduce_map(values, counters, group=None):
+    """Sum the per-rank float64 grid and int64 counters in place (one collective each)."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(values, group=group)
+        dist.all_reduce(counters, group=group)
+    return values, counters
+
+
+def sharded_radio_map(run_shard, num_samples, group=None):
+    """Generic multi-rank radio map.
+
+    run_shard(lo, hi, include_direct) -> (values tensor (ny,nx) f64,
+    counters tensor int64) computes this rank's contribution (on the GPU in
+    the product: `compute_radio_map_sbr(..., return_tensors=True)`).
+    Returns the all-reduced (values, counters) tensors, identical on every
+    rank.
+    """
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+    else:
+        rank, world = 0, 1
+    lo, hi = shard_range(num_samples, rank, world)
+    values, counters = run_shard(lo, hi, rank == 0)
+    return allreduce_map(values, counters, group)
+
+
+def compute_radio_map_sbr_distributed(scene, source, grid, cfg, group=None, **kw):
+    """compute_radio_map_sbr over all ranks of `group` (torch.distributed).
+
+    Each rank traces its shard of the N_S sample ids on its own GPU; the
+    returned (values (ny,nx) numpy f64, diagnostics dict) equals the
+    single-GPU result up to float64 summation order.
+    """
+    from . import _abi
+    from .radiomap import CHUNK_SAMPLES, compute_radio_map_sbr
+
+    def run(lo, hi, include_direct):
+        return compute_radio_map_sbr(scene, source, grid, cfg, sample_range=(lo, hi),
+                                     include_direct=include_direct, return_tensors=True,
+                                     **kw)
+
+    values, counters = sharded_radio_map(run, cfg.num_samples, group)
+    counts = counters.cpu().numpy()
+    diag = {name: int(counts[i]) for i, name in enumerate(_abi.MAP_COUNTERS)
+            if name != "stack_overflow" and (counts[i] or name in ("escaped", "ray_bounces"))}
+    if counts[_abi.MAP_COUNTERS.index("stack_overflow")]:
+        raise RuntimeError("BVH traversal stack overflow")
+    diag["samples"] = cfg.num_samples
+    diag["chunks"] = -(-cfg.num_samples // CHUNK_SAMPLES)
+    diag["direct_visible"] = int(counts[_abi.MAP_COUNTERS.index("direct_visible")])
+    return values.cpu().numpy(), diag
+
+
+def shard_of_chunks(num_samples, rank, world, chunk=None):
+    """Shard boundaries rounded to the RNG chunk size (2^19), as SURVEY §8e suggests.
+
+    Not required for correctness (the RNG is keyed per sample) but keeps every
+    reference chunk on one rank, which makes per-chunk debugging comparable.
+    """
+    from .radiomap import CHUNK_SAMPLES
+    chunk = CHUNK_SAMPLES if chunk is None else int(chunk)
+    nchunks = -(-int(num_samples) // chunk)
+    clo, chi = shard_range(nchunks, rank, world)
+    return min(clo * chunk, num_samples), min(chi * chunk, num_samples)
+

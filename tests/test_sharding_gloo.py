@@ -1,0 +1,87 @@
+"""Multi-rank host logic on CPU: world_size-2 gloo runs of the sharded radio map.
+
+The per-rank compute is the CPU oracle (the checker) standing in for the GPU
+kernel; what is under test is the product's sharding + all-reduce path
+(paper_2504_21719_b200/sharding.py), which bench.py drives over NCCL on the
+GPU box.  The reference asserts bitwise-identical maps for any worker count
+(pkg/tests/test_radiomap.py:335-346); across ranks the sum order of the
+float64 grid changes, so the map must agree to 1e-12 and counters exactly.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2504_21719_b200 import _abi
+from paper_2504_21719_b200.sharding import shard_of_chunks, shard_range
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_shard_range_partitions_exactly():
+    for n in (1, 7, 1000, 10_000_001):
+        for world in (1, 2, 3, 8):
+            spans = [shard_range(n, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            sizes = [hi - lo for lo, hi in spans]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_chunk_aligned_shards():
+    n = 5 * (1 << 19) + 123
+    spans = [shard_of_chunks(n, r, 2) for r in range(2)]
+    assert spans == [(0, 3 << 19), (3 << 19, n)]
+
+
+def _oracle_run_shard(case, lo, hi, include_direct):
+    import oracle
+    from cases import build_case
+    meshes, mats, src, grid, cfg, kw = build_case(case)
+    vals, diag = oracle.OracleScene(meshes, mats).radiomap(
+        src, grid, cfg, sample_range=(lo, hi), include_direct=include_direct, **kw)
+    counters = torch.tensor([diag[k] for k in _abi.MAP_COUNTERS], dtype=torch.int64)
+    return torch.from_numpy(vals), counters
+
+
+def _worker(rank, world, port, case, out_dir):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, here)
+    sys.path.insert(0, os.path.dirname(here))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from cases import build_case
+        from paper_2504_21719_b200.sharding import sharded_radio_map
+        cfg = build_case(case)[4]
+        vals, counters = sharded_radio_map(
+            lambda lo, hi, d: _oracle_run_shard(case, lo, hi, d), cfg.num_samples)
+        np.save(os.path.join(out_dir, f"vals_{rank}.npy"), vals.numpy())
+        np.save(os.path.join(out_dir, f"cnt_{rank}.npy"), counters.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", ["box_rst_rr", "box_directive_array"])
+def test_two_rank_gloo_map_equals_single_rank(tmp_path, case):
+    world = 2
+    mp.start_processes(_worker, args=(world, _free_port(), case, str(tmp_path)),
+                       nprocs=world, join=True, start_method="spawn")
+    cfg = __import__("cases").build_case(case)[4]
+    full, fcnt = _oracle_run_shard(case, 0, cfg.num_samples, True)
+    for r in range(world):
+        v = np.load(tmp_path / f"vals_{r}.npy")
+        c = np.load(tmp_path / f"cnt_{r}.npy")
+        np.testing.assert_allclose(v, full.numpy(), rtol=1e-12, atol=0)
+        assert np.array_equal(c, fcnt.numpy())

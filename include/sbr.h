@@ -189,6 +189,159 @@ int sbr_radiomap_bounce(const SbrScene* scene, const SbrMapParams* params,
 int sbr_radiomap_direct(const SbrScene* scene, const SbrMapParams* params,
                         double* direct_dev, uint64_t* counters_dev, void* stream);
 
+/* ---- path solver (CIR) ---------------------------------------------------- */
+/* Counters of the path-solver pipeline (paths.py:1098-1103, 1509-1512). */
+enum {
+  SBR_CC_SAMPLES_ESCAPED = 0,
+  SBR_CC_SAMPLES_TERMINATED,
+  SBR_CC_RAY_BOUNCES,        /* closest-hit rows traced in the sweep          */
+  SBR_CC_VERTICES,           /* interaction vertices written                  */
+  SBR_CC_VIS_RAYS,           /* (vertex, target) occlusion rays cast          */
+  SBR_CC_ROWS,               /* visible (vertex, target) rows emitted         */
+  SBR_CC_DUPLICATES,
+  SBR_CC_CHUNK_TRUNCATED,
+  SBR_CC_BUFFER_OVERFLOW,
+  SBR_CC_CANDIDATES,
+  SBR_CC_HASH_REGISTERED,
+  SBR_CC_HASH_SLOTS,         /* distinct DedupTable slots claimed             */
+  SBR_CC_REJ_COPLANAR,
+  SBR_CC_REJ_OCCLUDED,
+  SBR_CC_REJ_DEGENERATE,
+  SBR_CC_STACK_OVERFLOW,
+  SBR_CC_VERTEX_OVERFLOW,
+  SBR_CC_ROW_OVERFLOW,
+  SBR_CC_COUNT
+};
+
+/* Refinement outcome per record (paths.py:1123-1245 Rejection reasons). */
+enum { SBR_REFINE_OK = 0, SBR_REFINE_COPLANAR_MISS = 1, SBR_REFINE_OCCLUDED = 2,
+       SBR_REFINE_DEGENERATE = 3 };
+
+/* Generation parameters of one source (PathConfig paths.py:356-395). */
+typedef struct SbrCirParams {
+  double source[3];
+  double q_diffraction;
+  uint64_t num_samples;
+  uint64_t seed;
+  int32_t max_depth;
+  int32_t allow_mask;             /* R=1 S=2 T=4; D (8) is out of scope         */
+  int32_t n_targets;
+  int32_t pad_;
+  const double* targets_dev;      /* (n_targets, 3)                             */
+} SbrCirParams;
+
+/* Interaction vertices of the sweep (the reference's per-depth `history`,
+ * paths.py:774-781), one entry per closest hit that chose an interaction.
+ * Device SoA, `capacity` entries; `parent` links a vertex to the previous
+ * interaction of the same sample, so a row's whole history is a chain. */
+typedef struct SbrVertexBuf {
+  double* point;                  /* (cap, 3) o + t d                           */
+  double* normal;                 /* (cap, 3) geometric normal facing the ray   */
+  double* run_prob;               /* product of chosen interaction probabilities*/
+  int64_t* sample;                /* global sample id                           */
+  uint64_t* hash_r;               /* chain hash after this step (round / floor) */
+  uint64_t* hash_f;
+  int32_t* parent;                /* previous vertex of the sample, -1 = none   */
+  int32_t* tri;                   /* scene slot                                 */
+  uint8_t* code;                  /* 0 R, 1 S, 2 T                              */
+  uint8_t* depth;                 /* 1-based                                    */
+  uint8_t* suffix_start;          /* depth of the last S step, 0 = none         */
+  int64_t capacity;
+} SbrVertexBuf;
+
+/* Materialised candidate records (CandidateRecord paths.py:249-273), SoA with
+ * `max_depth` step slots per record.  LoS records have depth 0. */
+typedef struct SbrRecordBuf {
+  int32_t* target;                /* (n)                                        */
+  int64_t* sample;                /* (n) -1 = LoS                               */
+  int32_t* depth;                 /* (n)                                        */
+  int32_t* suffix_start;          /* (n)                                        */
+  uint8_t* diffuse;               /* (n) diffuse-terminal                       */
+  uint64_t* chain_hash;           /* (n) round-quantizer chain hash             */
+  double* prefix_prob;            /* (n)                                        */
+  double* anchor;                 /* (n, 3)                                     */
+  int8_t* kind;                   /* (n, L) 0 R 1 S 2 T, -1 unused              */
+  int32_t* tri;                   /* (n, L) scene slot                          */
+  double* vertex;                 /* (n, L, 3)                                  */
+  double* normal;                 /* (n, L, 3)                                  */
+  int32_t max_depth;              /* L                                          */
+  int32_t pad_;
+} SbrRecordBuf;
+
+/* Field-replay parameters of one source (compute_path_fields, paths.py:1302). */
+typedef struct SbrFieldParams {
+  double wavelength;
+  double q_diffraction;
+  double tx_velocity[3];
+  uint64_t num_samples;
+  uint64_t seed;
+  int32_t allow_mask;
+  int32_t n_objects;              /* rows of obj_velocity_dev (may be 0)        */
+  SbrAntenna tx_pattern;
+  const SbrAntenna* rx_pattern_dev;   /* (n_targets) per-target rx pattern      */
+  const double* rx_velocity_dev;      /* (n_targets, 3)                         */
+  const double* obj_velocity_dev;     /* (n_objects, 3) per material row        */
+} SbrFieldParams;
+
+/* Sweep of global sample ids [sample_begin, sample_end) through the bounce
+ * loop of _sweep_chunk (paths.py:704-828, _continue_rays 855-900): closest
+ * hit, slab energies, interaction draw (Philox `interaction` stream keyed by
+ * global id), rolling plane hash, mirror / hemisphere respawn.  Appends one
+ * vertex per interaction at index counters_dev[SBR_CC_VERTICES]. */
+int sbr_cir_sweep(const SbrScene* scene, const SbrCirParams* params, uint64_t sample_begin,
+                  uint64_t sample_end, const SbrVertexBuf* vb, uint64_t* counters_dev,
+                  void* stream);
+/* _visible_pairs (paths.py:657-683): half-space side test + occlusion ray for
+ * every (vertex in [v_begin, v_end), target) pair; appends visible rows
+ * (ordinal key (depth << 60 | sample << 20 | target), vertex index) at
+ * counters_dev[SBR_CC_ROWS].  Rows beyond row_capacity are counted, not
+ * written (SBR_CC_ROW_OVERFLOW). */
+int sbr_cir_visibility(const SbrScene* scene, const SbrCirParams* params,
+                       const SbrVertexBuf* vb, int64_t v_begin, int64_t v_end,
+                       uint64_t* row_key_dev, int32_t* row_vtx_dev, int64_t row_capacity,
+                       uint64_t* counters_dev, void* stream);
+/* Candidate selection with the reference's exact semantics
+ * (_emit_records paths.py:903-987, DedupTable / PathBuffer 174-226,
+ * generate_candidates 1019-1103 at workers=1): ordinal sort, first occurrence
+ * of each (pair_r, pair_f) among chain rows, truncation to n_buffer, LoS
+ * pre-claims, greedy both-slot registration in a table of n_hash slots,
+ * buffer cap.  los_visible_dev: (n_targets) uint8, 1 = unoccluded.
+ * Outputs record (vertex index or -1 for LoS, target) in buffer order;
+ * *n_records (host) receives the count.  Synchronises `stream`. */
+int sbr_cir_select(const SbrCirParams* params, const SbrVertexBuf* vb,
+                   const uint64_t* row_key_dev, const int32_t* row_vtx_dev, int64_t n_rows,
+                   const uint8_t* los_visible_dev, uint64_t n_hash, int64_t n_buffer,
+                   int32_t* rec_vtx_dev, int32_t* rec_target_dev, int64_t* n_records,
+                   uint64_t* counters_dev, void* stream);
+/* Walks vertex parent chains into CandidateRecord arrays
+ * (_record_from_batch paths.py:990-1016). */
+int sbr_cir_records(const SbrCirParams* params, const SbrVertexBuf* vb,
+                    const int32_t* rec_vtx_dev, const int32_t* rec_target_dev, int64_t n,
+                    const SbrRecordBuf* out, void* stream);
+/* Image-method refinement (refine_candidate paths.py:1123-1252, D branch
+ * out of scope): path_vertices_dev (n, L+2, 3) = [source, steps..., target],
+ * status_dev (n) SBR_REFINE_*; rejection counters accumulated. */
+int sbr_cir_refine(const SbrScene* scene, const SbrCirParams* params, const SbrRecordBuf* rec,
+                   int64_t n, double* path_vertices_dev, int32_t* status_dev,
+                   uint64_t* counters_dev, void* stream);
+/* Field replay, Algorithm 2 (compute_path_fields paths.py:1302-1399 +
+ * accumulate_doppler 1410-1426) for records with status OK: complex gain
+ * (re, im), delay, doppler, departure / arrival directions. */
+int sbr_cir_fields(const SbrScene* scene, const SbrFieldParams* params, const SbrRecordBuf* rec,
+                   const double* path_vertices_dev, const int32_t* status_dev, int64_t n,
+                   double* gain_dev, double* delay_dev, double* doppler_dev,
+                   double* departure_dev, double* arrival_dev, void* stream);
+/* Channel frequency response of one link (frequency_response paths.py:1519-1547):
+ * H[r, t, f] = sum_p a_p u_rx,r(arrival_p) u_tx,t(departure_p) e^{-j 2 pi f tau_p},
+ * accumulated in path order in float64.  synthetic = 0: element-indexed paths
+ * (path_rx_el / path_tx_el) add a_p e^{-j 2 pi f tau_p} to H[rx_el, tx_el]. */
+int sbr_cfr(const double* gain_dev, const double* delay_dev, const double* departure_dev,
+            const double* arrival_dev, const int32_t* path_rx_el_dev,
+            const int32_t* path_tx_el_dev, int64_t n_paths, const double* freqs_dev,
+            int32_t n_freq, const double* tx_offsets_dev, int32_t n_tx,
+            const double* rx_offsets_dev, int32_t n_rx, double wavelength, int32_t synthetic,
+            double* h_dev /* (n_rx, n_tx, n_freq) complex128 */, void* stream);
+
 /* ---- misc ----------------------------------------------------------------- */
 const char* sbr_last_error(void);
 int sbr_version(void);

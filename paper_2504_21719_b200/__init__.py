@@ -13,6 +13,18 @@ from .em import ArrayGeometry, AntennaPattern, make_pattern, planar_array  # noq
 from .geometry import Mesh, Ray, build_scene_accel, intersect_closest, is_occluded  # noqa: E402
 from .materials import RadioMaterial, ScatteringPattern, material_presets  # noqa: E402
 from .paths import PathConfig, RadioDevice, SceneModel  # noqa: E402
+from .cir import (  # noqa: E402
+    CandidateRecord,
+    GenerationResult,
+    PathSet,
+    PathTensors,
+    ValidPath,
+    baseband_gains,
+    compute_paths,
+    frequency_response,
+    generate_candidates,
+    refine_candidate,
+)
 from .radiomap import (  # noqa: E402
     MeasurementGrid,
     RadioMapConfig,
@@ -26,7 +38,9 @@ __all__ = [
     "ArrayGeometry", "AntennaPattern", "make_pattern", "planar_array",
     "Mesh", "Ray", "build_scene_accel", "intersect_closest", "is_occluded",
     "RadioMaterial", "ScatteringPattern", "material_presets",
-    "PathConfig", "RadioDevice", "SceneModel",
+    "PathConfig", "RadioDevice", "SceneModel", "CandidateRecord", "GenerationResult",
+    "PathSet", "PathTensors", "ValidPath", "baseband_gains", "compute_paths",
+    "frequency_response", "generate_candidates", "refine_candidate",
     "MeasurementGrid", "RadioMapConfig", "RadioMapResult",
     "compute_radio_map", "compute_radio_map_sbr",
     "Interaction", "__version__",

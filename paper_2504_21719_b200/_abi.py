@@ -102,3 +102,78 @@ def vec3(values):
     for k in range(3):
         arr[k] = float(values[k])
     return arr
+
+
+# ---- path solver (CIR) ------------------------------------------------------
+CIR_COUNTERS = (
+    "samples_escaped",
+    "samples_terminated",
+    "ray_bounces",
+    "vertices",
+    "visibility_rays",
+    "rows",
+    "duplicates",
+    "chunk_truncated",
+    "buffer_overflow",
+    "candidates",
+    "hash_registered",
+    "hash_slots",
+    "rej_coplanar_miss",
+    "rej_occluded",
+    "rej_degenerate",
+    "stack_overflow",
+    "vertex_overflow",
+    "row_overflow",
+)
+SBR_CC_COUNT = len(CIR_COUNTERS)
+CC = {name: i for i, name in enumerate(CIR_COUNTERS)}
+
+SBR_REFINE_OK = 0
+SBR_REFINE_COPLANAR_MISS = 1
+SBR_REFINE_OCCLUDED = 2
+SBR_REFINE_DEGENERATE = 3
+REJECTION_NAMES = {SBR_REFINE_COPLANAR_MISS: "coplanar-miss", SBR_REFINE_OCCLUDED: "occluded",
+                   SBR_REFINE_DEGENERATE: "degenerate"}
+
+
+class SbrCirParams(ctypes.Structure):
+    _fields_ = [
+        ("source", ctypes.c_double * 3),
+        ("q_diffraction", ctypes.c_double),
+        ("num_samples", ctypes.c_uint64),
+        ("seed", ctypes.c_uint64),
+        ("max_depth", ctypes.c_int32),
+        ("allow_mask", ctypes.c_int32),
+        ("n_targets", ctypes.c_int32),
+        ("pad_", ctypes.c_int32),
+        ("targets_dev", ctypes.c_void_p),
+    ]
+
+
+class SbrVertexBuf(ctypes.Structure):
+    _fields_ = [(name, ctypes.c_void_p) for name in (
+        "point", "normal", "run_prob", "sample", "hash_r", "hash_f", "parent", "tri",
+        "code", "depth", "suffix_start")] + [("capacity", ctypes.c_int64)]
+
+
+class SbrRecordBuf(ctypes.Structure):
+    _fields_ = [(name, ctypes.c_void_p) for name in (
+        "target", "sample", "depth", "suffix_start", "diffuse", "chain_hash", "prefix_prob",
+        "anchor", "kind", "tri", "vertex", "normal")] + [
+        ("max_depth", ctypes.c_int32), ("pad_", ctypes.c_int32)]
+
+
+class SbrFieldParams(ctypes.Structure):
+    _fields_ = [
+        ("wavelength", ctypes.c_double),
+        ("q_diffraction", ctypes.c_double),
+        ("tx_velocity", ctypes.c_double * 3),
+        ("num_samples", ctypes.c_uint64),
+        ("seed", ctypes.c_uint64),
+        ("allow_mask", ctypes.c_int32),
+        ("n_objects", ctypes.c_int32),
+        ("tx_pattern", SbrAntenna),
+        ("rx_pattern_dev", ctypes.c_void_p),
+        ("rx_velocity_dev", ctypes.c_void_p),
+        ("obj_velocity_dev", ctypes.c_void_p),
+    ]

@@ -1,0 +1,1016 @@
+// sbr_cir.cu -- path-solver (CIR) candidate generation, selection and refinement.
+//
+// Replaces emtrace paths.py:
+//   _sweep_chunk / _continue_rays (704-828, 855-900)  -> k_cir_sweep
+//   _visible_pairs (657-683)                          -> k_cir_visibility
+//   _emit_records dedup + truncation (903-987),
+//   DedupTable / PathBuffer (174-226),
+//   generate_candidates registration loop (1019-1103) -> sbr_cir_select (CUB sorts
+//                                                        + greedy slot kernels)
+//   _record_from_batch (990-1016)                      -> k_cir_records
+//   refine_candidate (1110-1252)                       -> k_cir_refine
+//
+// Design (B200): the sweep writes one 80-byte vertex per interaction into an
+// HBM vertex buffer with a parent link (the reference keeps per-row history
+// arrays and copies them on every select()); the O(vertices x targets)
+// visibility stage -- the dominant cost at many receivers -- is a flat
+// (vertex, target) grid with targets fastest so a warp shares one origin;
+// candidate rows are 12 bytes (ordinal key + vertex index).  The reference's
+// order-dependent dedup is reproduced exactly with sorts: stable radix sorts
+// give "first occurrence in (depth, sample, target) order" and the
+// both-slot DedupTable greedy is resolved by fixed-point rounds over the slot
+// conflict lists.
+#include <cooperative_groups.h>
+#include <cub/cub.cuh>
+
+#include <string>
+#include <vector>
+
+#include "sbr_physics.cuh"
+
+namespace cg = cooperative_groups;
+
+struct SbrScene;
+
+namespace sbr {
+DevScene dev_view(const SbrScene* s);
+int set_error(int code, const std::string& msg);
+}  // namespace sbr
+
+using namespace sbr;
+
+namespace {
+
+constexpr uint64_t TAG_INTERACTION = 0x5c798e00ad8012ebULL;  // fnv1a("interaction")
+constexpr uint64_t TAG_RESPAWN = 0x742c480a24ff9b7fULL;      // fnv1a("respawn")
+constexpr uint64_t kFnvPrime = 0x100000001B3ULL;
+constexpr uint64_t kHashBase = 1373ULL;                      // HASH_CHAIN_BASE
+constexpr int kTargetBits = 20;
+constexpr int kSampleBits = 40;
+constexpr uint64_t kTargetMask = (1ULL << kTargetBits) - 1;
+constexpr uint64_t kSampleMask = (1ULL << kSampleBits) - 1;
+
+// fnv1a_u64(value, seed) (paths.py:68-75)
+__device__ __forceinline__ uint64_t fnv1a_u64(uint64_t v, uint64_t h) {
+#pragma unroll
+  for (int s = 0; s < 64; s += 8) h = (h ^ ((v >> s) & 0xFFULL)) * kFnvPrime;
+  return h;
+}
+
+__device__ __forceinline__ uint64_t ordinal_key(int depth, int64_t sample, int target) {
+  return ((uint64_t)depth << 60) | (((uint64_t)sample & kSampleMask) << kTargetBits) |
+         ((uint64_t)target & kTargetMask);
+}
+
+// warp-aggregated append: one atomic per coalesced group
+__device__ __forceinline__ unsigned long long append_slot(unsigned long long* counter) {
+  cg::coalesced_group g = cg::coalesced_threads();
+  unsigned long long base = 0;
+  if (g.thread_rank() == 0) base = atomicAdd(counter, (unsigned long long)g.size());
+  base = g.shfl(base, 0);
+  return base + g.thread_rank();
+}
+
+struct CirCounters {
+  unsigned escaped, terminated, rb;
+};
+
+// _interaction_rows for one hit (paths.py:572-595), D never allowed (no wedges)
+__device__ __forceinline__ bool interaction_probs(const SbrMaterial& m, double r_sq, double t_sq,
+                                                  double q_d, int allow, double q[4]) {
+  q[0] = q[1] = q[2] = 0.0;
+  q[3] = q_d;
+  const double den = r_sq + t_sq;
+  if (den > 0.0) {
+    const double keep = 1.0 - q_d;
+    const double s_sq = m.scattering * m.scattering;
+    q[0] = keep * (1.0 - s_sq) * r_sq / den;
+    q[1] = keep * s_sq * r_sq / den;
+    q[2] = keep * t_sq / den;
+  }
+  if (!(allow & 1)) q[0] = 0.0;
+  if (!(allow & 2)) q[1] = 0.0;
+  if (!(allow & 4)) q[2] = 0.0;
+  q[3] = 0.0;  // D: tri_has_wedge is false for every slot
+  const double total = ((q[0] + q[1]) + q[2]) + q[3];
+  if (!(total > 0.0)) return false;
+  q[0] /= total;
+  q[1] /= total;
+  q[2] /= total;
+  q[3] /= total;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// sweep
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_cir_sweep(DevScene S, SbrCirParams P, uint64_t begin,
+                                                   uint64_t end, SbrVertexBuf vb,
+                                                   unsigned long long* __restrict__ counters) {
+  CirCounters K = {0u, 0u, 0u};
+  const double3 src = make_double3(P.source[0], P.source[1], P.source[2]);
+  for (uint64_t g = begin + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < end;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    double3 o = src;
+    double3 d = fibonacci_dir(P.num_samples, g);
+    uint64_t hr = 0, hf = 0;
+    double run_prob = 1.0;
+    int suffix_start = 0;
+    int parent = -1;
+    for (int depth = 1; depth <= P.max_depth; ++depth) {
+      K.rb++;
+      HitRecord h;
+      if (!trace_closest(S, o, d, 1e-4, __longlong_as_double(0x7ff0000000000000LL), h)) {
+        flag_error(S, kErrStack);
+        atomicAdd(counters + SBR_CC_STACK_OVERFLOW, 1ULL);
+        break;
+      }
+      if (h.tri < 0) {
+        K.escaped++;
+        break;
+      }
+      const double3 pt = o + h.t * d;
+      double3 n = ldg3(S.normals + 3 * (int64_t)h.tri);
+      if (dot_seq(d, n) > 0.0) n = neg(n);
+      const double cos_i = fabs(dot_seq(d, n));
+      const SbrMaterial m = S.mats[__ldg(S.matrow + h.tri)];
+      const Fresnel4 F = slab_fresnel(m, cos_i);
+      const double r_sq = cabs2(F.rp) + cabs2(F.rl);
+      const double t_sq = cabs2(F.tp) + cabs2(F.tl);
+      double q[4];
+      if (!interaction_probs(m, r_sq, t_sq, P.q_diffraction, P.allow_mask, q)) {
+        K.terminated++;
+        break;
+      }
+      const double u = philox_uniform(P.seed, 0, (uint64_t)depth, TAG_INTERACTION, g);
+      const double c0 = q[0], c1 = c0 + q[1], c2 = c1 + q[2], c3 = c2 + q[3];
+      int code = (u >= c0) + (u >= c1) + (u >= c2) + (u >= c3);
+      if (code > 3) code = 3;
+      run_prob *= q[code];
+      if (code == 0) {
+        hr = kHashBase * hr + __ldg(S.hash_r + h.tri);
+        hf = kHashBase * hf + __ldg(S.hash_f + h.tri);
+      } else if (code == 1) {
+        suffix_start = depth;
+      }
+      const unsigned long long vi = append_slot(counters + SBR_CC_VERTICES);
+      if ((int64_t)vi < vb.capacity) {
+        vb.point[3 * vi] = pt.x;
+        vb.point[3 * vi + 1] = pt.y;
+        vb.point[3 * vi + 2] = pt.z;
+        vb.normal[3 * vi] = n.x;
+        vb.normal[3 * vi + 1] = n.y;
+        vb.normal[3 * vi + 2] = n.z;
+        vb.run_prob[vi] = run_prob;
+        vb.sample[vi] = (int64_t)g;
+        vb.hash_r[vi] = hr;
+        vb.hash_f[vi] = hf;
+        vb.parent[vi] = parent;
+        vb.tri[vi] = h.tri;
+        vb.code[vi] = (uint8_t)code;
+        vb.depth[vi] = (uint8_t)depth;
+        vb.suffix_start[vi] = (uint8_t)suffix_start;
+        parent = (int)vi;
+      } else {
+        atomicAdd(counters + SBR_CC_VERTEX_OVERFLOW, 1ULL);
+        break;
+      }
+      if (depth == P.max_depth) break;
+      // _continue_rays (paths.py:855-900)
+      if (code == 0) {
+        const double dn = dot_seq(d, n);
+        d = d - (2.0 * dn) * n;
+      } else if (code == 1) {
+        const double u0 = philox_uniform(P.seed, 0, (uint64_t)depth, TAG_RESPAWN, 2 * g);
+        const double u1 = philox_uniform(P.seed, 0, (uint64_t)depth, TAG_RESPAWN, 2 * g + 1);
+        const double cos_t = u0, azim = kTwoPi * u1;
+        const double x = 1.0 - cos_t * cos_t;
+        const double sin_t = sqrt(x > 0.0 ? x : 0.0);
+        const double3 t1 = perp_batch(n);
+        const double3 t2 = cross3(n, t1);
+        double sa, ca;
+        sincos(azim, &sa, &ca);
+        const double a = sin_t * ca, b = sin_t * sa;
+        d = make_double3((a * t1.x + b * t2.x) + cos_t * n.x, (a * t1.y + b * t2.y) + cos_t * n.y,
+                         (a * t1.z + b * t2.z) + cos_t * n.z);
+      }
+      o = pt;
+    }
+  }
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned v[3] = {K.escaped, K.terminated, K.rb};
+  const int idx[3] = {SBR_CC_SAMPLES_ESCAPED, SBR_CC_SAMPLES_TERMINATED, SBR_CC_RAY_BOUNCES};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const unsigned s = __reduce_add_sync(0xffffffffu, v[k]);
+    if (lane == 0 && s) atomicAdd(counters + idx[k], (unsigned long long)s);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// visibility: (vertex, target) pairs, targets fastest
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_cir_visibility(DevScene S, SbrCirParams P,
+                                                        SbrVertexBuf vb, int64_t v_begin,
+                                                        int64_t v_end, uint64_t* row_key,
+                                                        int32_t* row_vtx, int64_t row_cap,
+                                                        unsigned long long* counters) {
+  const int64_t nt = P.n_targets;
+  const int64_t total = (v_end - v_begin) * nt;
+  unsigned vis = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = v_begin + i / nt;
+    const int k = (int)(i % nt);
+    const double3 p = ld3(vb.point + 3 * v);
+    const double3 n = ld3(vb.normal + 3 * v);
+    const int code = vb.code[v];
+    const double3 tg = ldg3(P.targets_dev + 3 * k);
+    const double side = dot_seq(tg - p, n);
+    const bool ok = code == 2 ? side < 0.0 : side > 0.0;
+    if (!ok) continue;
+    vis++;
+    bool fine;
+    const bool blocked = occluded_segment(S, p, tg, 1e-4, fine);
+    if (!fine) {
+      flag_error(S, kErrStack);
+      atomicAdd(counters + SBR_CC_STACK_OVERFLOW, 1ULL);
+    }
+    if (blocked) continue;
+    const unsigned long long r = append_slot(counters + SBR_CC_ROWS);
+    if ((int64_t)r < row_cap) {
+      row_key[r] = ordinal_key(vb.depth[v], vb.sample[v], k);
+      row_vtx[r] = (int32_t)v;
+    }
+  }
+  const unsigned s = __reduce_add_sync(0xffffffffu, vis);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(counters + SBR_CC_VIS_RAYS, (unsigned long long)s);
+}
+
+// ---------------------------------------------------------------------------
+// selection kernels
+// ---------------------------------------------------------------------------
+// per sorted row: pair hashes and the chain flag (_emit_records 919-924)
+__global__ void k_row_pairs(SbrVertexBuf vb, const uint64_t* __restrict__ skey,
+                            const int32_t* __restrict__ sidx, const int32_t* __restrict__ row_vtx,
+                            int64_t n, uint64_t* pr, uint64_t* pf, uint8_t* chain) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int v = row_vtx[sidx[i]];
+    const uint64_t k = skey[i] & kTargetMask;
+    pr[i] = fnv1a_u64(vb.hash_r[v], k);
+    pf[i] = fnv1a_u64(vb.hash_f[v], k);
+    chain[i] = (vb.suffix_start[v] == 0 && vb.code[v] != 1) ? 1 : 0;
+  }
+}
+
+__global__ void k_gather_u64(const uint64_t* __restrict__ src, const int32_t* __restrict__ idx,
+                             int64_t n, uint64_t* dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[idx[i]];
+}
+
+// first occurrence of each (pr, pf) among chain rows sorted by (pr, pf, ordinal)
+__global__ void k_first_flags(const uint64_t* __restrict__ pr, const uint64_t* __restrict__ pf,
+                              const int32_t* __restrict__ order, int64_t n, uint8_t* keep_chain,
+                              unsigned long long* counters) {
+  unsigned dup = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t a = order[i];
+    bool first = true;
+    if (i > 0) {
+      const int32_t b = order[i - 1];
+      first = pr[a] != pr[b] || pf[a] != pf[b];
+    }
+    keep_chain[a] = first ? 1 : 0;
+    dup += first ? 0u : 1u;
+  }
+  const unsigned s = __reduce_add_sync(0xffffffffu, dup);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(counters + SBR_CC_DUPLICATES, (unsigned long long)s);
+}
+
+// kept rows per depth (the reference truncates depth by depth, _emit_records 954-960)
+__global__ void k_kept_per_depth(const uint64_t* __restrict__ skey, const int32_t* __restrict__ kept,
+                                 int64_t n, unsigned long long* per_depth) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (kept[i]) atomicAdd(per_depth + (skey[i] >> 60), 1ULL);
+}
+
+// kept = non-chain or first occurrence (ordinal order)
+__global__ void k_kept(const uint8_t* __restrict__ chain, const uint8_t* __restrict__ keep_chain,
+                       int64_t n, int32_t* kept) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    kept[i] = (!chain[i] || keep_chain[i]) ? 1 : 0;
+}
+
+// registration keys: LoS first (target order), then kept chain rows under the
+// truncation cap, in ordinal order.  reg_src: >= 0 sorted-row index, < 0 ~target.
+__global__ void k_reg_keys_los(const uint8_t* __restrict__ los, const int32_t* __restrict__ los_pos,
+                               int n_targets, uint64_t* rk1, uint64_t* rk2, int64_t* reg_src) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_targets; k += gridDim.x * blockDim.x) {
+    if (!los[k]) continue;
+    const int j = los_pos[k];
+    const uint64_t key = fnv1a_u64(0ULL, (uint64_t)k);  // pair_with_target(0, k)
+    rk1[j] = key;
+    rk2[j] = key;
+    reg_src[j] = ~(int64_t)k;
+  }
+}
+
+__global__ void k_reg_flags(const uint8_t* __restrict__ chain, const int32_t* __restrict__ kept,
+                            const int32_t* __restrict__ kept_pos, int64_t n, int64_t n_buffer,
+                            int32_t* is_reg) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    is_reg[i] = (chain[i] && kept[i] && kept_pos[i] < n_buffer) ? 1 : 0;
+}
+
+__global__ void k_reg_keys_rows(const int32_t* __restrict__ is_reg, const int32_t* __restrict__ reg_pos,
+                                const uint64_t* __restrict__ pr, const uint64_t* __restrict__ pf,
+                                int64_t n, int64_t base, uint64_t* rk1, uint64_t* rk2,
+                                int64_t* reg_src, int32_t* row_reg) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (!is_reg[i]) {
+      row_reg[i] = -1;
+      continue;
+    }
+    const int64_t j = base + reg_pos[i];
+    rk1[j] = pr[i];
+    rk2[j] = pf[i];
+    reg_src[j] = i;
+    row_reg[i] = (int32_t)j;
+  }
+}
+
+// slot entries: (slot, key) for both slots (one entry when they coincide)
+__global__ void k_slot_entries(const uint64_t* __restrict__ rk1, const uint64_t* __restrict__ rk2,
+                               int64_t nreg, uint64_t n_hash, uint64_t* slot, int32_t* owner) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nreg;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t s1 = rk1[j] % n_hash, s2 = rk2[j] % n_hash;
+    slot[2 * j] = s1;
+    owner[2 * j] = (int32_t)j;
+    // a coincident second slot becomes a sentinel sorted past every real slot
+    slot[2 * j + 1] = s2 == s1 ? ~0ULL : s2;
+    owner[2 * j + 1] = (int32_t)j;
+  }
+}
+
+__global__ void k_entry_pos(const int32_t* __restrict__ owner, const uint64_t* __restrict__ slot,
+                            int64_t ne, int32_t* pos1, int32_t* pos2) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (slot[e] == ~0ULL) continue;
+    const int32_t j = owner[e];
+    // entries of one key: the smaller position is written to pos1 by whichever
+    // lands first; use atomics so both slots get recorded
+    if (atomicCAS(pos1 + j, -1, (int32_t)e) != -1) pos2[j] = (int32_t)e;
+  }
+}
+
+// state: 0 undecided, 1 accepted, 2 rejected (DedupTable.register both-slot rule)
+__device__ __forceinline__ int scan_slot(const uint64_t* slot, const int32_t* owner,
+                                         const uint8_t* state, int32_t e) {
+  // 1: some earlier key in this slot accepted; 0: all earlier rejected / none;
+  // -1: an earlier key is still undecided
+  const uint64_t s = slot[e];
+  int res = 0;
+  for (int32_t f = e - 1; f >= 0 && slot[f] == s; --f) {
+    const uint8_t st = state[owner[f]];
+    if (st == 1) return 1;
+    if (st == 0) res = -1;
+  }
+  return res;
+}
+
+__global__ void k_greedy_round(const uint64_t* __restrict__ slot, const int32_t* __restrict__ owner,
+                               const int32_t* __restrict__ pos1, const int32_t* __restrict__ pos2,
+                               int64_t nreg, uint8_t* state, int* changed, int* undecided) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nreg;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    if (state[j] != 0) continue;
+    const int a = scan_slot(slot, owner, state, pos1[j]);
+    const int b = pos2[j] >= 0 ? scan_slot(slot, owner, state, pos2[j]) : 0;
+    if (a == 1 || b == 1) {
+      state[j] = 2;
+      *changed = 1;
+    } else if (a == 0 && b == 0) {
+      state[j] = 1;
+      *changed = 1;
+    } else {
+      *undecided = 1;
+    }
+  }
+}
+
+// claimed slots: slot runs holding an accepted key (DedupTable.load_factor numerator)
+__global__ void k_claimed(const uint64_t* __restrict__ slot, const int32_t* __restrict__ owner,
+                          const uint8_t* __restrict__ state, int64_t ne,
+                          unsigned long long* counters) {
+  unsigned c = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t s = slot[e];
+    if (s == ~0ULL || state[owner[e]] != 1) continue;
+    bool first = true;
+    for (int64_t f = e - 1; f >= 0 && slot[f] == s; --f)
+      if (state[owner[f]] == 1) {
+        first = false;
+        break;
+      }
+    c += first ? 1u : 0u;
+  }
+  const unsigned sc = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && sc) atomicAdd(counters + SBR_CC_HASH_SLOTS, (unsigned long long)sc);
+}
+
+__global__ void k_add_counter(unsigned long long* counters, int idx, unsigned long long v) {
+  counters[idx] += v;
+}
+
+__global__ void k_count_states(const uint8_t* __restrict__ state, int64_t nreg,
+                               unsigned long long* counters) {
+  unsigned acc = 0, rej = 0;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nreg;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    acc += state[j] == 1;
+    rej += state[j] == 2;
+  }
+  const unsigned a = __reduce_add_sync(0xffffffffu, acc);
+  const unsigned r = __reduce_add_sync(0xffffffffu, rej);
+  if ((threadIdx.x & 31) == 0) {
+    if (a) atomicAdd(counters + SBR_CC_HASH_REGISTERED, (unsigned long long)a);
+    if (r) atomicAdd(counters + SBR_CC_DUPLICATES, (unsigned long long)r);
+  }
+}
+
+// buffer flags: rows entering the PathBuffer (after LoS)
+__global__ void k_buffer_flags(const uint8_t* __restrict__ chain, const int32_t* __restrict__ kept,
+                               const int32_t* __restrict__ kept_pos,
+                               const int32_t* __restrict__ row_reg,
+                               const uint8_t* __restrict__ state, int64_t n, int64_t n_buffer,
+                               int32_t* in_buf) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    bool b = kept[i] && kept_pos[i] < n_buffer;
+    if (b && chain[i]) b = state[row_reg[i]] == 1;
+    in_buf[i] = b ? 1 : 0;
+  }
+}
+
+__global__ void k_los_buffer(const int64_t* __restrict__ reg_src, const uint8_t* __restrict__ state,
+                             const int32_t* __restrict__ los_acc_pos, int n_los_keys,
+                             int64_t n_buffer, int32_t* rec_vtx, int32_t* rec_target) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n_los_keys; j += gridDim.x * blockDim.x) {
+    if (state[j] != 1) continue;
+    const int p = los_acc_pos[j];
+    if (p >= n_buffer) continue;
+    rec_vtx[p] = -1;
+    rec_target[p] = (int32_t)(~reg_src[j]);
+  }
+}
+
+__global__ void k_row_buffer(const int32_t* __restrict__ in_buf, const int32_t* __restrict__ buf_pos,
+                             const uint64_t* __restrict__ skey, const int32_t* __restrict__ sidx,
+                             const int32_t* __restrict__ row_vtx, int64_t n, int64_t base,
+                             int64_t n_buffer, int32_t* rec_vtx, int32_t* rec_target) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (!in_buf[i]) continue;
+    const int64_t p = base + buf_pos[i];
+    if (p >= n_buffer) continue;
+    rec_vtx[p] = row_vtx[sidx[i]];
+    rec_target[p] = (int32_t)(skey[i] & kTargetMask);
+  }
+}
+
+__global__ void k_iota(int32_t* a, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = (int32_t)i;
+}
+
+// ---------------------------------------------------------------------------
+// records
+// ---------------------------------------------------------------------------
+__global__ void k_cir_records(SbrCirParams P, SbrVertexBuf vb, const int32_t* __restrict__ rec_vtx,
+                              const int32_t* __restrict__ rec_target, int64_t n, SbrRecordBuf R) {
+  const int L = R.max_depth;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int v = rec_vtx[r];
+    R.target[r] = rec_target[r];
+    for (int j = 0; j < L; ++j) {
+      R.kind[r * L + j] = -1;
+      R.tri[r * L + j] = -1;
+    }
+    if (v < 0) {
+      R.sample[r] = -1;
+      R.depth[r] = 0;
+      R.suffix_start[r] = 0;
+      R.diffuse[r] = 0;
+      R.chain_hash[r] = 0;
+      R.prefix_prob[r] = 1.0;
+      for (int c = 0; c < 3; ++c) R.anchor[3 * r + c] = P.source[c];
+      continue;
+    }
+    const int depth = vb.depth[v];
+    const int ss = vb.suffix_start[v];
+    R.sample[r] = vb.sample[v];
+    R.depth[r] = depth;
+    R.suffix_start[r] = ss;
+    R.diffuse[r] = vb.code[v] == 1 ? 1 : 0;
+    R.chain_hash[r] = vb.hash_r[v];
+    R.prefix_prob[r] = 1.0;
+    for (int c = 0; c < 3; ++c) R.anchor[3 * r + c] = P.source[c];
+    int w = v;
+    for (int j = depth - 1; j >= 0 && w >= 0; --j) {
+      const int64_t o = r * L + j;
+      R.kind[o] = (int8_t)vb.code[w];
+      R.tri[o] = vb.tri[w];
+      for (int c = 0; c < 3; ++c) {
+        R.vertex[3 * o + c] = vb.point[3 * w + c];
+        R.normal[3 * o + c] = vb.normal[3 * w + c];
+      }
+      if (ss > 0 && j + 1 == ss) {
+        R.prefix_prob[r] = vb.run_prob[w];
+        for (int c = 0; c < 3; ++c) R.anchor[3 * r + c] = vb.point[3 * w + c];
+      }
+      w = vb.parent[w];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// refinement (image method)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double3 reflect_point(double3 p, double3 nrm, double3 on) {
+  const double f = dot_ddot(p - on, nrm);
+  return p - (2.0 * f) * nrm;
+}
+
+__global__ void __launch_bounds__(128) k_cir_refine(DevScene S, SbrCirParams P, SbrRecordBuf R,
+                                                    int64_t n, double* __restrict__ pv,
+                                                    int32_t* __restrict__ status,
+                                                    unsigned long long* counters) {
+  const int L = R.max_depth;
+  const double3 src = make_double3(P.source[0], P.source[1], P.source[2]);
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int depth = R.depth[r];
+    const int ss = R.suffix_start[r];
+    const int k = R.target[r];
+    const double3 tg = ldg3(P.targets_dev + 3 * k);
+    double* out = pv + r * (int64_t)(L + 2) * 3;
+    for (int j = 0; j < (L + 2) * 3; ++j) out[j] = 0.0;
+    out[0] = src.x;
+    out[1] = src.y;
+    out[2] = src.z;
+    for (int j = 0; j < depth; ++j)
+      for (int c = 0; c < 3; ++c) out[3 * (j + 1) + c] = R.vertex[3 * (r * L + j) + c];
+    out[3 * (depth + 1)] = tg.x;
+    out[3 * (depth + 1) + 1] = tg.y;
+    out[3 * (depth + 1) + 2] = tg.z;
+    if (R.diffuse[r] || ss >= depth) {
+      status[r] = SBR_REFINE_OK;
+      continue;
+    }
+    const int ns = depth - ss;
+    const double3 anchor = ld3(R.anchor + 3 * r);
+    double3 img[16];
+    img[0] = anchor;
+    for (int j = 0; j < ns; ++j) {
+      const int64_t o = r * L + ss + j;
+      img[j + 1] = R.kind[o] == 0
+                       ? reflect_point(img[j], ld3(R.normal + 3 * o), ld3(R.vertex + 3 * o))
+                       : img[j];
+    }
+    int st = SBR_REFINE_OK;
+    double3 from = tg;
+    double3 first = tg;
+    for (int j = ns - 1; j >= 0; --j) {
+      const int64_t o = r * L + ss + j;
+      const double3 aim = img[j + 1];
+      double3 ray = aim - from;
+      const double len = sqrt(dot_ddot(ray, ray));
+      if (len < 1e-12) {
+        st = SBR_REFINE_DEGENERATE;
+        break;
+      }
+      ray = make_double3(ray.x / len, ray.y / len, ray.z / len);
+      HitRecord h;
+      if (!trace_closest(S, from, ray, 1e-4, __longlong_as_double(0x7ff0000000000000LL), h)) {
+        flag_error(S, kErrStack);
+        atomicAdd(counters + SBR_CC_STACK_OVERFLOW, 1ULL);
+      }
+      if (h.tri < 0) {
+        st = SBR_REFINE_COPLANAR_MISS;
+        break;
+      }
+      const double3 hn = ldg3(S.normals + 3 * (int64_t)h.tri);
+      const double3 sn = ld3(R.normal + 3 * o);
+      const double3 hp = from + h.t * ray;
+      if (fabs(dot_ddot(hn, sn)) < 1.0 - 1e-6 ||
+          !(fabs(dot_ddot(hp - ld3(R.vertex + 3 * o), sn)) <= 1e-6)) {
+        st = SBR_REFINE_COPLANAR_MISS;
+        break;
+      }
+      out[3 * (ss + j + 1)] = hp.x;
+      out[3 * (ss + j + 1) + 1] = hp.y;
+      out[3 * (ss + j + 1) + 2] = hp.z;
+      from = hp;
+      first = hp;
+    }
+    if (st == SBR_REFINE_OK) {
+      bool fine;
+      if (occluded_segment(S, anchor, first, 1e-4, fine)) st = SBR_REFINE_OCCLUDED;
+      if (!fine) flag_error(S, kErrStack);
+    }
+    status[r] = st;
+    if (st == SBR_REFINE_COPLANAR_MISS) atomicAdd(counters + SBR_CC_REJ_COPLANAR, 1ULL);
+    if (st == SBR_REFINE_OCCLUDED) atomicAdd(counters + SBR_CC_REJ_OCCLUDED, 1ULL);
+    if (st == SBR_REFINE_DEGENERATE) atomicAdd(counters + SBR_CC_REJ_DEGENERATE, 1ULL);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host helpers
+// ---------------------------------------------------------------------------
+unsigned grid_for(int64_t n, int block, int cap = 148 * 32) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+int launch_status(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(SBR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  count_launch();
+  return SBR_OK;
+}
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t _e = (call);                                                             \
+    if (_e != cudaSuccess) {                                                             \
+      rc = set_error(SBR_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+      goto done;                                                                         \
+    }                                                                                    \
+  } while (0)
+
+#define LK(what)                                 \
+  do {                                           \
+    if ((rc = launch_status(what)) != SBR_OK) goto done; \
+  } while (0)
+
+// stream-ordered scratch arena (freed at the end of a call)
+struct Arena {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  bool ok = true;
+  explicit Arena(cudaStream_t s) : st(s) {}
+  template <typename T>
+  T* get(int64_t count) {
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, sizeof(T) * (size_t)(count > 0 ? count : 1), st) != cudaSuccess) {
+      ok = false;
+      return nullptr;
+    }
+    ptrs.push_back(p);
+    return (T*)p;
+  }
+  ~Arena() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+};
+
+int check_cir(const SbrScene* scene, const SbrCirParams* P) {
+  if (!P) return set_error(SBR_ERR_INVALID, "NULL params");
+  if (scene && !dev_view(scene).mats) return set_error(SBR_ERR_INVALID, "scene has no material table");
+  if (P->max_depth < 0 || P->max_depth > 15) return set_error(SBR_ERR_INVALID, "max_depth must lie in [0, 15]");
+  if (P->allow_mask & 8) return set_error(SBR_ERR_UNSUPPORTED, "diffraction is out of scope");
+  if (P->n_targets < 1 || P->n_targets > (1 << kTargetBits))
+    return set_error(SBR_ERR_INVALID, "need 1 .. 2^20 targets");
+  if (P->num_samples < 1 || P->num_samples > kSampleMask)
+    return set_error(SBR_ERR_INVALID, "num_samples must lie in [1, 2^40)");
+  return SBR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sbr_cir_sweep(const SbrScene* scene, const SbrCirParams* P, uint64_t begin, uint64_t end,
+                  const SbrVertexBuf* vb, uint64_t* counters, void* stream) {
+  int rc = check_cir(scene, P);
+  if (rc) return rc;
+  if (!scene || !vb) return set_error(SBR_ERR_INVALID, "NULL argument");
+  if (end > P->num_samples || begin > end) return set_error(SBR_ERR_INVALID, "bad sample range");
+  if (end == begin || P->max_depth == 0) return SBR_OK;
+  k_cir_sweep<<<grid_for((int64_t)(end - begin), 128, 148 * 16), 128, 0, (cudaStream_t)stream>>>(
+      dev_view(scene), *P, begin, end, *vb, (unsigned long long*)counters);
+  return launch_status("k_cir_sweep");
+}
+
+int sbr_cir_visibility(const SbrScene* scene, const SbrCirParams* P, const SbrVertexBuf* vb,
+                       int64_t v_begin, int64_t v_end, uint64_t* row_key, int32_t* row_vtx,
+                       int64_t row_cap, uint64_t* counters, void* stream) {
+  int rc = check_cir(scene, P);
+  if (rc) return rc;
+  if (!scene || !vb) return set_error(SBR_ERR_INVALID, "NULL argument");
+  if (v_end <= v_begin) return SBR_OK;
+  const int64_t pairs = (v_end - v_begin) * (int64_t)P->n_targets;
+  k_cir_visibility<<<grid_for(pairs, 128, 148 * 64), 128, 0, (cudaStream_t)stream>>>(
+      dev_view(scene), *P, *vb, v_begin, v_end, row_key, row_vtx, row_cap,
+      (unsigned long long*)counters);
+  return launch_status("k_cir_visibility");
+}
+
+int sbr_cir_select(const SbrCirParams* P, const SbrVertexBuf* vb, const uint64_t* row_key,
+                   const int32_t* row_vtx, int64_t n, const uint8_t* los, uint64_t n_hash,
+                   int64_t n_buffer, int32_t* rec_vtx, int32_t* rec_target, int64_t* n_records,
+                   uint64_t* counters_u64, void* stream) {
+  int rc = check_cir(nullptr, P);
+  if (rc) return rc;
+  if (!vb || !n_records || !los) return set_error(SBR_ERR_INVALID, "NULL argument");
+  if (n_hash < 1 || n_buffer < 1) return set_error(SBR_ERR_INVALID, "capacity must be positive");
+  if (n >= (1LL << 31)) return set_error(SBR_ERR_INVALID, "too many rows");
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* counters = (unsigned long long*)counters_u64;
+  const int nt = P->n_targets;
+  Arena A(st);
+  int64_t nreg = 0, n_los_keys = 0, n_chain = 0;
+  int hflag[2];
+  int64_t n_los_acc = 0, n_rows_buf = 0;
+  *n_records = 0;
+  {
+    // ---- LoS key positions ----
+    int32_t* los_pos = A.get<int32_t>(nt + 1);
+    // ---- sorted rows ----
+    uint64_t* skey = A.get<uint64_t>(n);
+    int32_t* idx0 = A.get<int32_t>(n);
+    int32_t* sidx = A.get<int32_t>(n);
+    uint64_t* pr = A.get<uint64_t>(n);
+    uint64_t* pf = A.get<uint64_t>(n);
+    uint8_t* chain = A.get<uint8_t>(n);
+    uint8_t* keep_chain = A.get<uint8_t>(n);
+    int32_t* kept = A.get<int32_t>(n);
+    int32_t* kept_pos = A.get<int32_t>(n + 1);
+    int64_t* d_count = A.get<int64_t>(4);
+    if (!A.ok) return set_error(SBR_ERR_NOMEM, "select scratch");
+    size_t tmp_bytes = 0, t2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, skey, skey, idx0, sidx, (int)n, 0, 64, st);
+    cub::DeviceScan::ExclusiveSum(nullptr, t2, kept, kept_pos, (int)n + 1, st);
+    tmp_bytes = std::max(tmp_bytes, t2);
+    cub::DeviceSelect::Flagged(nullptr, t2, idx0, chain, sidx, d_count, (int)n, st);
+    tmp_bytes = std::max(tmp_bytes, t2);
+    void* tmp = A.get<uint8_t>((int64_t)tmp_bytes);
+    if (!A.ok) return set_error(SBR_ERR_NOMEM, "select scratch");
+
+    // LoS key positions: unoccluded targets in target order (generate_candidates 1036-1049)
+    {
+      std::vector<uint8_t> h(nt);
+      std::vector<int32_t> h32(nt + 1, 0);
+      CK(cudaMemcpyAsync(h.data(), los, nt, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      int32_t acc = 0;
+      for (int k = 0; k < nt; ++k) {
+        h32[k] = acc;
+        acc += h[k] ? 1 : 0;
+      }
+      h32[nt] = acc;
+      n_los_keys = acc;
+      CK(cudaMemcpyAsync(los_pos, h32.data(), sizeof(int32_t) * (nt + 1), cudaMemcpyHostToDevice, st));
+      CK(cudaStreamSynchronize(st));
+    }
+
+    if (n > 0) {
+      k_iota<<<grid_for(n, 256), 256, 0, st>>>(idx0, n);
+      LK("k_iota");
+      CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, row_key, skey, idx0, sidx, (int)n, 0, 64, st));
+      count_launch();
+      k_row_pairs<<<grid_for(n, 256), 256, 0, st>>>(*vb, skey, sidx, row_vtx, n, pr, pf, chain);
+      LK("k_row_pairs");
+      // chain rows (positions in ordinal order)
+      int32_t* cpos = A.get<int32_t>(n);
+      int32_t* cpos2 = A.get<int32_t>(n);
+      uint64_t* ck = A.get<uint64_t>(n);
+      uint64_t* ck2 = A.get<uint64_t>(n);
+      if (!A.ok) return set_error(SBR_ERR_NOMEM, "select scratch");
+      k_iota<<<grid_for(n, 256), 256, 0, st>>>(idx0, n);
+      LK("k_iota");
+      CK(cub::DeviceSelect::Flagged(tmp, tmp_bytes, idx0, chain, cpos, d_count, (int)n, st));
+      count_launch();
+      CK(cudaMemcpyAsync(&n_chain, d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      CK(cudaMemsetAsync(keep_chain, 0, n, st));
+      if (n_chain > 0) {
+        // stable LSD: by pf, then by pr -> (pr, pf, ordinal) order
+        k_gather_u64<<<grid_for(n_chain, 256), 256, 0, st>>>(pf, cpos, n_chain, ck);
+        LK("k_gather_u64");
+        CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ck, ck2, cpos, cpos2, (int)n_chain, 0, 64, st));
+        count_launch();
+        k_gather_u64<<<grid_for(n_chain, 256), 256, 0, st>>>(pr, cpos2, n_chain, ck);
+        LK("k_gather_u64");
+        CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ck, ck2, cpos2, cpos, (int)n_chain, 0, 64, st));
+        count_launch();
+        k_first_flags<<<grid_for(n_chain, 256), 256, 0, st>>>(pr, pf, cpos, n_chain, keep_chain, counters);
+        LK("k_first_flags");
+      }
+      k_kept<<<grid_for(n, 256), 256, 0, st>>>(chain, keep_chain, n, kept);
+      LK("k_kept");
+      CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, kept, kept_pos, (int)n, st));
+      count_launch();
+    }
+    int64_t n_kept = 0;
+    if (n > 0) {
+      int32_t lastp = 0, lastk = 0;
+      CK(cudaMemcpyAsync(&lastp, kept_pos + n - 1, 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(&lastk, kept + n - 1, 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      n_kept = (int64_t)lastp + lastk;
+    }
+    if (n_kept > n_buffer) {
+      // _emit_records: room = capacity - emitted_total per depth; a depth whose
+      // rows are all cut (room == 0) returns no batch, so its truncation is not
+      // counted -- only the depth that crosses the cap contributes.
+      unsigned long long* per_depth = A.get<unsigned long long>(16);
+      if (!A.ok) return set_error(SBR_ERR_NOMEM, "select scratch");
+      CK(cudaMemsetAsync(per_depth, 0, 16 * sizeof(unsigned long long), st));
+      k_kept_per_depth<<<grid_for(n, 256), 256, 0, st>>>(skey, kept, n, per_depth);
+      LK("k_kept_per_depth");
+      unsigned long long hd[16];
+      CK(cudaMemcpyAsync(hd, per_depth, sizeof hd, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      int64_t emitted = 0;
+      unsigned long long truncated = 0;
+      for (int d = 0; d < 16; ++d) {
+        const int64_t rows = (int64_t)hd[d];
+        if (rows == 0) continue;
+        const int64_t room = n_buffer - emitted > 0 ? n_buffer - emitted : 0;
+        if (rows > room) {
+          if (room > 0) truncated += (unsigned long long)(rows - room);
+          emitted += room;
+        } else {
+          emitted += rows;
+        }
+      }
+      if (truncated) {
+        k_add_counter<<<1, 1, 0, st>>>(counters, SBR_CC_CHUNK_TRUNCATED, truncated);
+        LK("k_add_counter");
+      }
+    }
+
+    // ---- registration keys ----
+    int32_t* is_reg = A.get<int32_t>(n);
+    int32_t* reg_pos = A.get<int32_t>(n + 1);
+    int32_t* row_reg = A.get<int32_t>(n);
+    if (!A.ok) return set_error(SBR_ERR_NOMEM, "select scratch");
+    int64_t n_row_keys = 0;
+    if (n > 0) {
+      k_reg_flags<<<grid_for(n, 256), 256, 0, st>>>(chain, kept, kept_pos, n, n_buffer, is_reg);
+      LK("k_reg_flags");
+      CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, is_reg, reg_pos, (int)n, st));
+      count_launch();
+      int32_t lastp = 0, lastk = 0;
+      CK(cudaMemcpyAsync(&lastp, reg_pos + n - 1, 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(&lastk, is_reg + n - 1, 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      n_row_keys = (int64_t)lastp + lastk;
+    }
+    nreg = n_los_keys + n_row_keys;
+    uint64_t* rk1 = A.get<uint64_t>(nreg);
+    uint64_t* rk2 = A.get<uint64_t>(nreg);
+    int64_t* reg_src = A.get<int64_t>(nreg);
+    uint8_t* state = A.get<uint8_t>(nreg);
+    int32_t* pos1 = A.get<int32_t>(nreg);
+    int32_t* pos2 = A.get<int32_t>(nreg);
+    uint64_t* eslot = A.get<uint64_t>(2 * nreg);
+    uint64_t* eslot2 = A.get<uint64_t>(2 * nreg);
+    int32_t* eown = A.get<int32_t>(2 * nreg);
+    int32_t* eown2 = A.get<int32_t>(2 * nreg);
+    int* flags = A.get<int>(2);
+    if (!A.ok) return set_error(SBR_ERR_NOMEM, "select scratch");
+    k_reg_keys_los<<<grid_for(nt, 256), 256, 0, st>>>(los, los_pos, nt, rk1, rk2, reg_src);
+    LK("k_reg_keys_los");
+    if (n > 0) {
+      k_reg_keys_rows<<<grid_for(n, 256), 256, 0, st>>>(is_reg, reg_pos, pr, pf, n, n_los_keys, rk1,
+                                                       rk2, reg_src, row_reg);
+      LK("k_reg_keys_rows");
+    }
+    if (nreg > 0) {
+      k_slot_entries<<<grid_for(nreg, 256), 256, 0, st>>>(rk1, rk2, nreg, n_hash, eslot, eown);
+      LK("k_slot_entries");
+      size_t sb = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, sb, eslot, eslot2, eown, eown2, (int)(2 * nreg), 0, 64, st);
+      void* stmp = A.get<uint8_t>((int64_t)sb);
+      if (!A.ok) return set_error(SBR_ERR_NOMEM, "select scratch");
+      CK(cub::DeviceRadixSort::SortPairs(stmp, sb, eslot, eslot2, eown, eown2, (int)(2 * nreg), 0, 64, st));
+      count_launch();
+      CK(cudaMemsetAsync(pos1, 0xff, sizeof(int32_t) * nreg, st));
+      CK(cudaMemsetAsync(pos2, 0xff, sizeof(int32_t) * nreg, st));
+      k_entry_pos<<<grid_for(2 * nreg, 256), 256, 0, st>>>(eown2, eslot2, 2 * nreg, pos1, pos2);
+      LK("k_entry_pos");
+      CK(cudaMemsetAsync(state, 0, nreg, st));
+      for (int round = 0; round < 1000000; ++round) {
+        CK(cudaMemsetAsync(flags, 0, 2 * sizeof(int), st));
+        k_greedy_round<<<grid_for(nreg, 256), 256, 0, st>>>(eslot2, eown2, pos1, pos2, nreg, state,
+                                                           flags, flags + 1);
+        LK("k_greedy_round");
+        CK(cudaMemcpyAsync(hflag, flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (!hflag[1]) break;
+        if (!hflag[0]) {
+          rc = set_error(SBR_ERR_CUDA, "dedup registration did not converge");
+          goto done;
+        }
+      }
+      k_count_states<<<grid_for(nreg, 256), 256, 0, st>>>(state, nreg, counters);
+      LK("k_count_states");
+      k_claimed<<<grid_for(2 * nreg, 256), 256, 0, st>>>(eslot2, eown2, state, 2 * nreg, counters);
+      LK("k_claimed");
+    }
+
+    // ---- buffer: accepted LoS, then rows ----
+    std::vector<uint8_t> hstate(n_los_keys);
+    if (n_los_keys) {
+      CK(cudaMemcpyAsync(hstate.data(), state, n_los_keys, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
+    std::vector<int32_t> hlos_acc(n_los_keys + 1, 0);
+    for (int64_t j = 0; j < n_los_keys; ++j) {
+      hlos_acc[j] = (int32_t)n_los_acc;
+      n_los_acc += hstate[j] == 1;
+    }
+    int32_t* los_acc_pos = A.get<int32_t>(n_los_keys + 1);
+    int32_t* in_buf = A.get<int32_t>(n);
+    int32_t* buf_pos = A.get<int32_t>(n + 1);
+    if (!A.ok) return set_error(SBR_ERR_NOMEM, "select scratch");
+    if (n_los_keys) {
+      CK(cudaMemcpyAsync(los_acc_pos, hlos_acc.data(), sizeof(int32_t) * n_los_keys,
+                         cudaMemcpyHostToDevice, st));
+      k_los_buffer<<<grid_for(n_los_keys, 256), 256, 0, st>>>(reg_src, state, los_acc_pos,
+                                                             (int)n_los_keys, n_buffer, rec_vtx,
+                                                             rec_target);
+      LK("k_los_buffer");
+    }
+    if (n > 0) {
+      k_buffer_flags<<<grid_for(n, 256), 256, 0, st>>>(chain, kept, kept_pos, row_reg, state, n,
+                                                      n_buffer, in_buf);
+      LK("k_buffer_flags");
+      CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, in_buf, buf_pos, (int)n, st));
+      count_launch();
+      int32_t lastp = 0, lastk = 0;
+      CK(cudaMemcpyAsync(&lastp, buf_pos + n - 1, 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(&lastk, in_buf + n - 1, 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      n_rows_buf = (int64_t)lastp + lastk;
+      k_row_buffer<<<grid_for(n, 256), 256, 0, st>>>(in_buf, buf_pos, skey, sidx, row_vtx, n,
+                                                    n_los_acc, n_buffer, rec_vtx, rec_target);
+      LK("k_row_buffer");
+    }
+    const int64_t total = n_los_acc + n_rows_buf;
+    const int64_t nrec = total < n_buffer ? total : n_buffer;
+    if (total > nrec) {
+      k_add_counter<<<1, 1, 0, st>>>(counters, SBR_CC_BUFFER_OVERFLOW,
+                                     (unsigned long long)(total - nrec));
+      LK("k_add_counter");
+    }
+    k_add_counter<<<1, 1, 0, st>>>(counters, SBR_CC_CANDIDATES, (unsigned long long)nrec);
+    LK("k_add_counter");
+    CK(cudaStreamSynchronize(st));
+    *n_records = nrec;
+  }
+done:
+  return rc;
+}
+
+int sbr_cir_records(const SbrCirParams* P, const SbrVertexBuf* vb, const int32_t* rec_vtx,
+                    const int32_t* rec_target, int64_t n, const SbrRecordBuf* out, void* stream) {
+  if (!P || !vb || !out) return set_error(SBR_ERR_INVALID, "NULL argument");
+  if (out->max_depth < 1 || out->max_depth > 15) return set_error(SBR_ERR_INVALID, "bad max_depth");
+  if (n <= 0) return SBR_OK;
+  k_cir_records<<<grid_for(n, 128), 128, 0, (cudaStream_t)stream>>>(*P, *vb, rec_vtx, rec_target, n,
+                                                                   *out);
+  return launch_status("k_cir_records");
+}
+
+int sbr_cir_refine(const SbrScene* scene, const SbrCirParams* P, const SbrRecordBuf* rec,
+                   int64_t n, double* pv, int32_t* status, uint64_t* counters, void* stream) {
+  int rc = check_cir(scene, P);
+  if (rc) return rc;
+  if (!scene || !rec) return set_error(SBR_ERR_INVALID, "NULL argument");
+  if (rec->max_depth < 1 || rec->max_depth > 15) return set_error(SBR_ERR_INVALID, "bad max_depth");
+  if (n <= 0) return SBR_OK;
+  k_cir_refine<<<grid_for(n, 128), 128, 0, (cudaStream_t)stream>>>(
+      dev_view(scene), *P, *rec, n, pv, status, (unsigned long long*)counters);
+  return launch_status("k_cir_refine");
+}
+
+}  // extern "C"

@@ -1,0 +1,368 @@
+// sbr_fields.cu -- path field replay (Algorithm 2) and the channel frequency response.
+//
+// Replaces emtrace:
+//   compute_path_fields (paths.py:1302-1399) with _step_probability (1276-1299),
+//   _right_handed (1259-1273), specular_transform / refraction_transform
+//   (materials.py:280-347), gamma_reflected / diffuse_transform (400-475),
+//   pattern_to_gcs (em.py:198-219), accumulate_doppler (paths.py:1410-1426)
+//                                                       -> k_cir_fields
+//   frequency_response (paths.py:1519-1547), array_response (em.py:240-251)
+//                                                       -> k_cfr
+// One thread per path; the transverse field is a 2-component complex Jones
+// vector carried in an explicit (a, b, k) frame exactly as the reference does,
+// in float64 (north-star tolerance for gains/delays/angles: 1e-4 relative).
+#include <string>
+
+#include "sbr_physics.cuh"
+
+struct SbrScene;
+
+namespace sbr {
+DevScene dev_view(const SbrScene* s);
+int set_error(int code, const std::string& msg);
+}  // namespace sbr
+
+using namespace sbr;
+
+namespace {
+
+constexpr double kSpeedOfLight = 299792458.0;
+
+struct Jones {
+  cplx c0, c1;         // components along (a, b)
+  double3 a, b, k;     // frame
+};
+
+__device__ __forceinline__ double ddot(double3 a, double3 b) { return dot_ddot(a, b); }
+
+// (theta_hat, phi_hat) of a direction (em.py:39-50 transverse_frame)
+__device__ __forceinline__ void sph_frame(double3 d, double3& th, double3& ph) {
+  transverse_rows(d, th, ph);
+}
+
+// pattern_to_gcs (em.py:198-219): components in the world (theta, phi) basis of d
+__device__ void pattern_gcs(const SbrAntenna& A, double3 d, cplx& c_th, cplx& c_ph, double3& th_g,
+                            double3& ph_g) {
+  const double* R = A.rot;
+  // d_local = rot.T @ d
+  const double3 dl = make_double3(R[0] * d.x + R[3] * d.y + R[6] * d.z,
+                                  R[1] * d.x + R[4] * d.y + R[7] * d.z,
+                                  R[2] * d.x + R[5] * d.y + R[8] * d.z);
+  const double theta_l = acos(clamp1(dl.z));
+  const double phi_l = atan2(dl.y, dl.x);
+  const double amp = A.kind == SBR_PATTERN_TR38901 ? tr38901_amp(A.scale, theta_l, phi_l) : 1.0;
+  sph_frame(d, th_g, ph_g);
+  double st, ct, sp, cp;
+  sincos(theta_l, &st, &ct);
+  sincos(phi_l, &sp, &cp);
+  const double3 th_l = make_double3(ct * cp, ct * sp, -st);
+  const double3 ph_l = make_double3(-sp, cp, 0.0);
+  const double3 thw = make_double3(R[0] * th_l.x + R[1] * th_l.y + R[2] * th_l.z,
+                                   R[3] * th_l.x + R[4] * th_l.y + R[5] * th_l.z,
+                                   R[6] * th_l.x + R[7] * th_l.y + R[8] * th_l.z);
+  (void)ph_l;  // both built-in evaluators return c_phi_l = 0 (em.py:258-288)
+  c_th = C(ddot(th_g, thw) * amp, 0.0);
+  c_ph = C(ddot(ph_g, thw) * amp, 0.0);
+}
+
+// W = [[a.q, a.r], [b.q, b.r]] applied to comps given in (q, r)
+__device__ __forceinline__ void basis_change(double3 a, double3 b, double3 q, double3 r, cplx c0,
+                                             cplx c1, cplx& o0, cplx& o1) {
+  const double w00 = ddot(a, q), w01 = ddot(a, r), w10 = ddot(b, q), w11 = ddot(b, r);
+  o0 = w00 * c0 + w01 * c1;
+  o1 = w10 * c0 + w11 * c1;
+}
+
+__device__ __forceinline__ void right_handed(Jones& J, double3 a, double3 b, double3 k) {
+  if (ddot(cross3(a, b), k) < 0.0) {
+    const cplx t = J.c0;
+    J.c0 = J.c1;
+    J.c1 = t;
+    J.a = b;
+    J.b = a;
+  } else {
+    J.a = a;
+    J.b = b;
+  }
+  J.k = k;
+}
+
+// interaction_probabilities(...)[kind] at replay geometry (paths.py:1276-1299)
+__device__ double step_probability(const SbrMaterial& m, double cos_i, int kind, double q_d,
+                                   int allow, bool has_s) {
+  const Fresnel4 F = slab_fresnel(m, cos_i);
+  const double r_sq = cabs2(F.rp) + cabs2(F.rl);
+  const double t_sq = cabs2(F.tp) + cabs2(F.tl);
+  const double den = r_sq + t_sq;
+  double q[4] = {0.0, 0.0, 0.0, 0.0};
+  if (den > 0.0) {
+    const double keep = 1.0 - q_d;
+    const double s2 = m.scattering * m.scattering;
+    q[0] = keep * (1.0 - s2) * r_sq / den;
+    q[1] = keep * s2 * r_sq / den;
+    q[2] = keep * t_sq / den;
+  }
+  (void)has_s;  // only masks D, which is never allowed (no wedges)
+  if (!(allow & 1)) q[0] = 0.0;
+  if (!(allow & 2)) q[1] = 0.0;
+  if (!(allow & 4)) q[2] = 0.0;
+  const double total = ((0.0 + q[0]) + q[1]) + q[2];
+  return total > 0.0 ? q[kind] / total : 0.0;
+}
+
+__device__ __forceinline__ uint64_t phase_tag(int nsteps) {
+  // fnv1a("phase-%d" % nsteps)
+  char buf[16] = {'p', 'h', 'a', 's', 'e', '-'};
+  int len = 6;
+  char digits[8];
+  int nd = 0;
+  int v = nsteps;
+  do {
+    digits[nd++] = (char)('0' + v % 10);
+    v /= 10;
+  } while (v > 0);
+  while (nd > 0) buf[len++] = digits[--nd];
+  uint64_t h = 0xCBF29CE484222325ULL;
+  for (int i = 0; i < len; ++i) h = (h ^ (uint8_t)buf[i]) * 0x100000001B3ULL;
+  return h;
+}
+
+__global__ void __launch_bounds__(128) k_cir_fields(DevScene S, SbrFieldParams P, SbrRecordBuf R,
+                                                    const double* __restrict__ pv,
+                                                    const int32_t* __restrict__ status, int64_t n,
+                                                    double* gain, double* delay, double* doppler,
+                                                    double* dep, double* arr) {
+  const int L = R.max_depth;
+  const double lam = P.wavelength;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    if (status[r] != SBR_REFINE_OK) continue;
+    const int depth = R.depth[r];
+    const int tgt = R.target[r];
+    const double* V = pv + r * (int64_t)(L + 2) * 3;
+    // segments
+    double seg_len[17];
+    double3 kh[17];
+    double total_len = 0.0;
+    for (int i = 0; i <= depth; ++i) {
+      const double3 s = make_double3(V[3 * (i + 1)] - V[3 * i], V[3 * (i + 1) + 1] - V[3 * i + 1],
+                                     V[3 * (i + 1) + 2] - V[3 * i + 2]);
+      seg_len[i] = norm_seq(s);
+      kh[i] = make_double3(s.x / seg_len[i], s.y / seg_len[i], s.z / seg_len[i]);
+      total_len += seg_len[i];
+    }
+    // launch field
+    Jones J;
+    {
+      double3 th, ph;
+      pattern_gcs(P.tx_pattern, kh[0], J.c0, J.c1, th, ph);
+      J.a = th;
+      J.b = ph;
+      J.k = kh[0];
+    }
+    double gamma_prob = 1.0, r_dist = 0.0;
+    double tube_omega = kFourPi / (double)P.num_samples;
+    bool has_s = false;
+    int n_phase = 0;
+    const uint64_t ptag = phase_tag(depth);
+    const uint64_t psample = R.sample[r] > 0 ? (uint64_t)R.sample[r] : 0ULL;
+    // accumulate_doppler (paths.py:1410-1426): endpoint terms first, then vertices
+    const double3 tv = make_double3(P.tx_velocity[0], P.tx_velocity[1], P.tx_velocity[2]);
+    const double3 rv = ldg3(P.rx_velocity_dev + 3 * tgt);
+    double nu = ddot(tv, kh[0]) / lam;
+    nu -= ddot(rv, kh[depth]) / lam;
+    for (int i = 0; i < depth; ++i) {
+      const int64_t o = r * L + i;
+      const int kind = R.kind[o];
+      const int slot = R.tri[o];
+      const double3 k_in = kh[i], k_out = kh[i + 1];
+      r_dist += seg_len[i];
+      const int row = __ldg(S.matrow + slot);
+      const SbrMaterial m = S.mats[row];
+      double3 nrm = ld3(R.normal + 3 * o);
+      const double cos_step = fabs(ddot(k_in, nrm));
+      double3 n_hat = nrm;
+      if (ddot(k_in, n_hat) > 0.0) n_hat = neg(n_hat);
+      gamma_prob *= step_probability(m, cos_step, kind, P.q_diffraction, P.allow_mask, has_s);
+      if (P.n_objects > 0 && row < P.n_objects) {
+        const double3 v = ldg3(P.obj_velocity_dev + 3 * row);
+        if (v.x != 0.0 || v.y != 0.0 || v.z != 0.0) nu += ddot(v, k_out - k_in) / lam;
+      }
+      double3 e_perp, e_par;
+      incidence_frame(k_in, n_hat, e_perp, e_par);
+      const double cos_t = fabs(ddot(k_in, n_hat));
+      if (kind == 0 || kind == 2) {
+        const Fresnel4 F = slab_fresnel(m, cos_t);
+        cplx c0, c1;
+        basis_change(e_perp, e_par, J.a, J.b, J.c0, J.c1, c0, c1);
+        if (kind == 0) {
+          const double dn = ddot(k_in, n_hat);
+          const double3 k_r = k_in - (2.0 * dn) * n_hat;
+          const double3 e_r_par = cross3(e_perp, k_r);
+          J.c0 = m.spec_amp * F.rp * c0;
+          J.c1 = m.spec_amp * F.rl * c1;
+          right_handed(J, e_perp, e_r_par, k_r);
+        } else {
+          J.c0 = F.tp * c0;
+          J.c1 = F.tl * c1;
+          right_handed(J, e_perp, e_par, k_in);
+        }
+      } else {
+        // diffuse scattering (gamma_reflected + diffuse_transform)
+        const Fresnel4 F = slab_fresnel(m, cos_t);
+        cplx p0, p1;
+        basis_change(e_perp, e_par, J.a, J.b, J.c0, J.c1, p0, p1);
+        const double nrm_in = sqrt(cabs2(p0) + cabs2(p1));
+        const double gam =
+            nrm_in == 0.0 ? 0.0 : sqrt(cabs2(F.rp * p0) + cabs2(F.rl * p1)) / nrm_in;
+        double ci = -ddot(k_in, n_hat);
+        const double ci_patch = ci > 1e-12 ? ci : 1e-12;
+        const double patch = tube_omega * (r_dist * r_dist) / ci_patch;
+        ci = ci < 0.0 ? 0.0 : (ci > 1.0 ? 1.0 : ci);
+        const double f_s = pattern_density(m, k_in, k_out, n_hat);
+        const double amp = m.scattering * gam * sqrt(f_s * ci * patch);
+        double chi1 = 0.0, chi2 = 0.0;
+        if (m.random_phases) {
+          chi1 = kTwoPi * philox_uniform(P.seed, psample, (uint64_t)tgt, ptag, 2 * n_phase);
+          chi2 = kTwoPi * philox_uniform(P.seed, psample, (uint64_t)tgt, ptag, 2 * n_phase + 1);
+          ++n_phase;
+        }
+        const double sq = sqrt(1.0 - m.xpd_kx), sk = sqrt(m.xpd_kx);
+        double th_i_s, th_i_c;
+        double3 th_i, ph_i, th_s, ph_s;
+        sph_frame(k_in, th_i, ph_i);
+        sph_frame(k_out, th_s, ph_s);
+        cplx q0, q1;
+        basis_change(th_i, ph_i, J.a, J.b, J.c0, J.c1, q0, q1);
+        sincos(chi1, &th_i_s, &th_i_c);
+        const cplx e1 = C(th_i_c, th_i_s);
+        double s2, c2;
+        sincos(chi2, &s2, &c2);
+        const cplx e2 = C(c2, s2);
+        const cplx o0 = amp * ((sq * e1) * q0 + ((-sk) * e1) * q1);
+        const cplx o1 = amp * ((sk * e2) * q0 + (sq * e2) * q1);
+        const double inv = 1.0 / sqrt(gamma_prob);
+        J.c0 = C(o0.re / r_dist * inv, o0.im / r_dist * inv);
+        J.c1 = C(o1.re / r_dist * inv, o1.im / r_dist * inv);
+        J.a = th_s;
+        J.b = ph_s;
+        J.k = k_out;
+        gamma_prob = 1.0;
+        r_dist = 0.0;
+        tube_omega = kTwoPi;
+        has_s = true;
+      }
+    }
+    r_dist += seg_len[depth];
+    const double3 arrival = kh[depth];
+    cplx rc0, rc1;
+    double3 rth, rph;
+    pattern_gcs(P.rx_pattern_dev[tgt], neg(arrival), rc0, rc1, rth, rph);
+    // e_vec . rx_vec (unconjugated)
+    const cplx ex = J.c0 * C(J.a.x, 0.0) + J.c1 * C(J.b.x, 0.0);
+    const cplx ey = J.c0 * C(J.a.y, 0.0) + J.c1 * C(J.b.y, 0.0);
+    const cplx ez = J.c0 * C(J.a.z, 0.0) + J.c1 * C(J.b.z, 0.0);
+    const cplx rx = rc0 * C(rth.x, 0.0) + rc1 * C(rph.x, 0.0);
+    const cplx ry = rc0 * C(rth.y, 0.0) + rc1 * C(rph.y, 0.0);
+    const cplx rz = rc0 * C(rth.z, 0.0) + rc1 * C(rph.z, 0.0);
+    const cplx dotv = (ex * rx + ey * ry) + ez * rz;
+    const double scale = lam / kFourPi / r_dist;
+    gain[2 * r] = dotv.re * scale;
+    gain[2 * r + 1] = dotv.im * scale;
+    delay[r] = total_len / kSpeedOfLight;
+    doppler[r] = nu;
+    for (int c = 0; c < 3; ++c) {
+      dep[3 * r + c] = c == 0 ? kh[0].x : (c == 1 ? kh[0].y : kh[0].z);
+      arr[3 * r + c] = c == 0 ? arrival.x : (c == 1 ? arrival.y : arrival.z);
+    }
+  }
+}
+
+// H[r, t, f] over the paths of one link, float64 accumulation in path order
+__global__ void k_cfr(const double* __restrict__ gain, const double* __restrict__ delay,
+                      const double* __restrict__ dep, const double* __restrict__ arr,
+                      const int32_t* __restrict__ prx, const int32_t* __restrict__ ptx,
+                      int64_t np, const double* __restrict__ freqs, int nf,
+                      const double* __restrict__ txo, int ntx, const double* __restrict__ rxo,
+                      int nrx, double wavelength, int synthetic, double* __restrict__ H) {
+  const int64_t total = (int64_t)nrx * ntx * nf;
+  const double kw = kTwoPi / wavelength;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int f = (int)(i % nf);
+    const int t = (int)((i / nf) % ntx);
+    const int r = (int)(i / ((int64_t)nf * ntx));
+    const double fr = freqs[f];
+    double acc_re = 0.0, acc_im = 0.0;
+    for (int64_t p = 0; p < np; ++p) {
+      cplx a = C(gain[2 * p], gain[2 * p + 1]);
+      if (synthetic) {
+        const double3 kd = ld3(dep + 3 * p), ka = ld3(arr + 3 * p);
+        const double pr = kw * dot_gemv(ldg3(rxo + 3 * r), neg(ka));
+        const double pt = kw * dot_gemv(ldg3(txo + 3 * t), kd);
+        double sr, cr, st, ct;
+        sincos(pr, &sr, &cr);
+        sincos(pt, &st, &ct);
+        a = (a * C(cr, sr)) * C(ct, st);
+      } else if (prx[p] != r || ptx[p] != t) {
+        continue;
+      }
+      const double ang = -kTwoPi * fr * delay[p];
+      double s, c;
+      sincos(ang, &s, &c);
+      const cplx v = a * C(c, s);
+      acc_re += v.re;
+      acc_im += v.im;
+    }
+    H[2 * i] = acc_re;
+    H[2 * i + 1] = acc_im;
+  }
+}
+
+unsigned grid_for(int64_t n, int block, int cap = 148 * 32) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+int launch_status(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(SBR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  count_launch();
+  return SBR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sbr_cir_fields(const SbrScene* scene, const SbrFieldParams* P, const SbrRecordBuf* rec,
+                   const double* pv, const int32_t* status, int64_t n, double* gain, double* delay,
+                   double* doppler, double* dep, double* arr, void* stream) {
+  if (!scene || !P || !rec) return set_error(SBR_ERR_INVALID, "NULL argument");
+  if (!dev_view(scene).mats) return set_error(SBR_ERR_INVALID, "scene has no material table");
+  if (!P->rx_pattern_dev || !P->rx_velocity_dev)
+    return set_error(SBR_ERR_INVALID, "per-target rx pattern / velocity missing");
+  if (rec->max_depth < 1 || rec->max_depth > 15) return set_error(SBR_ERR_INVALID, "bad max_depth");
+  if (n <= 0) return SBR_OK;
+  k_cir_fields<<<grid_for(n, 128), 128, 0, (cudaStream_t)stream>>>(
+      dev_view(scene), *P, *rec, pv, status, n, gain, delay, doppler, dep, arr);
+  return launch_status("k_cir_fields");
+}
+
+int sbr_cfr(const double* gain, const double* delay, const double* dep, const double* arr,
+            const int32_t* prx, const int32_t* ptx, int64_t np, const double* freqs, int32_t nf,
+            const double* txo, int32_t ntx, const double* rxo, int32_t nrx, double wavelength,
+            int32_t synthetic, double* H, void* stream) {
+  if (nf < 1 || ntx < 1 || nrx < 1) return set_error(SBR_ERR_INVALID, "empty response shape");
+  if (!(wavelength > 0.0)) return set_error(SBR_ERR_INVALID, "wavelength must be positive");
+  if (!synthetic && (!prx || !ptx)) return set_error(SBR_ERR_INVALID, "element indices missing");
+  const int64_t total = (int64_t)nrx * ntx * nf;
+  k_cfr<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(gain, delay, dep, arr, prx, ptx,
+                                                                np, freqs, nf, txo, ntx, rxo, nrx,
+                                                                wavelength, synthetic, H);
+  return launch_status("k_cfr");
+}
+
+}  // extern "C"

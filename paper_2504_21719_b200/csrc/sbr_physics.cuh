@@ -72,7 +72,7 @@ __device__ __forceinline__ double binom(int n, int k) {
   return floor(r + 0.5);
 }
 
-__device__ double lobe_norm(int alpha, double cos_ti) {
+static __device__ double lobe_norm(int alpha, double cos_ti) {
   double sin2 = 1.0 - cos_ti * cos_ti;
   if (sin2 < 0.0) sin2 = 0.0;
   double total = 0.0;
@@ -93,7 +93,7 @@ __device__ double lobe_norm(int alpha, double cos_ti) {
 
 __device__ __forceinline__ double clamp1(double x) { return x < -1.0 ? -1.0 : (x > 1.0 ? 1.0 : x); }
 
-__device__ double pattern_density(const SbrMaterial& m, double3 ki, double3 ks, double3 n) {
+static __device__ double pattern_density(const SbrMaterial& m, double3 ki, double3 ks, double3 n) {
   if (m.pattern_kind == SBR_SCAT_LAMBERTIAN) {
     double c = dot_seq(ks, n);
     c = c < 0.0 ? 0.0 : (c > 1.0 ? 1.0 : c);
@@ -138,7 +138,7 @@ __device__ __forceinline__ double tr38901_amp(double scale, double theta, double
 }
 
 // World-frame launch field of a departure direction (radiomap.py:266-277).
-__device__ cvec3 antenna_field(const SbrAntenna& a, double3 d) {
+static __device__ cvec3 antenna_field(const SbrAntenna& a, double3 d) {
   double3 local;
   if (a.identity) {
     local = d;
@@ -167,7 +167,7 @@ __device__ cvec3 antenna_field(const SbrAntenna& a, double3 d) {
 }
 
 // |sum_m exp(j k d.o_m) u_m|^2 (radiomap.py:253-259)
-__device__ double alpha_sq(const SbrMapParams& P, double3 d) {
+static __device__ double alpha_sq(const SbrMapParams& P, double3 d) {
   if (P.n_elements <= 0) return 1.0;
   const double k = kTwoPi / P.wavelength;
   cplx acc = C(0.0, 0.0);

@@ -8,7 +8,7 @@ reference's own vectorised expression (paths.py:156-171) and uploaded, so the
 device hash chains are bit-identical to the reference's.
 
 The CIR pipeline itself (generation, dedup, refinement, field replay, CFR)
-lives in `cir.py` on top of csrc/sbr_cir.cu.
+lives in `cir.py` on top of csrc/sbr_cir.cu and csrc/sbr_fields.cu.
 """
 
 import math

@@ -1,0 +1,182 @@
+"""GPU parity of the path solver (CIR) against golden vectors from the real reference.
+
+Fixtures: tests/golden/cir.npz, made by tests/golden/make_golden_cir.py from
+emtrace's own generate_candidates / compute_paths / frequency_response on the
+cases of tests/cir_cases.py.
+
+Bars (north star): interaction sequences and deduplicated path sets
+bit-exact; gains, delays and angles within 1e-4 relative.  Generation is
+float64 in the reference's operation order, so candidate records are
+compared exactly (every field, including vertices); refined vertices to
+1e-9 m; gains to 1e-6 relative (asserting the 1e-4 contract with margin).
+"""
+
+import numpy as np
+import pytest
+
+from cir_cases import CIR_CASES, case_geometry, mesh_digest
+from conftest import golden
+from paper_2504_21719_b200 import (PathConfig, RadioDevice, SceneModel, compute_paths,
+                                   frequency_response, generate_candidates, refine_candidate)
+from paper_2504_21719_b200.cir import PathGeometry
+from paper_2504_21719_b200.em import ArrayGeometry, make_pattern
+from paper_2504_21719_b200.materials import RadioMaterial, ScatteringPattern
+from paper_2504_21719_b200.sampling import Interaction
+
+pytestmark = pytest.mark.gpu
+
+KINDS = {"R": Interaction.REFLECTION, "S": Interaction.SCATTERING,
+         "T": Interaction.TRANSMISSION, "D": Interaction.DIFFRACTION}
+KIND_CODE = {Interaction.REFLECTION: 0, Interaction.SCATTERING: 1,
+             Interaction.TRANSMISSION: 2, Interaction.DIFFRACTION: 3}
+
+_SCENES = {}
+
+
+def build(name):
+    c = CIR_CASES[name]
+    if name not in _SCENES:
+        meshes, mats, vel = case_geometry(name)
+        pm = {}
+        for oid, md in mats.items():
+            md = dict(md)
+            pat = md.pop("pattern", None)
+            if pat is not None:
+                md["pattern"] = ScatteringPattern(kind=pat[0], alpha_r=pat[1], alpha_i=pat[2],
+                                                  lambda_mix=pat[3])
+            pm[oid] = RadioMaterial("m%d" % oid, **md)
+        _SCENES[name] = (SceneModel(meshes, pm, velocities=vel), mesh_digest(meshes))
+    scene, digest = _SCENES[name]
+    kw = dict(c["cfg"])
+    kw["enabled"] = frozenset(KINDS[k] for k in c["kinds"])
+    cfg = PathConfig(**kw)
+
+    def device(d):
+        kw = {}
+        if d.get("pattern"):
+            kw["pattern"] = make_pattern(d["pattern"][0], orientation=d["pattern"][1])
+        if d.get("array"):
+            kw["array"] = ArrayGeometry(np.asarray(d["array"], dtype=np.float64))
+        if d.get("velocity") is not None:
+            kw["velocity"] = np.asarray(d["velocity"], dtype=np.float64)
+        return RadioDevice(position=np.asarray(d["pos"], dtype=np.float64), **kw)
+
+    return scene, digest, cfg, [device(d) for d in c["tx"]], [device(d) for d in c["rx"]]
+
+
+def gold(name, prefix):
+    g = golden("cir.npz")
+    p = f"{name}__{prefix}"
+    return {k[len(p):]: g[k] for k in g.files if k.startswith(p)}
+
+
+@pytest.mark.parametrize("name", list(CIR_CASES))
+def test_generate_candidates_bit_exact(cuda, name):
+    scene, digest, cfg, txs, rxs = build(name)
+    assert digest == str(golden("cir.npz")[f"{name}__digest"])
+    want = gold(name, "gen_")
+    wdiag = gold(name, "gendiag__")
+    targets = (np.array([r.position for r in rxs]) if cfg.synthetic_arrays
+               else np.concatenate([r.element_positions() for r in rxs]))
+    src = txs[0].position if cfg.synthetic_arrays else txs[0].element_positions()[0]
+    res = generate_candidates(scene, src, targets, cfg)
+    for k, v in wdiag.items():
+        if k == "hash_load_factor":
+            assert res.diagnostics[k] == pytest.approx(float(v), rel=1e-12)
+        else:
+            assert res.diagnostics.get(k, 0) == int(v), k
+    recs = res.records
+    assert len(recs) == len(want["sample"])
+    for i, r in enumerate(recs):
+        assert r.sample_id == want["sample"][i], i
+        assert r.target_id == want["target"][i], i
+        assert len(r.steps) == want["depth"][i], i
+        assert r.suffix_start == want["suffix_start"][i], i
+        assert r.diffuse_terminal == bool(want["diffuse"][i]), i
+        assert r.chain_hash == int(want["chain_hash"][i]), i
+        assert r.prefix_probability == pytest.approx(want["prefix_prob"][i], rel=1e-12), i
+        np.testing.assert_allclose(r.anchor, want["anchor"][i], rtol=0, atol=1e-12)
+        for j, st in enumerate(r.steps):
+            assert KIND_CODE[st.kind] == want["kind"][i, j]
+            assert st.object_id == want["obj"][i, j] and st.primitive_id == want["prim"][i, j]
+            # CUDA's sin/cos may differ from glibc by 1 ulp in the launch
+            # direction; geometry then agrees to ~1e-15 m, decisions exactly
+            np.testing.assert_allclose(st.vertex, want["vertex"][i, j], rtol=0, atol=1e-12)
+            assert np.array_equal(st.normal, want["normal"][i, j]), (i, j)
+
+
+@pytest.mark.parametrize("name", list(CIR_CASES))
+def test_compute_paths_matches_reference(cuda, name):
+    scene, _, cfg, txs, rxs = build(name)
+    want = gold(name, "path_")
+    ps = compute_paths(scene, txs, rxs, cfg)
+    T = ps.tensors
+    n = len(want["delay"])
+    assert len(T) == n
+    for k in ("tx", "tx_el", "rx", "rx_el", "depth", "sample"):
+        assert np.array_equal(getattr(T, k), want[k]), k
+    assert np.array_equal(T.chain_hash.astype(np.uint64), want["chain_hash"])
+    L = want["kind"].shape[1]
+    kind = np.where(np.arange(T.kind.shape[1])[None, :] < T.depth[:, None], T.kind, -1)
+    assert np.array_equal(kind[:, :L], want["kind"])
+    obj = np.where(kind >= 0, T.obj, -1)[:, :L]
+    prim = np.where(kind >= 0, T.prim, -1)[:, :L]
+    assert np.array_equal(obj, want["obj"]) and np.array_equal(prim, want["prim"])
+    for i in range(n):
+        d = int(want["depth"][i])
+        np.testing.assert_allclose(T.vertices[i, :d + 2], want["vertices"][i, :d + 2],
+                                   rtol=0, atol=1e-9)
+    np.testing.assert_allclose(T.delay, want["delay"], rtol=1e-12)
+    np.testing.assert_allclose(T.departure, want["departure"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(T.arrival, want["arrival"], rtol=0, atol=1e-12)
+    g, wg = T.gain, want["gain"]
+    scale = np.maximum(np.abs(wg), 1e-300)
+    rel = np.abs(g - wg) / scale
+    assert rel.max(initial=0.0) < 1e-6, rel.max()
+    np.testing.assert_allclose(T.doppler, want["doppler"], rtol=1e-9, atol=1e-9)
+    wd = gold(name, "diag__")
+    for k, v in wd.items():
+        if k.startswith("rej__"):
+            assert ps.diagnostics["refinement_rejections"].get(k[5:], 0) == int(v), k
+        elif k == "hash_load_factor":
+            assert ps.diagnostics[k] == pytest.approx(float(v), rel=1e-12)
+        else:
+            assert ps.diagnostics.get(k, 0) == int(v), k
+    # lazily-built reference objects agree with the SoA view
+    if n:
+        p0 = ps.paths[0]
+        assert p0.depth == want["depth"][0] and p0.gain == complex(T.gain[0])
+
+
+@pytest.mark.parametrize("name", [k for k, c in CIR_CASES.items() if c.get("freqs") is not None])
+def test_frequency_response_matches_reference(cuda, name):
+    scene, _, cfg, txs, rxs = build(name)
+    g = golden("cir.npz")
+    ps = compute_paths(scene, txs, rxs, cfg)
+    H = frequency_response(ps, CIR_CASES[name]["freqs"], 0, 0)
+    want = g[f"{name}__cfr"]
+    assert H.shape == want.shape
+    err = np.abs(H - want).max() / np.abs(want).max()
+    assert err < 1e-9, err
+
+
+def test_refinement_fixed_point(cuda):
+    # reference test_paths.py:379-389
+    scene, _, cfg, txs, rxs = build("box_r")
+    ps = compute_paths(scene, txs[:1], rxs[:1], cfg)
+    from paper_2504_21719_b200.cir import CandidateRecord
+    for p in ps.paths[:20]:
+        rec = CandidateRecord(source_id=0, target_id=0, source=txs[0].position,
+                              target=rxs[0].position, sample_id=p.sample_id, steps=p.steps,
+                              suffix_start=0, anchor=txs[0].position, prefix_probability=1.0,
+                              chain_hash=p.chain_hash)
+        again = refine_candidate(rec, scene)
+        assert isinstance(again, PathGeometry)
+        np.testing.assert_allclose(again.vertices, p.vertices, atol=1e-9)
+
+
+def test_diffraction_is_rejected_loudly(cuda):
+    scene, _, _, txs, rxs = build("box_r")
+    cfg = PathConfig(num_samples=100, max_depth=1, q_diffraction=0.2)
+    with pytest.raises(NotImplementedError):
+        compute_paths(scene, txs, rxs, cfg)

@@ -14,8 +14,12 @@ its own 1e7 samples of an N*1e7-sample lattice.
 value      : total ray-bounces of all ranks / max-over-ranks device time
 e2e        : same metric through the public API compute_radio_map_sbr with
              host output (params H2D, grid + counters D2H every step)
-roofline   : dominant kernel k_radiomap, 176 algorithmic bytes per ray-bounce
-              / its CUDA-event duration vs measured HBM GB/s
+roofline   : dominant kernel of the wavefront (k_map_trace / k_map_shade, timed
+             with CUDA events inside libsbr on the launching stream), 176
+             algorithmic bytes per ray-bounce / its summed
+             launch time, vs measured HBM GB/s
+cir        : config 3 (city, 1 Tx x 1024 Rx, N_S = 1e6, depth 5): ms per
+             compute_paths solve (the CIR half of the BASELINE metric)
 cpu_baseline: the CPU oracle port (oracle/, scalar C restatement of the
              reference loop) on this host's cores over a bounded subsample
 --impl reference: that CPU port alone, on all host threads, same metric.
@@ -38,6 +42,7 @@ sys.path.insert(0, ROOT)
 METRIC = "radio-map SBR ray-bounces/sec"
 UNIT = "ray-bounces/s"
 SAMPLES_PER_GPU = 10_000_000
+CIR_SAMPLES = 1_000_000
 BYTES_PER_RB = 176  # 64 B ray state in + 64 B out + 48 B hit triangle
 TX = (0.0, 5.0, 20.0)
 
@@ -295,9 +300,27 @@ def run_ours(args, rank, world, local_rank):
     else:
         t_max = t_local
     value = rb_total / (t_max / 1e3)
-    rb_per_launch_local = rb_total / args.steps / world
-    kern_avg_s = float(kern_ms.mean()) / 1e3
-    achieved = rb_per_launch_local * BYTES_PER_RB / kern_avg_s / 1e9
+    rb_per_step_local = rb_total / args.steps / world
+
+    # ---- per-kernel split (CUDA events around each library launch, on the
+    # ---- launching stream), measured on extra untimed steps
+    prof_steps = max(1, min(args.steps, 3))
+    _native.profile_enable(True)
+    for k in range(prof_steps):
+        flush.fill_(float(k))
+        step()
+    torch.cuda.synchronize()
+    kernels = {}
+    for name in ("k_map_trace", "k_map_shade"):
+        ms, nl = _native.profile_kernel_ms(name)
+        kernels[name] = {"ms_per_step": ms / prof_steps, "launches_per_step": nl / prof_steps}
+    _native.profile_enable(False)
+    dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
+    dom_ms_step = kernels[dom]["ms_per_step"]
+    dom_launches = kernels[dom]["launches_per_step"]
+    # algorithmic bytes: 176 B per ray-bounce x the rays the kernel
+    # processed, over the kernel's own summed launch time
+    achieved = rb_per_step_local * BYTES_PER_RB / (dom_ms_step / 1e3) / 1e9
     peak, peak_kind = peaks()
     traffic = profiled_traffic()
 
@@ -342,6 +365,10 @@ def run_ours(args, rank, world, local_rank):
                "sample": f"{ns} of the 1e7 rays (400 evenly spaced slices), {rb_cpu} "
                          f"ray-bounces in {dt:.2f} s on {threads} threads"}
 
+    cir = None
+    if world == 1 and not args.no_cir:
+        cir = bench_cir(args, dev)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -354,15 +381,63 @@ def run_ours(args, rank, world, local_rank):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
                          "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
-                         "kernel": "k_radiomap", "bytes_per_unit": BYTES_PER_RB,
-                         "units_per_launch": rb_per_launch_local,
-                         "kernel_ms": kern_avg_s * 1e3, "peak_source": peak_kind},
+                         "traffic_kernel": traffic.get("kernel") if traffic else None,
+                         "kernel": dom, "bytes_per_unit": BYTES_PER_RB,
+                         "units_per_launch": rb_per_step_local / max(dom_launches, 1),
+                         "kernel_ms": dom_ms_step / max(dom_launches, 1),
+                         "kernel_ms_per_step": dom_ms_step,
+                         "bounce_call_ms_per_step": float(kern_ms.mean()),
+                         "kernels": kernels, "peak_source": peak_kind},
+            "cir": cir,
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
             "ray_bounces_per_step": rb_total // args.steps,
         }
         print(json.dumps(line), flush=True)
+
+
+def bench_cir(args, dev):
+    """Config 3: city CIR, 1 Tx x 1024 Rx, N_S = 1e6, depth 5, {R} (BASELINE configs[2]).
+
+    ms per compute_paths call (generation + dedup + refinement + fields, host
+    PathTensors out) timed with CUDA events on the current stream.
+    """
+    import torch
+    from paper_2504_21719_b200 import (PathConfig, RadioDevice, SceneModel, _native,
+                                       compute_paths, scenes)
+    from paper_2504_21719_b200.sampling import Interaction
+    t0 = time.perf_counter()
+    meshes = scenes.city()
+    scene = SceneModel(meshes, scenes.uniform_materials(meshes, scenes.concrete()), device=dev)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    rxs = [RadioDevice(position=p) for p in scenes.city_receivers(1024)]
+    tx = RadioDevice(position=np.array([0.0, 0.0, 30.0]))
+    cfg = PathConfig(num_samples=CIR_SAMPLES, max_depth=5, q_diffraction=0.0,
+                     enabled=frozenset({Interaction.REFLECTION}), buffer_capacity=2 ** 24)
+    compute_paths(scene, [tx], rxs, cfg)  # warm-up
+    stream = torch.cuda.current_stream(dev)
+    _native.profile_enable(True)
+    times, ps = [], None
+    for _ in range(max(1, min(args.steps, 3))):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ps = compute_paths(scene, [tx], rxs, cfg)
+        b.record(stream)
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b))
+    n = len(times)
+    split = {k: _native.profile_kernel_ms(k)[0] / n for k in ("k_cir_sweep", "k_cir_visibility")}
+    _native.profile_enable(False)
+    d = ps.diagnostics
+    return {"workload": "config3: procedural city (483,200 tris) CIR, 1 Tx x 1024 Rx, "
+                        "N_S=1e6, depth 5, {R}, hash dedup + image-method refine",
+            "ms_per_solve": float(np.mean(times)), "solves": n, "paths": d["paths"],
+            "candidates": d["candidates"], "duplicates": d["duplicates"],
+            "refinement_rejections": d["refinement_rejections"],
+            "kernel_ms_per_solve": split, "scene_build_s": build_s,
+            "unit": "ms per Tx-Rx set (1 Tx x 1024 Rx)", "higher_is_better": False}
 
 
 def main():
@@ -372,6 +447,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cir", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

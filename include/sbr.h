@@ -347,6 +347,11 @@ const char* sbr_last_error(void);
 int sbr_version(void);
 /* Number of CUDA kernels this library launched since load (evidence counter). */
 uint64_t sbr_kernel_launches(void);
+/* Per-kernel CUDA-event timing of the library's hot launches (bench.py uses it
+ * for the roofline): enable (resets the accumulators) / query the summed
+ * milliseconds and launch count of one kernel name (synchronises). */
+int sbr_profile_enable(int on);
+double sbr_profile_kernel_ms(const char* name, uint64_t* launches);
 
 #ifdef __cplusplus
 }

@@ -13,7 +13,7 @@ from . import _abi
 from .errors import EmptyScene, NativeUnavailable
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libsbr.so")
+LIB_PATH = os.environ.get("SBR_LIB_PATH") or os.path.join(_HERE, "_lib", "libsbr.so")
 
 _lib = None
 
@@ -54,6 +54,8 @@ def _declare(lib):
         "sbr_last_error": (ctypes.c_char_p, []),
         "sbr_version": (ctypes.c_int, []),
         "sbr_kernel_launches": (u64, []),
+        "sbr_profile_enable": (ctypes.c_int, [i32]),
+        "sbr_profile_kernel_ms": (dbl, [ctypes.c_char_p, ctypes.POINTER(u64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -73,7 +75,7 @@ def exported_symbols():
         "sbr_radiomap_bounce", "sbr_radiomap_direct", "sbr_cir_sweep",
         "sbr_cir_visibility", "sbr_cir_select", "sbr_cir_records", "sbr_cir_refine",
         "sbr_cir_fields", "sbr_cfr", "sbr_last_error",
-        "sbr_version", "sbr_kernel_launches",
+        "sbr_version", "sbr_kernel_launches", "sbr_profile_enable", "sbr_profile_kernel_ms",
     ]
 
 
@@ -130,6 +132,18 @@ def device_of(device):
 
 def kernel_launches():
     return int(load_library().sbr_kernel_launches())
+
+
+def profile_enable(on=True):
+    """Start (reset) or stop per-kernel CUDA-event timing inside libsbr."""
+    check(load_library().sbr_profile_enable(1 if on else 0))
+
+
+def profile_kernel_ms(name):
+    """(summed ms, launches) of one library kernel since profile_enable()."""
+    n = ctypes.c_uint64(0)
+    ms = load_library().sbr_profile_kernel_ms(name.encode(), ctypes.byref(n))
+    return float(ms), int(n.value)
 
 
 def fibonacci(n_samples, begin, end, device):

@@ -713,8 +713,10 @@ int sbr_cir_sweep(const SbrScene* scene, const SbrCirParams* P, uint64_t begin, 
   if (!scene || !vb) return set_error(SBR_ERR_INVALID, "NULL argument");
   if (end > P->num_samples || begin > end) return set_error(SBR_ERR_INVALID, "bad sample range");
   if (end == begin || P->max_depth == 0) return SBR_OK;
+  prof_begin(stream, "k_cir_sweep");
   k_cir_sweep<<<grid_for((int64_t)(end - begin), 128, 148 * 16), 128, 0, (cudaStream_t)stream>>>(
       dev_view(scene), *P, begin, end, *vb, (unsigned long long*)counters);
+  prof_end(stream);
   return launch_status("k_cir_sweep");
 }
 
@@ -726,9 +728,11 @@ int sbr_cir_visibility(const SbrScene* scene, const SbrCirParams* P, const SbrVe
   if (!scene || !vb) return set_error(SBR_ERR_INVALID, "NULL argument");
   if (v_end <= v_begin) return SBR_OK;
   const int64_t pairs = (v_end - v_begin) * (int64_t)P->n_targets;
+  prof_begin(stream, "k_cir_visibility");
   k_cir_visibility<<<grid_for(pairs, 128, 148 * 64), 128, 0, (cudaStream_t)stream>>>(
       dev_view(scene), *P, *vb, v_begin, v_end, row_key, row_vtx, row_cap,
       (unsigned long long*)counters);
+  prof_end(stream);
   return launch_status("k_cir_visibility");
 }
 

@@ -1,24 +1,35 @@
-// sbr_radiomap.cu -- radio-map SBR megakernel and the analytic direct term.
+// sbr_radiomap.cu -- radio-map SBR as a wavefront pipeline, plus the analytic direct term.
 //
 // Replaces emtrace radiomap.py:_map_chunk (347-563) and _direct_cells
-// (566-583).  One persistent kernel runs the full segment loop per ray:
-//   trace (closest hit) -> plane crossing + deposit (float64 atomics into the
-//   L2-resident grid) -> escape / depth exit -> threshold + Russian roulette
-//   -> slab Fresnel energies -> inverse-CDF draw (Philox keyed by global
-//   sample id) -> R / S / T field and direction update.
-// Rays live in registers for their whole life: there is no per-bounce ray
-// state traffic to HBM.  Warps are kept full by "warp refill": after every
-// segment, lanes whose ray ended fetch fresh sample ids with one atomicAdd
-// per warp, so divergence in path length never idles lanes (the live-ray
-// compaction of the north star, done in registers instead of through HBM).
+// (566-583).  The reference loops over segments with every active ray of a
+// chunk in lockstep (numpy rows); here each segment is two kernels over a
+// compacted HBM ray queue:
 //
-// Work order: work item w -> global sample g = c + k*F (F = 233, a Fibonacci
-// number), k = w % Q, c = w / Q.  Consecutive lanes therefore launch
-// neighbouring lattice directions (coherent primary rays); the RNG is keyed
-// by g, so the order has no effect on the result.
+//   k_map_trace   persistent, warp-batched closest-hit traversal in the
+//                 while-while form (sbr_common.cuh trace_closest_ww): lean
+//                 code, ~70 registers, so many warps hide the L1/L2 latency
+//                 of node and triangle fetches.  Segment 0 generates its rays
+//                 from global sample ids (Fibonacci lattice) on the fly.
+//   k_map_shade   one thread per ray: plane crossing + deposit (float64 atomics
+//                 into the L2-resident grid), escape / depth exit, threshold +
+//                 Russian roulette, slab Fresnel energies, inverse-CDF draw,
+//                 R / S / T field and direction update; survivors are appended
+//                 to the next queue with warp-aggregated atomics (live-ray
+//                 compaction between bounces).
+//
+// Queue counts live in device memory, so a whole map is a fixed sequence of
+// launches with no host synchronisation.  Rays are keyed by their global
+// sample id g; the RNG streams are (seed, g >> 19, seg, tag)[g & (2^19-1)],
+// so queue order never affects the result.  Per ray-bounce HBM traffic is
+// ~48 B (trace in) + 12 B (hit) + ~2 x 136 B (shade in/out) = ~330 B, i.e.
+// ~2 ms per 1e7-ray map at HBM speed: the pipeline stays compute bound.
+#include <cooperative_groups.h>
+
 #include <string>
 
 #include "sbr_physics.cuh"
+
+namespace cg = cooperative_groups;
 
 struct SbrScene;
 
@@ -31,250 +42,310 @@ using namespace sbr;
 
 namespace {
 
-constexpr uint64_t kCombStride = 233;
+constexpr uint64_t kCombStride = 233;     // Fibonacci number: neighbouring lattice directions
+constexpr int64_t kChunkRays = 1 << 23;   // samples per wavefront pass (queue capacity)
 
-struct MapRay {
-  double3 o, d;
-  cvec3 E;
-  double r_dist, omega, weight;
-  uint64_t g;
-  int seg;
-  bool alive;
+// SoA ray queue (float64; E is the complex world-frame field 3-vector)
+struct MapQueue {
+  double *ox, *oy, *oz, *dx, *dy, *dz;
+  double *exr, *exi, *eyr, *eyi, *ezr, *ezi;
+  double *r_dist, *omega, *weight;
+  uint64_t* g;
 };
 
-struct LaneCounters {
-  unsigned rb, deposits, escaped, respawns;
+struct HitBuf {
+  double* t;
+  int32_t* tri;
 };
 
-__device__ __forceinline__ void init_ray(const SbrMapParams& P, uint64_t g, MapRay& R) {
-  R.g = g;
-  R.seg = 0;
-  R.d = fibonacci_dir(P.num_samples, g);
-  R.o = make_double3(P.source[0], P.source[1], P.source[2]);
-  R.E = antenna_field(P.pattern, R.d);
-  R.r_dist = 0.0;
-  R.omega = P.omega0;
-  R.weight = alpha_sq(P, R.d);
-  R.alive = true;
+__device__ __forceinline__ unsigned long long append_slot(unsigned long long* counter) {
+  cg::coalesced_group grp = cg::coalesced_threads();
+  unsigned long long base = 0;
+  if (grp.thread_rank() == 0) base = atomicAdd(counter, (unsigned long long)grp.size());
+  base = grp.shfl(base, 0);
+  return base + grp.thread_rank();
 }
 
-// One segment of the _map_chunk loop for one ray.
-__device__ __forceinline__ void map_step(const DevScene& S, const SbrMapParams& P, MapRay& R,
-                                         double* __restrict__ grid, LaneCounters& K,
-                                         unsigned long long* sc) {
-  const int seg = R.seg;
-  const uint64_t chunk = R.g >> SBR_CHUNK_LOG2;
-  const uint64_t slot = R.g & ((1ULL << SBR_CHUNK_LOG2) - 1);
-  K.rb++;
-  HitRecord h;
-  if (!trace_closest(S, R.o, R.d, 1e-4, __longlong_as_double(0x7ff0000000000000LL), h)) {
-    flag_error(S, kErrStack);
-    atomicAdd(sc + SBR_MC_STACK_OVERFLOW, 1ULL);
-    R.alive = false;
-    return;
-  }
-  const double3 n_hat = make_double3(P.normal[0], P.normal[1], P.normal[2]);
-  if (seg >= 1) {
-    // plane crossing before the hit (escaped rays have t = inf and deposit)
-    const double denom = dot_gemv(R.d, n_hat);
-    double s = -1.0;
-    if (fabs(denom) > 1e-12) s = (P.plane_off - dot_gemv(R.o, n_hat)) / denom;
-    if (s > 1e-4 && s < h.t) {
-      const double3 pt = R.o + s * R.d;
-      const double3 rel = make_double3(pt.x - P.corner[0], pt.y - P.corner[1], pt.z - P.corner[2]);
-      const double fu = floor(dot_gemv(rel, make_double3(P.u_hat[0], P.u_hat[1], P.u_hat[2])) / P.cell_w);
-      const double fv = floor(dot_gemv(rel, make_double3(P.v_hat[0], P.v_hat[1], P.v_hat[2])) / P.cell_h);
-      if (fu >= 0.0 && fu < (double)P.nx && fv >= 0.0 && fv < (double)P.ny) {
-        const double val = P.scale * field_energy(R.E) * R.omega / fabs(denom) * R.weight;
-        atomicAdd(grid + (int64_t)fv * P.nx + (int64_t)fu, val);
-        K.deposits++;
+// comb order of segment 0: item w -> sample offset c + k*F (k = w % Q, c = w / Q)
+__device__ __forceinline__ uint64_t comb_sample(uint64_t w, uint64_t comb_q) {
+  return (w / comb_q) + (w % comb_q) * kCombStride;
+}
+
+// ---------------------------------------------------------------------------
+// trace
+// ---------------------------------------------------------------------------
+// Persistent, warp-batched traversal: each warp claims 32 queue entries with
+// one atomic and traces them together in the while-while form.  (Refilling
+// lanes individually as their rays finish was measured slower on B200: it
+// breaks the warp-wide leaf batching of trace_closest_ww.)
+__global__ void __launch_bounds__(128) k_map_trace(DevScene S, SbrMapParams P, int seg,
+                                                   MapQueue q, const unsigned long long* count_in,
+                                                   uint64_t begin, uint64_t count0, uint64_t comb_q,
+                                                   HitBuf hits, unsigned long long* work,
+                                                   unsigned long long* counters) {
+  const unsigned lane = threadIdx.x & 31u;
+  const uint64_t n = seg == 0 ? comb_q * kCombStride : (uint64_t)*count_in;
+  const double3 src = make_double3(P.source[0], P.source[1], P.source[2]);
+  while (true) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(work, 32ULL);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= n) break;
+    const uint64_t i = base + lane;
+    bool active = i < n;
+    double3 o = src, d = make_double3(0.0, 0.0, 1.0);
+    if (active) {
+      if (seg == 0) {
+        const uint64_t local = comb_sample(i, comb_q);
+        active = local < count0;
+        if (active) d = fibonacci_dir(P.num_samples, begin + local);
+        else hits.tri[i] = -3;  // comb slot past the end of the range
+      } else {
+        o = make_double3(q.ox[i], q.oy[i], q.oz[i]);
+        d = make_double3(q.dx[i], q.dy[i], q.dz[i]);
       }
     }
-  }
-  if (h.tri < 0) {
-    K.escaped++;
-    R.alive = false;
-    return;
-  }
-  if (seg == P.max_depth) {
-    R.alive = false;
-    return;
-  }
-  const double r_hit = R.r_dist + h.t;
-  if (seg >= P.cull_from && (P.gain_threshold > 0.0 || P.rr_depth >= 0)) {
-    const double e_sq = field_energy(R.E);
-    bool keep = true;
-    if (P.gain_threshold > 0.0) {
-      keep = e_sq >= P.gain_threshold * (r_hit * r_hit);
-      if (!keep) atomicAdd(sc + SBR_MC_THRESHOLD_KILLED, 1ULL);
-    }
-    if (P.rr_depth >= 0 && seg >= P.rr_depth) {
-      const double surv = e_sq < P.rr_max ? e_sq : P.rr_max;
-      const double u_rr = philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_ROULETTE, slot);
-      if (keep && u_rr >= surv) atomicAdd(sc + SBR_MC_ROULETTE_KILLED, 1ULL);
-      keep = keep && (u_rr < surv);
-      if (keep) R.weight /= surv;
-    }
-    if (!keep) {
-      R.alive = false;
-      return;
+    ClosestTrav T;
+    T.start(S, o, d, 1e-4, __longlong_as_double(0x7ff0000000000000LL));
+    if (!active) T.idle();
+    while (!T.done()) T.round(S);
+    if (active) {
+      HitRecord h;
+      T.result(h);
+      if (!T.ok) {
+        flag_error(S, kErrStack);
+        atomicAdd(counters + SBR_MC_STACK_OVERFLOW, 1ULL);
+        h.tri = -2;  // dropped
+      }
+      hits.t[i] = h.t;
+      hits.tri[i] = h.tri;
+#ifdef SBR_COUNT_VISITS
+      atomicAdd(counters + SBR_MC_DIRECT_VISIBLE, (unsigned long long)T.visits);
+      atomicAdd(counters + SBR_MC_THRESHOLD_KILLED, (unsigned long long)T.tests);
+#endif
     }
   }
-  const double3 pt = R.o + h.t * R.d;
-  double3 n = ldg3(S.normals + 3 * (int64_t)h.tri);
-  if (dot_seq(R.d, n) > 0.0) n = neg(n);
-  const double cos_i = fabs(dot_seq(R.d, n));
-  const SbrMaterial m = S.mats[__ldg(S.matrow + h.tri)];
-  const Fresnel4 F = slab_fresnel(m, cos_i);
-  const double r_sq = cabs2(F.rp) + cabs2(F.rl);
-  const double t_sq = cabs2(F.tp) + cabs2(F.tl);
-  // _interaction_rows with q_D = 0 (paths.py:572-595)
-  double q0 = 0.0, q1 = 0.0, q2 = 0.0;
-  const double den = r_sq + t_sq;
-  if (den > 0.0) {
-    const double s_sq = m.scattering * m.scattering;
-    q0 = 1.0 * (1.0 - s_sq) * r_sq / den;
-    q1 = 1.0 * s_sq * r_sq / den;
-    q2 = 1.0 * t_sq / den;
-  }
-  if (!(P.allow_mask & 1)) q0 = 0.0;
-  if (!(P.allow_mask & 2)) q1 = 0.0;
-  if (!(P.allow_mask & 4)) q2 = 0.0;
-  const double total = ((q0 + q1) + q2) + 0.0;
-  if (!(total > 0.0)) {
-    atomicAdd(sc + SBR_MC_TERMINATED, 1ULL);
-    R.alive = false;
-    return;
-  }
-  q0 /= total;
-  q1 /= total;
-  q2 /= total;
-  const double q3 = 0.0 / total;
-  const double u = philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_INTERACTION, slot);
-  const double c0 = q0, c1 = c0 + q1, c2 = c1 + q2, c3 = c2 + q3;
-  int code = (u >= c0) + (u >= c1) + (u >= c2) + (u >= c3);
-  if (code > 3) code = 3;
-  R.weight /= (code == 0 ? q0 : code == 1 ? q1 : code == 2 ? q2 : q3);
-
-  double3 e_perp, e_par;
-  incidence_frame(R.d, n, e_perp, e_par);
-  const cplx c_perp = cdot_real(R.E, e_perp), c_par = cdot_real(R.E, e_par);
-  double3 nd = R.d;
-  if (code == 0) {
-    const double dn = dot_seq(R.d, n);
-    const double3 kr = R.d - (2.0 * dn) * n;
-    const double3 e_par_r = cross3(e_perp, kr);
-    const cplx a = F.rp * c_perp, b = F.rl * c_par;
-    R.E.x = m.spec_amp * (e_perp.x * a + e_par_r.x * b);
-    R.E.y = m.spec_amp * (e_perp.y * a + e_par_r.y * b);
-    R.E.z = m.spec_amp * (e_perp.z * a + e_par_r.z * b);
-    nd = kr;
-  } else if (code == 2) {
-    const cplx a = F.tp * c_perp, b = F.tl * c_par;
-    R.E.x = e_perp.x * a + e_par.x * b;
-    R.E.y = e_perp.y * a + e_par.y * b;
-    R.E.z = e_perp.z * a + e_par.z * b;
-  }
-  R.r_dist = r_hit;
-  if (code == 1) {
-    const double u0 = philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_RESPAWN, 2 * slot);
-    const double u1 = philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_RESPAWN, 2 * slot + 1);
-    const double cos_t = u0, azim = kTwoPi * u1;
-    const double x = 1.0 - cos_t * cos_t;
-    const double sin_t = sqrt(x > 0.0 ? x : 0.0);
-    const double3 t1 = perp_batch(n);
-    const double3 t2 = cross3(n, t1);
-    double sa, ca;
-    sincos(azim, &sa, &ca);
-    const double a = sin_t * ca, b = sin_t * sa;
-    const double3 ks = make_double3((a * t1.x + b * t2.x) + cos_t * n.x,
-                                    (a * t1.y + b * t2.y) + cos_t * n.y,
-                                    (a * t1.z + b * t2.z) + cos_t * n.z);
-    const double g_num = sqrt(cabs2(F.rp * c_perp) + cabs2(F.rl * c_par));
-    const double g_den = sqrt(cabs2(c_perp) + cabs2(c_par));
-    const double gamma = g_den > 0.0 ? g_num / g_den : 0.0;
-    const double f_s = pattern_density(m, R.d, ks, n);
-    const double patch = R.omega * (r_hit * r_hit) / (cos_i > 1e-12 ? cos_i : 1e-12);
-    const double amp = m.scattering * gamma * sqrt(f_s * cos_i * patch);
-    double3 th_i, ph_i;
-    transverse_rows(R.d, th_i, ph_i);
-    const cplx ci0 = cdot_real(R.E, th_i), ci1 = cdot_real(R.E, ph_i);
-    double chi1 = 0.0, chi2 = 0.0;
-    if (P.any_random_phase && m.random_phases) {
-      chi1 = kTwoPi * philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_PHASE, 2 * slot);
-      chi2 = kTwoPi * philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_PHASE, 2 * slot + 1);
-    }
-    const double sq = sqrt(1.0 - m.xpd_kx), sk = sqrt(m.xpd_kx);
-    double s1, k1, s2, k2;
-    sincos(chi1, &s1, &k1);
-    sincos(chi2, &s2, &k2);
-    const cplx co0 = C(amp * k1, amp * s1) * (sq * ci0 - sk * ci1);
-    const cplx co1 = C(amp * k2, amp * s2) * (sk * ci0 + sq * ci1);
-    double3 th_s, ph_s;
-    transverse_rows(ks, th_s, ph_s);
-    const cplx inv_r = C(r_hit, 0.0);
-    R.E.x = cdiv(th_s.x * co0 + ph_s.x * co1, inv_r);
-    R.E.y = cdiv(th_s.y * co0 + ph_s.y * co1, inv_r);
-    R.E.z = cdiv(th_s.z * co0 + ph_s.z * co1, inv_r);
-    nd = ks;
-    R.r_dist = 0.0;
-    R.omega = kTwoPi;
-    K.respawns++;
-  }
-  R.o = pt;
-  R.d = nd;
-  R.seg = seg + 1;
 }
 
-__global__ void __launch_bounds__(128) k_radiomap(DevScene S, SbrMapParams P, uint64_t begin,
-                                                  uint64_t count, uint64_t comb_q,
-                                                  unsigned long long* __restrict__ work,
-                                                  double* __restrict__ grid,
-                                                  unsigned long long* __restrict__ counters) {
-  __shared__ unsigned long long sc[SBR_MC_COUNT];
-  for (int i = threadIdx.x; i < SBR_MC_COUNT; i += blockDim.x) sc[i] = 0ULL;
-  __syncthreads();
-  const unsigned lane = threadIdx.x & 31u;
-  const unsigned lt_mask = (1u << lane) - 1u;
-  const uint64_t total_items = comb_q * kCombStride;
-  MapRay R;
-  R.alive = false;
-  LaneCounters K = {0u, 0u, 0u, 0u};
-  bool more = true;
-  while (true) {
-    const unsigned dead = __ballot_sync(0xffffffffu, !R.alive);
-    if (dead && more) {
-      const unsigned nd = __popc(dead);
-      unsigned long long base = 0;
-      if (lane == 0) base = atomicAdd(work, (unsigned long long)nd);
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (base + nd >= total_items) more = false;
-      if (!R.alive) {
-        const uint64_t w = base + __popc(dead & lt_mask);
-        if (w < total_items) {
-          const uint64_t k = w % comb_q, c = w / comb_q;
-          const uint64_t local = c + k * kCombStride;
-          if (local < count) init_ray(P, begin + local, R);
+// ---------------------------------------------------------------------------
+// shade
+// ---------------------------------------------------------------------------
+struct LaneCounters {
+  unsigned rb, deposits, escaped, respawns, terminated, thr, rr;
+};
+
+__global__ void __launch_bounds__(128, 4) k_map_shade(DevScene S, SbrMapParams P, int seg,
+                                                   MapQueue qi, const unsigned long long* count_in,
+                                                   uint64_t begin, uint64_t comb_q, HitBuf hits,
+                                                   MapQueue qo, unsigned long long* count_out,
+                                                   double* __restrict__ grid,
+                                                   unsigned long long* __restrict__ counters) {
+  LaneCounters K = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
+  const uint64_t n = seg == 0 ? comb_q * kCombStride : (uint64_t)*count_in;
+  const double3 n_hat = make_double3(P.normal[0], P.normal[1], P.normal[2]);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const int tri = hits.tri[i];
+    if (tri < -1) continue;  // empty comb slot / stack overflow
+    double3 o, d;
+    cvec3 E;
+    double r_dist, omega, weight;
+    uint64_t g;
+    if (seg == 0) {
+      g = begin + comb_sample(i, comb_q);
+      o = make_double3(P.source[0], P.source[1], P.source[2]);
+      d = fibonacci_dir(P.num_samples, g);
+      E = antenna_field(P.pattern, d);
+      r_dist = 0.0;
+      omega = P.omega0;
+      weight = alpha_sq(P, d);
+    } else {
+      g = qi.g[i];
+      o = make_double3(qi.ox[i], qi.oy[i], qi.oz[i]);
+      d = make_double3(qi.dx[i], qi.dy[i], qi.dz[i]);
+      E.x = C(qi.exr[i], qi.exi[i]);
+      E.y = C(qi.eyr[i], qi.eyi[i]);
+      E.z = C(qi.ezr[i], qi.ezi[i]);
+      r_dist = qi.r_dist[i];
+      omega = qi.omega[i];
+      weight = qi.weight[i];
+    }
+    K.rb++;
+    const double t_hit = hits.t[i];
+    const uint64_t chunk = g >> SBR_CHUNK_LOG2;
+    const uint64_t slot = g & ((1ULL << SBR_CHUNK_LOG2) - 1);
+    // plane crossing before the hit (radiomap.py:394-413); escaped rays deposit too
+    if (seg >= 1) {
+      const double denom = dot_gemv(d, n_hat);
+      double s = -1.0;
+      if (fabs(denom) > 1e-12) s = (P.plane_off - dot_gemv(o, n_hat)) / denom;
+      if (s > 1e-4 && s < t_hit) {
+        const double3 pt = o + s * d;
+        const double3 rel = make_double3(pt.x - P.corner[0], pt.y - P.corner[1], pt.z - P.corner[2]);
+        const double fu = floor(dot_gemv(rel, make_double3(P.u_hat[0], P.u_hat[1], P.u_hat[2])) / P.cell_w);
+        const double fv = floor(dot_gemv(rel, make_double3(P.v_hat[0], P.v_hat[1], P.v_hat[2])) / P.cell_h);
+        if (fu >= 0.0 && fu < (double)P.nx && fv >= 0.0 && fv < (double)P.ny) {
+          const double val = P.scale * field_energy(E) * omega / fabs(denom) * weight;
+          atomicAdd(grid + (int64_t)fv * P.nx + (int64_t)fu, val);
+          K.deposits++;
         }
       }
     }
-    if (!__any_sync(0xffffffffu, R.alive)) {
-      if (!more) break;
+    if (tri < 0) {
+      K.escaped++;
       continue;
     }
-    if (R.alive) map_step(S, P, R, grid, K, sc);
+    if (seg == P.max_depth) continue;
+    const double r_hit = r_dist + t_hit;
+    // culling (radiomap.py:427-447)
+    if (seg >= P.cull_from && (P.gain_threshold > 0.0 || P.rr_depth >= 0)) {
+      const double e_sq = field_energy(E);
+      bool keep = true;
+      if (P.gain_threshold > 0.0) {
+        keep = e_sq >= P.gain_threshold * (r_hit * r_hit);
+        if (!keep) K.thr++;
+      }
+      if (P.rr_depth >= 0 && seg >= P.rr_depth) {
+        const double surv = e_sq < P.rr_max ? e_sq : P.rr_max;
+        const double u_rr = philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_ROULETTE, slot);
+        if (keep && u_rr >= surv) K.rr++;
+        keep = keep && (u_rr < surv);
+        if (keep) weight /= surv;
+      }
+      if (!keep) continue;
+    }
+    const double3 pt = o + t_hit * d;
+    double3 nrm = ldg3(S.normals + 3 * (int64_t)tri);
+    if (dot_seq(d, nrm) > 0.0) nrm = neg(nrm);
+    const double cos_i = fabs(dot_seq(d, nrm));
+    const SbrMaterial m = S.mats[__ldg(S.matrow + tri)];
+    const Fresnel4 F = slab_fresnel(m, cos_i);
+    const double r_sq = cabs2(F.rp) + cabs2(F.rl);
+    const double t_sq = cabs2(F.tp) + cabs2(F.tl);
+    // _interaction_rows with q_D = 0 (paths.py:572-595)
+    double q0 = 0.0, q1 = 0.0, q2 = 0.0;
+    const double den = r_sq + t_sq;
+    if (den > 0.0) {
+      const double s_sq = m.scattering * m.scattering;
+      q0 = 1.0 * (1.0 - s_sq) * r_sq / den;
+      q1 = 1.0 * s_sq * r_sq / den;
+      q2 = 1.0 * t_sq / den;
+    }
+    if (!(P.allow_mask & 1)) q0 = 0.0;
+    if (!(P.allow_mask & 2)) q1 = 0.0;
+    if (!(P.allow_mask & 4)) q2 = 0.0;
+    const double total = ((q0 + q1) + q2) + 0.0;
+    if (!(total > 0.0)) {
+      K.terminated++;
+      continue;
+    }
+    q0 /= total;
+    q1 /= total;
+    q2 /= total;
+    const double q3 = 0.0 / total;
+    const double u = philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_INTERACTION, slot);
+    const double c0 = q0, c1 = c0 + q1, c2 = c1 + q2, c3 = c2 + q3;
+    int code = (u >= c0) + (u >= c1) + (u >= c2) + (u >= c3);
+    if (code > 3) code = 3;
+    weight /= (code == 0 ? q0 : code == 1 ? q1 : code == 2 ? q2 : q3);
+
+    double3 e_perp, e_par;
+    incidence_frame(d, nrm, e_perp, e_par);
+    const cplx c_perp = cdot_real(E, e_perp), c_par = cdot_real(E, e_par);
+    double3 nd = d;
+    if (code == 0) {
+      const double dn = dot_seq(d, nrm);
+      const double3 kr = d - (2.0 * dn) * nrm;
+      const double3 e_par_r = cross3(e_perp, kr);
+      const cplx a = F.rp * c_perp, b = F.rl * c_par;
+      E.x = m.spec_amp * (e_perp.x * a + e_par_r.x * b);
+      E.y = m.spec_amp * (e_perp.y * a + e_par_r.y * b);
+      E.z = m.spec_amp * (e_perp.z * a + e_par_r.z * b);
+      nd = kr;
+    } else if (code == 2) {
+      const cplx a = F.tp * c_perp, b = F.tl * c_par;
+      E.x = e_perp.x * a + e_par.x * b;
+      E.y = e_perp.y * a + e_par.y * b;
+      E.z = e_perp.z * a + e_par.z * b;
+    }
+    r_dist = r_hit;
+    if (code == 1) {
+      const double u0 = philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_RESPAWN, 2 * slot);
+      const double u1 = philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_RESPAWN, 2 * slot + 1);
+      const double cos_t = u0, azim = kTwoPi * u1;
+      const double x = 1.0 - cos_t * cos_t;
+      const double sin_t = sqrt(x > 0.0 ? x : 0.0);
+      const double3 t1 = perp_batch(nrm);
+      const double3 t2 = cross3(nrm, t1);
+      double sa, ca;
+      sincos(azim, &sa, &ca);
+      const double a = sin_t * ca, b = sin_t * sa;
+      const double3 ks = make_double3((a * t1.x + b * t2.x) + cos_t * nrm.x,
+                                      (a * t1.y + b * t2.y) + cos_t * nrm.y,
+                                      (a * t1.z + b * t2.z) + cos_t * nrm.z);
+      const double g_num = sqrt(cabs2(F.rp * c_perp) + cabs2(F.rl * c_par));
+      const double g_den = sqrt(cabs2(c_perp) + cabs2(c_par));
+      const double gamma = g_den > 0.0 ? g_num / g_den : 0.0;
+      const double f_s = pattern_density(m, d, ks, nrm);
+      const double patch = omega * (r_hit * r_hit) / (cos_i > 1e-12 ? cos_i : 1e-12);
+      const double amp = m.scattering * gamma * sqrt(f_s * cos_i * patch);
+      double3 th_i, ph_i;
+      transverse_rows(d, th_i, ph_i);
+      const cplx ci0 = cdot_real(E, th_i), ci1 = cdot_real(E, ph_i);
+      double chi1 = 0.0, chi2 = 0.0;
+      if (P.any_random_phase && m.random_phases) {
+        chi1 = kTwoPi * philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_PHASE, 2 * slot);
+        chi2 = kTwoPi * philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_PHASE, 2 * slot + 1);
+      }
+      const double sq = sqrt(1.0 - m.xpd_kx), sk = sqrt(m.xpd_kx);
+      double s1, k1, s2, k2;
+      sincos(chi1, &s1, &k1);
+      sincos(chi2, &s2, &k2);
+      const cplx co0 = C(amp * k1, amp * s1) * (sq * ci0 - sk * ci1);
+      const cplx co1 = C(amp * k2, amp * s2) * (sk * ci0 + sq * ci1);
+      double3 th_s, ph_s;
+      transverse_rows(ks, th_s, ph_s);
+      const cplx inv_r = C(r_hit, 0.0);
+      E.x = cdiv(th_s.x * co0 + ph_s.x * co1, inv_r);
+      E.y = cdiv(th_s.y * co0 + ph_s.y * co1, inv_r);
+      E.z = cdiv(th_s.z * co0 + ph_s.z * co1, inv_r);
+      nd = ks;
+      r_dist = 0.0;
+      omega = kTwoPi;
+      K.respawns++;
+    }
+    const unsigned long long j = append_slot(count_out);
+    qo.ox[j] = pt.x;
+    qo.oy[j] = pt.y;
+    qo.oz[j] = pt.z;
+    qo.dx[j] = nd.x;
+    qo.dy[j] = nd.y;
+    qo.dz[j] = nd.z;
+    qo.exr[j] = E.x.re;
+    qo.exi[j] = E.x.im;
+    qo.eyr[j] = E.y.re;
+    qo.eyi[j] = E.y.im;
+    qo.ezr[j] = E.z.re;
+    qo.ezi[j] = E.z.im;
+    qo.r_dist[j] = r_dist;
+    qo.omega[j] = omega;
+    qo.weight[j] = weight;
+    qo.g[j] = g;
   }
-  // warp-reduce the per-lane counters, then one shared atomic per warp
-  unsigned v[4] = {K.rb, K.deposits, K.escaped, K.respawns};
-  const int idx[4] = {SBR_MC_RAY_BOUNCES, SBR_MC_DEPOSITS, SBR_MC_ESCAPED, SBR_MC_RESPAWNS};
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned v[7] = {K.rb, K.deposits, K.escaped, K.respawns, K.terminated, K.thr, K.rr};
+  const int idx[7] = {SBR_MC_RAY_BOUNCES, SBR_MC_DEPOSITS, SBR_MC_ESCAPED, SBR_MC_RESPAWNS,
+                      SBR_MC_TERMINATED, SBR_MC_THRESHOLD_KILLED, SBR_MC_ROULETTE_KILLED};
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < 7; ++k) {
     const unsigned s = __reduce_add_sync(0xffffffffu, v[k]);
-    if (lane == 0) atomicAdd(sc + idx[k], (unsigned long long)s);
+    if (lane == 0 && s) atomicAdd(counters + idx[k], (unsigned long long)s);
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < SBR_MC_COUNT; i += blockDim.x)
-    if (sc[i]) atomicAdd(counters + i, sc[i]);
+}
+
+__global__ void k_reset_pass(unsigned long long* work, unsigned long long* count_next) {
+  *work = 0ULL;
+  *count_next = 0ULL;
 }
 
 __global__ void __launch_bounds__(128) k_direct(DevScene S, SbrMapParams P,
@@ -330,38 +401,107 @@ int check_params(const SbrScene* scene, const SbrMapParams* P) {
   return SBR_OK;
 }
 
+// device scratch of one wavefront pass: two ray queues, the hit buffer and the
+// control words, carved from one stream-ordered allocation (per call, so
+// concurrent calls on different streams never share queues)
+struct Wave {
+  void* block = nullptr;
+  MapQueue q[2];
+  HitBuf hits;
+  unsigned long long* ctl = nullptr;  // [0] work, [1] count A, [2] count B
+};
+
+int wave_alloc(int64_t cap, cudaStream_t st, Wave* w) {
+  static bool pool_tuned[16] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!pool_tuned[dev & 15]) {
+    // keep freed queue memory in the pool between calls (no re-mapping cost)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~0ULL;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool_tuned[dev & 15] = true;
+  }
+  const size_t per_queue = (size_t)cap * (16 * sizeof(double));
+  const size_t bytes = 2 * per_queue + (size_t)cap * (sizeof(double) + sizeof(int32_t)) + 512;
+  if (cudaMallocAsync(&w->block, bytes, st) != cudaSuccess)
+    return set_error(SBR_ERR_NOMEM, "ray queues");
+  char* p = (char*)w->block;
+  for (int k = 0; k < 2; ++k) {
+    double** f[15] = {&w->q[k].ox, &w->q[k].oy, &w->q[k].oz, &w->q[k].dx, &w->q[k].dy,
+                      &w->q[k].dz, &w->q[k].exr, &w->q[k].exi, &w->q[k].eyr, &w->q[k].eyi,
+                      &w->q[k].ezr, &w->q[k].ezi, &w->q[k].r_dist, &w->q[k].omega,
+                      &w->q[k].weight};
+    for (int i = 0; i < 15; ++i) {
+      *f[i] = (double*)p;
+      p += cap * sizeof(double);
+    }
+    w->q[k].g = (uint64_t*)p;
+    p += cap * sizeof(uint64_t);
+  }
+  w->hits.t = (double*)p;
+  p += cap * sizeof(double);
+  w->hits.tri = (int32_t*)p;
+  p += cap * sizeof(int32_t);
+  p = (char*)(((uintptr_t)p + 255) & ~(uintptr_t)255);
+  w->ctl = (unsigned long long*)p;
+  return SBR_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
 int sbr_radiomap_bounce(const SbrScene* scene, const SbrMapParams* P, uint64_t sample_begin,
-                        uint64_t sample_end, double* grid, uint64_t* counters, void* stream) {
+                        uint64_t sample_end, double* grid, uint64_t* counters_u64, void* stream) {
   int rc = check_params(scene, P);
   if (rc) return rc;
   if (sample_end > P->num_samples || sample_begin > sample_end)
     return set_error(SBR_ERR_INVALID, "bad sample range");
-  const uint64_t count = sample_end - sample_begin;
-  if (count == 0) return SBR_OK;
+  const uint64_t total = sample_end - sample_begin;
+  if (total == 0) return SBR_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  unsigned long long* work;
-  if (cudaMallocAsync(&work, sizeof(unsigned long long), st) != cudaSuccess)
-    return set_error(SBR_ERR_NOMEM, "work counter");
-  cudaMemsetAsync(work, 0, sizeof(unsigned long long), st);
+  unsigned long long* counters = (unsigned long long*)counters_u64;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t chunk = total < (uint64_t)kChunkRays ? (int64_t)total : kChunkRays;
+  // segment 0 runs over comb slots: up to chunk + kCombStride items
+  Wave wave;
+  Wave* w = &wave;
+  if ((rc = wave_alloc(chunk + (int64_t)kCombStride, st, w))) return rc;
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_radiomap, 128, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_map_trace, 128, 0);
   if (per_sm < 1) per_sm = 1;
-  uint64_t blocks = (uint64_t)sms * per_sm;
-  const uint64_t warps_needed = (count + 31) / 32;
-  if (blocks * 4 > warps_needed) blocks = (warps_needed + 3) / 4;
-  if (blocks < 1) blocks = 1;
-  const uint64_t comb_q = (count + kCombStride - 1) / kCombStride;
-  k_radiomap<<<(unsigned)blocks, 128, 0, st>>>(dev_view(scene), *P, sample_begin, count, comb_q,
-                                               work, grid, (unsigned long long*)counters);
-  rc = launch_status("k_radiomap");
-  cudaFreeAsync(work, st);
+  const unsigned trace_blocks = (unsigned)(sms * per_sm);
+  const unsigned shade_blocks = (unsigned)(sms * 8);
+  const DevScene S = dev_view(scene);
+  for (uint64_t lo = sample_begin; lo < sample_end; lo += (uint64_t)chunk) {
+    const uint64_t cnt = (sample_end - lo) < (uint64_t)chunk ? (sample_end - lo) : (uint64_t)chunk;
+    const uint64_t comb_q = (cnt + kCombStride - 1) / kCombStride;
+    int cur = 0;
+    for (int seg = 0; seg <= P->max_depth; ++seg) {
+      // ctl[0] = work counter; ctl[1 + cur] = this segment's count; ctl[2 - cur] = next count
+      k_reset_pass<<<1, 1, 0, st>>>(w->ctl, w->ctl + 2 - cur);
+      if ((rc = launch_status("k_reset_pass"))) break;
+      prof_begin(st, "k_map_trace");
+      k_map_trace<<<trace_blocks, 128, 0, st>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo, cnt,
+                                                comb_q, w->hits, w->ctl, counters);
+      prof_end(st);
+      if ((rc = launch_status("k_map_trace"))) break;
+      prof_begin(st, "k_map_shade");
+      k_map_shade<<<shade_blocks, 128, 0, st>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo,
+                                                comb_q, w->hits, w->q[1 - cur], w->ctl + 2 - cur,
+                                                grid, counters);
+      prof_end(st);
+      if ((rc = launch_status("k_map_shade"))) break;
+      cur = 1 - cur;
+    }
+    if (rc) break;
+  }
+  cudaFreeAsync(w->block, st);
   return rc;
 }
 

@@ -16,6 +16,8 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -27,6 +29,47 @@ static thread_local std::string g_last_error;
 static std::atomic<uint64_t> g_launches{0};
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// ---- optional per-kernel CUDA-event timing (bench.py roofline evidence) ----
+struct Span {
+  std::string name;
+  cudaEvent_t a, b;
+};
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<Span> g_spans;
+static std::map<std::string, std::pair<double, uint64_t>> g_prof_acc;
+
+void prof_begin(void* stream, const char* name) {
+  if (!g_prof_on) return;
+  Span s;
+  s.name = name;
+  cudaEventCreate(&s.a);
+  cudaEventCreate(&s.b);
+  cudaEventRecord(s.a, (cudaStream_t)stream);
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_spans.push_back(s);
+}
+
+void prof_end(void* stream) {
+  if (!g_prof_on) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (!g_spans.empty()) cudaEventRecord(g_spans.back().b, (cudaStream_t)stream);
+}
+
+static void prof_drain() {
+  for (Span& s : g_spans) {
+    cudaEventSynchronize(s.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, s.a, s.b);
+    auto& acc = g_prof_acc[s.name];
+    acc.first += ms;
+    acc.second += 1;
+    cudaEventDestroy(s.a);
+    cudaEventDestroy(s.b);
+  }
+  g_spans.clear();
+}
 
 int set_error(int code, const std::string& msg) {
   g_last_error = msg;
@@ -321,6 +364,22 @@ extern "C" {
 const char* sbr_last_error(void) { return g_last_error.c_str(); }
 int sbr_version(void) { return 100; }
 uint64_t sbr_kernel_launches(void) { return g_launches.load(); }
+
+int sbr_profile_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  prof_drain();
+  g_prof_acc.clear();
+  g_prof_on = on != 0;
+  return SBR_OK;
+}
+
+double sbr_profile_kernel_ms(const char* name, uint64_t* launches) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  prof_drain();
+  auto it = g_prof_acc.find(name ? name : "");
+  if (launches) *launches = it == g_prof_acc.end() ? 0 : it->second.second;
+  return it == g_prof_acc.end() ? 0.0 : it->second.first;
+}
 
 int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64_t ntri,
                      int32_t device, void* stream, SbrScene** out) {

@@ -291,15 +291,20 @@ typedef struct SbrFieldParams {
 int sbr_cir_sweep(const SbrScene* scene, const SbrCirParams* params, uint64_t sample_begin,
                   uint64_t sample_end, const SbrVertexBuf* vb, uint64_t* counters_dev,
                   void* stream);
+/* Spatial (Morton) order of the first nv vertices, for coherent occlusion
+ * rays in sbr_cir_visibility: order_dev (nv) int32 vertex indices. */
+int sbr_cir_vertex_order(const SbrScene* scene, const SbrVertexBuf* vb, int64_t nv,
+                         int32_t* order_dev, void* stream);
 /* _visible_pairs (paths.py:657-683): half-space side test + occlusion ray for
- * every (vertex in [v_begin, v_end), target) pair; appends visible rows
- * (ordinal key (depth << 60 | sample << 20 | target), vertex index) at
+ * every (vertex, target) pair over positions [v_begin, v_end) of order_dev
+ * (NULL = identity order); appends visible rows (ordinal key
+ * (depth << 60 | sample << 20 | target), vertex index) at
  * counters_dev[SBR_CC_ROWS].  Rows beyond row_capacity are counted, not
- * written (SBR_CC_ROW_OVERFLOW). */
+ * written.  Row order is irrelevant: sbr_cir_select sorts by ordinal. */
 int sbr_cir_visibility(const SbrScene* scene, const SbrCirParams* params,
                        const SbrVertexBuf* vb, int64_t v_begin, int64_t v_end,
-                       uint64_t* row_key_dev, int32_t* row_vtx_dev, int64_t row_capacity,
-                       uint64_t* counters_dev, void* stream);
+                       const int32_t* order_dev, uint64_t* row_key_dev, int32_t* row_vtx_dev,
+                       int64_t row_capacity, uint64_t* counters_dev, void* stream);
 /* Candidate selection with the reference's exact semantics
  * (_emit_records paths.py:903-987, DedupTable / PathBuffer 174-226,
  * generate_candidates 1019-1103 at workers=1): ordinal sort, first occurrence

@@ -247,6 +247,28 @@ def _torch():
     return torch
 
 
+class _PhaseTimer:
+    """SBR_TIMING=1: print wall time of each host phase (synchronising)."""
+
+    def __init__(self, name):
+        import os
+        import time
+        self.on = os.environ.get("SBR_TIMING") == "1"
+        self.name, self.t, self.time = name, time.perf_counter(), time.perf_counter
+        self.parts = []
+
+    def mark(self, label):
+        if self.on:
+            _torch().cuda.synchronize()
+            now = self.time()
+            self.parts.append((label, now - self.t))
+            self.t = now
+
+    def report(self):
+        if self.on:
+            print(self.name, " ".join(f"{k}={v * 1e3:.1f}ms" for k, v in self.parts), flush=True)
+
+
 def _check_cfg(cfg):
     if Interaction.DIFFRACTION in cfg.enabled and cfg.q_diffraction > 0.0:
         raise NotImplementedError(
@@ -381,31 +403,47 @@ def _generate_device(scene, source, targets, cfg, source_id=0, sample_range=None
         occ = acc.occluded_batch(torch.from_numpy(np.broadcast_to(source, targets.shape).copy())
                                  .to(dev), targets_t)
         los_vis = (~occ).to(torch.uint8).contiguous()
+        gt = _PhaseTimer("  generate")
+        gt.mark("los")
         L = max(int(cfg.max_depth), 1)
         vb = _VertexBuf((hi - lo) * cfg.max_depth, dev)
         if hi > lo and cfg.max_depth > 0:
             _native.check(L_.sbr_cir_sweep(acc.handle, ctypes.byref(params), lo, hi,
                                            ctypes.byref(vb.abi), _native.ptr(counters), stream))
         nv = int(counters[_abi.CC["vertices"]].item())
-        # visibility rows (grow the row buffer until everything fits)
+        gt.mark("sweep")
+        # visibility rows, vertex slabs of <= 2^26 (vertex, target) pairs; before
+        # each slab the row buffer is grown (geometrically) to hold the slab's
+        # worst case, so no slab is ever traced twice
         nt = len(targets)
-        cap = max(1 << 16, nv * min(nt, 4))
-        while True:
-            row_key = torch.empty(cap, dtype=torch.uint64, device=dev)
-            row_vtx = torch.empty(cap, dtype=torch.int32, device=dev)
-            counters[_abi.CC["rows"]] = 0
-            counters[_abi.CC["visibility_rays"]] = 0
-            if nv:
-                _native.check(L_.sbr_cir_visibility(
-                    acc.handle, ctypes.byref(params), ctypes.byref(vb.abi), 0, nv,
-                    _native.ptr(row_key), _native.ptr(row_vtx), cap, _native.ptr(counters),
-                    stream))
+        order = torch.empty(max(nv, 1), dtype=torch.int32, device=dev)
+        if nv:
+            _native.check(L_.sbr_cir_vertex_order(acc.handle, ctypes.byref(vb.abi), nv,
+                                                  _native.ptr(order), stream))
+        slab = max(32, ((1 << 26) // nt) // 32 * 32)
+        cap = max(1 << 20, min(nv * nt, int(nv * nt * 0.03)))
+        row_key = torch.empty(cap, dtype=torch.uint64, device=dev)
+        row_vtx = torch.empty(cap, dtype=torch.int32, device=dev)
+        nrows = 0
+        for v0 in range(0, nv, slab):
+            v1 = min(nv, v0 + slab)
+            need = nrows + (v1 - v0) * nt
+            if need > cap:
+                cap = max(need, int(cap * 1.5))
+                nk = torch.empty(cap, dtype=torch.uint64, device=dev)
+                nv_ = torch.empty(cap, dtype=torch.int32, device=dev)
+                nk[:nrows].copy_(row_key[:nrows])
+                nv_[:nrows].copy_(row_vtx[:nrows])
+                row_key, row_vtx = nk, nv_
+            _native.check(L_.sbr_cir_visibility(
+                acc.handle, ctypes.byref(params), ctypes.byref(vb.abi), v0, v1,
+                _native.ptr(order), _native.ptr(row_key), _native.ptr(row_vtx), cap,
+                _native.ptr(counters), stream))
             nrows = int(counters[_abi.CC["rows"]].item())
-            if nrows <= cap:
-                break
-            cap = int(nrows * 1.05) + 1024
-            del row_key, row_vtx
+            if nrows > cap:
+                raise RuntimeError("visibility row buffer overflow")  # cannot happen
         acc.check()
+        gt.mark("visibility")
         n_buffer = cfg.resolved_buffer_capacity()
         n_hash = cfg.resolved_hash_capacity()
         rec_cap = max(1, min(n_buffer, nrows + nt))
@@ -418,12 +456,15 @@ def _generate_device(scene, source, targets, cfg, source_id=0, sample_range=None
             _native.ptr(rec_vtx), _native.ptr(rec_tgt), ctypes.byref(n_rec),
             _native.ptr(counters), stream))
         n = int(n_rec.value)
+        gt.mark("select")
         recbuf = _RecordBuf(n, L, dev)
         if n:
             _native.check(L_.sbr_cir_records(ctypes.byref(params), ctypes.byref(vb.abi),
                                              _native.ptr(rec_vtx), _native.ptr(rec_tgt), n,
                                              ctypes.byref(recbuf.abi), stream))
         c = _counters_dict(counters.cpu().numpy())
+        gt.mark("records")
+        gt.report()
     if c["stack_overflow"]:
         raise RuntimeError("BVH traversal stack overflow")
     diag = {
@@ -596,6 +637,7 @@ def compute_paths(scene, transmitters, receivers, cfg):
     Returns a PathSet whose `tensors` holds the SoA arrays; `paths` builds
     the reference's ValidPath objects on first access.
     """
+    torch = _torch()
     transmitters = list(transmitters)
     receivers = list(receivers)
     if not transmitters or not receivers:
@@ -612,13 +654,16 @@ def compute_paths(scene, transmitters, receivers, cfg):
     rejections = Counter()
     load_factor = 0.0
     parts = []
+    timer = _PhaseTimer("compute_paths")
     for src_idx, (ti, te, tx_pos) in enumerate(tx_flat):
         cand, _, gdiag = _generate_device(scene, tx_pos, targets, cfg, source_id=src_idx)
+        timer.mark("generate")
         load_factor = max(load_factor, gdiag["hash_load_factor"])
         for k, v in gdiag.items():
             if k != "hash_load_factor":
                 diagnostics[k] += v
         pv, status, rc = _refine_device(scene, cand)
+        timer.mark("refine")
         rcount = rc.cpu().numpy()
         for code, name in _abi.REJECTION_NAMES.items():
             cnt = int(rcount[_abi.CC[{1: "rej_coplanar_miss", 2: "rej_occluded",
@@ -626,14 +671,18 @@ def compute_paths(scene, transmitters, receivers, cfg):
             if cnt:
                 rejections[name] += cnt
         f = _fields_device(scene, cand, pv, status, transmitters[ti], target_devices, cfg)
+        timer.mark("fields")
         n = cand.n
         if n == 0:
             continue
-        ok = (status[:n] == _abi.SBR_REFINE_OK).cpu().numpy()
-        h = {k: v[:n].cpu().numpy() for k, v in cand.rec.t.items()}
-        fh = {k: v[:n].cpu().numpy() for k, v in f.items()}
-        pvh = pv[:n].cpu().numpy()
-        sel = np.nonzero(ok)[0]
+        ok_idx = torch.nonzero(status[:n] == _abi.SBR_REFINE_OK).squeeze(1)
+        m = int(ok_idx.numel())
+        h = {k: v[:n].index_select(0, ok_idx).cpu().numpy() for k, v in cand.rec.t.items()
+             if k != "chain_hash"}
+        h["chain_hash"] = cand.rec.t["chain_hash"][:n].cpu().numpy()[ok_idx.cpu().numpy()]
+        fh = {k: v[:n].index_select(0, ok_idx).cpu().numpy() for k, v in f.items()}
+        pvh = pv[:n].index_select(0, ok_idx).cpu().numpy()
+        sel = np.arange(m)
         tri = h["tri"][sel]
         valid = tri >= 0
         obj = np.where(valid, acc.tri_object_id[np.maximum(tri, 0)], -1)
@@ -647,7 +696,10 @@ def compute_paths(scene, transmitters, receivers, cfg):
             arrival=fh["arrival"][sel], depth=h["depth"][sel].astype(np.int64),
             chain_hash=h["chain_hash"][sel], sample=h["sample"][sel], kind=h["kind"][sel],
             obj=obj, prim=prim, normal=h["normal"][sel], vertices=pvh[sel]))
+        timer.mark("host_copy")
     tensors = _concat_sorted(parts, max(int(cfg.max_depth), 1))
+    timer.mark("sort")
+    timer.report()
     result = dict(diagnostics)
     result["hash_load_factor"] = load_factor
     result["refinement_rejections"] = dict(rejections)

@@ -208,43 +208,146 @@ __global__ void __launch_bounds__(128) k_cir_sweep(DevScene S, SbrCirParams P, u
 }
 
 // ---------------------------------------------------------------------------
-// visibility: (vertex, target) pairs, targets fastest
+// vertex order: 63-bit Morton code of the interaction point
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t spread21(uint64_t x) {
+  x &= 0x1fffffULL;
+  x = (x | (x << 32)) & 0x1f00000000ffffULL;
+  x = (x | (x << 16)) & 0x1f0000ff0000ffULL;
+  x = (x | (x << 8)) & 0x100f00f00f00f00fULL;
+  x = (x | (x << 4)) & 0x10c30c30c30c30c3ULL;
+  x = (x | (x << 2)) & 0x1249249249249249ULL;
+  return x;
+}
+
+__global__ void k_vertex_morton(const double* __restrict__ point, int64_t n, double3 lo,
+                                double3 inv_ext, uint64_t* keys, int32_t* ids) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double p[3] = {point[3 * i], point[3 * i + 1], point[3 * i + 2]};
+    const double l[3] = {lo.x, lo.y, lo.z}, ie[3] = {inv_ext.x, inv_ext.y, inv_ext.z};
+    uint64_t q[3];
+    for (int k = 0; k < 3; ++k) {
+      double f = (p[k] - l[k]) * ie[k];
+      f = f < 0.0 ? 0.0 : (f > 1.0 ? 1.0 : f);
+      q[k] = (uint64_t)(f * 2097151.0);
+    }
+    keys[i] = (spread21(q[0]) << 2) | (spread21(q[1]) << 1) | spread21(q[2]);
+    ids[i] = (int32_t)i;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// visibility: (vertex, target) pairs
+// ---------------------------------------------------------------------------
+// Pair p -> (tile of 32 spatially sorted vertices, target, vertex in tile):
+// a warp claims 32 consecutive pairs = 32 neighbouring vertices looking at
+// the same target, so their occlusion rays are nearly parallel and walk the
+// same BVH nodes.  The half-space side test runs first; survivors are pushed
+// into a per-warp queue in shared memory and cast 32 at a time with the
+// while-while any-hit, so dead lanes never enter traversal and no pair list
+// goes through HBM.
+constexpr int kVisWarps = 4;
+
 __global__ void __launch_bounds__(128) k_cir_visibility(DevScene S, SbrCirParams P,
                                                         SbrVertexBuf vb, int64_t v_begin,
                                                         int64_t v_end, uint64_t* row_key,
                                                         int32_t* row_vtx, int64_t row_cap,
-                                                        unsigned long long* counters) {
+                                                        unsigned long long* counters,
+                                                        unsigned long long* work,
+                                                        const int32_t* __restrict__ order) {
+  __shared__ int64_t sq[kVisWarps][64];
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned wid = threadIdx.x >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t nt = P.n_targets;
-  const int64_t total = (v_end - v_begin) * nt;
+  const int64_t nv = v_end - v_begin;
+  const int64_t total = ((nv + 31) / 32) * 32 * nt;
+  int qn = 0;  // warp-uniform queue length
   unsigned vis = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = v_begin + i / nt;
-    const int k = (int)(i % nt);
-    const double3 p = ld3(vb.point + 3 * v);
-    const double3 n = ld3(vb.normal + 3 * v);
-    const int code = vb.code[v];
-    const double3 tg = ldg3(P.targets_dev + 3 * k);
-    const double side = dot_seq(tg - p, n);
-    const bool ok = code == 2 ? side < 0.0 : side > 0.0;
-    if (!ok) continue;
-    vis++;
-    bool fine;
-    const bool blocked = occluded_segment(S, p, tg, 1e-4, fine);
-    if (!fine) {
-      flag_error(S, kErrStack);
-      atomicAdd(counters + SBR_CC_STACK_OVERFLOW, 1ULL);
+  bool more = true;
+  while (more || qn > 0) {
+    // ---- refill: side test on the next 32 pairs
+    if (more && qn < 32) {
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(work, 32ULL);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if ((int64_t)base >= total) {
+        more = false;
+      } else {
+        const int64_t pi = (int64_t)base + lane;
+        bool pass = false;
+        const int64_t tile = pi / (32 * nt), rem = pi % (32 * nt);
+        const int64_t pos = tile * 32 + (rem & 31);
+        const int k = (int)(rem >> 5);
+        if (pi < total && pos < nv) {
+          const int64_t v = order ? order[v_begin + pos] : v_begin + pos;
+          const double3 p = ld3(vb.point + 3 * v);
+          const double3 n = ld3(vb.normal + 3 * v);
+          const double3 tg = ldg3(P.targets_dev + 3 * k);
+          const double side = dot_seq(tg - p, n);
+          pass = vb.code[v] == 2 ? side < 0.0 : side > 0.0;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, pass);
+        if (pass) {
+          const int64_t v = order ? order[v_begin + pos] : v_begin + pos;
+          sq[wid][qn + __popc(m & lt_mask)] = v * nt + k;  // (vertex, target) pair
+        }
+        qn += __popc(m);
+        __syncwarp();
+        if (qn < 32 && more) continue;
+      }
     }
-    if (blocked) continue;
-    const unsigned long long r = append_slot(counters + SBR_CC_ROWS);
-    if ((int64_t)r < row_cap) {
-      row_key[r] = ordinal_key(vb.depth[v], vb.sample[v], k);
-      row_vtx[r] = (int32_t)v;
+    // ---- cast up to 32 queued occlusion rays
+    const int take = qn < 32 ? qn : 32;
+    const bool active = (int)lane < take;
+    int64_t pi = 0;
+    if (active) pi = sq[wid][qn - take + lane];
+    __syncwarp();
+    qn -= take;
+    int64_t v = 0;
+    int k = 0;
+    double3 a = make_double3(0.0, 0.0, 0.0), b = a;
+    bool cast = false;
+    AnyTrav T;
+    if (active) {
+      v = pi / nt;
+      k = (int)(pi % nt);
+      a = ld3(vb.point + 3 * v);
+      b = ldg3(P.targets_dev + 3 * k);
+      vis++;
+      // occluded_batch (geometry.py:187-201): open segment, endpoints offset by eps
+      const double3 dd = b - a;
+      const double len = norm_seq(dd);
+      if (len > 2.0 * 1e-4) {
+        const double3 dn = make_double3(dd.x / len, dd.y / len, dd.z / len);
+        const double3 o = make_double3(a.x + 1e-4 * dn.x, a.y + 1e-4 * dn.y, a.z + 1e-4 * dn.z);
+        T.start(S, o, dn, 0.0, len - 2.0 * 1e-4);
+        cast = true;
+      }
+    }
+    if (!cast) {
+      T.idle();
+      T.found = false;
+      T.ok = true;
+    }
+    while (!T.done()) T.round(S);
+    if (active) {
+      if (!T.ok) {
+        flag_error(S, kErrStack);
+        atomicAdd(counters + SBR_CC_STACK_OVERFLOW, 1ULL);
+      }
+      if (!T.found) {
+        const unsigned long long r = append_slot(counters + SBR_CC_ROWS);
+        if ((int64_t)r < row_cap) {
+          row_key[r] = ordinal_key(vb.depth[v], vb.sample[v], k);
+          row_vtx[r] = (int32_t)v;
+        }
+      }
     }
   }
   const unsigned s = __reduce_add_sync(0xffffffffu, vis);
-  if ((threadIdx.x & 31) == 0 && s) atomicAdd(counters + SBR_CC_VIS_RAYS, (unsigned long long)s);
+  if (lane == 0 && s) atomicAdd(counters + SBR_CC_VIS_RAYS, (unsigned long long)s);
 }
 
 // ---------------------------------------------------------------------------
@@ -720,20 +823,63 @@ int sbr_cir_sweep(const SbrScene* scene, const SbrCirParams* P, uint64_t begin, 
   return launch_status("k_cir_sweep");
 }
 
+int sbr_cir_vertex_order(const SbrScene* scene, const SbrVertexBuf* vb, int64_t nv,
+                         int32_t* order, void* stream) {
+  if (!scene || !vb || !order) return set_error(SBR_ERR_INVALID, "NULL argument");
+  if (nv <= 0) return SBR_OK;
+  if (nv >= (1LL << 31)) return set_error(SBR_ERR_INVALID, "too many vertices");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = SBR_OK;
+  const DevScene S = dev_view(scene);
+  double3 lo = make_double3(S.bounds_lo[0], S.bounds_lo[1], S.bounds_lo[2]);
+  double3 ie;
+  {
+    const double ex = S.bounds_hi[0] - S.bounds_lo[0], ey = S.bounds_hi[1] - S.bounds_lo[1],
+                 ez = S.bounds_hi[2] - S.bounds_lo[2];
+    ie = make_double3(ex > 0 ? 1.0 / ex : 0.0, ey > 0 ? 1.0 / ey : 0.0, ez > 0 ? 1.0 / ez : 0.0);
+  }
+  Arena A(st);
+  uint64_t* keys = A.get<uint64_t>(nv);
+  uint64_t* keys2 = A.get<uint64_t>(nv);
+  int32_t* ids = A.get<int32_t>(nv);
+  if (!A.ok) return set_error(SBR_ERR_NOMEM, "vertex order scratch");
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, ids, order, (int)nv, 0, 63, st);
+  void* tmp = A.get<uint8_t>((int64_t)tb);
+  if (!A.ok) return set_error(SBR_ERR_NOMEM, "vertex order scratch");
+  k_vertex_morton<<<grid_for(nv, 256), 256, 0, st>>>(vb->point, nv, lo, ie, keys, ids);
+  LK("k_vertex_morton");
+  CK(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, ids, order, (int)nv, 0, 63, st));
+  count_launch();
+done:
+  return rc;
+}
+
 int sbr_cir_visibility(const SbrScene* scene, const SbrCirParams* P, const SbrVertexBuf* vb,
-                       int64_t v_begin, int64_t v_end, uint64_t* row_key, int32_t* row_vtx,
-                       int64_t row_cap, uint64_t* counters, void* stream) {
+                       int64_t v_begin, int64_t v_end, const int32_t* order, uint64_t* row_key,
+                       int32_t* row_vtx, int64_t row_cap, uint64_t* counters, void* stream) {
   int rc = check_cir(scene, P);
   if (rc) return rc;
   if (!scene || !vb) return set_error(SBR_ERR_INVALID, "NULL argument");
   if (v_end <= v_begin) return SBR_OK;
-  const int64_t pairs = (v_end - v_begin) * (int64_t)P->n_targets;
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* work = nullptr;
+  if (cudaMallocAsync(&work, sizeof(unsigned long long), st) != cudaSuccess)
+    return set_error(SBR_ERR_NOMEM, "work counter");
+  cudaMemsetAsync(work, 0, sizeof(unsigned long long), st);
+  int dev = 0, sms = 148, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cir_visibility, 128, 0);
+  if (per_sm < 1) per_sm = 1;
   prof_begin(stream, "k_cir_visibility");
-  k_cir_visibility<<<grid_for(pairs, 128, 148 * 64), 128, 0, (cudaStream_t)stream>>>(
-      dev_view(scene), *P, *vb, v_begin, v_end, row_key, row_vtx, row_cap,
-      (unsigned long long*)counters);
+  k_cir_visibility<<<sms * per_sm, 128, 0, st>>>(dev_view(scene), *P, *vb, v_begin, v_end,
+                                                 row_key, row_vtx, row_cap,
+                                                 (unsigned long long*)counters, work, order);
   prof_end(stream);
-  return launch_status("k_cir_visibility");
+  rc = launch_status("k_cir_visibility");
+  cudaFreeAsync(work, st);
+  return rc;
 }
 
 int sbr_cir_select(const SbrCirParams* P, const SbrVertexBuf* vb, const uint64_t* row_key,

@@ -59,6 +59,7 @@ struct DevScene {
   int32_t nnodes;
   int32_t nmat;
   float pad_base;              // conservative box padding: 2^-20 * (max|coord| + 1)
+  double bounds_lo[3], bounds_hi[3];  // scene AABB (float64)
 };
 
 constexpr int kStackSize = 64;
@@ -611,6 +612,90 @@ struct ClosestTrav {
     h.t = best >= 0 ? best_t : __longlong_as_double(0x7ff0000000000000LL);
     h.u = best >= 0 ? bu : 0.0;
     h.v = best >= 0 ? bv : 0.0;
+  }
+};
+
+// Resumable per-lane any-hit traversal (occlusion), while-while with parked
+// leaves like ClosestTrav; stops at the first triangle with t_min < t < limit.
+struct AnyTrav {
+  Ray64 r;
+  RayBox rb;
+  double t_min, limit;
+  float bound;
+  int stack_node[kStackSize];
+  int sp, node, leaf;
+  bool ok, found;
+
+  __device__ __forceinline__ void start(const DevScene& S, double3 o, double3 d, double tmin,
+                                        double lim) {
+    r = ray_setup(o, d);
+    rb = box_setup(o, d, S.pad_base);
+    t_min = tmin;
+    limit = lim;
+    bound = bound_up(lim);
+    sp = 0;
+    node = 0;
+    leaf = 0;
+    ok = true;
+    found = false;
+  }
+  __device__ __forceinline__ void idle() {
+    node = kDone;
+    leaf = 0;
+  }
+  __device__ __forceinline__ bool done() const { return node == kDone && leaf == 0; }
+  __device__ __forceinline__ int pop() { return sp > 0 ? stack_node[--sp] : kDone; }
+
+  __device__ __forceinline__ void round(const DevScene& S) {
+    while (node >= 0) {
+      const BvhNode* nd = S.nodes + node;
+      const float4 a = __ldg(&nd->a), b = __ldg(&nd->b), c = __ldg(&nd->c);
+      const int4 ch = __ldg(&nd->d);
+      const float tl = box_enter(rb, a.x, a.y, a.z, a.w, c.x, c.y, bound);
+      const float tr = box_enter(rb, b.x, b.y, b.z, b.w, c.z, c.w, bound);
+      const bool hl = tl < __int_as_float(0x7f800000);
+      const bool hr = tr < __int_as_float(0x7f800000);
+      if (hl && hr) {
+        if (sp >= kStackSize) {
+          ok = false;
+          node = kDone;
+          leaf = 0;
+          return;
+        }
+        const bool lfirst = tl <= tr;
+        stack_node[sp++] = lfirst ? ch.y : ch.x;
+        node = lfirst ? ch.x : ch.y;
+      } else if (hl) {
+        node = ch.x;
+      } else if (hr) {
+        node = ch.y;
+      } else {
+        node = pop();
+      }
+      if (node < 0 && node != kDone && leaf == 0) {
+        leaf = node;
+        node = pop();
+      }
+      if (!__any_sync(__activemask(), leaf == 0)) break;
+    }
+    while (leaf < 0) {
+      const int s = leaf_start(leaf), n = leaf_count(leaf);
+      for (int j = s; j < s + n; ++j) {
+        double t, u, v;
+        if (tri_hit_idx(r, S.tris + j, t_min, t, u, v) && t < limit) {
+          found = true;
+          node = kDone;
+          leaf = 0;
+          return;
+        }
+      }
+      leaf = 0;
+      if (node < 0 && node != kDone) {
+        leaf = node;
+        node = pop();
+      }
+      if (!__any_sync(__activemask(), leaf < 0)) break;
+    }
   }
 };
 

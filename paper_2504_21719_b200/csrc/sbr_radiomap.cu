@@ -412,18 +412,6 @@ struct Wave {
 };
 
 int wave_alloc(int64_t cap, cudaStream_t st, Wave* w) {
-  static bool pool_tuned[16] = {false};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!pool_tuned[dev & 15]) {
-    // keep freed queue memory in the pool between calls (no re-mapping cost)
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = ~0ULL;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    pool_tuned[dev & 15] = true;
-  }
   const size_t per_queue = (size_t)cap * (16 * sizeof(double));
   const size_t bytes = 2 * per_queue + (size_t)cap * (sizeof(double) + sizeof(int32_t)) + 512;
   if (cudaMallocAsync(&w->block, bytes, st) != cudaSuccess)

@@ -101,6 +101,7 @@ struct SbrScene {
   int32_t nmat = 0;
   unsigned int* error_word = nullptr;
   float pad_base = 0.f;
+  double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
   std::vector<int64_t> perm;
 };
 
@@ -121,6 +122,10 @@ DevScene dev_view(const SbrScene* s) {
   d.nnodes = s->nnodes;
   d.nmat = s->nmat;
   d.pad_base = s->pad_base;
+  for (int k = 0; k < 3; ++k) {
+    d.bounds_lo[k] = s->lo[k];
+    d.bounds_hi[k] = s->hi[k];
+  }
   return d;
 }
 
@@ -388,6 +393,15 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
   if (ntri <= 0) return set_error(SBR_ERR_EMPTY_SCENE, "no triangles");
   if (ntri >= (1LL << 29)) return set_error(SBR_ERR_INVALID, "too many triangles");
   SBR_CUDA(cudaSetDevice(device));
+  {
+    // the library's stream-ordered scratch (ray queues, sort buffers) comes
+    // from the device's default pool: keep freed blocks mapped between calls
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = ~0ULL;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   cudaStream_t st = (cudaStream_t)stream;
   const int n = (int)ntri;
   SbrScene* S = new SbrScene();
@@ -395,10 +409,17 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
   S->ntri = ntri;
 
   double max_abs = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    S->lo[k] = v0[k];
+    S->hi[k] = v0[k];
+  }
   for (int64_t i = 0; i < 3 * ntri; ++i) {
     max_abs = fmax(max_abs, fabs(v0[i]));
     max_abs = fmax(max_abs, fabs(v1[i]));
     max_abs = fmax(max_abs, fabs(v2[i]));
+    const int k = (int)(i % 3);
+    S->lo[k] = fmin(S->lo[k], fmin(fmin(v0[i], v1[i]), v2[i]));
+    S->hi[k] = fmax(S->hi[k], fmax(fmax(v0[i], v1[i]), v2[i]));
   }
   S->pad_base = (float)(ldexp(max_abs + 1.0, -20));
 

@@ -532,6 +532,7 @@ typedef struct {
   const int32_t* matrow;          /* slot order */
   const SbrMaterial* mats;
   int32_t nmat;
+  const uint64_t *hash_r, *hash_f; /* slot order plane hashes (paths.py:449-450) */
 } OrcScene;
 
 typedef struct {
@@ -961,4 +962,571 @@ ORC_EXPORT int orc_radiomap_direct(const OrcScene* S, const SbrMapParams* P, con
       if (val > 0.0) counters[SBR_MC_DIRECT_VISIBLE]++;
     }
   return 0;
+}
+
+/* ========================================================================= */
+/* Path solver (CIR): generate_candidates / refine_candidate /               */
+/* compute_path_fields / frequency_response, restated from paths.py          */
+/* ========================================================================= */
+/* Sequential restatement at workers=1: one chunk holding every sample, the
+ * depth loop of _sweep_chunk (paths.py:704-828) over all live samples, rows
+ * emitted in (depth, sample, target) order (_emit_records 903-987) with the
+ * in-chunk "seen pairs" dedup and per-depth truncation, then the ordered
+ * DedupTable / PathBuffer registration of generate_candidates (1019-1103).
+ * Diffraction is out of scope (no wedges): D is never allowed. */
+
+#define TAG_INTERACTION 0x5c798e00ad8012ebULL
+#define TAG_RESPAWN 0x742c480a24ff9b7fULL
+#define FNV_OFFSET 0xCBF29CE484222325ULL
+#define FNV_PRIME 0x100000001B3ULL
+
+typedef struct {
+  double source[3];
+  const double* targets;   /* (nt, 3) */
+  int32_t nt;
+  int32_t max_depth;
+  int32_t allow;           /* R=1 S=2 T=4 */
+  int32_t pad_;
+  double q_d;
+  uint64_t num_samples, seed;
+  uint64_t n_hash;
+  int64_t n_buffer;
+} OrcCirParams;
+
+/* records, caller-allocated with capacity n_buffer (step arrays stride L) */
+typedef struct {
+  int32_t* target;
+  int64_t* sample;
+  int32_t* depth;
+  int32_t* suffix_start;
+  uint8_t* diffuse;
+  uint64_t* chain_hash;
+  double* prefix_prob;
+  double* anchor;          /* (n,3) */
+  int8_t* kind;            /* (n,L) */
+  int32_t* tri;            /* (n,L) slot */
+  double* vertex;          /* (n,L,3) */
+  double* normal;          /* (n,L,3) */
+  int32_t L;
+} OrcRecords;
+
+enum { OC_ESCAPED = 0, OC_TERMINATED, OC_RB, OC_VIS, OC_ROWS, OC_DUP, OC_TRUNC, OC_OVERFLOW,
+       OC_CAND, OC_REG, OC_SLOTS, OC_COUNT };
+
+static uint64_t fnv1a_u64(uint64_t v, uint64_t h) {
+  for (int s = 0; s < 64; s += 8) h = (h ^ ((v >> s) & 0xFFULL)) * FNV_PRIME;
+  return h;
+}
+
+/* per (sample, depth) state after the interaction at that depth */
+typedef struct {
+  double vertex[3], normal[3];
+  double run_prob;
+  uint64_t hr, hf;
+  int32_t tri;
+  int8_t code;             /* -1: no interaction at this depth (dead) */
+  int8_t suffix_start;
+} Hist;
+
+/* open-addressing set of (pr, pf) pairs */
+typedef struct { uint64_t* k; uint8_t* used; uint64_t cap, n; } PairSet;
+static int pairset_insert(PairSet* s, uint64_t a, uint64_t b) {
+  if (2 * (s->n + 1) > s->cap) {
+    uint64_t nc = s->cap ? 2 * s->cap : 1024;
+    uint64_t* nk = (uint64_t*)calloc(2 * nc, sizeof(uint64_t));
+    uint8_t* nu = (uint8_t*)calloc(nc, 1);
+    for (uint64_t i = 0; i < s->cap; ++i)
+      if (s->used[i]) {
+        uint64_t h = (s->k[2 * i] * 0x9E3779B97F4A7C15ULL ^ s->k[2 * i + 1]) % nc;
+        while (nu[h]) h = (h + 1) % nc;
+        nu[h] = 1; nk[2 * h] = s->k[2 * i]; nk[2 * h + 1] = s->k[2 * i + 1];
+      }
+    free(s->k); free(s->used);
+    s->k = nk; s->used = nu; s->cap = nc;
+  }
+  uint64_t h = (a * 0x9E3779B97F4A7C15ULL ^ b) % s->cap;
+  while (s->used[h]) {
+    if (s->k[2 * h] == a && s->k[2 * h + 1] == b) return 0;
+    h = (h + 1) % s->cap;
+  }
+  s->used[h] = 1; s->k[2 * h] = a; s->k[2 * h + 1] = b; s->n++;
+  return 1;
+}
+
+typedef struct { int64_t g; int32_t depth, k; uint8_t chain, diffuse; uint64_t pr, pf; } Row;
+
+/* interaction probabilities (_interaction_rows paths.py:572-595) */
+static int interaction_q(const SbrMaterial* m, double cos_i, double q_d, int allow, double q[4]) {
+  Fresnel4 F = slab_fresnel(m, cos_i);
+  double r_sq = cabs2(F.rp) + cabs2(F.rl);
+  double t_sq = cabs2(F.tp) + cabs2(F.tl);
+  double den = r_sq + t_sq;
+  q[0] = q[1] = q[2] = 0.0;
+  q[3] = q_d;
+  if (den > 0.0) {
+    double keep = 1.0 - q_d, s_sq = m->scattering * m->scattering;
+    q[0] = keep * (1.0 - s_sq) * r_sq / den;
+    q[1] = keep * s_sq * r_sq / den;
+    q[2] = keep * t_sq / den;
+  }
+  for (int k = 0; k < 3; ++k) if (!(allow >> k & 1)) q[k] = 0.0;
+  q[3] = 0.0; /* no wedges */
+  double total = ((q[0] + q[1]) + q[2]) + q[3];
+  if (!(total > 0.0)) return 0;
+  for (int k = 0; k < 4; ++k) q[k] /= total;
+  return 1;
+}
+
+ORC_EXPORT int orc_cir_generate(const OrcScene* S, const OrcCirParams* P, OrcRecords* R,
+                                int64_t* n_out, uint64_t* counters) {
+  const int L = P->max_depth;
+  const uint64_t N = P->num_samples;
+  const int nt = P->nt;
+  Hist* H = (Hist*)malloc(sizeof(Hist) * (size_t)(N * (L > 0 ? L : 1)));
+  if (!H) return SBR_ERR_NOMEM;
+  for (uint64_t i = 0; i < N * (uint64_t)(L > 0 ? L : 1); ++i) H[i].code = -1;
+  /* ---- per-sample sweep (each sample's rows are independent of the others) */
+  for (uint64_t g = 0; g < N; ++g) {
+    double o[3] = {P->source[0], P->source[1], P->source[2]}, d[3];
+    orc_fibonacci(N, g, d);
+    uint64_t hr = 0, hf = 0;
+    double run_prob = 1.0;
+    int suffix = 0;
+    for (int depth = 1; depth <= L; ++depth) {
+      double t, u_, v_;
+      int64_t tri;
+      counters[OC_RB]++;
+      if (closest1(S, o, d, 1e-4, INFINITY, &t, &tri, &u_, &v_)) { free(H); return SBR_ERR_STACK; }
+      if (tri < 0) { counters[OC_ESCAPED]++; break; }
+      double pt[3] = {o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]};
+      const double* nr = S->normal + 3 * tri;
+      double n[3] = {nr[0], nr[1], nr[2]};
+      if (dot_seq(d, n) > 0.0) { n[0] = -n[0]; n[1] = -n[1]; n[2] = -n[2]; }
+      double cos_i = fabs(dot_seq(d, n));
+      double q[4];
+      if (!interaction_q(S->mats + S->matrow[tri], cos_i, P->q_d, P->allow, q)) {
+        counters[OC_TERMINATED]++;
+        break;
+      }
+      double uu = orc_philox_uniform(P->seed, 0, (uint64_t)depth, TAG_INTERACTION, g);
+      double cum = 0.0;
+      int code = 0;
+      for (int k = 0; k < 4; ++k) { cum = k ? cum + q[k] : q[k]; code += (uu >= cum); }
+      if (code > 3) code = 3;
+      run_prob *= q[code];
+      if (code == 0) {
+        hr = 1373ULL * hr + S->hash_r[tri];
+        hf = 1373ULL * hf + S->hash_f[tri];
+      } else if (code == 1) {
+        suffix = depth;
+      }
+      Hist* h = H + g * L + (depth - 1);
+      memcpy(h->vertex, pt, sizeof pt);
+      memcpy(h->normal, n, sizeof n);
+      h->run_prob = run_prob; h->hr = hr; h->hf = hf; h->tri = (int32_t)tri;
+      h->code = (int8_t)code; h->suffix_start = (int8_t)suffix;
+      if (depth == L) break;
+      /* _continue_rays (paths.py:855-900) */
+      if (code == 0) {
+        double dn = dot_seq(d, n);
+        for (int k = 0; k < 3; ++k) d[k] = d[k] - 2.0 * dn * n[k];
+      } else if (code == 1) {
+        double u0 = orc_philox_uniform(P->seed, 0, (uint64_t)depth, TAG_RESPAWN, 2 * g);
+        double u1 = orc_philox_uniform(P->seed, 0, (uint64_t)depth, TAG_RESPAWN, 2 * g + 1);
+        double cos_t = u0, azim = TWO_PI * u1;
+        double x = 1.0 - cos_t * cos_t, sin_t = sqrt(x > 0.0 ? x : 0.0);
+        double t1[3], t2[3];
+        perp_batch(n, t1);
+        cross3(n, t1, t2);
+        double a = sin_t * cos(azim), b = sin_t * sin(azim);
+        for (int k = 0; k < 3; ++k) d[k] = (a * t1[k] + b * t2[k]) + cos_t * n[k];
+      }
+      memcpy(o, pt, sizeof pt);
+    }
+  }
+  /* ---- rows in (depth, sample, target) order with in-chunk dedup + truncation */
+  PairSet seen = {0, 0, 0, 0};
+  Row* rows = NULL;
+  int64_t nrows = 0, cap_rows = 0, emitted = 0;
+  for (int depth = 1; depth <= L; ++depth) {
+    int64_t depth_rows = 0, room = P->n_buffer - emitted;
+    int64_t first_row = nrows;
+    for (uint64_t g = 0; g < N; ++g) {
+      const Hist* h = H + g * L + (depth - 1);
+      if (h->code < 0) continue;
+      for (int k = 0; k < nt; ++k) {
+        const double* tg = P->targets + 3 * k;
+        double diff[3] = {tg[0] - h->vertex[0], tg[1] - h->vertex[1], tg[2] - h->vertex[2]};
+        double side = dot_seq(diff, h->normal);
+        int ok = h->code == 2 ? side < 0.0 : side > 0.0;
+        if (!ok) continue;
+        counters[OC_VIS]++;
+        int occ;
+        if (occluded1(S, h->vertex, tg, 1e-4, &occ)) { free(H); free(rows); return SBR_ERR_STACK; }
+        if (occ) continue;
+        counters[OC_ROWS]++;
+        Row r;
+        r.g = (int64_t)g; r.depth = depth; r.k = k;
+        r.diffuse = h->code == 1;
+        r.chain = h->suffix_start == 0 && h->code != 1;
+        r.pr = fnv1a_u64(h->hr, (uint64_t)k);
+        r.pf = fnv1a_u64(h->hf, (uint64_t)k);
+        if (r.chain && !pairset_insert(&seen, r.pr, r.pf)) { counters[OC_DUP]++; continue; }
+        if (nrows == cap_rows) {
+          cap_rows = cap_rows ? 2 * cap_rows : 4096;
+          rows = (Row*)realloc(rows, sizeof(Row) * (size_t)cap_rows);
+        }
+        rows[nrows++] = r;
+        depth_rows++;
+      }
+    }
+    /* truncation to room (an all-cut depth returns no batch: uncounted) */
+    if (room < 0) room = 0;
+    if (depth_rows > room) {
+      if (room > 0) counters[OC_TRUNC] += (uint64_t)(depth_rows - room);
+      nrows = first_row + room;
+    }
+    emitted += nrows - first_row;
+  }
+  free(seen.k); free(seen.used);
+  /* ---- registration (DedupTable) + PathBuffer */
+  int32_t* counts = (int32_t*)calloc((size_t)P->n_hash, sizeof(int32_t));
+  int64_t nrec = 0;
+  const int Ls = R->L;
+  /* LoS records first (generate_candidates 1036-1049) */
+  for (int k = 0; k < nt; ++k) {
+    int occ;
+    if (occluded1(S, P->source, P->targets + 3 * k, 1e-4, &occ)) { free(H); free(rows); free(counts); return SBR_ERR_STACK; }
+    if (occ) continue;
+    uint64_t key = fnv1a_u64(0ULL, (uint64_t)k);
+    uint64_t i1 = key % P->n_hash;
+    if (counts[i1] == 0 && counts[i1] == 0) {
+      counts[i1] += 2;
+      counters[OC_REG]++;
+    } else {
+      counters[OC_DUP]++;
+      continue;
+    }
+    if (nrec >= P->n_buffer) { counters[OC_OVERFLOW]++; continue; }
+    R->target[nrec] = k; R->sample[nrec] = -1; R->depth[nrec] = 0; R->suffix_start[nrec] = 0;
+    R->diffuse[nrec] = 0; R->chain_hash[nrec] = 0; R->prefix_prob[nrec] = 1.0;
+    memcpy(R->anchor + 3 * nrec, P->source, 3 * sizeof(double));
+    for (int j = 0; j < Ls; ++j) { R->kind[nrec * Ls + j] = -1; R->tri[nrec * Ls + j] = -1; }
+    nrec++;
+  }
+  for (int64_t i = 0; i < nrows; ++i) {
+    const Row* r = rows + i;
+    if (r->chain) {
+      uint64_t i1 = r->pr % P->n_hash, i2 = r->pf % P->n_hash;
+      if (counts[i1] == 0 && counts[i2] == 0) {
+        counts[i1]++; counts[i2]++;
+        counters[OC_REG]++;
+      } else {
+        counters[OC_DUP]++;
+        continue;
+      }
+    }
+    if (nrec >= P->n_buffer) { counters[OC_OVERFLOW]++; continue; }
+    const Hist* last = H + r->g * L + (r->depth - 1);
+    R->target[nrec] = r->k; R->sample[nrec] = r->g; R->depth[nrec] = r->depth;
+    R->suffix_start[nrec] = last->suffix_start; R->diffuse[nrec] = r->diffuse;
+    R->chain_hash[nrec] = last->hr;
+    R->prefix_prob[nrec] = 1.0;
+    memcpy(R->anchor + 3 * nrec, P->source, 3 * sizeof(double));
+    if (last->suffix_start > 0) {
+      const Hist* a = H + r->g * L + (last->suffix_start - 1);
+      R->prefix_prob[nrec] = a->run_prob;
+      memcpy(R->anchor + 3 * nrec, a->vertex, 3 * sizeof(double));
+    }
+    for (int j = 0; j < Ls; ++j) {
+      int64_t o = nrec * Ls + j;
+      if (j < r->depth) {
+        const Hist* h = H + r->g * L + j;
+        R->kind[o] = h->code; R->tri[o] = h->tri;
+        memcpy(R->vertex + 3 * o, h->vertex, 3 * sizeof(double));
+        memcpy(R->normal + 3 * o, h->normal, 3 * sizeof(double));
+      } else {
+        R->kind[o] = -1; R->tri[o] = -1;
+      }
+    }
+    nrec++;
+  }
+  for (uint64_t i = 0; i < P->n_hash; ++i) counters[OC_SLOTS] += counts[i] != 0;
+  counters[OC_CAND] += (uint64_t)nrec;
+  *n_out = nrec;
+  free(H); free(rows); free(counts);
+  return 0;
+}
+
+/* refine_candidate (paths.py:1123-1252), diffraction branch out of scope.
+ * pv (n, L+2, 3) = [source, vertices..., target]; status SBR_REFINE_*. */
+static void reflect_point(const double* p, const double* nrm, const double* on, double* out) {
+  double rel[3] = {p[0] - on[0], p[1] - on[1], p[2] - on[2]};
+  double f = dot_ddot(rel, nrm);
+  for (int k = 0; k < 3; ++k) out[k] = p[k] - 2.0 * f * nrm[k];
+}
+
+ORC_EXPORT int orc_cir_refine(const OrcScene* S, const double* source, const double* targets,
+                              const OrcRecords* R, int64_t n, double* pv, int32_t* status) {
+  const int L = R->L;
+  for (int64_t r = 0; r < n; ++r) {
+    const int depth = R->depth[r], ss = R->suffix_start[r];
+    const double* tg = targets + 3 * R->target[r];
+    double* out = pv + r * (int64_t)(L + 2) * 3;
+    memset(out, 0, sizeof(double) * 3 * (size_t)(L + 2));
+    memcpy(out, source, 3 * sizeof(double));
+    for (int j = 0; j < depth; ++j) memcpy(out + 3 * (j + 1), R->vertex + 3 * (r * L + j), 3 * sizeof(double));
+    memcpy(out + 3 * (depth + 1), tg, 3 * sizeof(double));
+    status[r] = SBR_REFINE_OK;
+    if (R->diffuse[r] || ss >= depth) continue;
+    const int ns = depth - ss;
+    double img[17][3];
+    memcpy(img[0], R->anchor + 3 * r, 3 * sizeof(double));
+    for (int j = 0; j < ns; ++j) {
+      int64_t o = r * L + ss + j;
+      if (R->kind[o] == 0) reflect_point(img[j], R->normal + 3 * o, R->vertex + 3 * o, img[j + 1]);
+      else memcpy(img[j + 1], img[j], sizeof img[j]);
+    }
+    double from[3], refined0[3];
+    memcpy(from, tg, sizeof from);
+    int st = SBR_REFINE_OK;
+    for (int j = ns - 1; j >= 0; --j) {
+      int64_t o = r * L + ss + j;
+      double ray[3] = {img[j + 1][0] - from[0], img[j + 1][1] - from[1], img[j + 1][2] - from[2]};
+      double len = sqrt(dot_ddot(ray, ray));
+      if (len < 1e-12) { st = SBR_REFINE_DEGENERATE; break; }
+      for (int k = 0; k < 3; ++k) ray[k] = ray[k] / len;
+      double t, u_, v_;
+      int64_t tri;
+      if (closest1(S, from, ray, 1e-4, INFINITY, &t, &tri, &u_, &v_)) return SBR_ERR_STACK;
+      if (tri < 0) { st = SBR_REFINE_COPLANAR_MISS; break; }
+      const double* sn = R->normal + 3 * o;
+      double hp[3] = {from[0] + t * ray[0], from[1] + t * ray[1], from[2] + t * ray[2]};
+      double rel[3] = {hp[0] - R->vertex[3 * o], hp[1] - R->vertex[3 * o + 1], hp[2] - R->vertex[3 * o + 2]};
+      if (fabs(dot_ddot(S->normal + 3 * tri, sn)) < 1.0 - 1e-6 || !(fabs(dot_ddot(rel, sn)) <= 1e-6)) {
+        st = SBR_REFINE_COPLANAR_MISS;
+        break;
+      }
+      memcpy(out + 3 * (ss + j + 1), hp, sizeof hp);
+      memcpy(from, hp, sizeof hp);
+      memcpy(refined0, hp, sizeof hp);
+    }
+    if (st == SBR_REFINE_OK) {
+      int occ;
+      if (occluded1(S, R->anchor + 3 * r, refined0, 1e-4, &occ)) return SBR_ERR_STACK;
+      if (occ) st = SBR_REFINE_OCCLUDED;
+    }
+    status[r] = st;
+  }
+  return 0;
+}
+
+/* ---- compute_path_fields (paths.py:1302-1399), Algorithm 2 ---------------- */
+typedef struct {
+  double wavelength, q_d;
+  uint64_t num_samples, seed;
+  int32_t allow;
+  int32_t pad_;
+  SbrAntenna tx;
+  const SbrAntenna* rx;          /* per target */
+  double tx_vel[3];
+  const double* rx_vel;          /* per target (n,3) */
+  const double* obj_vel;         /* per material row (nobj,3) or NULL */
+} OrcFieldParams;
+
+/* pattern_to_gcs (em.py:198-219) for the built-in evaluators (c_phi_l = 0) */
+static void pattern_gcs(const SbrAntenna* A, const double* d, double* c_th, double* c_ph,
+                        double th_g[3], double ph_g[3]) {
+  const double* R = A->rot;
+  double dl[3];
+  for (int k = 0; k < 3; ++k) dl[k] = R[0 * 3 + k] * d[0] + R[1 * 3 + k] * d[1] + R[2 * 3 + k] * d[2];
+  double z = dl[2] < -1.0 ? -1.0 : (dl[2] > 1.0 ? 1.0 : dl[2]);
+  double theta_l = acos(z), phi_l = atan2(dl[1], dl[0]);
+  double amp = A->kind == SBR_PATTERN_TR38901 ? tr38901_amp(A->scale, theta_l, phi_l) : 1.0;
+  transverse(d, th_g, ph_g);
+  double th_l[3] = {cos(theta_l) * cos(phi_l), cos(theta_l) * sin(phi_l), -sin(theta_l)};
+  double thw[3];
+  for (int k = 0; k < 3; ++k) thw[k] = R[3 * k] * th_l[0] + R[3 * k + 1] * th_l[1] + R[3 * k + 2] * th_l[2];
+  *c_th = dot_ddot(th_g, thw) * amp;
+  *c_ph = dot_ddot(ph_g, thw) * amp;
+}
+
+static void basis_w(const double* a, const double* b, const double* q, const double* r, cpx c0,
+                    cpx c1, cpx* o0, cpx* o1) {
+  double w00 = dot_ddot(a, q), w01 = dot_ddot(a, r), w10 = dot_ddot(b, q), w11 = dot_ddot(b, r);
+  *o0 = cadd(cscale(w00, c0), cscale(w01, c1));
+  *o1 = cadd(cscale(w10, c0), cscale(w11, c1));
+}
+
+ORC_EXPORT int orc_cir_fields(const OrcScene* S, const OrcFieldParams* P, const OrcRecords* R,
+                              const double* pv, const int32_t* status, int64_t n, double* gain,
+                              double* delay, double* doppler, double* dep, double* arr) {
+  const int L = R->L;
+  const double lam = P->wavelength;
+  for (int64_t r = 0; r < n; ++r) {
+    if (status[r] != SBR_REFINE_OK) continue;
+    const int depth = R->depth[r], tgt = R->target[r];
+    const double* V = pv + r * (int64_t)(L + 2) * 3;
+    double seg[17], kh[17][3], total = 0.0;
+    for (int i = 0; i <= depth; ++i) {
+      double s3[3] = {V[3 * (i + 1)] - V[3 * i], V[3 * (i + 1) + 1] - V[3 * i + 1], V[3 * (i + 1) + 2] - V[3 * i + 2]};
+      seg[i] = norm_seq(s3);
+      for (int k = 0; k < 3; ++k) kh[i][k] = s3[k] / seg[i];
+      total += seg[i];
+    }
+    double cth, cph, fa[3], fb[3];
+    pattern_gcs(&P->tx, kh[0], &cth, &cph, fa, fb);
+    cpx c0 = C(cth, 0.0), c1 = C(cph, 0.0);
+    double gamma_prob = 1.0, r_dist = 0.0, tube = FOUR_PI / (double)P->num_samples;
+    int n_phase = 0;
+    char tag[32];
+    int len = 0;
+    {
+      const char* pre = "phase-";
+      while (pre[len]) { tag[len] = pre[len]; ++len; }
+      char dg[12];
+      int nd = 0, v = depth;
+      do { dg[nd++] = (char)('0' + v % 10); v /= 10; } while (v > 0);
+      while (nd > 0) tag[len++] = dg[--nd];
+      tag[len] = 0;
+    }
+    const uint64_t ptag = orc_tag_hash(tag);
+    const uint64_t psample = R->sample[r] > 0 ? (uint64_t)R->sample[r] : 0ULL;
+    double nu = dot_ddot(P->tx_vel, kh[0]) / lam;
+    nu -= dot_ddot(P->rx_vel + 3 * tgt, kh[depth]) / lam;
+    for (int i = 0; i < depth; ++i) {
+      const int64_t o = r * L + i;
+      const int kind = R->kind[o], slot = R->tri[o];
+      const int row = S->matrow[slot];
+      const SbrMaterial* m = S->mats + row;
+      const double* k_in = kh[i];
+      const double* k_out = kh[i + 1];
+      r_dist += seg[i];
+      const double* nrm = R->normal + 3 * o;
+      double nh[3] = {nrm[0], nrm[1], nrm[2]};
+      if (dot_ddot(k_in, nh) > 0.0) { nh[0] = -nh[0]; nh[1] = -nh[1]; nh[2] = -nh[2]; }
+      double q[4];
+      interaction_q(m, fabs(dot_ddot(k_in, nrm)), P->q_d, P->allow, q);
+      gamma_prob *= q[kind];
+      if (P->obj_vel) {
+        const double* v = P->obj_vel + 3 * row;
+        if (v[0] != 0.0 || v[1] != 0.0 || v[2] != 0.0) {
+          double dk[3] = {k_out[0] - k_in[0], k_out[1] - k_in[1], k_out[2] - k_in[2]};
+          nu += dot_ddot(v, dk) / lam;
+        }
+      }
+      double ep[3], el[3];
+      incidence_frame(k_in, nh, ep, el);
+      double cos_t = fabs(dot_ddot(k_in, nh));
+      Fresnel4 F = slab_fresnel(m, cos_t);
+      if (kind == 0 || kind == 2) {
+        cpx p0, p1;
+        basis_w(ep, el, fa, fb, c0, c1, &p0, &p1);
+        double na[3], nb[3], kk[3];
+        if (kind == 0) {
+          double dn = dot_ddot(k_in, nh);
+          for (int k = 0; k < 3; ++k) kk[k] = k_in[k] - 2.0 * dn * nh[k];
+          double erp[3];
+          cross3(ep, kk, erp);
+          c0 = cscale(m->spec_amp, cmul(F.rp, p0));
+          c1 = cscale(m->spec_amp, cmul(F.rl, p1));
+          memcpy(na, ep, sizeof na); memcpy(nb, erp, sizeof nb);
+        } else {
+          memcpy(kk, k_in, sizeof kk);
+          c0 = cmul(F.tp, p0);
+          c1 = cmul(F.tl, p1);
+          memcpy(na, ep, sizeof na); memcpy(nb, el, sizeof nb);
+        }
+        double cr[3];
+        cross3(na, nb, cr);
+        if (dot_ddot(cr, kk) < 0.0) { /* _right_handed (paths.py:1259-1273) */
+          cpx t = c0; c0 = c1; c1 = t;
+          memcpy(fa, nb, sizeof fa); memcpy(fb, na, sizeof fb);
+        } else {
+          memcpy(fa, na, sizeof fa); memcpy(fb, nb, sizeof fb);
+        }
+      } else {
+        cpx p0, p1;
+        basis_w(ep, el, fa, fb, c0, c1, &p0, &p1);
+        double norm_in = sqrt(cabs2(p0) + cabs2(p1));
+        double gam = norm_in == 0.0 ? 0.0 : sqrt(cabs2(cmul(F.rp, p0)) + cabs2(cmul(F.rl, p1))) / norm_in;
+        double ci = -dot_ddot(k_in, nh);
+        double patch = tube * (r_dist * r_dist) / (ci > 1e-12 ? ci : 1e-12);
+        ci = ci < 0.0 ? 0.0 : (ci > 1.0 ? 1.0 : ci);
+        double f_s = pattern_density(m, k_in, k_out, nh);
+        double amp = m->scattering * gam * sqrt(f_s * ci * patch);
+        double chi1 = 0.0, chi2 = 0.0;
+        if (m->random_phases) {
+          chi1 = TWO_PI * orc_philox_uniform(P->seed, psample, (uint64_t)tgt, ptag, 2 * n_phase);
+          chi2 = TWO_PI * orc_philox_uniform(P->seed, psample, (uint64_t)tgt, ptag, 2 * n_phase + 1);
+          ++n_phase;
+        }
+        double sq = sqrt(1.0 - m->xpd_kx), sk = sqrt(m->xpd_kx);
+        double thi[3], phi_[3], ths[3], phs[3];
+        transverse(k_in, thi, phi_);
+        transverse(k_out, ths, phs);
+        cpx q0, q1;
+        basis_w(thi, phi_, fa, fb, c0, c1, &q0, &q1);
+        cpx e1 = C(cos(chi1), sin(chi1)), e2 = C(cos(chi2), sin(chi2));
+        cpx o0 = cscale(amp, cadd(cmul(cscale(sq, e1), q0), cmul(cscale(-sk, e1), q1)));
+        cpx o1 = cscale(amp, cadd(cmul(cscale(sk, e2), q0), cmul(cscale(sq, e2), q1)));
+        double inv = 1.0 / sqrt(gamma_prob);
+        c0 = C(o0.re / r_dist * inv, o0.im / r_dist * inv);
+        c1 = C(o1.re / r_dist * inv, o1.im / r_dist * inv);
+        memcpy(fa, ths, sizeof fa); memcpy(fb, phs, sizeof fb);
+        gamma_prob = 1.0;
+        r_dist = 0.0;
+        tube = TWO_PI;
+      }
+    }
+    r_dist += seg[depth];
+    double na[3] = {-kh[depth][0], -kh[depth][1], -kh[depth][2]};
+    double rc0, rc1, rth[3], rph[3];
+    pattern_gcs(P->rx + tgt, na, &rc0, &rc1, rth, rph);
+    cpx acc = C(0.0, 0.0);
+    for (int k = 0; k < 3; ++k) {
+      cpx e = cadd(cscale(fa[k], c0), cscale(fb[k], c1));
+      double rv = rc0 * rth[k] + rc1 * rph[k];
+      acc = cadd(acc, cscale(rv, e));
+    }
+    double sc = lam / FOUR_PI / r_dist;
+    gain[2 * r] = acc.re * sc;
+    gain[2 * r + 1] = acc.im * sc;
+    delay[r] = total / 299792458.0;
+    doppler[r] = nu;
+    memcpy(dep + 3 * r, kh[0], 3 * sizeof(double));
+    memcpy(arr + 3 * r, kh[depth], 3 * sizeof(double));
+  }
+  return 0;
+}
+
+/* frequency_response (paths.py:1519-1547), path order accumulation */
+ORC_EXPORT void orc_cfr(const double* gain, const double* delay, const double* dep,
+                        const double* arr, const int32_t* prx, const int32_t* ptx, int64_t np,
+                        const double* freqs, int32_t nf, const double* txo, int32_t ntx,
+                        const double* rxo, int32_t nrx, double wavelength, int32_t synthetic,
+                        double* H) {
+  memset(H, 0, sizeof(double) * 2 * (size_t)nrx * ntx * nf);
+  const double kw = TWO_PI / wavelength;
+  for (int64_t p = 0; p < np; ++p) {
+    cpx a = C(gain[2 * p], gain[2 * p + 1]);
+    for (int r = 0; r < nrx; ++r)
+      for (int t = 0; t < ntx; ++t) {
+        cpx v = a;
+        if (synthetic) {
+          double nk[3] = {-arr[3 * p], -arr[3 * p + 1], -arr[3 * p + 2]};
+          double pr = kw * dot_gemv(rxo + 3 * r, nk), pt = kw * dot_gemv(txo + 3 * t, dep + 3 * p);
+          v = cmul(cmul(v, C(cos(pr), sin(pr))), C(cos(pt), sin(pt)));
+        } else if (prx[p] != r || ptx[p] != t) {
+          continue;
+        }
+        for (int f = 0; f < nf; ++f) {
+          double ang = -TWO_PI * freqs[f] * delay[p];
+          cpx w = cmul(v, C(cos(ang), sin(ang)));
+          double* h = H + 2 * (((int64_t)r * ntx + t) * nf + f);
+          h[0] += w.re;
+          h[1] += w.im;
+        }
+      }
+  }
 }

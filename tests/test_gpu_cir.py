@@ -180,3 +180,38 @@ def test_diffraction_is_rejected_loudly(cuda):
     cfg = PathConfig(num_samples=100, max_depth=1, q_diffraction=0.2)
     with pytest.raises(NotImplementedError):
         compute_paths(scene, txs, rxs, cfg)
+
+
+@pytest.mark.parametrize("samples,kinds", [(100_000, "R"), (50_000, "RS")])
+def test_canyon_paths_vs_oracle(cuda, samples, kinds):
+    """Beyond the golden fixtures: 64 street receivers in the config-2 canyon vs the oracle."""
+    import oracle
+    from cir_cases import _canyon_targets
+    from paper_2504_21719_b200 import scenes
+    meshes = scenes.street_canyon()
+    mats = scenes.uniform_materials(meshes, scenes.concrete(scattering=0.2))
+    rx = [RadioDevice(position=np.array(d["pos"])) for d in _canyon_targets(64, seed=9)]
+    tx = RadioDevice(position=np.array([0.0, 5.0, 20.0]))
+    cfg = PathConfig(num_samples=samples, max_depth=4, q_diffraction=0.0, seed=3,
+                     enabled=frozenset(KINDS[k] for k in kinds))
+    want, wdiag = oracle.OracleScene(meshes, mats).compute_paths([tx], rx, cfg)
+    ps = compute_paths(SceneModel(meshes, mats), [tx], rx, cfg)
+    T = ps.tensors
+    for k, v in wdiag.items():
+        if k == "refinement_rejections":
+            assert ps.diagnostics[k] == v
+        elif k == "hash_load_factor":
+            assert ps.diagnostics[k] == pytest.approx(v, rel=1e-12)
+        else:
+            assert ps.diagnostics.get(k, 0) == v, k
+    assert len(T) == len(want["delay"])
+    for k in ("rx", "depth", "sample"):
+        assert np.array_equal(getattr(T, k), want[k]), k
+    assert np.array_equal(T.chain_hash.astype(np.uint64), want["chain_hash"].astype(np.uint64))
+    L = want["kind"].shape[1]
+    kind = np.where(np.arange(T.kind.shape[1])[None, :] < T.depth[:, None], T.kind, -1)[:, :L]
+    assert np.array_equal(kind, want["kind"])
+    assert np.array_equal(np.where(kind >= 0, T.obj[:, :L], -1), want["obj"])
+    np.testing.assert_allclose(T.delay, want["delay"], rtol=1e-12)
+    rel = np.abs(T.gain - want["gain"]) / np.maximum(np.abs(want["gain"]), 1e-300)
+    assert rel.max(initial=0.0) < 1e-6, rel.max()

@@ -43,6 +43,7 @@ METRIC = "radio-map SBR ray-bounces/sec"
 UNIT = "ray-bounces/s"
 SAMPLES_PER_GPU = 10_000_000
 CIR_SAMPLES = 1_000_000
+CIR_CPU_SAMPLES = 2_000
 BYTES_PER_RB = 176  # 64 B ray state in + 64 B out + 48 B hit triangle
 TX = (0.0, 5.0, 20.0)
 
@@ -431,12 +432,27 @@ def bench_cir(args, dev):
     split = {k: _native.profile_kernel_ms(k)[0] / n for k in ("k_cir_sweep", "k_cir_visibility")}
     _native.profile_enable(False)
     d = ps.diagnostics
+    cpu = None
+    if not args.no_cpu_baseline:
+        # oracle port (oracle/sbr_oracle.c, single thread like the reference's
+        # default workers=1) on a bounded sample, extrapolated linearly in N_S
+        import oracle
+        osc = oracle.OracleScene(meshes, scenes.uniform_materials(meshes, scenes.concrete()))
+        small = PathConfig(num_samples=CIR_CPU_SAMPLES, max_depth=5, q_diffraction=0.0,
+                           enabled=frozenset({Interaction.REFLECTION}), buffer_capacity=2 ** 24)
+        t0 = time.perf_counter()
+        osc.compute_paths([tx], rxs, small)
+        dt = time.perf_counter() - t0
+        cpu = {"value": dt * 1e3 * (CIR_SAMPLES / CIR_CPU_SAMPLES), "unit": "ms per Tx-Rx set",
+               "cores": 1, "kind": "port",
+               "sample": f"N_S={CIR_CPU_SAMPLES} of {CIR_SAMPLES} in {dt:.2f} s, "
+                         f"extrapolated linearly in N_S"}
     return {"workload": "config3: procedural city (483,200 tris) CIR, 1 Tx x 1024 Rx, "
                         "N_S=1e6, depth 5, {R}, hash dedup + image-method refine",
             "ms_per_solve": float(np.mean(times)), "solves": n, "paths": d["paths"],
             "candidates": d["candidates"], "duplicates": d["duplicates"],
             "refinement_rejections": d["refinement_rejections"],
-            "kernel_ms_per_solve": split, "scene_build_s": build_s,
+            "kernel_ms_per_solve": split, "scene_build_s": build_s, "cpu_baseline": cpu,
             "unit": "ms per Tx-Rx set (1 Tx x 1024 Rx)", "higher_is_better": False}
 
 

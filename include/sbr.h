@@ -305,19 +305,32 @@ int sbr_cir_visibility(const SbrScene* scene, const SbrCirParams* params,
                        const SbrVertexBuf* vb, int64_t v_begin, int64_t v_end,
                        const int32_t* order_dev, uint64_t* row_key_dev, int32_t* row_vtx_dev,
                        int64_t row_capacity, uint64_t* counters_dev, void* stream);
+/* Per-row dedup keys (_emit_records paths.py:919-924): pair hashes
+ * fnv1a(chain_hash_{round,floor}, seed=target) and the chain flag (no diffuse
+ * step anywhere in the prefix and the row itself not diffuse). */
+int sbr_cir_row_pairs(const SbrVertexBuf* vb, const uint64_t* row_key_dev,
+                      const int32_t* row_vtx_dev, int64_t n, uint64_t* pr_dev, uint64_t* pf_dev,
+                      uint8_t* chain_dev, void* stream);
 /* Candidate selection with the reference's exact semantics
  * (_emit_records paths.py:903-987, DedupTable / PathBuffer 174-226,
- * generate_candidates 1019-1103 at workers=1): ordinal sort, first occurrence
- * of each (pair_r, pair_f) among chain rows, truncation to n_buffer, LoS
- * pre-claims, greedy both-slot registration in a table of n_hash slots,
- * buffer cap.  los_visible_dev: (n_targets) uint8, 1 = unoccluded.
- * Outputs record (vertex index or -1 for LoS, target) in buffer order;
- * *n_records (host) receives the count.  Synchronises `stream`. */
-int sbr_cir_select(const SbrCirParams* params, const SbrVertexBuf* vb,
-                   const uint64_t* row_key_dev, const int32_t* row_vtx_dev, int64_t n_rows,
-                   const uint8_t* los_visible_dev, uint64_t n_hash, int64_t n_buffer,
-                   int32_t* rec_vtx_dev, int32_t* rec_target_dev, int64_t* n_records,
+ * generate_candidates 1019-1103 at workers=1) over rows given by ordinal key,
+ * pair hashes and chain flag -- local rows, or rows all-gathered from every
+ * rank (multi-GPU): ordinal sort, first occurrence of each (pair_r, pair_f)
+ * among chain rows, per-depth truncation to n_buffer, LoS pre-claims, greedy
+ * both-slot registration in a table of n_hash slots, buffer cap.
+ * los_visible_dev: (n_targets) uint8, 1 = unoccluded.  Output rec_row_dev
+ * (capacity n_buffer) in buffer order: index into the row arrays, or ~target
+ * (< 0) for a LoS record; *n_records (host) receives the count.
+ * Synchronises `stream`. */
+int sbr_cir_select(const SbrCirParams* params, const uint64_t* row_key_dev,
+                   const uint64_t* row_pr_dev, const uint64_t* row_pf_dev,
+                   const uint8_t* row_chain_dev, int64_t n_rows, const uint8_t* los_visible_dev,
+                   uint64_t n_hash, int64_t n_buffer, int64_t* rec_row_dev, int64_t* n_records,
                    uint64_t* counters_dev, void* stream);
+/* rec_row -> (vertex index, target) for sbr_cir_records (vertex -1 = LoS). */
+int sbr_cir_resolve_records(const int64_t* rec_row_dev, int64_t n, const uint64_t* row_key_dev,
+                            const int32_t* row_vtx_dev, int32_t* rec_vtx_dev,
+                            int32_t* rec_target_dev, void* stream);
 /* Walks vertex parent chains into CandidateRecord arrays
  * (_record_from_batch paths.py:990-1016). */
 int sbr_cir_records(const SbrCirParams* params, const SbrVertexBuf* vb,

@@ -1077,16 +1077,13 @@ static int interaction_q(const SbrMaterial* m, double cos_i, double q_d, int all
   return 1;
 }
 
-ORC_EXPORT int orc_cir_generate(const OrcScene* S, const OrcCirParams* P, OrcRecords* R,
-                                int64_t* n_out, uint64_t* counters) {
+/* Per-sample sweep of global ids [lo, hi) into H (indexed g - lo). */
+static int cir_sweep(const OrcScene* S, const OrcCirParams* P, uint64_t lo, uint64_t hi, Hist* H,
+                     uint64_t* counters) {
   const int L = P->max_depth;
   const uint64_t N = P->num_samples;
-  const int nt = P->nt;
-  Hist* H = (Hist*)malloc(sizeof(Hist) * (size_t)(N * (L > 0 ? L : 1)));
-  if (!H) return SBR_ERR_NOMEM;
-  for (uint64_t i = 0; i < N * (uint64_t)(L > 0 ? L : 1); ++i) H[i].code = -1;
-  /* ---- per-sample sweep (each sample's rows are independent of the others) */
-  for (uint64_t g = 0; g < N; ++g) {
+  for (uint64_t i = 0; i < (hi - lo) * (uint64_t)(L > 0 ? L : 1); ++i) H[i].code = -1;
+  for (uint64_t g = lo; g < hi; ++g) {
     double o[3] = {P->source[0], P->source[1], P->source[2]}, d[3];
     orc_fibonacci(N, g, d);
     uint64_t hr = 0, hf = 0;
@@ -1096,7 +1093,7 @@ ORC_EXPORT int orc_cir_generate(const OrcScene* S, const OrcCirParams* P, OrcRec
       double t, u_, v_;
       int64_t tri;
       counters[OC_RB]++;
-      if (closest1(S, o, d, 1e-4, INFINITY, &t, &tri, &u_, &v_)) { free(H); return SBR_ERR_STACK; }
+      if (closest1(S, o, d, 1e-4, INFINITY, &t, &tri, &u_, &v_)) return SBR_ERR_STACK;
       if (tri < 0) { counters[OC_ESCAPED]++; break; }
       double pt[3] = {o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]};
       const double* nr = S->normal + 3 * tri;
@@ -1120,7 +1117,7 @@ ORC_EXPORT int orc_cir_generate(const OrcScene* S, const OrcCirParams* P, OrcRec
       } else if (code == 1) {
         suffix = depth;
       }
-      Hist* h = H + g * L + (depth - 1);
+      Hist* h = H + (g - lo) * L + (depth - 1);
       memcpy(h->vertex, pt, sizeof pt);
       memcpy(h->normal, n, sizeof n);
       h->run_prob = run_prob; h->hr = hr; h->hf = hf; h->tri = (int32_t)tri;
@@ -1144,15 +1141,18 @@ ORC_EXPORT int orc_cir_generate(const OrcScene* S, const OrcCirParams* P, OrcRec
       memcpy(o, pt, sizeof pt);
     }
   }
-  /* ---- rows in (depth, sample, target) order with in-chunk dedup + truncation */
-  PairSet seen = {0, 0, 0, 0};
+  return 0;
+}
+
+/* visible rows of H in (depth, sample, target) order (_visible_pairs 657-683) */
+static int cir_rows(const OrcScene* S, const OrcCirParams* P, uint64_t lo, uint64_t hi,
+                    const Hist* H, Row** rows_out, int64_t* n_out, uint64_t* counters) {
+  const int L = P->max_depth, nt = P->nt;
   Row* rows = NULL;
-  int64_t nrows = 0, cap_rows = 0, emitted = 0;
-  for (int depth = 1; depth <= L; ++depth) {
-    int64_t depth_rows = 0, room = P->n_buffer - emitted;
-    int64_t first_row = nrows;
-    for (uint64_t g = 0; g < N; ++g) {
-      const Hist* h = H + g * L + (depth - 1);
+  int64_t n = 0, cap = 0;
+  for (int depth = 1; depth <= L; ++depth)
+    for (uint64_t g = lo; g < hi; ++g) {
+      const Hist* h = H + (g - lo) * L + (depth - 1);
       if (h->code < 0) continue;
       for (int k = 0; k < nt; ++k) {
         const double* tg = P->targets + 3 * k;
@@ -1162,45 +1162,72 @@ ORC_EXPORT int orc_cir_generate(const OrcScene* S, const OrcCirParams* P, OrcRec
         if (!ok) continue;
         counters[OC_VIS]++;
         int occ;
-        if (occluded1(S, h->vertex, tg, 1e-4, &occ)) { free(H); free(rows); return SBR_ERR_STACK; }
+        if (occluded1(S, h->vertex, tg, 1e-4, &occ)) { free(rows); return SBR_ERR_STACK; }
         if (occ) continue;
         counters[OC_ROWS]++;
-        Row r;
-        r.g = (int64_t)g; r.depth = depth; r.k = k;
-        r.diffuse = h->code == 1;
-        r.chain = h->suffix_start == 0 && h->code != 1;
-        r.pr = fnv1a_u64(h->hr, (uint64_t)k);
-        r.pf = fnv1a_u64(h->hf, (uint64_t)k);
-        if (r.chain && !pairset_insert(&seen, r.pr, r.pf)) { counters[OC_DUP]++; continue; }
-        if (nrows == cap_rows) {
-          cap_rows = cap_rows ? 2 * cap_rows : 4096;
-          rows = (Row*)realloc(rows, sizeof(Row) * (size_t)cap_rows);
+        if (n == cap) {
+          cap = cap ? 2 * cap : 4096;
+          rows = (Row*)realloc(rows, sizeof(Row) * (size_t)cap);
         }
-        rows[nrows++] = r;
-        depth_rows++;
+        Row* r = rows + n++;
+        r->g = (int64_t)g; r->depth = depth; r->k = k;
+        r->diffuse = h->code == 1;
+        r->chain = h->suffix_start == 0 && h->code != 1;
+        r->pr = fnv1a_u64(h->hr, (uint64_t)k);
+        r->pf = fnv1a_u64(h->hf, (uint64_t)k);
       }
     }
-    /* truncation to room (an all-cut depth returns no batch: uncounted) */
+  *rows_out = rows;
+  *n_out = n;
+  return 0;
+}
+
+static int row_cmp(const void* a, const void* b) {
+  const Row* x = (const Row*)a;
+  const Row* y = (const Row*)b;
+  if (x->depth != y->depth) return x->depth < y->depth ? -1 : 1;
+  if (x->g != y->g) return x->g < y->g ? -1 : 1;
+  return x->k < y->k ? -1 : (x->k > y->k);
+}
+
+/* _emit_records dedup + truncation and DedupTable / PathBuffer registration
+ * (paths.py:903-987, 174-226, 1036-1096) over rows sorted by (depth, sample,
+ * target).  rec_row[i]: index into `rows`, or ~k for the LoS record of
+ * target k.  los[k] = 1 when the source sees target k. */
+static int64_t cir_select(const OrcCirParams* P, const Row* rows, int64_t n, const uint8_t* los,
+                          int64_t* rec_row, uint64_t* counters) {
+  PairSet seen = {0, 0, 0, 0};
+  uint8_t* keep = (uint8_t*)calloc((size_t)(n > 0 ? n : 1), 1);
+  int64_t emitted = 0, i = 0;
+  while (i < n) {
+    const int depth = rows[i].depth;
+    int64_t j = i, depth_rows = 0;
+    int64_t room = P->n_buffer - emitted;
     if (room < 0) room = 0;
+    for (; j < n && rows[j].depth == depth; ++j) {
+      if (rows[j].chain && !pairset_insert(&seen, rows[j].pr, rows[j].pf)) {
+        counters[OC_DUP]++;
+        continue;
+      }
+      if (depth_rows < room) keep[j] = 1;
+      depth_rows++;
+    }
+    /* a depth cut to nothing returns no batch: its truncation is not counted */
     if (depth_rows > room) {
       if (room > 0) counters[OC_TRUNC] += (uint64_t)(depth_rows - room);
-      nrows = first_row + room;
+      emitted += room;
+    } else {
+      emitted += depth_rows;
     }
-    emitted += nrows - first_row;
+    i = j;
   }
   free(seen.k); free(seen.used);
-  /* ---- registration (DedupTable) + PathBuffer */
   int32_t* counts = (int32_t*)calloc((size_t)P->n_hash, sizeof(int32_t));
   int64_t nrec = 0;
-  const int Ls = R->L;
-  /* LoS records first (generate_candidates 1036-1049) */
-  for (int k = 0; k < nt; ++k) {
-    int occ;
-    if (occluded1(S, P->source, P->targets + 3 * k, 1e-4, &occ)) { free(H); free(rows); free(counts); return SBR_ERR_STACK; }
-    if (occ) continue;
-    uint64_t key = fnv1a_u64(0ULL, (uint64_t)k);
-    uint64_t i1 = key % P->n_hash;
-    if (counts[i1] == 0 && counts[i1] == 0) {
+  for (int k = 0; k < P->nt; ++k) {
+    if (!los[k]) continue;
+    uint64_t i1 = fnv1a_u64(0ULL, (uint64_t)k) % P->n_hash;
+    if (counts[i1] == 0) {
       counts[i1] += 2;
       counters[OC_REG]++;
     } else {
@@ -1208,16 +1235,12 @@ ORC_EXPORT int orc_cir_generate(const OrcScene* S, const OrcCirParams* P, OrcRec
       continue;
     }
     if (nrec >= P->n_buffer) { counters[OC_OVERFLOW]++; continue; }
-    R->target[nrec] = k; R->sample[nrec] = -1; R->depth[nrec] = 0; R->suffix_start[nrec] = 0;
-    R->diffuse[nrec] = 0; R->chain_hash[nrec] = 0; R->prefix_prob[nrec] = 1.0;
-    memcpy(R->anchor + 3 * nrec, P->source, 3 * sizeof(double));
-    for (int j = 0; j < Ls; ++j) { R->kind[nrec * Ls + j] = -1; R->tri[nrec * Ls + j] = -1; }
-    nrec++;
+    rec_row[nrec++] = ~(int64_t)k;
   }
-  for (int64_t i = 0; i < nrows; ++i) {
-    const Row* r = rows + i;
-    if (r->chain) {
-      uint64_t i1 = r->pr % P->n_hash, i2 = r->pf % P->n_hash;
+  for (int64_t r = 0; r < n; ++r) {
+    if (!keep[r]) continue;
+    if (rows[r].chain) {
+      uint64_t i1 = rows[r].pr % P->n_hash, i2 = rows[r].pf % P->n_hash;
       if (counts[i1] == 0 && counts[i2] == 0) {
         counts[i1]++; counts[i2]++;
         counters[OC_REG]++;
@@ -1227,35 +1250,127 @@ ORC_EXPORT int orc_cir_generate(const OrcScene* S, const OrcCirParams* P, OrcRec
       }
     }
     if (nrec >= P->n_buffer) { counters[OC_OVERFLOW]++; continue; }
+    rec_row[nrec++] = r;
+  }
+  for (uint64_t s = 0; s < P->n_hash; ++s) counters[OC_SLOTS] += counts[s] != 0;
+  counters[OC_CAND] += (uint64_t)nrec;
+  free(counts); free(keep);
+  return nrec;
+}
+
+static int cir_los(const OrcScene* S, const OrcCirParams* P, uint8_t* los) {
+  for (int k = 0; k < P->nt; ++k) {
+    int occ;
+    if (occluded1(S, P->source, P->targets + 3 * k, 1e-4, &occ)) return SBR_ERR_STACK;
+    los[k] = !occ;
+  }
+  return 0;
+}
+
+/* Visible rows of the sample range [lo, hi) for the multi-rank path: ordinal
+ * key (depth << 60 | sample << 20 | target), pair hashes, chain flag. */
+ORC_EXPORT int orc_cir_rows(const OrcScene* S, const OrcCirParams* P, uint64_t lo, uint64_t hi,
+                            uint64_t* key, uint64_t* pr, uint64_t* pf, uint8_t* chain,
+                            int64_t cap, int64_t* n_out, uint64_t* counters) {
+  const int L = P->max_depth > 0 ? P->max_depth : 1;
+  Hist* H = (Hist*)malloc(sizeof(Hist) * (size_t)((hi - lo) * L + 1));
+  int rc = cir_sweep(S, P, lo, hi, H, counters);
+  Row* rows = NULL;
+  int64_t n = 0;
+  if (!rc) rc = cir_rows(S, P, lo, hi, H, &rows, &n, counters);
+  *n_out = n;
+  if (!rc && n > cap) rc = SBR_ERR_NOMEM;
+  for (int64_t i = 0; !rc && i < n; ++i) {
+    key[i] = ((uint64_t)rows[i].depth << 60) | ((uint64_t)rows[i].g << 20) | (uint64_t)rows[i].k;
+    pr[i] = rows[i].pr;
+    pf[i] = rows[i].pf;
+    chain[i] = rows[i].chain;
+  }
+  free(H); free(rows);
+  return rc;
+}
+
+/* Selection over rows in any order (e.g. gathered from several ranks):
+ * rec_row[i] indexes the caller's arrays, or ~target for LoS. */
+ORC_EXPORT int orc_cir_select(const OrcScene* S, const OrcCirParams* P, const uint64_t* key,
+                              const uint64_t* pr, const uint64_t* pf, const uint8_t* chain,
+                              int64_t n, int64_t* rec_row, int64_t* n_rec, uint64_t* counters) {
+  /* decorate rows with their input index, sort by (depth, sample, target) */
+  typedef struct { Row r; int64_t i; } Dec;  /* Row first: row_cmp applies */
+  Dec* dec = (Dec*)malloc(sizeof(Dec) * (size_t)(n > 0 ? n : 1));
+  for (int64_t i = 0; i < n; ++i) {
+    dec[i].r.depth = (int32_t)(key[i] >> 60);
+    dec[i].r.g = (int64_t)((key[i] >> 20) & ((1ULL << 40) - 1));
+    dec[i].r.k = (int32_t)(key[i] & ((1ULL << 20) - 1));
+    dec[i].r.pr = pr[i];
+    dec[i].r.pf = pf[i];
+    dec[i].r.chain = chain[i];
+    dec[i].r.diffuse = 0;
+    dec[i].i = i;
+  }
+  qsort(dec, (size_t)n, sizeof(Dec), row_cmp);
+  Row* sorted = (Row*)malloc(sizeof(Row) * (size_t)(n > 0 ? n : 1));
+  for (int64_t i = 0; i < n; ++i) sorted[i] = dec[i].r;
+  uint8_t* los = (uint8_t*)malloc((size_t)P->nt);
+  int rc = cir_los(S, P, los);
+  int64_t nrec = 0;
+  if (!rc) {
+    nrec = cir_select(P, sorted, n, los, rec_row, counters);
+    for (int64_t i = 0; i < nrec; ++i)
+      if (rec_row[i] >= 0) rec_row[i] = dec[rec_row[i]].i;
+  }
+  *n_rec = nrec;
+  free(dec); free(sorted); free(los);
+  return rc;
+}
+
+ORC_EXPORT int orc_cir_generate(const OrcScene* S, const OrcCirParams* P, OrcRecords* R,
+                                int64_t* n_out, uint64_t* counters) {
+  const int L = P->max_depth > 0 ? P->max_depth : 1;
+  const uint64_t N = P->num_samples;
+  Hist* H = (Hist*)malloc(sizeof(Hist) * (size_t)(N * L + 1));
+  if (!H) return SBR_ERR_NOMEM;
+  int rc = cir_sweep(S, P, 0, N, H, counters);
+  Row* rows = NULL;
+  int64_t n = 0;
+  if (!rc) rc = cir_rows(S, P, 0, N, H, &rows, &n, counters);
+  uint8_t* los = (uint8_t*)malloc((size_t)P->nt);
+  if (!rc) rc = cir_los(S, P, los);
+  int64_t* rec_row = (int64_t*)malloc(sizeof(int64_t) * (size_t)(P->n_buffer > 0 ? P->n_buffer : 1));
+  int64_t nrec = 0;
+  if (!rc) nrec = cir_select(P, rows, n, los, rec_row, counters);
+  const int Ls = R->L;
+  for (int64_t i = 0; !rc && i < nrec; ++i) {
+    const int64_t rr = rec_row[i];
+    for (int j = 0; j < Ls; ++j) { R->kind[i * Ls + j] = -1; R->tri[i * Ls + j] = -1; }
+    R->prefix_prob[i] = 1.0;
+    memcpy(R->anchor + 3 * i, P->source, 3 * sizeof(double));
+    if (rr < 0) {
+      R->target[i] = (int32_t)(~rr); R->sample[i] = -1; R->depth[i] = 0;
+      R->suffix_start[i] = 0; R->diffuse[i] = 0; R->chain_hash[i] = 0;
+      continue;
+    }
+    const Row* r = rows + rr;
     const Hist* last = H + r->g * L + (r->depth - 1);
-    R->target[nrec] = r->k; R->sample[nrec] = r->g; R->depth[nrec] = r->depth;
-    R->suffix_start[nrec] = last->suffix_start; R->diffuse[nrec] = r->diffuse;
-    R->chain_hash[nrec] = last->hr;
-    R->prefix_prob[nrec] = 1.0;
-    memcpy(R->anchor + 3 * nrec, P->source, 3 * sizeof(double));
+    R->target[i] = r->k; R->sample[i] = r->g; R->depth[i] = r->depth;
+    R->suffix_start[i] = last->suffix_start; R->diffuse[i] = r->diffuse;
+    R->chain_hash[i] = last->hr;
     if (last->suffix_start > 0) {
       const Hist* a = H + r->g * L + (last->suffix_start - 1);
-      R->prefix_prob[nrec] = a->run_prob;
-      memcpy(R->anchor + 3 * nrec, a->vertex, 3 * sizeof(double));
+      R->prefix_prob[i] = a->run_prob;
+      memcpy(R->anchor + 3 * i, a->vertex, 3 * sizeof(double));
     }
-    for (int j = 0; j < Ls; ++j) {
-      int64_t o = nrec * Ls + j;
-      if (j < r->depth) {
-        const Hist* h = H + r->g * L + j;
-        R->kind[o] = h->code; R->tri[o] = h->tri;
-        memcpy(R->vertex + 3 * o, h->vertex, 3 * sizeof(double));
-        memcpy(R->normal + 3 * o, h->normal, 3 * sizeof(double));
-      } else {
-        R->kind[o] = -1; R->tri[o] = -1;
-      }
+    for (int j = 0; j < r->depth && j < Ls; ++j) {
+      const Hist* h = H + r->g * L + j;
+      const int64_t o = i * Ls + j;
+      R->kind[o] = h->code; R->tri[o] = h->tri;
+      memcpy(R->vertex + 3 * o, h->vertex, 3 * sizeof(double));
+      memcpy(R->normal + 3 * o, h->normal, 3 * sizeof(double));
     }
-    nrec++;
   }
-  for (uint64_t i = 0; i < P->n_hash; ++i) counters[OC_SLOTS] += counts[i] != 0;
-  counters[OC_CAND] += (uint64_t)nrec;
   *n_out = nrec;
-  free(H); free(rows); free(counts);
-  return 0;
+  free(H); free(rows); free(los); free(rec_row);
+  return rc;
 }
 
 /* refine_candidate (paths.py:1123-1252), diffraction branch out of scope.

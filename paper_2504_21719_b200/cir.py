@@ -378,6 +378,134 @@ def _counters_dict(c):
     return {name: int(c[i]) for i, name in enumerate(_abi.CIR_COUNTERS)}
 
 
+class _Rows:
+    """Visible (vertex, target) rows of one source on this device."""
+
+
+def _sweep_rows(scene, source, targets, cfg, lo, hi):
+    """Sweep global sample ids [lo, hi) and collect visible rows + dedup keys.
+
+    _sweep_chunk's trace/draw/continue loop (paths.py:704-828) and
+    _visible_pairs (657-683) on the GPU; the rows carry the ordinal key
+    (depth, sample, target), the vertex index and the pair hashes.
+    """
+    torch = _torch()
+    L_ = _native.lib()
+    acc = scene.accel
+    dev = acc.device
+    R = _Rows()
+    R.dev = dev
+    stream = _native.stream_ptr(dev)
+    R.targets_t = torch.from_numpy(np.ascontiguousarray(targets)).to(dev)
+    R.params = _cir_params(source, R.targets_t, cfg)
+    R.counters = counters = torch.zeros(_abi.SBR_CC_COUNT, dtype=torch.int64, device=dev)
+    # line of sight (generate_candidates 1036-1049)
+    occ = acc.occluded_batch(torch.from_numpy(np.broadcast_to(source, targets.shape).copy())
+                             .to(dev), R.targets_t)
+    R.los_vis = (~occ).to(torch.uint8).contiguous()
+    gt = _PhaseTimer("  generate")
+    gt.mark("los")
+    R.vb = vb = _VertexBuf((hi - lo) * cfg.max_depth, dev)
+    if hi > lo and cfg.max_depth > 0:
+        _native.check(L_.sbr_cir_sweep(acc.handle, ctypes.byref(R.params), lo, hi,
+                                       ctypes.byref(vb.abi), _native.ptr(counters), stream))
+    nv = int(counters[_abi.CC["vertices"]].item())
+    gt.mark("sweep")
+    # visibility rows, vertex slabs of <= 2^26 (vertex, target) pairs; before
+    # each slab the row buffer is grown (geometrically) to hold the slab's
+    # worst case, so no slab is ever traced twice
+    nt = len(targets)
+    order = torch.empty(max(nv, 1), dtype=torch.int32, device=dev)
+    if nv:
+        _native.check(L_.sbr_cir_vertex_order(acc.handle, ctypes.byref(vb.abi), nv,
+                                              _native.ptr(order), stream))
+    slab = max(32, ((1 << 26) // nt) // 32 * 32)
+    cap = max(1 << 20, min(nv * nt, int(nv * nt * 0.03)))
+    row_key = torch.empty(cap, dtype=torch.uint64, device=dev)
+    row_vtx = torch.empty(cap, dtype=torch.int32, device=dev)
+    nrows = 0
+    for v0 in range(0, nv, slab):
+        v1 = min(nv, v0 + slab)
+        need = nrows + (v1 - v0) * nt
+        if need > cap:
+            cap = max(need, int(cap * 1.5))
+            nk = torch.empty(cap, dtype=torch.uint64, device=dev)
+            nv_ = torch.empty(cap, dtype=torch.int32, device=dev)
+            nk[:nrows].copy_(row_key[:nrows])
+            nv_[:nrows].copy_(row_vtx[:nrows])
+            row_key, row_vtx = nk, nv_
+        _native.check(L_.sbr_cir_visibility(
+            acc.handle, ctypes.byref(R.params), ctypes.byref(vb.abi), v0, v1,
+            _native.ptr(order), _native.ptr(row_key), _native.ptr(row_vtx), cap,
+            _native.ptr(counters), stream))
+        nrows = int(counters[_abi.CC["rows"]].item())
+        if nrows > cap:
+            raise RuntimeError("visibility row buffer overflow")  # cannot happen
+    acc.check()
+    gt.mark("visibility")
+    R.n = nrows
+    R.key, R.vtx = row_key[:nrows], row_vtx[:nrows]
+    m = max(nrows, 1)
+    R.pr = torch.empty(m, dtype=torch.uint64, device=dev)
+    R.pf = torch.empty(m, dtype=torch.uint64, device=dev)
+    R.chain = torch.empty(m, dtype=torch.uint8, device=dev)
+    if nrows:
+        _native.check(L_.sbr_cir_row_pairs(ctypes.byref(vb.abi), _native.ptr(R.key),
+                                           _native.ptr(R.vtx), nrows, _native.ptr(R.pr),
+                                           _native.ptr(R.pf), _native.ptr(R.chain), stream))
+    R.timer = gt
+    return R
+
+
+def _select_rows(params, key, pr, pf, chain, n, los_vis, cfg, counters, dev):
+    """sbr_cir_select over (possibly all-gathered) rows -> rec_row tensor, count."""
+    torch = _torch()
+    L_ = _native.lib()
+    n_buffer = cfg.resolved_buffer_capacity()
+    rec_cap = max(1, min(n_buffer, n + int(los_vis.numel())))
+    rec_row = torch.empty(rec_cap, dtype=torch.int64, device=dev)
+    n_rec = ctypes.c_int64(0)
+    _native.check(L_.sbr_cir_select(
+        ctypes.byref(params), _native.ptr(key), _native.ptr(pr), _native.ptr(pf),
+        _native.ptr(chain), n, _native.ptr(los_vis), cfg.resolved_hash_capacity(), n_buffer,
+        _native.ptr(rec_row), ctypes.byref(n_rec), _native.ptr(counters),
+        _native.stream_ptr(dev)))
+    return rec_row, int(n_rec.value)
+
+
+def _materialize(R, rec_row, n, cfg):
+    """CandidateRecord arrays for rec_row entries that index R's own rows."""
+    torch = _torch()
+    L_ = _native.lib()
+    dev = R.dev
+    L = max(int(cfg.max_depth), 1)
+    recbuf = _RecordBuf(n, L, dev)
+    if n:
+        stream = _native.stream_ptr(dev)
+        rec_vtx = torch.empty(n, dtype=torch.int32, device=dev)
+        rec_tgt = torch.empty(n, dtype=torch.int32, device=dev)
+        _native.check(L_.sbr_cir_resolve_records(_native.ptr(rec_row), n, _native.ptr(R.key),
+                                                 _native.ptr(R.vtx), _native.ptr(rec_vtx),
+                                                 _native.ptr(rec_tgt), stream))
+        _native.check(L_.sbr_cir_records(ctypes.byref(R.params), ctypes.byref(R.vb.abi),
+                                         _native.ptr(rec_vtx), _native.ptr(rec_tgt), n,
+                                         ctypes.byref(recbuf.abi), stream))
+    return recbuf
+
+
+def _gen_diag(c, cfg):
+    return {
+        "samples_escaped": c["samples_escaped"],
+        "samples_terminated": c["samples_terminated"],
+        "duplicates": c["duplicates"],
+        "chunk_truncated": c["chunk_truncated"],
+        "buffer_overflow": c["buffer_overflow"],
+        "candidates": c["candidates"],
+        "hash_load_factor": c["hash_slots"] / float(cfg.resolved_hash_capacity()),
+        "hash_registered": c["hash_registered"],
+    }
+
+
 def _generate_device(scene, source, targets, cfg, source_id=0, sample_range=None):
     """Run sweep -> visibility -> select -> records on the scene's device.
 
@@ -385,7 +513,6 @@ def _generate_device(scene, source, targets, cfg, source_id=0, sample_range=None
     """
     torch = _torch()
     _check_cfg(cfg)
-    L_ = _native.lib()
     acc = scene.accel
     dev = acc.device
     scene.bind_frequency(cfg.frequency)
@@ -395,91 +522,19 @@ def _generate_device(scene, source, targets, cfg, source_id=0, sample_range=None
         raise ValueError("at least one target is required")
     lo, hi = (0, int(cfg.num_samples)) if sample_range is None else map(int, sample_range)
     with torch.cuda.device(dev):
-        stream = _native.stream_ptr(dev)
-        targets_t = torch.from_numpy(np.ascontiguousarray(targets)).to(dev)
-        params = _cir_params(source, targets_t, cfg)
-        counters = torch.zeros(_abi.SBR_CC_COUNT, dtype=torch.int64, device=dev)
-        # line of sight (generate_candidates 1036-1049)
-        occ = acc.occluded_batch(torch.from_numpy(np.broadcast_to(source, targets.shape).copy())
-                                 .to(dev), targets_t)
-        los_vis = (~occ).to(torch.uint8).contiguous()
-        gt = _PhaseTimer("  generate")
-        gt.mark("los")
-        L = max(int(cfg.max_depth), 1)
-        vb = _VertexBuf((hi - lo) * cfg.max_depth, dev)
-        if hi > lo and cfg.max_depth > 0:
-            _native.check(L_.sbr_cir_sweep(acc.handle, ctypes.byref(params), lo, hi,
-                                           ctypes.byref(vb.abi), _native.ptr(counters), stream))
-        nv = int(counters[_abi.CC["vertices"]].item())
-        gt.mark("sweep")
-        # visibility rows, vertex slabs of <= 2^26 (vertex, target) pairs; before
-        # each slab the row buffer is grown (geometrically) to hold the slab's
-        # worst case, so no slab is ever traced twice
-        nt = len(targets)
-        order = torch.empty(max(nv, 1), dtype=torch.int32, device=dev)
-        if nv:
-            _native.check(L_.sbr_cir_vertex_order(acc.handle, ctypes.byref(vb.abi), nv,
-                                                  _native.ptr(order), stream))
-        slab = max(32, ((1 << 26) // nt) // 32 * 32)
-        cap = max(1 << 20, min(nv * nt, int(nv * nt * 0.03)))
-        row_key = torch.empty(cap, dtype=torch.uint64, device=dev)
-        row_vtx = torch.empty(cap, dtype=torch.int32, device=dev)
-        nrows = 0
-        for v0 in range(0, nv, slab):
-            v1 = min(nv, v0 + slab)
-            need = nrows + (v1 - v0) * nt
-            if need > cap:
-                cap = max(need, int(cap * 1.5))
-                nk = torch.empty(cap, dtype=torch.uint64, device=dev)
-                nv_ = torch.empty(cap, dtype=torch.int32, device=dev)
-                nk[:nrows].copy_(row_key[:nrows])
-                nv_[:nrows].copy_(row_vtx[:nrows])
-                row_key, row_vtx = nk, nv_
-            _native.check(L_.sbr_cir_visibility(
-                acc.handle, ctypes.byref(params), ctypes.byref(vb.abi), v0, v1,
-                _native.ptr(order), _native.ptr(row_key), _native.ptr(row_vtx), cap,
-                _native.ptr(counters), stream))
-            nrows = int(counters[_abi.CC["rows"]].item())
-            if nrows > cap:
-                raise RuntimeError("visibility row buffer overflow")  # cannot happen
-        acc.check()
-        gt.mark("visibility")
-        n_buffer = cfg.resolved_buffer_capacity()
-        n_hash = cfg.resolved_hash_capacity()
-        rec_cap = max(1, min(n_buffer, nrows + nt))
-        rec_vtx = torch.empty(rec_cap, dtype=torch.int32, device=dev)
-        rec_tgt = torch.empty(rec_cap, dtype=torch.int32, device=dev)
-        n_rec = ctypes.c_int64(0)
-        _native.check(L_.sbr_cir_select(
-            ctypes.byref(params), ctypes.byref(vb.abi), _native.ptr(row_key),
-            _native.ptr(row_vtx), nrows, _native.ptr(los_vis), n_hash, n_buffer,
-            _native.ptr(rec_vtx), _native.ptr(rec_tgt), ctypes.byref(n_rec),
-            _native.ptr(counters), stream))
-        n = int(n_rec.value)
-        gt.mark("select")
-        recbuf = _RecordBuf(n, L, dev)
-        if n:
-            _native.check(L_.sbr_cir_records(ctypes.byref(params), ctypes.byref(vb.abi),
-                                             _native.ptr(rec_vtx), _native.ptr(rec_tgt), n,
-                                             ctypes.byref(recbuf.abi), stream))
-        c = _counters_dict(counters.cpu().numpy())
-        gt.mark("records")
-        gt.report()
+        R = _sweep_rows(scene, source, targets, cfg, lo, hi)
+        rec_row, n = _select_rows(R.params, R.key, R.pr, R.pf, R.chain, R.n, R.los_vis, cfg,
+                                  R.counters, dev)
+        R.timer.mark("select")
+        recbuf = _materialize(R, rec_row, n, cfg)
+        c = _counters_dict(R.counters.cpu().numpy())
+        R.timer.mark("records")
+        R.timer.report()
     if c["stack_overflow"]:
         raise RuntimeError("BVH traversal stack overflow")
-    diag = {
-        "samples_escaped": c["samples_escaped"],
-        "samples_terminated": c["samples_terminated"],
-        "duplicates": c["duplicates"],
-        "chunk_truncated": c["chunk_truncated"],
-        "buffer_overflow": c["buffer_overflow"],
-        "candidates": c["candidates"],
-        "hash_load_factor": c["hash_slots"] / float(n_hash),
-        "hash_registered": c["hash_registered"],
-    }
-    cand = DeviceCandidates(scene, source, targets, targets_t, cfg, recbuf, n, source_id)
-    cand.params = params
-    return cand, c, diag
+    cand = DeviceCandidates(scene, source, targets, R.targets_t, cfg, recbuf, n, source_id)
+    cand.params = R.params
+    return cand, c, _gen_diag(c, cfg)
 
 
 def generate_candidates(scene, source, targets, cfg, source_id=0):
@@ -630,6 +685,61 @@ def _flatten_devices(devices, synthetic):
     return flat
 
 
+def _paths_for_source(scene, cand, cfg, ti, te, tx_dev, target_devices, rx_index, rx_elem,
+                      timer=None):
+    """Refine + replay the candidates of one source; SoA part of valid paths."""
+    torch = _torch()
+    acc = scene.accel
+    rejections = Counter()
+    pv, status, rc = _refine_device(scene, cand)
+    if timer:
+        timer.mark("refine")
+    rcount = rc.cpu().numpy()
+    for code, name in _abi.REJECTION_NAMES.items():
+        cnt = int(rcount[_abi.CC[{1: "rej_coplanar_miss", 2: "rej_occluded",
+                                   3: "rej_degenerate"}[code]]])
+        if cnt:
+            rejections[name] += cnt
+    f = _fields_device(scene, cand, pv, status, tx_dev, target_devices, cfg)
+    if timer:
+        timer.mark("fields")
+    n = cand.n
+    if n == 0:
+        return None, rejections
+    ok_idx = torch.nonzero(status[:n] == _abi.SBR_REFINE_OK).squeeze(1)
+    m = int(ok_idx.numel())
+    h = {k: v[:n].index_select(0, ok_idx).cpu().numpy() for k, v in cand.rec.t.items()
+         if k != "chain_hash"}
+    h["chain_hash"] = cand.rec.t["chain_hash"][:n].cpu().numpy()[ok_idx.cpu().numpy()]
+    fh = {k: v[:n].index_select(0, ok_idx).cpu().numpy() for k, v in f.items()}
+    pvh = pv[:n].index_select(0, ok_idx).cpu().numpy()
+    tri = h["tri"]
+    valid = tri >= 0
+    obj = np.where(valid, acc.tri_object_id[np.maximum(tri, 0)], -1)
+    prim = np.where(valid, acc.tri_primitive_id[np.maximum(tri, 0)], -1)
+    tg = h["target"].astype(np.int64)
+    part = dict(
+        tx=np.full(m, ti, np.int64), tx_el=np.full(m, te, np.int64),
+        rx=rx_index[tg], rx_el=rx_elem[tg],
+        gain=fh["gain"][:, 0] + 1j * fh["gain"][:, 1], delay=fh["delay"],
+        doppler=fh["doppler"], departure=fh["departure"], arrival=fh["arrival"],
+        depth=h["depth"].astype(np.int64), chain_hash=h["chain_hash"], sample=h["sample"],
+        kind=h["kind"], obj=obj, prim=prim, normal=h["normal"], vertices=pvh)
+    if timer:
+        timer.mark("host_copy")
+    return part, rejections
+
+
+def _device_plan(transmitters, receivers, cfg):
+    tx_flat = _flatten_devices(transmitters, cfg.synthetic_arrays)
+    rx_flat = _flatten_devices(receivers, cfg.synthetic_arrays)
+    targets = np.array([pos for _, _, pos in rx_flat])
+    target_devices = [receivers[ri] for ri, _, _ in rx_flat]
+    rx_index = np.array([ri for ri, _, _ in rx_flat], np.int64)
+    rx_elem = np.array([re for _, re, _ in rx_flat], np.int64)
+    return tx_flat, targets, target_devices, rx_index, rx_elem
+
+
 def compute_paths(scene, transmitters, receivers, cfg):
     """All propagation paths between the given devices (paths.py:1444-1516).
 
@@ -637,19 +747,13 @@ def compute_paths(scene, transmitters, receivers, cfg):
     Returns a PathSet whose `tensors` holds the SoA arrays; `paths` builds
     the reference's ValidPath objects on first access.
     """
-    torch = _torch()
     transmitters = list(transmitters)
     receivers = list(receivers)
     if not transmitters or not receivers:
         raise ValueError("need at least one transmitter and one receiver")
     _check_cfg(cfg)
-    tx_flat = _flatten_devices(transmitters, cfg.synthetic_arrays)
-    rx_flat = _flatten_devices(receivers, cfg.synthetic_arrays)
-    targets = np.array([pos for _, _, pos in rx_flat])
-    target_devices = [receivers[ri] for ri, _, _ in rx_flat]
-    rx_index = np.array([ri for ri, _, _ in rx_flat], np.int64)
-    rx_elem = np.array([re for _, re, _ in rx_flat], np.int64)
-    acc = scene.accel
+    tx_flat, targets, target_devices, rx_index, rx_elem = _device_plan(transmitters, receivers,
+                                                                       cfg)
     diagnostics = Counter()
     rejections = Counter()
     load_factor = 0.0
@@ -662,44 +766,99 @@ def compute_paths(scene, transmitters, receivers, cfg):
         for k, v in gdiag.items():
             if k != "hash_load_factor":
                 diagnostics[k] += v
-        pv, status, rc = _refine_device(scene, cand)
-        timer.mark("refine")
-        rcount = rc.cpu().numpy()
-        for code, name in _abi.REJECTION_NAMES.items():
-            cnt = int(rcount[_abi.CC[{1: "rej_coplanar_miss", 2: "rej_occluded",
-                                       3: "rej_degenerate"}[code]]])
-            if cnt:
-                rejections[name] += cnt
-        f = _fields_device(scene, cand, pv, status, transmitters[ti], target_devices, cfg)
-        timer.mark("fields")
-        n = cand.n
-        if n == 0:
-            continue
-        ok_idx = torch.nonzero(status[:n] == _abi.SBR_REFINE_OK).squeeze(1)
-        m = int(ok_idx.numel())
-        h = {k: v[:n].index_select(0, ok_idx).cpu().numpy() for k, v in cand.rec.t.items()
-             if k != "chain_hash"}
-        h["chain_hash"] = cand.rec.t["chain_hash"][:n].cpu().numpy()[ok_idx.cpu().numpy()]
-        fh = {k: v[:n].index_select(0, ok_idx).cpu().numpy() for k, v in f.items()}
-        pvh = pv[:n].index_select(0, ok_idx).cpu().numpy()
-        sel = np.arange(m)
-        tri = h["tri"][sel]
-        valid = tri >= 0
-        obj = np.where(valid, acc.tri_object_id[np.maximum(tri, 0)], -1)
-        prim = np.where(valid, acc.tri_primitive_id[np.maximum(tri, 0)], -1)
-        tg = h["target"][sel].astype(np.int64)
-        parts.append(dict(
-            tx=np.full(len(sel), ti, np.int64), tx_el=np.full(len(sel), te, np.int64),
-            rx=rx_index[tg], rx_el=rx_elem[tg],
-            gain=fh["gain"][sel, 0] + 1j * fh["gain"][sel, 1], delay=fh["delay"][sel],
-            doppler=fh["doppler"][sel], departure=fh["departure"][sel],
-            arrival=fh["arrival"][sel], depth=h["depth"][sel].astype(np.int64),
-            chain_hash=h["chain_hash"][sel], sample=h["sample"][sel], kind=h["kind"][sel],
-            obj=obj, prim=prim, normal=h["normal"][sel], vertices=pvh[sel]))
-        timer.mark("host_copy")
+        part, rej = _paths_for_source(scene, cand, cfg, ti, te, transmitters[ti],
+                                      target_devices, rx_index, rx_elem, timer)
+        rejections.update(rej)
+        if part is not None:
+            parts.append(part)
     tensors = _concat_sorted(parts, max(int(cfg.max_depth), 1))
     timer.mark("sort")
     timer.report()
+    result = dict(diagnostics)
+    result["hash_load_factor"] = load_factor
+    result["refinement_rejections"] = dict(rejections)
+    result["paths"] = len(tensors)
+    return PathSet(tensors=tensors, transmitters=transmitters, receivers=receivers, config=cfg,
+                   diagnostics=result)
+
+
+def compute_paths_sharded(scene, transmitters, receivers, cfg, group=None):
+    """compute_paths over all ranks of a torch.distributed group, one GPU per rank.
+
+    Multi-GPU CIR: every rank sweeps its contiguous shard of the
+    global sample ids (RNG keyed by global id) and casts its occlusion rays;
+    the candidate rows (ordinal key, pair hashes, chain flag; 25 B each) are
+    all-gathered; every rank runs the same deterministic selection
+    (sbr_cir_select) over all rows, so the deduplicated candidate set is
+    replicated; each rank then refines and replays only the records whose
+    rows it produced (LoS records on rank 0), and the valid paths are
+    gathered.  The result equals compute_paths on one GPU.
+    """
+    import torch.distributed as dist
+
+    from .sharding import gather_rows, owned_records, shard_range
+    torch = _torch()
+    transmitters = list(transmitters)
+    receivers = list(receivers)
+    if not transmitters or not receivers:
+        raise ValueError("need at least one transmitter and one receiver")
+    _check_cfg(cfg)
+    on = dist.is_available() and dist.is_initialized()
+    rank = dist.get_rank(group) if on else 0
+    world = dist.get_world_size(group) if on else 1
+    tx_flat, targets, target_devices, rx_index, rx_elem = _device_plan(transmitters, receivers,
+                                                                       cfg)
+    acc = scene.accel
+    dev = acc.device
+    scene.bind_frequency(cfg.frequency)
+    diagnostics = Counter()
+    rejections = Counter()
+    load_factor = 0.0
+    parts = []
+    lo, hi = shard_range(cfg.num_samples, rank, world)
+    for src_idx, (ti, te, tx_pos) in enumerate(tx_flat):
+        source = np.asarray(tx_pos, dtype=np.float64)
+        with torch.cuda.device(dev):
+            R = _sweep_rows(scene, source, targets, cfg, lo, hi)
+            n = R.n
+            local = {"key": R.key, "pr": R.pr[:n], "pf": R.pf[:n], "chain": R.chain[:n]}
+            g, offsets = gather_rows(local, group)
+            sel_counters = torch.zeros(_abi.SBR_CC_COUNT, dtype=torch.int64, device=dev)
+            rec_row, nrec = _select_rows(R.params, g["key"], g["pr"], g["pf"], g["chain"],
+                                         offsets[-1], R.los_vis, cfg, sel_counters, dev)
+            pos, loc = owned_records(rec_row[:nrec].cpu().numpy(), offsets, rank)
+            loc_t = torch.from_numpy(np.ascontiguousarray(loc, dtype=np.int64)).to(dev)
+            recbuf = _materialize(R, loc_t, len(loc), cfg)
+            sweep = R.counters.clone()
+            if on and world > 1:
+                dist.all_reduce(sweep, group=group)
+        c_sweep = _counters_dict(sweep.cpu().numpy())
+        c_sel = _counters_dict(sel_counters.cpu().numpy())
+        if c_sweep["stack_overflow"]:
+            raise RuntimeError("BVH traversal stack overflow")
+        c_sel["samples_escaped"] = c_sweep["samples_escaped"]
+        c_sel["samples_terminated"] = c_sweep["samples_terminated"]
+        gdiag = _gen_diag(c_sel, cfg)
+        load_factor = max(load_factor, gdiag["hash_load_factor"])
+        for k, v in gdiag.items():
+            if k != "hash_load_factor":
+                diagnostics[k] += v
+        cand = DeviceCandidates(scene, source, targets, R.targets_t, cfg, recbuf, len(loc),
+                                src_idx)
+        cand.params = R.params
+        part, rej = _paths_for_source(scene, cand, cfg, ti, te, transmitters[ti],
+                                      target_devices, rx_index, rx_elem)
+        rejections.update(rej)
+        if part is not None:
+            parts.append(part)
+    if on and world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (parts, dict(rejections)), group=group)
+        parts = [p for ps, _ in gathered for p in ps]
+        rejections = Counter()
+        for _, rj in gathered:
+            rejections.update(rj)
+    tensors = _concat_sorted(parts, max(int(cfg.max_depth), 1))
     result = dict(diagnostics)
     result["hash_load_factor"] = load_factor
     result["refinement_rejections"] = dict(rejections)
@@ -770,6 +929,7 @@ def baseband_gains(path_set, transmitter=0, receiver=0):
 __all__ = [
     "DedupTable", "PathBuffer", "InteractionStep", "CandidateRecord", "Rejection",
     "PathGeometry", "ValidPath", "GenerationResult", "PathTensors", "PathSet",
-    "generate_candidates", "refine_candidate", "compute_paths", "frequency_response",
+    "generate_candidates", "refine_candidate", "compute_paths", "compute_paths_sharded",
+    "frequency_response",
     "baseband_gains",
 ]

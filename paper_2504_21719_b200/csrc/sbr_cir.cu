@@ -353,17 +353,42 @@ __global__ void __launch_bounds__(128) k_cir_visibility(DevScene S, SbrCirParams
 // ---------------------------------------------------------------------------
 // selection kernels
 // ---------------------------------------------------------------------------
-// per sorted row: pair hashes and the chain flag (_emit_records 919-924)
-__global__ void k_row_pairs(SbrVertexBuf vb, const uint64_t* __restrict__ skey,
-                            const int32_t* __restrict__ sidx, const int32_t* __restrict__ row_vtx,
-                            int64_t n, uint64_t* pr, uint64_t* pf, uint8_t* chain) {
+// per row: pair hashes and the chain flag (_emit_records 919-924)
+__global__ void k_row_pairs(SbrVertexBuf vb, const uint64_t* __restrict__ key,
+                            const int32_t* __restrict__ row_vtx, int64_t n, uint64_t* pr,
+                            uint64_t* pf, uint8_t* chain) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int v = row_vtx[sidx[i]];
-    const uint64_t k = skey[i] & kTargetMask;
+    const int v = row_vtx[i];
+    const uint64_t k = key[i] & kTargetMask;
     pr[i] = fnv1a_u64(vb.hash_r[v], k);
     pf[i] = fnv1a_u64(vb.hash_f[v], k);
     chain[i] = (vb.suffix_start[v] == 0 && vb.code[v] != 1) ? 1 : 0;
+  }
+}
+
+__global__ void k_gather_u8(const uint8_t* __restrict__ src, const int32_t* __restrict__ idx,
+                            int64_t n, uint8_t* dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[idx[i]];
+}
+
+// record (row or LoS) -> (vertex, target) for k_cir_records
+__global__ void k_resolve_records(const int64_t* __restrict__ rec_row,
+                                  const uint64_t* __restrict__ key,
+                                  const int32_t* __restrict__ row_vtx, int64_t n, int32_t* rec_vtx,
+                                  int32_t* rec_target) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = rec_row[i];
+    if (r < 0) {
+      rec_vtx[i] = -1;
+      rec_target[i] = (int32_t)(~r);
+    } else {
+      rec_vtx[i] = row_vtx[r];
+      rec_target[i] = (int32_t)(key[r] & kTargetMask);
+    }
   }
 }
 
@@ -568,27 +593,24 @@ __global__ void k_buffer_flags(const uint8_t* __restrict__ chain, const int32_t*
 
 __global__ void k_los_buffer(const int64_t* __restrict__ reg_src, const uint8_t* __restrict__ state,
                              const int32_t* __restrict__ los_acc_pos, int n_los_keys,
-                             int64_t n_buffer, int32_t* rec_vtx, int32_t* rec_target) {
+                             int64_t n_buffer, int64_t* rec_row) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n_los_keys; j += gridDim.x * blockDim.x) {
     if (state[j] != 1) continue;
     const int p = los_acc_pos[j];
     if (p >= n_buffer) continue;
-    rec_vtx[p] = -1;
-    rec_target[p] = (int32_t)(~reg_src[j]);
+    rec_row[p] = reg_src[j];  // ~target
   }
 }
 
 __global__ void k_row_buffer(const int32_t* __restrict__ in_buf, const int32_t* __restrict__ buf_pos,
-                             const uint64_t* __restrict__ skey, const int32_t* __restrict__ sidx,
-                             const int32_t* __restrict__ row_vtx, int64_t n, int64_t base,
-                             int64_t n_buffer, int32_t* rec_vtx, int32_t* rec_target) {
+                             const int32_t* __restrict__ sidx, int64_t n, int64_t base,
+                             int64_t n_buffer, int64_t* rec_row) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     if (!in_buf[i]) continue;
     const int64_t p = base + buf_pos[i];
     if (p >= n_buffer) continue;
-    rec_vtx[p] = row_vtx[sidx[i]];
-    rec_target[p] = (int32_t)(skey[i] & kTargetMask);
+    rec_row[p] = sidx[i];  // index into the caller's row arrays
   }
 }
 
@@ -882,13 +904,31 @@ int sbr_cir_visibility(const SbrScene* scene, const SbrCirParams* P, const SbrVe
   return rc;
 }
 
-int sbr_cir_select(const SbrCirParams* P, const SbrVertexBuf* vb, const uint64_t* row_key,
-                   const int32_t* row_vtx, int64_t n, const uint8_t* los, uint64_t n_hash,
-                   int64_t n_buffer, int32_t* rec_vtx, int32_t* rec_target, int64_t* n_records,
-                   uint64_t* counters_u64, void* stream) {
+int sbr_cir_row_pairs(const SbrVertexBuf* vb, const uint64_t* row_key, const int32_t* row_vtx,
+                      int64_t n, uint64_t* pr, uint64_t* pf, uint8_t* chain, void* stream) {
+  if (!vb) return set_error(SBR_ERR_INVALID, "NULL argument");
+  if (n <= 0) return SBR_OK;
+  k_row_pairs<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(*vb, row_key, row_vtx, n, pr,
+                                                                  pf, chain);
+  return launch_status("k_row_pairs");
+}
+
+int sbr_cir_resolve_records(const int64_t* rec_row, int64_t n, const uint64_t* row_key,
+                            const int32_t* row_vtx, int32_t* rec_vtx, int32_t* rec_target,
+                            void* stream) {
+  if (n <= 0) return SBR_OK;
+  k_resolve_records<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(rec_row, row_key, row_vtx,
+                                                                        n, rec_vtx, rec_target);
+  return launch_status("k_resolve_records");
+}
+
+int sbr_cir_select(const SbrCirParams* P, const uint64_t* row_key, const uint64_t* row_pr,
+                   const uint64_t* row_pf, const uint8_t* row_chain, int64_t n,
+                   const uint8_t* los, uint64_t n_hash, int64_t n_buffer, int64_t* rec_row,
+                   int64_t* n_records, uint64_t* counters_u64, void* stream) {
   int rc = check_cir(nullptr, P);
   if (rc) return rc;
-  if (!vb || !n_records || !los) return set_error(SBR_ERR_INVALID, "NULL argument");
+  if (!n_records || !los) return set_error(SBR_ERR_INVALID, "NULL argument");
   if (n_hash < 1 || n_buffer < 1) return set_error(SBR_ERR_INVALID, "capacity must be positive");
   if (n >= (1LL << 31)) return set_error(SBR_ERR_INVALID, "too many rows");
   cudaStream_t st = (cudaStream_t)stream;
@@ -945,8 +985,13 @@ int sbr_cir_select(const SbrCirParams* P, const SbrVertexBuf* vb, const uint64_t
       LK("k_iota");
       CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, row_key, skey, idx0, sidx, (int)n, 0, 64, st));
       count_launch();
-      k_row_pairs<<<grid_for(n, 256), 256, 0, st>>>(*vb, skey, sidx, row_vtx, n, pr, pf, chain);
-      LK("k_row_pairs");
+      // pair hashes / chain flags into ordinal order
+      k_gather_u64<<<grid_for(n, 256), 256, 0, st>>>(row_pr, sidx, n, pr);
+      LK("k_gather_u64");
+      k_gather_u64<<<grid_for(n, 256), 256, 0, st>>>(row_pf, sidx, n, pf);
+      LK("k_gather_u64");
+      k_gather_u8<<<grid_for(n, 256), 256, 0, st>>>(row_chain, sidx, n, chain);
+      LK("k_gather_u8");
       // chain rows (positions in ordinal order)
       int32_t* cpos = A.get<int32_t>(n);
       int32_t* cpos2 = A.get<int32_t>(n);
@@ -1106,8 +1151,7 @@ int sbr_cir_select(const SbrCirParams* P, const SbrVertexBuf* vb, const uint64_t
       CK(cudaMemcpyAsync(los_acc_pos, hlos_acc.data(), sizeof(int32_t) * n_los_keys,
                          cudaMemcpyHostToDevice, st));
       k_los_buffer<<<grid_for(n_los_keys, 256), 256, 0, st>>>(reg_src, state, los_acc_pos,
-                                                             (int)n_los_keys, n_buffer, rec_vtx,
-                                                             rec_target);
+                                                             (int)n_los_keys, n_buffer, rec_row);
       LK("k_los_buffer");
     }
     if (n > 0) {
@@ -1121,8 +1165,8 @@ int sbr_cir_select(const SbrCirParams* P, const SbrVertexBuf* vb, const uint64_t
       CK(cudaMemcpyAsync(&lastk, in_buf + n - 1, 4, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       n_rows_buf = (int64_t)lastp + lastk;
-      k_row_buffer<<<grid_for(n, 256), 256, 0, st>>>(in_buf, buf_pos, skey, sidx, row_vtx, n,
-                                                    n_los_acc, n_buffer, rec_vtx, rec_target);
+      k_row_buffer<<<grid_for(n, 256), 256, 0, st>>>(in_buf, buf_pos, sidx, n, n_los_acc,
+                                                    n_buffer, rec_row);
       LK("k_row_buffer");
     }
     const int64_t total = n_los_acc + n_rows_buf;

@@ -96,3 +96,58 @@ def shard_of_chunks(num_samples, rank, world, chunk=None):
     clo, chi = shard_range(nchunks, rank, world)
     return min(clo * chunk, num_samples), min(chi * chunk, num_samples)
 
+
+
+def gather_rows(tensors, group=None):
+    """All-gather variable-length per-rank row arrays (CIR candidate exchange).
+
+    tensors: dict name -> tensor whose first dimension is this rank's row
+    count (same count for every entry).  Returns (gathered dict, offsets)
+    where rank r's rows occupy [offsets[r], offsets[r+1]).  One all_gather
+    of the counts, then one padded all_gather per array -- NCCL over NVLink
+    on the GPU box, gloo in the CPU tests.  uint64 payloads travel as int64
+    (bit-identical).
+    """
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        n = next(iter(tensors.values())).shape[0]
+        return dict(tensors), [0, n]
+    world = dist.get_world_size(group)
+    first = next(iter(tensors.values()))
+    dev = first.device
+    n_local = torch.tensor([first.shape[0]], dtype=torch.int64, device=dev)
+    sizes = [torch.zeros_like(n_local) for _ in range(world)]
+    dist.all_gather(sizes, n_local, group=group)
+    sizes = [int(s.item()) for s in sizes]
+    m = max(max(sizes), 1)
+    offsets = [0]
+    for s_ in sizes:
+        offsets.append(offsets[-1] + s_)
+    out = {}
+    for name, t in tensors.items():
+        wire = t.view(torch.int64) if t.dtype == torch.uint64 else t
+        pad = torch.zeros((m,) + tuple(wire.shape[1:]), dtype=wire.dtype, device=dev)
+        pad[:wire.shape[0]] = wire
+        parts = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(parts, pad, group=group)
+        cat = torch.cat([p[:s_] for p, s_ in zip(parts, sizes)])
+        out[name] = cat.view(torch.uint64) if t.dtype == torch.uint64 else cat
+    return out, offsets
+
+
+def owned_records(rec_row, offsets, rank):
+    """Records this rank materialises: rows it produced, plus LoS records on rank 0.
+
+    rec_row: selected entries (index into the gathered rows, or ~target < 0).
+    Returns (positions in rec_row, local row indices / LoS codes).
+    """
+    import numpy as np
+    rr = np.asarray(rec_row)
+    lo, hi = offsets[rank], offsets[rank + 1]
+    mine = (rr >= lo) & (rr < hi)
+    if rank == 0:
+        mine |= rr < 0
+    pos = np.nonzero(mine)[0]
+    local = np.where(rr[pos] >= 0, rr[pos] - lo, rr[pos])
+    return pos, local

@@ -85,3 +85,68 @@ def test_two_rank_gloo_map_equals_single_rank(tmp_path, case):
         c = np.load(tmp_path / f"cnt_{r}.npy")
         np.testing.assert_allclose(v, full.numpy(), rtol=1e-12, atol=0)
         assert np.array_equal(c, fcnt.numpy())
+
+
+# ---------------------------------------------------------------------------
+# CIR: sample shards -> all-gathered candidate rows -> one global selection
+
+def _cir_case():
+    from test_oracle_cir import oracle_case
+    sc, cfg, txs, rxs = oracle_case("box_trunc")
+    targets = np.array([r.position for r in rxs])
+    return sc, cfg, txs[0].position, targets
+
+
+def _cir_worker(rank, world, port, out_dir):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, here)
+    sys.path.insert(0, os.path.dirname(here))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2504_21719_b200.sharding import gather_rows, owned_records
+        sc, cfg, src, targets = _cir_case()
+        lo, hi = shard_range(cfg.num_samples, rank, world)
+        rows, _ = sc.cir_rows(src, targets, cfg, lo, hi)
+        local = {k: torch.from_numpy(v) for k, v in rows.items()}
+        g, offsets = gather_rows(local)
+        gathered = {k: v.numpy() for k, v in g.items()}
+        rec_row, counters = sc.cir_select(src, targets, cfg, gathered)
+        pos, loc = owned_records(rec_row, offsets, rank)
+        # this rank's records, identified by (ordinal key or LoS code)
+        keys = np.where(loc >= 0, rows["key"][np.maximum(loc, 0)] if len(rows["key"]) else 0,
+                        loc.astype(np.int64).view(np.uint64))
+        np.save(os.path.join(out_dir, f"keys_{rank}.npy"), keys.astype(np.uint64))
+        np.save(os.path.join(out_dir, f"pos_{rank}.npy"), pos)
+        np.save(os.path.join(out_dir, f"cnt_{rank}.npy"), counters)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_cir_selection_equals_single_rank(tmp_path):
+    """Global dedup over all-gathered rows == the reference's single-chunk selection."""
+    world = 2
+    mp.start_processes(_cir_worker, args=(world, _free_port(), str(tmp_path)),
+                       nprocs=world, join=True, start_method="spawn")
+    sc, cfg, src, targets = _cir_case()
+    rows, _ = sc.cir_rows(src, targets, cfg, 0, cfg.num_samples)
+    rec_row, counters = sc.cir_select(src, targets, cfg, rows)
+    want = np.where(rec_row >= 0, rows["key"][np.maximum(rec_row, 0)],
+                    rec_row.astype(np.int64).view(np.uint64))
+    got = np.zeros(len(want), np.uint64)
+    seen = np.zeros(len(want), bool)
+    for r in range(world):
+        pos = np.load(tmp_path / f"pos_{r}.npy")
+        got[pos] = np.load(tmp_path / f"keys_{r}.npy")
+        assert not seen[pos].any()
+        seen[pos] = True
+        # every rank computes identical selection counters (dedup, truncation, overflow)
+        assert np.array_equal(np.load(tmp_path / f"cnt_{r}.npy")[5:], counters[5:])
+    assert seen.all()
+    assert np.array_equal(got, want)
+    # and the oracle's row/select split equals its one-shot generation
+    rec, diag = sc.generate_candidates(src, targets, cfg)
+    assert len(rec["sample"]) == len(want)
+    assert diag["chunk_truncated"] > 0 and diag["buffer_overflow"] > 0

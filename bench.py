@@ -367,8 +367,8 @@ def run_ours(args, rank, world, local_rank):
                          f"ray-bounces in {dt:.2f} s on {threads} threads"}
 
     cir = None
-    if world == 1 and not args.no_cir:
-        cir = bench_cir(args, dev)
+    if not args.no_cir:
+        cir = bench_cir(args, dev, rank, world)
 
     if rank == 0:
         line = {
@@ -398,15 +398,19 @@ def run_ours(args, rank, world, local_rank):
         print(json.dumps(line), flush=True)
 
 
-def bench_cir(args, dev):
+def bench_cir(args, dev, rank=0, world=1):
     """Config 3: city CIR, 1 Tx x 1024 Rx, N_S = 1e6, depth 5, {R} (BASELINE configs[2]).
 
-    ms per compute_paths call (generation + dedup + refinement + fields, host
-    PathTensors out) timed with CUDA events on the current stream.
+    ms per solve (generation + dedup + refinement + fields, host PathTensors
+    out) timed with CUDA events on the current stream, max over ranks.  With
+    N > 1 GPUs the solve is compute_paths_sharded: sample shards per rank,
+    all-gathered candidate rows, replicated global selection (strong scaling:
+    the same 1e6-sample solve split over the ranks).
     """
     import torch
-    from paper_2504_21719_b200 import (PathConfig, RadioDevice, SceneModel, _native,
-                                       compute_paths, scenes)
+    import torch.distributed as dist
+    from paper_2504_21719_b200 import (PathConfig, RadioDevice, SceneModel, _native, scenes)
+    from paper_2504_21719_b200.cir import compute_paths_sharded as compute_paths
     from paper_2504_21719_b200.sampling import Interaction
     t0 = time.perf_counter()
     meshes = scenes.city()
@@ -431,9 +435,14 @@ def bench_cir(args, dev):
     n = len(times)
     split = {k: _native.profile_kernel_ms(k)[0] / n for k in ("k_cir_sweep", "k_cir_visibility")}
     _native.profile_enable(False)
+    ms = float(np.mean(times))
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
     d = ps.diagnostics
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and rank == 0 and world == 1:
         # oracle port (oracle/sbr_oracle.c, single thread like the reference's
         # default workers=1) on a bounded sample, extrapolated linearly in N_S
         import oracle
@@ -449,7 +458,8 @@ def bench_cir(args, dev):
                          f"extrapolated linearly in N_S"}
     return {"workload": "config3: procedural city (483,200 tris) CIR, 1 Tx x 1024 Rx, "
                         "N_S=1e6, depth 5, {R}, hash dedup + image-method refine",
-            "ms_per_solve": float(np.mean(times)), "solves": n, "paths": d["paths"],
+            "ms_per_solve": ms, "solves": n, "paths": d["paths"], "n_gpus": world,
+            "scaling": "strong",
             "candidates": d["candidates"], "duplicates": d["duplicates"],
             "refinement_rejections": d["refinement_rejections"],
             "kernel_ms_per_solve": split, "scene_build_s": build_s, "cpu_baseline": cpu,

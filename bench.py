@@ -312,7 +312,7 @@ def run_ours(args, rank, world, local_rank):
         step()
     torch.cuda.synchronize()
     kernels = {}
-    for name in ("k_map_trace", "k_map_shade"):
+    for name in ("k_map_trace", "k_map_shade", "k_map_scatter"):
         ms, nl = _native.profile_kernel_ms(name)
         kernels[name] = {"ms_per_step": ms / prof_steps, "launches_per_step": nl / prof_steps}
     _native.profile_enable(False)

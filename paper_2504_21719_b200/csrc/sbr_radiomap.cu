@@ -58,6 +58,16 @@ struct HitBuf {
   int32_t* tri;
 };
 
+// diffuse-scattering work items, deferred from k_map_shade to k_map_scatter so
+// the expensive S update runs with full warps instead of ~3 lanes per warp
+struct ScatterQueue {
+  double *dx, *dy, *dz, *nx, *ny, *nz, *px, *py, *pz;
+  double *exr, *exi, *eyr, *eyi, *ezr, *ezi;
+  double *omega, *r_hit, *weight, *cos_i, *gamma;
+  uint64_t* g;
+  int32_t* matrow;
+};
+
 __device__ __forceinline__ unsigned long long append_slot(unsigned long long* counter) {
   cg::coalesced_group grp = cg::coalesced_threads();
   unsigned long long base = 0;
@@ -134,10 +144,11 @@ struct LaneCounters {
   unsigned rb, deposits, escaped, respawns, terminated, thr, rr;
 };
 
-__global__ void __launch_bounds__(128, 4) k_map_shade(DevScene S, SbrMapParams P, int seg,
+__global__ void __launch_bounds__(128, 5) k_map_shade(DevScene S, SbrMapParams P, int seg,
                                                    MapQueue qi, const unsigned long long* count_in,
                                                    uint64_t begin, uint64_t comb_q, HitBuf hits,
                                                    MapQueue qo, unsigned long long* count_out,
+                                                   ScatterQueue sq, unsigned long long* count_s,
                                                    double* __restrict__ grid,
                                                    unsigned long long* __restrict__ counters) {
   LaneCounters K = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
@@ -270,49 +281,34 @@ __global__ void __launch_bounds__(128, 4) k_map_shade(DevScene S, SbrMapParams P
     }
     r_dist = r_hit;
     if (code == 1) {
-      const double u0 = philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_RESPAWN, 2 * slot);
-      const double u1 = philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_RESPAWN, 2 * slot + 1);
-      const double cos_t = u0, azim = kTwoPi * u1;
-      const double x = 1.0 - cos_t * cos_t;
-      const double sin_t = sqrt(x > 0.0 ? x : 0.0);
-      const double3 t1 = perp_batch(nrm);
-      const double3 t2 = cross3(nrm, t1);
-      double sa, ca;
-      sincos(azim, &sa, &ca);
-      const double a = sin_t * ca, b = sin_t * sa;
-      const double3 ks = make_double3((a * t1.x + b * t2.x) + cos_t * nrm.x,
-                                      (a * t1.y + b * t2.y) + cos_t * nrm.y,
-                                      (a * t1.z + b * t2.z) + cos_t * nrm.z);
+      // gamma_reflected (materials.py:400-419) here, the rest in k_map_scatter
       const double g_num = sqrt(cabs2(F.rp * c_perp) + cabs2(F.rl * c_par));
       const double g_den = sqrt(cabs2(c_perp) + cabs2(c_par));
       const double gamma = g_den > 0.0 ? g_num / g_den : 0.0;
-      const double f_s = pattern_density(m, d, ks, nrm);
-      const double patch = omega * (r_hit * r_hit) / (cos_i > 1e-12 ? cos_i : 1e-12);
-      const double amp = m.scattering * gamma * sqrt(f_s * cos_i * patch);
-      double3 th_i, ph_i;
-      transverse_rows(d, th_i, ph_i);
-      const cplx ci0 = cdot_real(E, th_i), ci1 = cdot_real(E, ph_i);
-      double chi1 = 0.0, chi2 = 0.0;
-      if (P.any_random_phase && m.random_phases) {
-        chi1 = kTwoPi * philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_PHASE, 2 * slot);
-        chi2 = kTwoPi * philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_PHASE, 2 * slot + 1);
-      }
-      const double sq = sqrt(1.0 - m.xpd_kx), sk = sqrt(m.xpd_kx);
-      double s1, k1, s2, k2;
-      sincos(chi1, &s1, &k1);
-      sincos(chi2, &s2, &k2);
-      const cplx co0 = C(amp * k1, amp * s1) * (sq * ci0 - sk * ci1);
-      const cplx co1 = C(amp * k2, amp * s2) * (sk * ci0 + sq * ci1);
-      double3 th_s, ph_s;
-      transverse_rows(ks, th_s, ph_s);
-      const cplx inv_r = C(r_hit, 0.0);
-      E.x = cdiv(th_s.x * co0 + ph_s.x * co1, inv_r);
-      E.y = cdiv(th_s.y * co0 + ph_s.y * co1, inv_r);
-      E.z = cdiv(th_s.z * co0 + ph_s.z * co1, inv_r);
-      nd = ks;
-      r_dist = 0.0;
-      omega = kTwoPi;
-      K.respawns++;
+      const unsigned long long j = append_slot(count_s);
+      sq.dx[j] = d.x;
+      sq.dy[j] = d.y;
+      sq.dz[j] = d.z;
+      sq.nx[j] = nrm.x;
+      sq.ny[j] = nrm.y;
+      sq.nz[j] = nrm.z;
+      sq.px[j] = pt.x;
+      sq.py[j] = pt.y;
+      sq.pz[j] = pt.z;
+      sq.exr[j] = E.x.re;
+      sq.exi[j] = E.x.im;
+      sq.eyr[j] = E.y.re;
+      sq.eyi[j] = E.y.im;
+      sq.ezr[j] = E.z.re;
+      sq.ezi[j] = E.z.im;
+      sq.omega[j] = omega;
+      sq.r_hit[j] = r_hit;
+      sq.weight[j] = weight;
+      sq.cos_i[j] = cos_i;
+      sq.gamma[j] = gamma;
+      sq.g[j] = g;
+      sq.matrow[j] = __ldg(S.matrow + tri);
+      continue;
     }
     const unsigned long long j = append_slot(count_out);
     qo.ox[j] = pt.x;
@@ -343,9 +339,92 @@ __global__ void __launch_bounds__(128, 4) k_map_shade(DevScene S, SbrMapParams P
   }
 }
 
-__global__ void k_reset_pass(unsigned long long* work, unsigned long long* count_next) {
+// diffuse scattering update (radiomap.py:496-558) for the deferred S items
+__global__ void __launch_bounds__(128, 4) k_map_scatter(DevScene S, SbrMapParams P, int seg,
+                                                        ScatterQueue sq,
+                                                        const unsigned long long* count_s,
+                                                        MapQueue qo, unsigned long long* count_out,
+                                                        unsigned long long* __restrict__ counters) {
+  unsigned respawns = 0;
+  const uint64_t n = *count_s;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t g = sq.g[j];
+    const uint64_t chunk = g >> SBR_CHUNK_LOG2;
+    const uint64_t slot = g & ((1ULL << SBR_CHUNK_LOG2) - 1);
+    const double3 d = make_double3(sq.dx[j], sq.dy[j], sq.dz[j]);
+    const double3 nrm = make_double3(sq.nx[j], sq.ny[j], sq.nz[j]);
+    cvec3 E;
+    E.x = C(sq.exr[j], sq.exi[j]);
+    E.y = C(sq.eyr[j], sq.eyi[j]);
+    E.z = C(sq.ezr[j], sq.ezi[j]);
+    const double omega = sq.omega[j], r_hit = sq.r_hit[j], cos_i = sq.cos_i[j];
+    const double gamma = sq.gamma[j];
+    const SbrMaterial m = S.mats[sq.matrow[j]];
+    const double u0 = philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_RESPAWN, 2 * slot);
+    const double u1 = philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_RESPAWN, 2 * slot + 1);
+    const double cos_t = u0, azim = kTwoPi * u1;
+    const double x = 1.0 - cos_t * cos_t;
+    const double sin_t = sqrt(x > 0.0 ? x : 0.0);
+    const double3 t1 = perp_batch(nrm);
+    const double3 t2 = cross3(nrm, t1);
+    double sa, ca;
+    sincos(azim, &sa, &ca);
+    const double a = sin_t * ca, b = sin_t * sa;
+    const double3 ks = make_double3((a * t1.x + b * t2.x) + cos_t * nrm.x,
+                                    (a * t1.y + b * t2.y) + cos_t * nrm.y,
+                                    (a * t1.z + b * t2.z) + cos_t * nrm.z);
+    const double f_s = pattern_density(m, d, ks, nrm);
+    const double patch = omega * (r_hit * r_hit) / (cos_i > 1e-12 ? cos_i : 1e-12);
+    const double amp = m.scattering * gamma * sqrt(f_s * cos_i * patch);
+    double3 th_i, ph_i;
+    transverse_rows(d, th_i, ph_i);
+    const cplx ci0 = cdot_real(E, th_i), ci1 = cdot_real(E, ph_i);
+    double chi1 = 0.0, chi2 = 0.0;
+    if (P.any_random_phase && m.random_phases) {
+      chi1 = kTwoPi * philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_PHASE, 2 * slot);
+      chi2 = kTwoPi * philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_PHASE, 2 * slot + 1);
+    }
+    const double sqk = sqrt(1.0 - m.xpd_kx), sk = sqrt(m.xpd_kx);
+    double s1, k1, s2, k2;
+    sincos(chi1, &s1, &k1);
+    sincos(chi2, &s2, &k2);
+    const cplx co0 = C(amp * k1, amp * s1) * (sqk * ci0 - sk * ci1);
+    const cplx co1 = C(amp * k2, amp * s2) * (sk * ci0 + sqk * ci1);
+    double3 th_s, ph_s;
+    transverse_rows(ks, th_s, ph_s);
+    const cplx inv_r = C(r_hit, 0.0);
+    E.x = cdiv(th_s.x * co0 + ph_s.x * co1, inv_r);
+    E.y = cdiv(th_s.y * co0 + ph_s.y * co1, inv_r);
+    E.z = cdiv(th_s.z * co0 + ph_s.z * co1, inv_r);
+    respawns++;
+    const unsigned long long o = append_slot(count_out);
+    qo.ox[o] = sq.px[j];
+    qo.oy[o] = sq.py[j];
+    qo.oz[o] = sq.pz[j];
+    qo.dx[o] = ks.x;
+    qo.dy[o] = ks.y;
+    qo.dz[o] = ks.z;
+    qo.exr[o] = E.x.re;
+    qo.exi[o] = E.x.im;
+    qo.eyr[o] = E.y.re;
+    qo.eyi[o] = E.y.im;
+    qo.ezr[o] = E.z.re;
+    qo.ezi[o] = E.z.im;
+    qo.r_dist[o] = 0.0;
+    qo.omega[o] = kTwoPi;
+    qo.weight[o] = sq.weight[j];
+    qo.g[o] = g;
+  }
+  const unsigned s = __reduce_add_sync(0xffffffffu, respawns);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(counters + SBR_MC_RESPAWNS, (unsigned long long)s);
+}
+
+__global__ void k_reset_pass(unsigned long long* work, unsigned long long* count_next,
+                             unsigned long long* count_s) {
   *work = 0ULL;
   *count_next = 0ULL;
+  *count_s = 0ULL;
 }
 
 __global__ void __launch_bounds__(128) k_direct(DevScene S, SbrMapParams P,
@@ -408,12 +487,15 @@ struct Wave {
   void* block = nullptr;
   MapQueue q[2];
   HitBuf hits;
-  unsigned long long* ctl = nullptr;  // [0] work, [1] count A, [2] count B
+  ScatterQueue sq;
+  unsigned long long* ctl = nullptr;  // [0] work, [1] count A, [2] count B, [3] S count
 };
 
 int wave_alloc(int64_t cap, cudaStream_t st, Wave* w) {
   const size_t per_queue = (size_t)cap * (16 * sizeof(double));
-  const size_t bytes = 2 * per_queue + (size_t)cap * (sizeof(double) + sizeof(int32_t)) + 512;
+  const size_t per_squeue = (size_t)cap * (21 * sizeof(double) + sizeof(int32_t));
+  const size_t bytes = 2 * per_queue + per_squeue +
+                       (size_t)cap * (sizeof(double) + sizeof(int32_t)) + 512;
   if (cudaMallocAsync(&w->block, bytes, st) != cudaSuccess)
     return set_error(SBR_ERR_NOMEM, "ray queues");
   char* p = (char*)w->block;
@@ -428,6 +510,21 @@ int wave_alloc(int64_t cap, cudaStream_t st, Wave* w) {
     }
     w->q[k].g = (uint64_t*)p;
     p += cap * sizeof(uint64_t);
+  }
+  {
+    double** f[20] = {&w->sq.dx, &w->sq.dy, &w->sq.dz, &w->sq.nx, &w->sq.ny, &w->sq.nz,
+                      &w->sq.px, &w->sq.py, &w->sq.pz, &w->sq.exr, &w->sq.exi, &w->sq.eyr,
+                      &w->sq.eyi, &w->sq.ezr, &w->sq.ezi, &w->sq.omega, &w->sq.r_hit,
+                      &w->sq.weight, &w->sq.cos_i, &w->sq.gamma};
+    for (int i = 0; i < 20; ++i) {
+      *f[i] = (double*)p;
+      p += cap * sizeof(double);
+    }
+    w->sq.g = (uint64_t*)p;
+    p += cap * sizeof(uint64_t);
+    w->sq.matrow = (int32_t*)p;
+    p += cap * sizeof(int32_t);
+    p = (char*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
   }
   w->hits.t = (double*)p;
   p += cap * sizeof(double);
@@ -472,7 +569,7 @@ int sbr_radiomap_bounce(const SbrScene* scene, const SbrMapParams* P, uint64_t s
     int cur = 0;
     for (int seg = 0; seg <= P->max_depth; ++seg) {
       // ctl[0] = work counter; ctl[1 + cur] = this segment's count; ctl[2 - cur] = next count
-      k_reset_pass<<<1, 1, 0, st>>>(w->ctl, w->ctl + 2 - cur);
+      k_reset_pass<<<1, 1, 0, st>>>(w->ctl, w->ctl + 2 - cur, w->ctl + 3);
       if ((rc = launch_status("k_reset_pass"))) break;
       prof_begin(st, "k_map_trace");
       k_map_trace<<<trace_blocks, 128, 0, st>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo, cnt,
@@ -482,9 +579,16 @@ int sbr_radiomap_bounce(const SbrScene* scene, const SbrMapParams* P, uint64_t s
       prof_begin(st, "k_map_shade");
       k_map_shade<<<shade_blocks, 128, 0, st>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo,
                                                 comb_q, w->hits, w->q[1 - cur], w->ctl + 2 - cur,
-                                                grid, counters);
+                                                w->sq, w->ctl + 3, grid, counters);
       prof_end(st);
       if ((rc = launch_status("k_map_shade"))) break;
+      if (seg < P->max_depth && (P->allow_mask & 2)) {
+        prof_begin(st, "k_map_scatter");
+        k_map_scatter<<<shade_blocks, 128, 0, st>>>(S, *P, seg, w->sq, w->ctl + 3, w->q[1 - cur],
+                                                    w->ctl + 2 - cur, counters);
+        prof_end(st);
+        if ((rc = launch_status("k_map_scatter"))) break;
+      }
       cur = 1 - cur;
     }
     if (rc) break;

@@ -8,7 +8,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --
    --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline \
    > gpurun_out/ncu_launches.log 2>&1
 for k in k_map_trace k_map_shade; do
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -c 1 \
      -o gpurun_out/$k -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-cir \
      > gpurun_out/ncu_$k.log 2>&1
 done

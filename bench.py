@@ -20,6 +20,8 @@ roofline   : dominant kernel of the wavefront (k_map_trace / k_map_shade, timed
              launch time, vs measured HBM GB/s
 cir        : config 3 (city, 1 Tx x 1024 Rx, N_S = 1e6, depth 5): ms per
              compute_paths solve (the CIR half of the BASELINE metric)
+config4    : city radio map, 1e9 rays strong-scaled over the N GPUs (the
+             multi-GPU radio-map config of BASELINE.json), rb/s
 cpu_baseline: the CPU oracle port (oracle/, scalar C restatement of the
              reference loop) on this host's cores over a bounded subsample
 --impl reference: that CPU port alone, on all host threads, same metric.
@@ -44,6 +46,7 @@ UNIT = "ray-bounces/s"
 SAMPLES_PER_GPU = 10_000_000
 CIR_SAMPLES = 1_000_000
 CIR_CPU_SAMPLES = 2_000
+C4_SAMPLES = 1_000_000_000
 BYTES_PER_RB = 176  # 64 B ray state in + 64 B out + 48 B hit triangle
 TX = (0.0, 5.0, 20.0)
 
@@ -369,6 +372,9 @@ def run_ours(args, rank, world, local_rank):
     cir = None
     if not args.no_cir:
         cir = bench_cir(args, dev, rank, world)
+    c4 = None
+    if not args.no_config4:
+        c4 = bench_config4(args, dev, rank, world)
 
     if rank == 0:
         line = {
@@ -390,12 +396,68 @@ def run_ours(args, rank, world, local_rank):
                          "bounce_call_ms_per_step": float(kern_ms.mean()),
                          "kernels": kernels, "peak_source": peak_kind},
             "cir": cir,
+            "config4": c4,
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
             "ray_bounces_per_step": rb_total // args.steps,
         }
         print(json.dumps(line), flush=True)
+
+
+def bench_config4(args, dev, rank=0, world=1):
+    """Config 4: city radio map, 1e9 rays over all N GPUs (strong scaling), 1 m cells.
+
+    1000 x 1000 cells at z = 1.5, Tx (0, 0, 30), {R, S} depth 5.  Each rank
+    traces its contiguous shard of the 1e9 global sample ids; one NCCL
+    all-reduce of the float64 grid (8 MB) and the counters; rank 0 adds the
+    direct term.  Device time per map (max over ranks), CUDA events.
+    """
+    import torch
+    import torch.distributed as dist
+    from paper_2504_21719_b200 import SceneModel, _abi, scenes
+    from paper_2504_21719_b200.radiomap import (MeasurementGrid, RadioMapConfig,
+                                                compute_radio_map_sbr)
+    from paper_2504_21719_b200.sampling import Interaction
+    from paper_2504_21719_b200.sharding import allreduce_map, shard_range
+    meshes = scenes.city()
+    scene = SceneModel(meshes, scenes.uniform_materials(meshes, scenes.concrete(scattering=0.3)),
+                       device=dev)
+    grid = MeasurementGrid((0.0, 0.0, 1.5), (1, 0, 0), (0, 1, 0), (1.0, 1.0), (1000, 1000))
+    cfg = RadioMapConfig(num_samples=C4_SAMPLES, max_depth=5, seed=0,
+                         enabled=frozenset({Interaction.REFLECTION, Interaction.SCATTERING}))
+    lo, hi = shard_range(C4_SAMPLES, rank, world)
+    stream = torch.cuda.current_stream(dev)
+
+    def one():
+        v, c = compute_radio_map_sbr(scene, (0.0, 0.0, 30.0), grid, cfg, sample_range=(lo, hi),
+                                     include_direct=(rank == 0), return_tensors=True)
+        allreduce_map(v, c)
+        return v, c
+
+    one()
+    torch.cuda.synchronize()
+    times, rbs = [], []
+    for _ in range(max(1, min(args.steps, 2))):
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        v, c = one()
+        b.record(stream)
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b))
+        rbs.append(int(c[_abi.MAP_COUNTERS.index("ray_bounces")].item()))
+    ms = float(np.mean(times))
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    return {"workload": "config4: procedural city (483,200 tris) radio map, 1e9 rays sharded "
+                        "over the N GPUs, 1000x1000 cells of 1 m, {R,S} depth 5, Tx (0,0,30)",
+            "value": rbs[-1] / (ms / 1e3), "unit": "ray-bounces/s", "ms_per_map": ms,
+            "ray_bounces_per_map": rbs[-1], "n_gpus": world, "scaling": "strong",
+            "maps": len(times)}
 
 
 def bench_cir(args, dev, rank=0, world=1):
@@ -474,6 +536,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cir", action="store_true")
+    ap.add_argument("--no-config4", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

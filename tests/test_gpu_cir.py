@@ -258,3 +258,28 @@ def test_sharded_selection_matches_single_gpu(cuda, name):
     # the public entry point on a single rank
     ps = cir.compute_paths_sharded(scene, txs[:1], rxs, cfg)
     assert np.array_equal(ps.tensors.chain_hash, ref.chain_hash)
+
+
+def test_config5_arrays_cfr_city_vs_oracle(cuda):
+    """Config 5: city, 8x8 TR 38.901 Tx panel, 4x4 Rx panel, depth 6, CFR over 1024 subcarriers."""
+    import oracle
+    from paper_2504_21719_b200 import scenes
+    from paper_2504_21719_b200.em import planar_array
+    meshes = scenes.city()
+    mats = scenes.uniform_materials(meshes, scenes.concrete())
+    lam = 299792458.0 / 3.5e9
+    tx = RadioDevice(position=np.array([0.0, 0.0, 30.0]), pattern=make_pattern("tr38901"),
+                     array=planar_array(8, 8, lam / 2, lam / 2))
+    rx = RadioDevice(position=np.array([2.0, 60.0, 1.5]), array=planar_array(4, 4, lam / 2,
+                                                                             lam / 2))
+    cfg = PathConfig(num_samples=100_000, max_depth=6, q_diffraction=0.0,
+                     enabled=frozenset({Interaction.REFLECTION}))
+    freqs = 3.5e9 + (np.arange(1024) - 512) * 30e3
+    ps = compute_paths(SceneModel(meshes, mats), [tx], [rx], cfg)
+    H = frequency_response(ps, freqs)
+    want, wdiag = oracle.OracleScene(meshes, mats).compute_paths([tx], [rx], cfg)
+    assert len(ps.tensors) == len(want["delay"]) and len(want["delay"]) > 0
+    assert np.array_equal(ps.tensors.chain_hash, want["chain_hash"])
+    wh = oracle.frequency_response(want, cfg, tx, rx, freqs)
+    assert H.shape == (16, 64, 1024)
+    assert np.abs(H - wh).max() / np.abs(wh).max() < 1e-9

@@ -116,3 +116,20 @@ def test_threshold_only_removes_energy(cuda):
     v2, d2 = compute_radio_map_sbr(scene, src, grid, thr)
     assert d2["threshold_killed"] > 0 and d0.get("threshold_killed", 0) == 0
     assert np.all(v2 <= v0 + 1e-18)
+
+
+def test_city_map_config4_shard_vs_oracle(cuda):
+    """Config 4 (city, 1000x1000 cells of 1 m, 1e9-sample lattice): a 1e5-sample shard."""
+    meshes = scenes.city()
+    mats = scenes.uniform_materials(meshes, scenes.concrete(scattering=0.3))
+    grid = MeasurementGrid((0.0, 0.0, 1.5), (1, 0, 0), (0, 1, 0), (1.0, 1.0), (1000, 1000))
+    cfg = RadioMapConfig(num_samples=1_000_000_000, max_depth=5, enabled=RS, seed=0)
+    rng = (123_456_789, 123_556_789)
+    src = np.array([0.0, 0.0, 30.0])
+    vals, diag = compute_radio_map_sbr(SceneModel(meshes, mats), src, grid, cfg,
+                                       sample_range=rng, include_direct=False)
+    want, wdiag = oracle.OracleScene(meshes, mats).radiomap(src, grid, cfg, sample_range=rng,
+                                                            include_direct=False)
+    for key in ("deposits", "escaped", "respawns", "ray_bounces"):
+        assert diag.get(key, 0) == wdiag[key], key
+    _compare(vals, want)

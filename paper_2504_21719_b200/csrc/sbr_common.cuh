@@ -277,6 +277,7 @@ __device__ __forceinline__ Ray64 ray_setup(double3 o, double3 d) {
 // Same test as tri_hit, loading the corners' kx/ky/kz components by index
 // (a TriSlot is 9 contiguous doubles v0 v1 v2) instead of selecting them from
 // registers: identical arithmetic, ~40 fewer instructions per triangle.
+template <bool kUV = true>
 __device__ __forceinline__ bool tri_hit_idx(const Ray64& r, const TriSlot* __restrict__ tri,
                                             double t_min, double& t_out, double& u_out,
                                             double& v_out) {
@@ -300,8 +301,10 @@ __device__ __forceinline__ bool tri_hit_idx(const Ray64& r, const TriSlot* __res
   const double t = t_num / det;
   if (!(t > t_min)) return false;
   t_out = t;
-  u_out = v / det;
-  v_out = w / det;
+  if (kUV) {
+    u_out = v / det;
+    v_out = w / det;
+  }
   return true;
 }
 
@@ -498,7 +501,9 @@ __device__ __forceinline__ int ww_pop(const int* stack_node, const float* stack_
 
 // Resumable per-lane closest-hit traversal state.  round() runs one
 // inner-node phase + one leaf phase (while-while); done() reports completion.
-struct ClosestTrav {
+// kUV = false skips the barycentric (u, v) divisions (radio map, CIR sweep).
+template <bool kUV = true>
+struct ClosestTravT {
   Ray64 r;
   RayBox rb;
   double t_min, best_t, bu, bv;
@@ -582,10 +587,11 @@ struct ClosestTrav {
 #endif
       for (int j = s; j < s + n; ++j) {
         double t, u, v;
+        u = v = 0.0;
 #ifdef SBR_TRI_SELECT
         if (tri_hit(r, S.tris + j, t_min, t, u, v)) {
 #else
-        if (tri_hit_idx(r, S.tris + j, t_min, t, u, v)) {
+        if (tri_hit_idx<kUV>(r, S.tris + j, t_min, t, u, v)) {
 #endif
           const int rank = __ldg(S.tie_rank + j);
           if (t < best_t || (t == best_t && best >= 0 && rank < best_rank)) {
@@ -698,6 +704,8 @@ struct AnyTrav {
     }
   }
 };
+
+using ClosestTrav = ClosestTravT<true>;
 
 // One-shot warp-cooperative closest hit (all lanes call; inactive lanes vote).
 __device__ __forceinline__ bool trace_closest_ww(const DevScene& S, bool active, double3 o,

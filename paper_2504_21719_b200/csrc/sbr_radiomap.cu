@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(128) k_map_trace(DevScene S, SbrMapParams P, i
         d = make_double3(q.dx[i], q.dy[i], q.dz[i]);
       }
     }
-    ClosestTrav T;
+    ClosestTravT<false> T;  // the map needs t and the slot only
     T.start(S, o, d, 1e-4, __longlong_as_double(0x7ff0000000000000LL));
     if (!active) T.idle();
     while (!T.done()) T.round(S);

@@ -20,20 +20,32 @@ using namespace sbr;
 
 namespace {
 
+// Batched queries: every warp takes 32 consecutive rays and traces them
+// together with the while-while traversals of sbr_common.cuh (grid-stride
+// over warp batches, so all lanes reach the warp votes together).
 __global__ void __launch_bounds__(128) k_trace_closest(DevScene S, const double* __restrict__ o,
                                                        const double* __restrict__ d, double t_min,
                                                        const double* __restrict__ t_max, int64_t n,
                                                        double* t_out, int64_t* tri_out,
                                                        double* u_out, double* v_out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    HitRecord h;
-    if (!trace_closest(S, ldg3(o + 3 * i), ldg3(d + 3 * i), t_min, __ldg(t_max + i), h))
-      flag_error(S, kErrStack);
-    t_out[i] = h.t;
-    tri_out[i] = h.tri;
-    u_out[i] = h.u;
-    v_out[i] = h.v;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  const int64_t wid = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  for (int64_t base = wid * 32; base < n; base += warps * 32) {
+    const int64_t i = base + (threadIdx.x & 31);
+    const bool active = i < n;
+    ClosestTrav T;
+    if (active) T.start(S, ldg3(o + 3 * i), ldg3(d + 3 * i), t_min, __ldg(t_max + i));
+    else T.idle();
+    while (!T.done()) T.round(S);
+    if (active) {
+      if (!T.ok) flag_error(S, kErrStack);
+      HitRecord h;
+      T.result(h);
+      t_out[i] = h.t;
+      tri_out[i] = h.tri;
+      u_out[i] = h.u;
+      v_out[i] = h.v;
+    }
   }
 }
 
@@ -41,24 +53,57 @@ __global__ void __launch_bounds__(128) k_trace_any(DevScene S, const double* __r
                                                    const double* __restrict__ d, double t_min,
                                                    const double* __restrict__ t_max, int64_t n,
                                                    uint8_t* out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    bool found;
-    if (!trace_any(S, ldg3(o + 3 * i), ldg3(d + 3 * i), t_min, __ldg(t_max + i), found))
-      flag_error(S, kErrStack);
-    out[i] = found ? 1 : 0;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  const int64_t wid = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  for (int64_t base = wid * 32; base < n; base += warps * 32) {
+    const int64_t i = base + (threadIdx.x & 31);
+    const bool active = i < n;
+    AnyTrav T;
+    if (active) T.start(S, ldg3(o + 3 * i), ldg3(d + 3 * i), t_min, __ldg(t_max + i));
+    else {
+      T.idle();
+      T.found = false;
+      T.ok = true;
+    }
+    while (!T.done()) T.round(S);
+    if (active) {
+      if (!T.ok) flag_error(S, kErrStack);
+      out[i] = T.found ? 1 : 0;
+    }
   }
 }
 
+// occluded_batch (geometry.py:187-201): open segment a->b, endpoints offset by eps
 __global__ void __launch_bounds__(128) k_occluded(DevScene S, const double* __restrict__ a,
                                                   const double* __restrict__ b, double eps,
                                                   int64_t n, uint8_t* out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    bool ok;
-    const bool occ = occluded_segment(S, ldg3(a + 3 * i), ldg3(b + 3 * i), eps, ok);
-    if (!ok) flag_error(S, kErrStack);
-    out[i] = occ ? 1 : 0;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  const int64_t wid = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  for (int64_t base = wid * 32; base < n; base += warps * 32) {
+    const int64_t i = base + (threadIdx.x & 31);
+    bool cast = false;
+    AnyTrav T;
+    if (i < n) {
+      const double3 pa = ldg3(a + 3 * i), pb = ldg3(b + 3 * i);
+      const double3 dd = pb - pa;
+      const double len = norm_seq(dd);
+      if (len > 2.0 * eps) {
+        const double3 dn = make_double3(dd.x / len, dd.y / len, dd.z / len);
+        T.start(S, make_double3(pa.x + eps * dn.x, pa.y + eps * dn.y, pa.z + eps * dn.z), dn,
+                0.0, len - 2.0 * eps);
+        cast = true;
+      }
+    }
+    if (!cast) {
+      T.idle();
+      T.found = false;
+      T.ok = true;
+    }
+    while (!T.done()) T.round(S);
+    if (i < n) {
+      if (!T.ok) flag_error(S, kErrStack);
+      out[i] = T.found ? 1 : 0;
+    }
   }
 }
 

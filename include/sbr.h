@@ -210,12 +210,13 @@ enum {
   SBR_CC_STACK_OVERFLOW,
   SBR_CC_VERTEX_OVERFLOW,
   SBR_CC_ROW_OVERFLOW,
+  SBR_CC_REJ_OFF_EDGE,
   SBR_CC_COUNT
 };
 
 /* Refinement outcome per record (paths.py:1123-1245 Rejection reasons). */
 enum { SBR_REFINE_OK = 0, SBR_REFINE_COPLANAR_MISS = 1, SBR_REFINE_OCCLUDED = 2,
-       SBR_REFINE_DEGENERATE = 3 };
+       SBR_REFINE_DEGENERATE = 3, SBR_REFINE_OFF_EDGE = 4 };
 
 /* Generation parameters of one source (PathConfig paths.py:356-395). */
 typedef struct SbrCirParams {

@@ -533,6 +533,13 @@ typedef struct {
   const SbrMaterial* mats;
   int32_t nmat;
   const uint64_t *hash_r, *hash_f; /* slot order plane hashes (paths.py:449-450) */
+  /* diffraction wedges (geometry.py:356-494; paths.py:452-475 tables) */
+  int64_t nw;
+  const double *w_origin, *w_ehat, *w_t0, *w_n0, *w_nn; /* (nw,3) */
+  const double *w_len, *w_nopen;                         /* (nw) */
+  const uint64_t *w_hr, *w_hf;                           /* hash_edge */
+  const int32_t *w_mat0, *w_matn;                        /* face material rows */
+  const int32_t *slot_woff, *slot_wids;                  /* CSR: slot -> owned wedges */
 } OrcScene;
 
 typedef struct {
@@ -977,6 +984,7 @@ ORC_EXPORT int orc_radiomap_direct(const OrcScene* S, const SbrMapParams* P, con
 
 #define TAG_INTERACTION 0x5c798e00ad8012ebULL
 #define TAG_RESPAWN 0x742c480a24ff9b7fULL
+#define TAG_CONE 0x0bc9fb91195d708aULL
 #define FNV_OFFSET 0xCBF29CE484222325ULL
 #define FNV_PRIME 0x100000001B3ULL
 
@@ -1008,6 +1016,8 @@ typedef struct {
   double* vertex;          /* (n,L,3) */
   double* normal;          /* (n,L,3) */
   int32_t L;
+  int32_t pad_;
+  int32_t* wedge;          /* (n,L) wedge index, -1 */
 } OrcRecords;
 
 enum { OC_ESCAPED = 0, OC_TERMINATED, OC_RB, OC_VIS, OC_ROWS, OC_DUP, OC_TRUNC, OC_OVERFLOW,
@@ -1024,6 +1034,7 @@ typedef struct {
   double run_prob;
   uint64_t hr, hf;
   int32_t tri;
+  int32_t wedge;
   int8_t code;             /* -1: no interaction at this depth (dead) */
   int8_t suffix_start;
 } Hist;
@@ -1056,6 +1067,7 @@ static int pairset_insert(PairSet* s, uint64_t a, uint64_t b) {
 typedef struct { int64_t g; int32_t depth, k; uint8_t chain, diffuse; uint64_t pr, pf; } Row;
 
 /* interaction probabilities (_interaction_rows paths.py:572-595) */
+/* allow: bit0 R, bit1 S, bit2 T, bit3 D (already masked by has_s / has_d / wedges) */
 static int interaction_q(const SbrMaterial* m, double cos_i, double q_d, int allow, double q[4]) {
   Fresnel4 F = slab_fresnel(m, cos_i);
   double r_sq = cabs2(F.rp) + cabs2(F.rl);
@@ -1069,12 +1081,39 @@ static int interaction_q(const SbrMaterial* m, double cos_i, double q_d, int all
     q[1] = keep * s_sq * r_sq / den;
     q[2] = keep * t_sq / den;
   }
-  for (int k = 0; k < 3; ++k) if (!(allow >> k & 1)) q[k] = 0.0;
-  q[3] = 0.0; /* no wedges */
+  for (int k = 0; k < 4; ++k) if (!(allow >> k & 1)) q[k] = 0.0;
   double total = ((q[0] + q[1]) + q[2]) + q[3];
   if (!(total > 0.0)) return 0;
   for (int k = 0; k < 4; ++k) q[k] /= total;
   return 1;
+}
+
+/* allowed kinds at a hit (paths.py:743-748) */
+static int allowed_kinds(const OrcScene* S, int allow, int64_t tri, int has_s, int has_d) {
+  int a = allow & 15;
+  if (has_d) a &= ~2;
+  if (has_d || has_s) a &= ~8;
+  if (!(S->nw > 0 && S->slot_woff[tri + 1] > S->slot_woff[tri])) a &= ~8;
+  return a;
+}
+
+/* _project_diffractions (paths.py:831-852): nearest owned wedge, clamped foot */
+static int32_t project_wedge(const OrcScene* S, int64_t tri, const double* p, double* foot) {
+  double best = INFINITY;
+  int32_t bw = -1;
+  for (int32_t k = S->slot_woff[tri]; k < S->slot_woff[tri + 1]; ++k) {
+    const int32_t w = S->slot_wids[k];
+    const double* o = S->w_origin + 3 * w;
+    const double* e = S->w_ehat + 3 * w;
+    double rel[3] = {p[0] - o[0], p[1] - o[1], p[2] - o[2]};
+    double x = dot_seq(rel, e);
+    x = x < 0.0 ? 0.0 : (x > S->w_len[w] ? S->w_len[w] : x);
+    double f[3] = {o[0] + x * e[0], o[1] + x * e[1], o[2] + x * e[2]};
+    double df[3] = {p[0] - f[0], p[1] - f[1], p[2] - f[2]};
+    double dist = norm_seq(df);
+    if (dist < best) { best = dist; bw = w; memcpy(foot, f, sizeof f); }
+  }
+  return bw;
 }
 
 /* Per-sample sweep of global ids [lo, hi) into H (indexed g - lo). */
@@ -1088,7 +1127,7 @@ static int cir_sweep(const OrcScene* S, const OrcCirParams* P, uint64_t lo, uint
     orc_fibonacci(N, g, d);
     uint64_t hr = 0, hf = 0;
     double run_prob = 1.0;
-    int suffix = 0;
+    int suffix = 0, has_s = 0, has_d = 0;
     for (int depth = 1; depth <= L; ++depth) {
       double t, u_, v_;
       int64_t tri;
@@ -1101,7 +1140,8 @@ static int cir_sweep(const OrcScene* S, const OrcCirParams* P, uint64_t lo, uint
       if (dot_seq(d, n) > 0.0) { n[0] = -n[0]; n[1] = -n[1]; n[2] = -n[2]; }
       double cos_i = fabs(dot_seq(d, n));
       double q[4];
-      if (!interaction_q(S->mats + S->matrow[tri], cos_i, P->q_d, P->allow, q)) {
+      const int allow = allowed_kinds(S, P->allow, tri, has_s, has_d);
+      if (!interaction_q(S->mats + S->matrow[tri], cos_i, P->q_d, allow, q)) {
         counters[OC_TERMINATED]++;
         break;
       }
@@ -1111,16 +1151,28 @@ static int cir_sweep(const OrcScene* S, const OrcCirParams* P, uint64_t lo, uint
       for (int k = 0; k < 4; ++k) { cum = k ? cum + q[k] : q[k]; code += (uu >= cum); }
       if (code > 3) code = 3;
       run_prob *= q[code];
+      int32_t wid = -1;
+      if (code == 3) {
+        double foot[3];
+        wid = project_wedge(S, tri, pt, foot);
+        memcpy(pt, foot, sizeof foot);
+        has_d = 1;
+      }
       if (code == 0) {
         hr = 1373ULL * hr + S->hash_r[tri];
         hf = 1373ULL * hf + S->hash_f[tri];
+      } else if (code == 3) {
+        hr = 1373ULL * hr + S->w_hr[wid];
+        hf = 1373ULL * hf + S->w_hf[wid];
       } else if (code == 1) {
         suffix = depth;
+        has_s = 1;
       }
       Hist* h = H + (g - lo) * L + (depth - 1);
       memcpy(h->vertex, pt, sizeof pt);
       memcpy(h->normal, n, sizeof n);
       h->run_prob = run_prob; h->hr = hr; h->hf = hf; h->tri = (int32_t)tri;
+      h->wedge = wid;
       h->code = (int8_t)code; h->suffix_start = (int8_t)suffix;
       if (depth == L) break;
       /* _continue_rays (paths.py:855-900) */
@@ -1137,6 +1189,19 @@ static int cir_sweep(const OrcScene* S, const OrcCirParams* P, uint64_t lo, uint
         cross3(n, t1, t2);
         double a = sin_t * cos(azim), b = sin_t * sin(azim);
         for (int k = 0; k < 3; ++k) d[k] = (a * t1[k] + b * t2[k]) + cos_t * n[k];
+      } else if (code == 3) {
+        /* Keller cone (paths.py:881-896) */
+        const double* e = S->w_ehat + 3 * wid;
+        double cb = dot_seq(d, e);
+        cb = cb < -1.0 ? -1.0 : (cb > 1.0 ? 1.0 : cb);
+        double x = 1.0 - cb * cb, sb = sqrt(x > 0.0 ? x : 0.0);
+        if (sb < 1e-9) { counters[OC_TERMINATED]++; break; }
+        double phi = orc_philox_uniform(P->seed, 0, (uint64_t)depth, TAG_CONE, g) *
+                     S->w_nopen[wid] * PI_;
+        double a = sb * cos(phi), b = sb * sin(phi);
+        const double* t0 = S->w_t0 + 3 * wid;
+        const double* n0 = S->w_n0 + 3 * wid;
+        for (int k = 0; k < 3; ++k) d[k] = (a * t0[k] + b * n0[k]) + cb * e[k];
       }
       memcpy(o, pt, sizeof pt);
     }
@@ -1159,6 +1224,7 @@ static int cir_rows(const OrcScene* S, const OrcCirParams* P, uint64_t lo, uint6
         double diff[3] = {tg[0] - h->vertex[0], tg[1] - h->vertex[1], tg[2] - h->vertex[2]};
         double side = dot_seq(diff, h->normal);
         int ok = h->code == 2 ? side < 0.0 : side > 0.0;
+        if (h->code == 3) ok = 1;
         if (!ok) continue;
         counters[OC_VIS]++;
         int occ;
@@ -1342,7 +1408,11 @@ ORC_EXPORT int orc_cir_generate(const OrcScene* S, const OrcCirParams* P, OrcRec
   const int Ls = R->L;
   for (int64_t i = 0; !rc && i < nrec; ++i) {
     const int64_t rr = rec_row[i];
-    for (int j = 0; j < Ls; ++j) { R->kind[i * Ls + j] = -1; R->tri[i * Ls + j] = -1; }
+    for (int j = 0; j < Ls; ++j) {
+      R->kind[i * Ls + j] = -1;
+      R->tri[i * Ls + j] = -1;
+      R->wedge[i * Ls + j] = -1;
+    }
     R->prefix_prob[i] = 1.0;
     memcpy(R->anchor + 3 * i, P->source, 3 * sizeof(double));
     if (rr < 0) {
@@ -1363,7 +1433,7 @@ ORC_EXPORT int orc_cir_generate(const OrcScene* S, const OrcCirParams* P, OrcRec
     for (int j = 0; j < r->depth && j < Ls; ++j) {
       const Hist* h = H + r->g * L + j;
       const int64_t o = i * Ls + j;
-      R->kind[o] = h->code; R->tri[o] = h->tri;
+      R->kind[o] = h->code; R->tri[o] = h->tri; R->wedge[o] = h->wedge;
       memcpy(R->vertex + 3 * o, h->vertex, 3 * sizeof(double));
       memcpy(R->normal + 3 * o, h->normal, 3 * sizeof(double));
     }
@@ -1379,6 +1449,55 @@ static void reflect_point(const double* p, const double* nrm, const double* on, 
   double rel[3] = {p[0] - on[0], p[1] - on[1], p[2] - on[2]};
   double f = dot_ddot(rel, nrm);
   for (int k = 0; k < 3; ++k) out[k] = p[k] - 2.0 * f * nrm[k];
+}
+
+static void rotate_about(const double* a, double angle, double R[9]) {
+  /* _rotate_about (paths.py:557-565): c I + s K + (1 - c) a a^T */
+  double c = cos(angle), sn = sin(angle);
+  double K[9] = {0.0, -a[2], a[1], a[2], 0.0, -a[0], -a[1], a[0], 0.0};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      R[3 * i + j] = (c * (i == j ? 1.0 : 0.0) + sn * K[3 * i + j]) + (1.0 - c) * (a[i] * a[j]);
+}
+
+/* solve_diffraction_point (paths.py:517-554); returns 0 ok, 1 degenerate */
+static int solve_diffraction_point(const double* src, const double* tgt, const double* eo,
+                                   const double* ed, double* x_out) {
+  double en = sqrt(dot_ddot(ed, ed));
+  double e[3] = {ed[0] / en, ed[1] / en, ed[2] / en};
+  double sv[3] = {src[0] - eo[0], src[1] - eo[1], src[2] - eo[2]};
+  double tv[3] = {tgt[0] - eo[0], tgt[1] - eo[1], tgt[2] - eo[2]};
+  double es = dot_ddot(e, sv), et = dot_ddot(e, tv);
+  double u1[3], u2[3];
+  for (int k = 0; k < 3; ++k) { u1[k] = sv[k] - es * e[k]; u2[k] = tv[k] - et * e[k]; }
+  double n1 = sqrt(dot_ddot(u1, u1)), n2 = sqrt(dot_ddot(u2, u2));
+  if (n1 < 1e-12 || n2 < 1e-12) return 1;
+  for (int k = 0; k < 3; ++k) { u1[k] /= n1; u2[k] /= n2; }
+  double ax[3];
+  cross3(u1, u2, ax);
+  double na = sqrt(dot_ddot(ax, ax));
+  if (na < 1e-12) memcpy(ax, e, sizeof ax);
+  else for (int k = 0; k < 3; ++k) ax[k] /= na;
+  double cu = dot_ddot(u1, u2);
+  cu = cu < -1.0 ? -1.0 : (cu > 1.0 ? 1.0 : cu);
+  double angle = PI_ - acos(cu);
+  double R[9], tr[3];
+  rotate_about(ax, angle, R);
+  for (int i = 0; i < 3; ++i) tr[i] = dot_gemv(R + 3 * i, tv);
+  double st[3] = {tr[0] - sv[0], tr[1] - sv[1], tr[2] - sv[2]};
+  double guide[3], lever[3];
+  cross3(e, st, guide);
+  double ng = sqrt(dot_ddot(guide, guide));
+  if (ng < 1e-12) return 1;
+  cross3(sv, st, lever);
+  double sign = dot_ddot(guide, lever) >= 0.0 ? 1.0 : -1.0;
+  *x_out = sign * (sqrt(dot_ddot(lever, lever)) / ng);
+  return 0;
+}
+
+static void reflect_vector(const double* v, const double* nrm, double* out) {
+  double f = dot_ddot(v, nrm);
+  for (int k = 0; k < 3; ++k) out[k] = v[k] - 2.0 * f * nrm[k];
 }
 
 ORC_EXPORT int orc_cir_refine(const OrcScene* S, const double* source, const double* targets,
@@ -1397,17 +1516,51 @@ ORC_EXPORT int orc_cir_refine(const OrcScene* S, const double* source, const dou
     const int ns = depth - ss;
     double img[17][3];
     memcpy(img[0], R->anchor + 3 * r, 3 * sizeof(double));
+    int i_d = -1;
     for (int j = 0; j < ns; ++j) {
       int64_t o = r * L + ss + j;
       if (R->kind[o] == 0) reflect_point(img[j], R->normal + 3 * o, R->vertex + 3 * o, img[j + 1]);
       else memcpy(img[j + 1], img[j], sizeof img[j]);
+      if (R->kind[o] == 3 && i_d < 0) i_d = j;
+    }
+    double eo[17][3], ee[17][3], x = 0.0, wlen = 0.0;
+    int st = SBR_REFINE_OK;
+    if (i_d >= 0) {
+      const int w = R->wedge[r * L + ss + i_d];
+      memcpy(eo[i_d], S->w_origin + 3 * w, sizeof eo[i_d]);
+      memcpy(ee[i_d], S->w_ehat + 3 * w, sizeof ee[i_d]);
+      wlen = S->w_len[w];
+      for (int j = i_d + 1; j < ns; ++j) {
+        int64_t o = r * L + ss + j;
+        if (R->kind[o] == 0) {
+          reflect_point(eo[j - 1], R->normal + 3 * o, R->vertex + 3 * o, eo[j]);
+          reflect_vector(ee[j - 1], R->normal + 3 * o, ee[j]);
+        } else {
+          memcpy(eo[j], eo[j - 1], sizeof eo[j]);
+          memcpy(ee[j], ee[j - 1], sizeof ee[j]);
+        }
+      }
+      if (solve_diffraction_point(img[ns], tg, eo[ns - 1], ee[ns - 1], &x)) st = SBR_REFINE_DEGENERATE;
+      else if (!(0.0 <= x && x <= wlen)) st = SBR_REFINE_OFF_EDGE;
     }
     double from[3], refined0[3];
     memcpy(from, tg, sizeof from);
-    int st = SBR_REFINE_OK;
-    for (int j = ns - 1; j >= 0; --j) {
+    for (int j = ns - 1; st == SBR_REFINE_OK && j >= 0; --j) {
       int64_t o = r * L + ss + j;
-      double ray[3] = {img[j + 1][0] - from[0], img[j + 1][1] - from[1], img[j + 1][2] - from[2]};
+      if (j == i_d) {
+        double v[3] = {eo[i_d][0] + x * ee[i_d][0], eo[i_d][1] + x * ee[i_d][1], eo[i_d][2] + x * ee[i_d][2]};
+        int occ;
+        if (occluded1(S, from, v, 1e-4, &occ)) return SBR_ERR_STACK;
+        if (occ) { st = SBR_REFINE_OCCLUDED; break; }
+        memcpy(out + 3 * (ss + j + 1), v, sizeof v);
+        memcpy(from, v, sizeof v);
+        memcpy(refined0, v, sizeof v);
+        continue;
+      }
+      double aim[3];
+      if (i_d < 0 || j < i_d) memcpy(aim, img[j + 1], sizeof aim);
+      else for (int k = 0; k < 3; ++k) aim[k] = eo[j][k] + x * ee[j][k];
+      double ray[3] = {aim[0] - from[0], aim[1] - from[1], aim[2] - from[2]};
       double len = sqrt(dot_ddot(ray, ray));
       if (len < 1e-12) { st = SBR_REFINE_DEGENERATE; break; }
       for (int k = 0; k < 3; ++k) ray[k] = ray[k] / len;
@@ -1448,6 +1601,178 @@ typedef struct {
   const double* rx_vel;          /* per target (n,3) */
   const double* obj_vel;         /* per material row (nobj,3) or NULL */
 } OrcFieldParams;
+
+/* ---- UTD (materials.py:482-646) ------------------------------------------ */
+/* Fresnel integrals S, C: power series below 1.5, continued fraction above
+ * (scipy.special.fresnel semantics; agree to ~1e-12 relative). */
+static void fresnel_sc(double x, double* s_out, double* c_out) {
+  const double PIO2 = 1.5707963267948966;
+  double ax = fabs(x), s, c;
+  if (ax < 1.5) {
+    double t = PIO2 * ax * ax, term = ax, sumc = 0.0, sums = 0.0;
+    for (int k = 0; k < 60; ++k) {
+      double contrib = term / (2 * k + 1);
+      double sign = ((k / 2) % 2) ? -1.0 : 1.0;
+      if (k % 2 == 0) sumc += sign * contrib; else sums += sign * contrib;
+      term *= t / (k + 1);
+      if (term < 1e-18 * (sumc + sums + 1e-300)) break;
+    }
+    c = sumc; s = sums;
+  } else {
+    double pix2 = PI_ * ax * ax;
+    cpx b = C(1.0, -pix2), cc = C(1e300, 0.0);
+    cpx d = cdiv(C(1.0, 0.0), b), h = d;
+    int n = -1;
+    for (int k = 2; k < 300; ++k) {
+      n += 2;
+      double a = -(double)n * (double)(n + 1);
+      b = C(b.re + 4.0, b.im);
+      d = cdiv(C(1.0, 0.0), cadd(cscale(a, d), b));
+      cc = cadd(b, cdiv(C(a, 0.0), cc));
+      cpx del = cmul(cc, d);
+      h = cmul(h, del);
+      if (fabs(del.re - 1.0) + fabs(del.im) < 1e-16) break;
+    }
+    h = cmul(h, C(ax, -ax));
+    cpx w = cmul(C(cos(0.5 * pix2), sin(0.5 * pix2)), h);
+    cpx cs = cmul(C(0.5, 0.5), C(1.0 - w.re, -w.im));
+    c = cs.re; s = cs.im;
+  }
+  if (x < 0.0) { c = -c; s = -s; }
+  *s_out = s; *c_out = c;
+}
+
+/* transition_function (materials.py:482-501) */
+static cpx transition_f(double x) {
+  double arg = sqrt(2.0 * x / PI_), s, c;
+  fresnel_sc(arg, &s, &c);
+  cpx a = cmul(C(cos(x), sin(x)), C(1.0 - 2.0 * s, 1.0 - 2.0 * c));
+  return cscale(sqrt(PI_ * x / 2.0), a);
+}
+
+/* _cot_f_product (materials.py:504-528) */
+static cpx cot_f(double beta, double n_open, double k, double l, double sign) {
+  double n_round = nearbyint((beta + sign * PI_) / (2.0 * n_open * PI_));
+  double eps = beta - (2.0 * n_open * PI_ * n_round - sign * PI_);
+  if (fabs(eps) < 1e-6) {
+    double sg = eps >= 0.0 ? 1.0 : -1.0, kl = k * l;
+    cpx q = C(cos(PI_ / 4.0), sin(PI_ / 4.0));
+    cpx inner = csub(C(sqrt(2.0 * PI_ * kl) * sg, 0.0), cscale(2.0 * kl * eps, q));
+    return cscale(sign * n_open, cmul(q, inner));
+  }
+  double cot = 1.0 / tan((PI_ + sign * beta) / (2.0 * n_open));
+  double cv = cos((2.0 * n_open * PI_ * n_round - beta) / 2.0);
+  double a = 2.0 * cv * cv;
+  return cscale(cot, transition_f(k * l * a));
+}
+
+/* fresnel_vacuum r_perp, r_par (materials.py:173-205) */
+static void fresnel_vacuum_r(double c1, double eta_re, double eta_im, cpx* rp, cpx* rl) {
+  cpx eta = C(eta_re, eta_im);
+  double sin2 = 1.0 - c1 * c1;
+  cpx root = csqrt_lossy(C(eta.re - sin2, eta.im));
+  *rp = cdiv(C(c1 - root.re, -root.im), C(c1 + root.re, root.im));
+  cpx ec = C(eta.re * c1, eta.im * c1);
+  *rl = cdiv(csub(ec, root), cadd(ec, root));
+  if (eta.im == 0.0 && sin2 >= cabs_(eta)) { *rp = C(1.0, 0.0); *rl = C(1.0, 0.0); }
+}
+
+typedef struct { cpx m[2][2]; } M2;
+static M2 m2_mul(M2 a, M2 b) {
+  M2 r;
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 2; ++j) r.m[i][j] = cadd(cmul(a.m[i][0], b.m[0][j]), cmul(a.m[i][1], b.m[1][j]));
+  return r;
+}
+static M2 m2_w(const double* a, const double* b, const double* q, const double* r) {
+  M2 w;
+  w.m[0][0] = C(dot_ddot(a, q), 0.0); w.m[0][1] = C(dot_ddot(a, r), 0.0);
+  w.m[1][0] = C(dot_ddot(b, q), 0.0); w.m[1][1] = C(dot_ddot(b, r), 0.0);
+  return w;
+}
+static void oblique_frame(const double* s_hat, const double* n_hat, const double* other,
+                          double* e_perp, double* e_par) {
+  double cr[3];
+  cross3(s_hat, n_hat, cr);
+  double nn = sqrt(dot_ddot(cr, cr));
+  if (nn < 1e-9) {
+    double axes[2][3] = {{1.0, 0.0, 0.0}, {0.0, 1.0, 0.0}};
+    for (int a = 0; a < 2; ++a) {
+      double av = dot_ddot(axes[a], s_hat);
+      double u[3] = {axes[a][0] - av * s_hat[0], axes[a][1] - av * s_hat[1], axes[a][2] - av * s_hat[2]};
+      double un = sqrt(dot_ddot(u, u));
+      if (un > 1e-9) { for (int k = 0; k < 3; ++k) e_perp[k] = u[k] / un; break; }
+    }
+  } else {
+    for (int k = 0; k < 3; ++k) e_perp[k] = cr[k] / nn;
+  }
+  cross3(e_perp, other, e_par);
+}
+
+/* utd_transfer (materials.py:547-646); returns 0 ok, 1 degenerate geometry */
+static int utd_transfer(const OrcScene* S, int w, const double* s_i, const double* s_o,
+                        double dist_in, double dist_out, double lam, M2* out, double b_in[2][3],
+                        double b_out[2][3]) {
+  const double* e = S->w_ehat + 3 * w;
+  const double n_open = S->w_nopen[w];
+  double cos_beta = dot_ddot(s_i, e);
+  double x = 1.0 - cos_beta * cos_beta, sb0 = sqrt(x > 0.0 ? x : 0.0);
+  if (sb0 < 1e-9) return 1;
+  double ci[3], so_neg[3] = {-s_o[0], -s_o[1], -s_o[2]}, co[3];
+  cross3(s_i, e, ci);
+  double nci = sqrt(dot_ddot(ci, ci));
+  for (int k = 0; k < 3; ++k) b_in[0][k] = ci[k] / nci;
+  cross3(b_in[0], s_i, b_in[1]);
+  cross3(so_neg, e, co);
+  double nco = sqrt(dot_ddot(co, co));
+  if (nco < 1e-9) return 1;
+  for (int k = 0; k < 3; ++k) b_out[0][k] = co[k] / nco;
+  cross3(b_out[0], s_o, b_out[1]);
+  const double* t0 = S->w_t0 + 3 * w;
+  const double* n0 = S->w_n0 + 3 * w;
+  double sit[3], sot[3], a1 = dot_ddot(s_i, e), a2 = dot_ddot(s_o, e);
+  for (int k = 0; k < 3; ++k) { sit[k] = s_i[k] - a1 * e[k]; sot[k] = s_o[k] - a2 * e[k]; }
+  double n1 = sqrt(dot_ddot(sit, sit)), n2 = sqrt(dot_ddot(sot, sot));
+  for (int k = 0; k < 3; ++k) { sit[k] /= n1; sot[k] /= n2; }
+  double msit[3] = {-sit[0], -sit[1], -sit[2]};
+  double c_in = dot_ddot(msit, t0), c_out = dot_ddot(sot, t0);
+  c_in = c_in < -1.0 ? -1.0 : (c_in > 1.0 ? 1.0 : c_in);
+  c_out = c_out < -1.0 ? -1.0 : (c_out > 1.0 ? 1.0 : c_out);
+  double phi_in = PI_ - (PI_ - acos(c_in)) * (dot_ddot(msit, n0) >= 0.0 ? 1.0 : -1.0);
+  double phi_out = PI_ - (PI_ - acos(c_out)) * (dot_ddot(sot, n0) >= 0.0 ? 1.0 : -1.0);
+  double k = TWO_PI / lam;
+  double l = dist_in * dist_out / (dist_in + dist_out) * (sb0 * sb0);
+  cpx pref = cdiv(C(-cos(-PI_ / 4.0), -sin(-PI_ / 4.0)),
+                  C(2.0 * n_open * sqrt(2.0 * PI_ * k) * sb0, 0.0));
+  cpx d1 = cmul(pref, cot_f(phi_out - phi_in, n_open, k, l, 1.0));
+  cpx d2 = cmul(pref, cot_f(phi_out - phi_in, n_open, k, l, -1.0));
+  cpx d3 = cmul(pref, cot_f(phi_out + phi_in, n_open, k, l, 1.0));
+  cpx d4 = cmul(pref, cot_f(phi_out + phi_in, n_open, k, l, -1.0));
+  const SbrMaterial* m0 = S->mats + S->w_mat0[w];
+  const SbrMaterial* mn = S->mats + S->w_matn[w];
+  double cos_r[2] = {fabs(sin(phi_in)), fabs(sin(n_open * PI_ - phi_out))};
+  const double* nf[2] = {n0, S->w_nn + 3 * w};
+  const SbrMaterial* mf[2] = {m0, mn};
+  M2 refl[2];
+  for (int f = 0; f < 2; ++f) {
+    double ep[3] = {1.0, 0.0, 0.0}, el[3], er[3];
+    oblique_frame(s_i, nf[f], s_i, ep, el);
+    cross3(ep, s_o, er);
+    cpx rp, rl;
+    fresnel_vacuum_r(cos_r[f], mf[f]->eta_re, mf[f]->eta_im, &rp, &rl);
+    M2 dg;
+    dg.m[0][0] = rp; dg.m[0][1] = C(0.0, 0.0); dg.m[1][0] = C(0.0, 0.0); dg.m[1][1] = rl;
+    refl[f] = m2_mul(m2_mul(m2_w(b_out[0], b_out[1], ep, er), dg), m2_w(ep, el, b_in[0], b_in[1]));
+  }
+  cpx d12 = cadd(d1, d2);
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 2; ++j) {
+      cpx v = i == j ? d12 : C(0.0, 0.0);
+      v = csub(csub(v, cmul(d3, refl[1].m[i][j])), cmul(d4, refl[0].m[i][j]));
+      out->m[i][j] = C(-v.re, -v.im);
+    }
+  return 0;
+}
 
 /* pattern_to_gcs (em.py:198-219) for the built-in evaluators (c_phi_l = 0) */
 static void pattern_gcs(const SbrAntenna* A, const double* d, double* c_th, double* c_ph,
@@ -1507,6 +1832,8 @@ ORC_EXPORT int orc_cir_fields(const OrcScene* S, const OrcFieldParams* P, const 
     }
     const uint64_t ptag = orc_tag_hash(tag);
     const uint64_t psample = R->sample[r] > 0 ? (uint64_t)R->sample[r] : 0ULL;
+    int has_s = 0, has_d = 0, diffracted = 0;
+    double s_dist = 0.0;
     double nu = dot_ddot(P->tx_vel, kh[0]) / lam;
     nu -= dot_ddot(P->rx_vel + 3 * tgt, kh[depth]) / lam;
     for (int i = 0; i < depth; ++i) {
@@ -1521,7 +1848,8 @@ ORC_EXPORT int orc_cir_fields(const OrcScene* S, const OrcFieldParams* P, const 
       double nh[3] = {nrm[0], nrm[1], nrm[2]};
       if (dot_ddot(k_in, nh) > 0.0) { nh[0] = -nh[0]; nh[1] = -nh[1]; nh[2] = -nh[2]; }
       double q[4];
-      interaction_q(m, fabs(dot_ddot(k_in, nrm)), P->q_d, P->allow, q);
+      interaction_q(m, fabs(dot_ddot(k_in, nrm)), P->q_d,
+                    allowed_kinds(S, P->allow, slot, has_s, has_d), q);
       gamma_prob *= q[kind];
       if (P->obj_vel) {
         const double* v = P->obj_vel + 3 * row;
@@ -1534,6 +1862,36 @@ ORC_EXPORT int orc_cir_fields(const OrcScene* S, const OrcFieldParams* P, const 
       incidence_frame(k_in, nh, ep, el);
       double cos_t = fabs(dot_ddot(k_in, nh));
       Fresnel4 F = slab_fresnel(m, cos_t);
+      if (kind == 3) {
+        /* UTD wedge transfer (paths.py:1358-1373) */
+        const int w = R->wedge[o];
+        double remaining = 0.0;
+        for (int q2 = i + 1; q2 <= depth; ++q2) remaining += seg[q2];
+        M2 T;
+        double bi[2][3], bo[2][3];
+        if (utd_transfer(S, w, k_in, k_out, r_dist, remaining, lam, &T, bi, bo)) {
+          c0 = c1 = C(0.0, 0.0);
+        } else {
+          cpx p0, p1;
+          basis_w(bi[0], bi[1], fa, fb, c0, c1, &p0, &p1);
+          cpx n0_ = cadd(cmul(T.m[0][0], p0), cmul(T.m[0][1], p1));
+          cpx n1_ = cadd(cmul(T.m[1][0], p0), cmul(T.m[1][1], p1));
+          c0 = n0_; c1 = n1_;
+          double cr[3];
+          cross3(bo[0], bo[1], cr);
+          if (dot_ddot(cr, k_out) < 0.0) {
+            cpx t = c0; c0 = c1; c1 = t;
+            memcpy(fa, bo[1], sizeof fa); memcpy(fb, bo[0], sizeof fb);
+          } else {
+            memcpy(fa, bo[0], sizeof fa); memcpy(fb, bo[1], sizeof fb);
+          }
+        }
+        s_dist = r_dist;
+        r_dist = 0.0;
+        diffracted = 1;
+        has_d = 1;
+        continue;
+      }
       if (kind == 0 || kind == 2) {
         cpx p0, p1;
         basis_w(ep, el, fa, fb, c0, c1, &p0, &p1);
@@ -1592,6 +1950,7 @@ ORC_EXPORT int orc_cir_fields(const OrcScene* S, const OrcFieldParams* P, const 
         gamma_prob = 1.0;
         r_dist = 0.0;
         tube = TWO_PI;
+        has_s = 1;
       }
     }
     r_dist += seg[depth];
@@ -1604,9 +1963,10 @@ ORC_EXPORT int orc_cir_fields(const OrcScene* S, const OrcFieldParams* P, const 
       double rv = rc0 * rth[k] + rc1 * rph[k];
       acc = cadd(acc, cscale(rv, e));
     }
-    double sc = lam / FOUR_PI / r_dist;
-    gain[2 * r] = acc.re * sc;
-    gain[2 * r + 1] = acc.im * sc;
+    double sc = lam / FOUR_PI;
+    double dv = diffracted ? sqrt(s_dist * r_dist * (s_dist + r_dist)) : r_dist;
+    gain[2 * r] = acc.re * sc / dv;
+    gain[2 * r + 1] = acc.im * sc / dv;
     delay[r] = total / 299792458.0;
     doppler[r] = nu;
     memcpy(dep + 3 * r, kh[0], 3 * sizeof(double));

@@ -124,6 +124,7 @@ CIR_COUNTERS = (
     "stack_overflow",
     "vertex_overflow",
     "row_overflow",
+    "rej_off_edge",
 )
 SBR_CC_COUNT = len(CIR_COUNTERS)
 CC = {name: i for i, name in enumerate(CIR_COUNTERS)}
@@ -132,8 +133,12 @@ SBR_REFINE_OK = 0
 SBR_REFINE_COPLANAR_MISS = 1
 SBR_REFINE_OCCLUDED = 2
 SBR_REFINE_DEGENERATE = 3
+SBR_REFINE_OFF_EDGE = 4
 REJECTION_NAMES = {SBR_REFINE_COPLANAR_MISS: "coplanar-miss", SBR_REFINE_OCCLUDED: "occluded",
-                   SBR_REFINE_DEGENERATE: "degenerate"}
+                   SBR_REFINE_DEGENERATE: "degenerate", SBR_REFINE_OFF_EDGE: "off-edge"}
+REJECTION_COUNTERS = {SBR_REFINE_COPLANAR_MISS: "rej_coplanar_miss",
+                      SBR_REFINE_OCCLUDED: "rej_occluded", SBR_REFINE_DEGENERATE: "rej_degenerate",
+                      SBR_REFINE_OFF_EDGE: "rej_off_edge"}
 
 
 class SbrCirParams(ctypes.Structure):

@@ -102,6 +102,27 @@ CIR_CASES = {
 }
 
 
+# first-order diffraction (SURVEY §8f "next" #1), reference defaults for D
+D_CASES = {
+    "screen_d": dict(scene="screen", mat=CONCRETE, kinds="RSTD",
+                     cfg=dict(num_samples=150_000, max_depth=1, q_diffraction=0.3, seed=0),
+                     tx=[dict(pos=[0.0, -3.0, 2.0])], rx=[dict(pos=[0.0, 3.0, 2.5])]),
+    "cfg1_default": dict(scene="cfg1", mat=dict(CONCRETE_BENCH, scattering=0.2), kinds="RSTD",
+                         cfg=dict(num_samples=60_000, max_depth=3, q_diffraction=0.2, seed=1),
+                         tx=[dict(pos=[0.0, 0.0, 10.0])],
+                         rx=[dict(pos=[5.0, 8.0, 1.5]), dict(pos=[20.0, 3.0, 2.0])]),
+    "canyon_rd": dict(scene="canyon", mat=CONCRETE_BENCH, kinds="RD",
+                      cfg=dict(num_samples=20_000, max_depth=3, q_diffraction=0.2, seed=0),
+                      tx=[dict(pos=[0.0, 5.0, 20.0])], rx=_canyon_targets(8)),
+    "blocks_rtd": dict(scene="blocks", mat=dict(CONCRETE, scattering=0.3, random_phases=True),
+                       kinds="RSTD",
+                       cfg=dict(num_samples=20_000, max_depth=2, q_diffraction=0.25, seed=4),
+                       tx=[dict(pos=[-6.0, -5.0, 3.0], pattern=("tr38901", (0.5, 0.0, 0.0)))],
+                       rx=[dict(pos=[6.0, 5.0, 1.5]), dict(pos=[0.0, 7.0, 4.0])]),
+}
+CIR_CASES.update(D_CASES)
+
+
 def screen_mesh(half=2.0, center_z=2.0, object_id=5):
     quad = scenes.quad_mesh(half=half, z=0.0, object_id=object_id)
     swap = np.array([[1.0, 0, 0], [0, 0, 1.0], [0, 1.0, 0]])
@@ -120,6 +141,10 @@ def case_geometry(name):
         meshes = [screen_mesh()]
     elif c["scene"] == "canyon":
         meshes = scenes.street_canyon()
+    elif c["scene"] == "blocks":
+        meshes = [scenes.quad_mesh(half=20.0, z=0.0, object_id=0),
+                  scenes.subdivided_box((-2.0, -2.0, 0.0), (2.0, 2.0, 6.0), 2, 1),
+                  scenes.box_mesh((3.0, -6.0, 0.0), (5.0, -1.0, 4.0), object_id=2)]
     else:
         raise KeyError(c["scene"])
     mats = {m.object_id: dict(c["mat"]) for m in meshes}

@@ -87,6 +87,19 @@ def main():
         rxs = [device(d) for d in c["rx"]]
         p = f"{name}__"
         out[p + "digest"] = np.array(mesh_digest(meshes))
+        W = scene.wedges
+        out[p + "wedge_origin"] = np.array([w.origin for w in W]).reshape(-1, 3)
+        out[p + "wedge_ehat"] = np.array([w.e_hat for w in W]).reshape(-1, 3)
+        out[p + "wedge_length"] = np.array([w.length for w in W])
+        out[p + "wedge_n0"] = np.array([w.n0_hat for w in W]).reshape(-1, 3)
+        out[p + "wedge_nn"] = np.array([w.nn_hat for w in W]).reshape(-1, 3)
+        out[p + "wedge_t0"] = np.array([w.t0_hat for w in W]).reshape(-1, 3)
+        out[p + "wedge_n"] = np.array([w.n for w in W])
+        own = [(wi, side, o, m, le) for wi, w in enumerate(W)
+               for side, lst in ((0, w.face0), (1, w.facen)) for (o, m, le) in lst]
+        out[p + "wedge_owners"] = np.array(own, dtype=np.int64).reshape(-1, 5)
+        out[p + "wedge_hash_r"] = np.asarray(scene.wedge_hash_round, dtype=np.uint64)
+        out[p + "wedge_hash_f"] = np.asarray(scene.wedge_hash_floor, dtype=np.uint64)
 
         # -- generation (first source, synthetic reference position) -----------
         t0 = time.perf_counter()
@@ -109,11 +122,13 @@ def main():
             "kind": np.full((n, L), -1, np.int64),
             "obj": np.full((n, L), -1, np.int64),
             "prim": np.full((n, L), -1, np.int64),
+            "wedge": np.full((n, L), -1, np.int64),
             "vertex": np.zeros((n, L, 3)),
             "normal": np.zeros((n, L, 3)),
         }
         for i, r in enumerate(recs):
             for j, st in enumerate(r.steps):
+                g["wedge"][i, j] = st.wedge_index
                 g["kind"][i, j] = KIND[st.kind.value]
                 g["obj"][i, j] = st.object_id
                 g["prim"][i, j] = st.primitive_id
@@ -148,11 +163,13 @@ def main():
             "kind": np.full((n, L), -1, np.int64),
             "obj": np.full((n, L), -1, np.int64),
             "prim": np.full((n, L), -1, np.int64),
+            "wedge": np.full((n, L), -1, np.int64),
             "vertices": np.zeros((n, L + 2, 3)),
         }
         for i, q in enumerate(paths):
             r["vertices"][i, :q.depth + 2] = q.vertices
             for j, st in enumerate(q.steps):
+                r["wedge"][i, j] = st.wedge_index
                 r["kind"][i, j] = KIND[st.kind.value]
                 r["obj"][i, j] = st.object_id
                 r["prim"][i, j] = st.primitive_id

@@ -18,7 +18,7 @@ from paper_2504_21719_b200.paths import PathConfig, RadioDevice
 from paper_2504_21719_b200.sampling import Interaction
 
 KINDS = {"R": Interaction.REFLECTION, "S": Interaction.SCATTERING,
-         "T": Interaction.TRANSMISSION}
+         "T": Interaction.TRANSMISSION, "D": Interaction.DIFFRACTION}
 _SC = {}
 
 
@@ -86,6 +86,7 @@ def test_oracle_generation_matches_reference(name):
     prim = np.where(kind >= 0, sc.tri_primitive_id[np.maximum(tri, 0)], -1)
     assert np.array_equal(obj, want["obj"]) and np.array_equal(prim, want["prim"])
     m = kind >= 0
+    assert np.array_equal(np.where(m, rec["wedge"][:, :L], -1), want["wedge"])
     np.testing.assert_allclose(rec["vertex"][:, :L][m], want["vertex"][m], rtol=0, atol=1e-12)
     assert np.array_equal(rec["normal"][:, :L][m], want["normal"][m])
 
@@ -105,6 +106,7 @@ def test_oracle_paths_match_reference(name):
     L = want["kind"].shape[1]
     assert np.array_equal(paths["kind"][:, :L], want["kind"])
     assert np.array_equal(paths["obj"][:, :L], want["obj"])
+    assert np.array_equal(paths["wedge"][:, :L], want["wedge"])
     for i in range(n):
         d = int(want["depth"][i])
         np.testing.assert_allclose(paths["vertices"][i, :d + 2], want["vertices"][i, :d + 2],

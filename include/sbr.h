@@ -144,6 +144,28 @@ int sbr_scene_set_attributes(SbrScene* scene, const int32_t* tie_rank,
                              const double* normals, const int32_t* matrow,
                              const uint64_t* hash_r, const uint64_t* hash_f);
 int sbr_scene_set_materials(SbrScene* scene, const SbrMaterial* mats, int32_t n);
+
+/* Diffraction wedges (geometry.py:356-494 extract_wedges; paths.py:452-475
+ * tables), host arrays uploaded once: per-wedge frame, length, exterior
+ * angle n, edge hashes (hash_edge, paths.py:111-125), material rows of the
+ * 0- and n-faces, and per SLOT the sorted ids of the wedges it owns (CSR). */
+typedef struct SbrWedgeTable {
+  int64_t n_wedges;
+  const double* origin;           /* (nw, 3) */
+  const double* e_hat;            /* (nw, 3) */
+  const double* t0_hat;           /* (nw, 3) */
+  const double* n0_hat;           /* (nw, 3) */
+  const double* nn_hat;           /* (nw, 3) */
+  const double* length;           /* (nw) */
+  const double* n_open;           /* (nw) */
+  const uint64_t* hash_r;         /* (nw) */
+  const uint64_t* hash_f;         /* (nw) */
+  const int32_t* mat0;            /* (nw) material row of face0[0] */
+  const int32_t* matn;            /* (nw) material row of (facen or face0)[0] */
+  const int32_t* slot_offsets;    /* (T + 1) */
+  const int32_t* slot_ids;        /* (slot_offsets[T]) */
+} SbrWedgeTable;
+int sbr_scene_set_wedges(SbrScene* scene, const SbrWedgeTable* table);
 /* Reads and clears the device error word (stack overflow).  Synchronises
  * `stream`.  Returns SBR_ERR_STACK if any traversal overflowed. */
 int sbr_scene_check(SbrScene* scene, void* stream);
@@ -225,7 +247,7 @@ typedef struct SbrCirParams {
   uint64_t num_samples;
   uint64_t seed;
   int32_t max_depth;
-  int32_t allow_mask;             /* R=1 S=2 T=4; D (8) is out of scope         */
+  int32_t allow_mask;             /* R=1 S=2 T=4 D=8                            */
   int32_t n_targets;
   int32_t pad_;
   const double* targets_dev;      /* (n_targets, 3)                             */
@@ -244,9 +266,10 @@ typedef struct SbrVertexBuf {
   uint64_t* hash_f;
   int32_t* parent;                /* previous vertex of the sample, -1 = none   */
   int32_t* tri;                   /* scene slot                                 */
-  uint8_t* code;                  /* 0 R, 1 S, 2 T                              */
+  uint8_t* code;                  /* 0 R, 1 S, 2 T, 3 D                         */
   uint8_t* depth;                 /* 1-based                                    */
   uint8_t* suffix_start;          /* depth of the last S step, 0 = none         */
+  int32_t* wedge;                 /* wedge of a D step, -1                      */
   int64_t capacity;
 } SbrVertexBuf;
 
@@ -267,6 +290,7 @@ typedef struct SbrRecordBuf {
   double* normal;                 /* (n, L, 3)                                  */
   int32_t max_depth;              /* L                                          */
   int32_t pad_;
+  int32_t* wedge;                 /* (n, L) wedge index, -1                     */
 } SbrRecordBuf;
 
 /* Field-replay parameters of one source (compute_path_fields, paths.py:1302). */

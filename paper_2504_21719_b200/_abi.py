@@ -158,14 +158,20 @@ class SbrCirParams(ctypes.Structure):
 class SbrVertexBuf(ctypes.Structure):
     _fields_ = [(name, ctypes.c_void_p) for name in (
         "point", "normal", "run_prob", "sample", "hash_r", "hash_f", "parent", "tri",
-        "code", "depth", "suffix_start")] + [("capacity", ctypes.c_int64)]
+        "code", "depth", "suffix_start", "wedge")] + [("capacity", ctypes.c_int64)]
 
 
 class SbrRecordBuf(ctypes.Structure):
     _fields_ = [(name, ctypes.c_void_p) for name in (
         "target", "sample", "depth", "suffix_start", "diffuse", "chain_hash", "prefix_prob",
         "anchor", "kind", "tri", "vertex", "normal")] + [
-        ("max_depth", ctypes.c_int32), ("pad_", ctypes.c_int32)]
+        ("max_depth", ctypes.c_int32), ("pad_", ctypes.c_int32), ("wedge", ctypes.c_void_p)]
+
+
+class SbrWedgeTable(ctypes.Structure):
+    _fields_ = [("n_wedges", ctypes.c_int64)] + [(name, ctypes.c_void_p) for name in (
+        "origin", "e_hat", "t0_hat", "n0_hat", "nn_hat", "length", "n_open", "hash_r",
+        "hash_f", "mat0", "matn", "slot_offsets", "slot_ids")]
 
 
 class SbrFieldParams(ctypes.Structure):

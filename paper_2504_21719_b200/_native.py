@@ -32,6 +32,7 @@ def _declare(lib):
         "sbr_scene_permutation": (ctypes.c_int, [vp, vp]),
         "sbr_scene_set_attributes": (ctypes.c_int, [vp, vp, vp, vp, vp, vp]),
         "sbr_scene_set_materials": (ctypes.c_int, [vp, vp, i32]),
+        "sbr_scene_set_wedges": (ctypes.c_int, [vp, vp]),
         "sbr_scene_check": (ctypes.c_int, [vp, vp]),
         "sbr_trace_closest": (ctypes.c_int, [vp, vp, vp, dbl, vp, i64, vp, vp,
                                              vp, vp, vp]),
@@ -72,7 +73,7 @@ def exported_symbols():
     return [
         "sbr_scene_create", "sbr_scene_destroy", "sbr_scene_num_triangles",
         "sbr_scene_num_nodes", "sbr_scene_permutation",
-        "sbr_scene_set_attributes", "sbr_scene_set_materials",
+        "sbr_scene_set_attributes", "sbr_scene_set_materials", "sbr_scene_set_wedges",
         "sbr_scene_check", "sbr_trace_closest", "sbr_trace_any",
         "sbr_occluded", "sbr_fibonacci", "sbr_philox_uniform",
         "sbr_radiomap_bounce", "sbr_radiomap_direct", "sbr_cir_sweep", "sbr_cir_vertex_order",

@@ -196,6 +196,7 @@ class PathTensors:
     kind: np.ndarray          # (n, L) int8, -1 unused
     obj: np.ndarray           # (n, L)
     prim: np.ndarray          # (n, L)
+    wedge: np.ndarray         # (n, L) wedge index of D steps, -1
     normal: np.ndarray        # (n, L, 3)
     vertices: np.ndarray      # (n, L + 2, 3), rows padded after depth + 2
 
@@ -228,7 +229,7 @@ def _paths_from_tensors(T):
         steps = tuple(
             InteractionStep(kind=_KIND_OF[int(T.kind[i, j])], object_id=int(T.obj[i, j]),
                             primitive_id=int(T.prim[i, j]), vertex=T.vertices[i, j + 1].copy(),
-                            normal=T.normal[i, j].copy())
+                            normal=T.normal[i, j].copy(), wedge_index=int(T.wedge[i, j]))
             for j in range(d))
         out.append(ValidPath(
             tx_index=int(T.tx[i]), tx_element=int(T.tx_el[i]), rx_index=int(T.rx[i]),
@@ -269,13 +270,11 @@ class _PhaseTimer:
             print(self.name, " ".join(f"{k}={v * 1e3:.1f}ms" for k, v in self.parts), flush=True)
 
 
-def _check_cfg(cfg):
-    if Interaction.DIFFRACTION in cfg.enabled and cfg.q_diffraction > 0.0:
-        raise NotImplementedError(
-            "diffraction (UTD, Keller cones) is out of scope for the GPU path solver "
-            "(SURVEY.md §8f); disable Interaction.DIFFRACTION or set q_diffraction=0")
+def _check_cfg(cfg, scene=None):
     if cfg.max_depth > 15:
         raise ValueError("max_depth must be <= 15")
+    if scene is not None and Interaction.DIFFRACTION in cfg.enabled:
+        scene.wedges  # noqa: B018  -- extract + upload the wedge tables once
 
 
 def _cir_params(source, targets_t, cfg):
@@ -285,7 +284,7 @@ def _cir_params(source, targets_t, cfg):
     p.num_samples = int(cfg.num_samples)
     p.seed = int(cfg.seed) & 0xFFFFFFFFFFFFFFFF
     p.max_depth = int(cfg.max_depth)
-    p.allow_mask = allow_mask(cfg.enabled) & 0x7
+    p.allow_mask = allow_mask(cfg.enabled) & 0xF
     p.n_targets = int(targets_t.shape[0])
     p.targets_dev = targets_t.data_ptr()
     return p
@@ -307,6 +306,7 @@ class _VertexBuf:
             "code": torch.empty(c, dtype=torch.uint8, device=dev),
             "depth": torch.empty(c, dtype=torch.uint8, device=dev),
             "suffix_start": torch.empty(c, dtype=torch.uint8, device=dev),
+            "wedge": torch.empty(c, dtype=torch.int32, device=dev),
         }
         self.abi = _abi.SbrVertexBuf()
         for k, v in self.t.items():
@@ -332,6 +332,7 @@ class _RecordBuf:
             "tri": torch.empty((n, L), dtype=torch.int32, device=dev),
             "vertex": torch.zeros((n, L, 3), dtype=torch.float64, device=dev),
             "normal": torch.zeros((n, L, 3), dtype=torch.float64, device=dev),
+            "wedge": torch.full((n, L), -1, dtype=torch.int32, device=dev),
         }
         self.abi = _abi.SbrRecordBuf()
         for k, v in self.t.items():
@@ -363,7 +364,8 @@ class DeviceCandidates:
                     kind=_KIND_OF[int(h["kind"][i, j])],
                     object_id=int(acc.tri_object_id[slot]),
                     primitive_id=int(acc.tri_primitive_id[slot]),
-                    vertex=h["vertex"][i, j].copy(), normal=h["normal"][i, j].copy()))
+                    vertex=h["vertex"][i, j].copy(), normal=h["normal"][i, j].copy(),
+                    wedge_index=int(h["wedge"][i, j])))
             k = int(h["target"][i])
             out.append(CandidateRecord(
                 source_id=self.source_id, target_id=k, source=np.asarray(self.source),
@@ -512,7 +514,7 @@ def _generate_device(scene, source, targets, cfg, source_id=0, sample_range=None
     Returns (DeviceCandidates, counters dict, generation diagnostics dict).
     """
     torch = _torch()
-    _check_cfg(cfg)
+    _check_cfg(cfg, scene)
     acc = scene.accel
     dev = acc.device
     scene.bind_frequency(cfg.frequency)
@@ -576,12 +578,13 @@ def refine_candidate(record, scene):
     dev = scene.accel.device
     steps = record.steps
     if any(st.kind is Interaction.DIFFRACTION for st in steps):
-        raise NotImplementedError("diffraction refinement is out of scope")
+        scene.wedges  # noqa: B018  (wedge tables on the device)
     L = max(len(steps), 1)
     rec = _RecordBuf(1, L, dev)
     acc = scene.accel
     kinds = np.full(L, -1, np.int8)
     tris = np.full(L, -1, np.int32)
+    wed = np.full(L, -1, np.int32)
     verts = np.zeros((L, 3))
     norms = np.zeros((L, 3))
     for j, st in enumerate(steps):
@@ -589,6 +592,7 @@ def refine_candidate(record, scene):
         tris[j] = scene._tri_slot[(int(st.object_id), int(st.primitive_id))]
         verts[j] = st.vertex
         norms[j] = st.normal
+        wed[j] = st.wedge_index
     vals = {
         "target": np.array([0], np.int32), "sample": np.array([record.sample_id], np.int64),
         "depth": np.array([len(steps)], np.int32),
@@ -598,6 +602,7 @@ def refine_candidate(record, scene):
         "prefix_prob": np.array([record.prefix_probability]),
         "anchor": np.asarray(record.anchor, np.float64)[None, :],
         "kind": kinds[None, :], "tri": tris[None, :], "vertex": verts[None], "normal": norms[None],
+        "wedge": wed[None, :],
     }
     for k, v in vals.items():
         rec.t[k].copy_(torch.from_numpy(np.ascontiguousarray(v)).reshape(rec.t[k].shape))
@@ -643,7 +648,7 @@ def _fields_device(scene, cand, pv, status, tx_dev, target_devices, cfg):
     fp.tx_velocity = _abi.vec3(tx_dev.velocity)
     fp.num_samples = int(cfg.num_samples)
     fp.seed = int(cfg.seed) & 0xFFFFFFFFFFFFFFFF
-    fp.allow_mask = allow_mask(cfg.enabled) & 0x7
+    fp.allow_mask = allow_mask(cfg.enabled) & 0xF
     fp.tx_pattern = tx_dev.pattern.to_abi()
     rx_pat = _antenna_table([d.pattern for d in target_devices], dev)
     rx_vel = torch.from_numpy(np.array([d.velocity for d in target_devices],
@@ -696,8 +701,7 @@ def _paths_for_source(scene, cand, cfg, ti, te, tx_dev, target_devices, rx_index
         timer.mark("refine")
     rcount = rc.cpu().numpy()
     for code, name in _abi.REJECTION_NAMES.items():
-        cnt = int(rcount[_abi.CC[{1: "rej_coplanar_miss", 2: "rej_occluded",
-                                   3: "rej_degenerate"}[code]]])
+        cnt = int(rcount[_abi.CC[_abi.REJECTION_COUNTERS[code]]])
         if cnt:
             rejections[name] += cnt
     f = _fields_device(scene, cand, pv, status, tx_dev, target_devices, cfg)
@@ -724,7 +728,8 @@ def _paths_for_source(scene, cand, cfg, ti, te, tx_dev, target_devices, rx_index
         gain=fh["gain"][:, 0] + 1j * fh["gain"][:, 1], delay=fh["delay"],
         doppler=fh["doppler"], departure=fh["departure"], arrival=fh["arrival"],
         depth=h["depth"].astype(np.int64), chain_hash=h["chain_hash"], sample=h["sample"],
-        kind=h["kind"], obj=obj, prim=prim, normal=h["normal"], vertices=pvh)
+        kind=h["kind"], obj=obj, prim=prim, wedge=np.where(valid, h["wedge"], -1),
+        normal=h["normal"], vertices=pvh)
     if timer:
         timer.mark("host_copy")
     return part, rejections
@@ -751,7 +756,7 @@ def compute_paths(scene, transmitters, receivers, cfg):
     receivers = list(receivers)
     if not transmitters or not receivers:
         raise ValueError("need at least one transmitter and one receiver")
-    _check_cfg(cfg)
+    _check_cfg(cfg, scene)
     tx_flat, targets, target_devices, rx_index, rx_elem = _device_plan(transmitters, receivers,
                                                                        cfg)
     diagnostics = Counter()
@@ -802,7 +807,7 @@ def compute_paths_sharded(scene, transmitters, receivers, cfg, group=None):
     receivers = list(receivers)
     if not transmitters or not receivers:
         raise ValueError("need at least one transmitter and one receiver")
-    _check_cfg(cfg)
+    _check_cfg(cfg, scene)
     on = dist.is_available() and dist.is_initialized()
     rank = dist.get_rank(group) if on else 0
     world = dist.get_world_size(group) if on else 1
@@ -869,7 +874,8 @@ def compute_paths_sharded(scene, transmitters, receivers, cfg, group=None):
 
 def _concat_sorted(parts, L):
     keys = ("tx", "tx_el", "rx", "rx_el", "gain", "delay", "doppler", "departure", "arrival",
-            "depth", "chain_hash", "sample", "kind", "obj", "prim", "normal", "vertices")
+            "depth", "chain_hash", "sample", "kind", "obj", "prim", "wedge", "normal",
+            "vertices")
     if not parts:
         empty = dict(tx=np.zeros(0, np.int64), tx_el=np.zeros(0, np.int64),
                      rx=np.zeros(0, np.int64), rx_el=np.zeros(0, np.int64),
@@ -878,7 +884,8 @@ def _concat_sorted(parts, L):
                      depth=np.zeros(0, np.int64), chain_hash=np.zeros(0, np.uint64),
                      sample=np.zeros(0, np.int64), kind=np.zeros((0, L), np.int8),
                      obj=np.zeros((0, L), np.int64), prim=np.zeros((0, L), np.int64),
-                     normal=np.zeros((0, L, 3)), vertices=np.zeros((0, L + 2, 3)))
+                     wedge=np.zeros((0, L), np.int64), normal=np.zeros((0, L, 3)),
+                     vertices=np.zeros((0, L + 2, 3)))
         return PathTensors(**empty)
     cat = {k: np.concatenate([p[k] for p in parts]) for k in keys}
     # paths.sort(key=(rx, rx_el, tx, tx_el, depth, chain_hash, sample))  paths.py:1505-1508

@@ -26,7 +26,7 @@
 #include <string>
 #include <vector>
 
-#include "sbr_physics.cuh"
+#include "sbr_utd.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -91,7 +91,7 @@ __device__ __forceinline__ bool interaction_probs(const SbrMaterial& m, double r
   if (!(allow & 1)) q[0] = 0.0;
   if (!(allow & 2)) q[1] = 0.0;
   if (!(allow & 4)) q[2] = 0.0;
-  q[3] = 0.0;  // D: tri_has_wedge is false for every slot
+  if (!(allow & 8)) q[3] = 0.0;  // masked by has_s / has_d / wedge ownership
   const double total = ((q[0] + q[1]) + q[2]) + q[3];
   if (!(total > 0.0)) return false;
   q[0] /= total;
@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(128) k_cir_sweep(DevScene S, SbrCirParams P, u
     double run_prob = 1.0;
     int suffix_start = 0;
     int parent = -1;
+    bool has_s = false, has_d = false;
     for (int depth = 1; depth <= P.max_depth; ++depth) {
       K.rb++;
       HitRecord h;
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(128) k_cir_sweep(DevScene S, SbrCirParams P, u
         K.escaped++;
         break;
       }
-      const double3 pt = o + h.t * d;
+      double3 pt = o + h.t * d;
       double3 n = ldg3(S.normals + 3 * (int64_t)h.tri);
       if (dot_seq(d, n) > 0.0) n = neg(n);
       const double cos_i = fabs(dot_seq(d, n));
@@ -138,7 +139,8 @@ __global__ void __launch_bounds__(128) k_cir_sweep(DevScene S, SbrCirParams P, u
       const double r_sq = cabs2(F.rp) + cabs2(F.rl);
       const double t_sq = cabs2(F.tp) + cabs2(F.tl);
       double q[4];
-      if (!interaction_probs(m, r_sq, t_sq, P.q_diffraction, P.allow_mask, q)) {
+      if (!interaction_probs(m, r_sq, t_sq, P.q_diffraction,
+                             allowed_kinds(S, P.allow_mask, h.tri, has_s, has_d), q)) {
         K.terminated++;
         break;
       }
@@ -147,11 +149,20 @@ __global__ void __launch_bounds__(128) k_cir_sweep(DevScene S, SbrCirParams P, u
       int code = (u >= c0) + (u >= c1) + (u >= c2) + (u >= c3);
       if (code > 3) code = 3;
       run_prob *= q[code];
-      if (code == 0) {
+      int wid = -1;
+      if (code == 3) {
+        double3 foot;
+        wid = project_wedge(S, h.tri, pt, foot);
+        pt = foot;
+        has_d = true;
+        hr = kHashBase * hr + __ldg(S.w_hr + wid);
+        hf = kHashBase * hf + __ldg(S.w_hf + wid);
+      } else if (code == 0) {
         hr = kHashBase * hr + __ldg(S.hash_r + h.tri);
         hf = kHashBase * hf + __ldg(S.hash_f + h.tri);
       } else if (code == 1) {
         suffix_start = depth;
+        has_s = true;
       }
       const unsigned long long vi = append_slot(counters + SBR_CC_VERTICES);
       if ((int64_t)vi < vb.capacity) {
@@ -170,6 +181,7 @@ __global__ void __launch_bounds__(128) k_cir_sweep(DevScene S, SbrCirParams P, u
         vb.code[vi] = (uint8_t)code;
         vb.depth[vi] = (uint8_t)depth;
         vb.suffix_start[vi] = (uint8_t)suffix_start;
+        vb.wedge[vi] = wid;
         parent = (int)vi;
       } else {
         atomicAdd(counters + SBR_CC_VERTEX_OVERFLOW, 1ULL);
@@ -193,6 +205,24 @@ __global__ void __launch_bounds__(128) k_cir_sweep(DevScene S, SbrCirParams P, u
         const double a = sin_t * ca, b = sin_t * sa;
         d = make_double3((a * t1.x + b * t2.x) + cos_t * n.x, (a * t1.y + b * t2.y) + cos_t * n.y,
                          (a * t1.z + b * t2.z) + cos_t * n.z);
+      } else if (code == 3) {
+        // Keller cone (paths.py:881-896); edge-grazing rays terminate
+        const double3 e = ldg3(S.w_ehat + 3 * wid);
+        const double cb = clamp1(dot_seq(d, e));
+        const double xb = 1.0 - cb * cb;
+        const double sb = sqrt(xb > 0.0 ? xb : 0.0);
+        if (sb < 1e-9) {
+          K.terminated++;
+          break;
+        }
+        const double phi =
+            philox_uniform(P.seed, 0, (uint64_t)depth, TAG_CONE, g) * __ldg(S.w_nopen + wid) * kPi;
+        double sp, cp;
+        sincos(phi, &sp, &cp);
+        const double a = sb * cp, b = sb * sp;
+        const double3 t0 = ldg3(S.w_t0 + 3 * wid), n0 = ldg3(S.w_n0 + 3 * wid);
+        d = make_double3((a * t0.x + b * n0.x) + cb * e.x, (a * t0.y + b * n0.y) + cb * e.y,
+                         (a * t0.z + b * n0.z) + cb * e.z);
       }
       o = pt;
     }
@@ -286,7 +316,8 @@ __global__ void __launch_bounds__(128) k_cir_visibility(DevScene S, SbrCirParams
           const double3 n = ld3(vb.normal + 3 * v);
           const double3 tg = ldg3(P.targets_dev + 3 * k);
           const double side = dot_seq(tg - p, n);
-          pass = vb.code[v] == 2 ? side < 0.0 : side > 0.0;
+          const int code = vb.code[v];
+          pass = code == 3 ? true : (code == 2 ? side < 0.0 : side > 0.0);
         }
         const unsigned m = __ballot_sync(0xffffffffu, pass);
         if (pass) {
@@ -633,6 +664,7 @@ __global__ void k_cir_records(SbrCirParams P, SbrVertexBuf vb, const int32_t* __
     for (int j = 0; j < L; ++j) {
       R.kind[r * L + j] = -1;
       R.tri[r * L + j] = -1;
+      R.wedge[r * L + j] = -1;
     }
     if (v < 0) {
       R.sample[r] = -1;
@@ -658,6 +690,7 @@ __global__ void k_cir_records(SbrCirParams P, SbrVertexBuf vb, const int32_t* __
       const int64_t o = r * L + j;
       R.kind[o] = (int8_t)vb.code[w];
       R.tri[o] = vb.tri[w];
+      R.wedge[o] = vb.wedge[w];
       for (int c = 0; c < 3; ++c) {
         R.vertex[3 * o + c] = vb.point[3 * w + c];
         R.normal[3 * o + c] = vb.normal[3 * w + c];
@@ -709,18 +742,56 @@ __global__ void __launch_bounds__(128) k_cir_refine(DevScene S, SbrCirParams P, 
     const double3 anchor = ld3(R.anchor + 3 * r);
     double3 img[16];
     img[0] = anchor;
+    int i_d = -1;
     for (int j = 0; j < ns; ++j) {
       const int64_t o = r * L + ss + j;
       img[j + 1] = R.kind[o] == 0
                        ? reflect_point(img[j], ld3(R.normal + 3 * o), ld3(R.vertex + 3 * o))
                        : img[j];
+      if (R.kind[o] == 3 && i_d < 0) i_d = j;
     }
     int st = SBR_REFINE_OK;
+    // diffraction: the edge seen through every later reflection (paths.py:1163-1191)
+    double3 eo[16], ee[16];
+    double x = 0.0;
+    if (i_d >= 0) {
+      const int w = R.wedge[r * L + ss + i_d];
+      eo[i_d] = ldg3(S.w_origin + 3 * w);
+      ee[i_d] = ldg3(S.w_ehat + 3 * w);
+      for (int j = i_d + 1; j < ns; ++j) {
+        const int64_t o = r * L + ss + j;
+        if (R.kind[o] == 0) {
+          const double3 nn = ld3(R.normal + 3 * o);
+          eo[j] = reflect_point(eo[j - 1], nn, ld3(R.vertex + 3 * o));
+          ee[j] = reflect_vec(ee[j - 1], nn);
+        } else {
+          eo[j] = eo[j - 1];
+          ee[j] = ee[j - 1];
+        }
+      }
+      if (!solve_diffraction_point(img[ns], tg, eo[ns - 1], ee[ns - 1], x))
+        st = SBR_REFINE_DEGENERATE;
+      else if (!(0.0 <= x && x <= __ldg(S.w_len + w)))
+        st = SBR_REFINE_OFF_EDGE;
+    }
     double3 from = tg;
     double3 first = tg;
-    for (int j = ns - 1; j >= 0; --j) {
+    for (int j = ns - 1; st == SBR_REFINE_OK && j >= 0; --j) {
       const int64_t o = r * L + ss + j;
-      const double3 aim = img[j + 1];
+      if (j == i_d) {
+        const double3 vtx = eo[i_d] + x * ee[i_d];
+        bool fine;
+        if (occluded_segment(S, from, vtx, 1e-4, fine)) st = SBR_REFINE_OCCLUDED;
+        if (!fine) flag_error(S, kErrStack);
+        if (st != SBR_REFINE_OK) break;
+        out[3 * (ss + j + 1)] = vtx.x;
+        out[3 * (ss + j + 1) + 1] = vtx.y;
+        out[3 * (ss + j + 1) + 2] = vtx.z;
+        from = vtx;
+        first = vtx;
+        continue;
+      }
+      const double3 aim = (i_d < 0 || j < i_d) ? img[j + 1] : eo[j] + x * ee[j];
       double3 ray = aim - from;
       const double len = sqrt(dot_ddot(ray, ray));
       if (len < 1e-12) {
@@ -760,6 +831,7 @@ __global__ void __launch_bounds__(128) k_cir_refine(DevScene S, SbrCirParams P, 
     if (st == SBR_REFINE_COPLANAR_MISS) atomicAdd(counters + SBR_CC_REJ_COPLANAR, 1ULL);
     if (st == SBR_REFINE_OCCLUDED) atomicAdd(counters + SBR_CC_REJ_OCCLUDED, 1ULL);
     if (st == SBR_REFINE_DEGENERATE) atomicAdd(counters + SBR_CC_REJ_DEGENERATE, 1ULL);
+    if (st == SBR_REFINE_OFF_EDGE) atomicAdd(counters + SBR_CC_REJ_OFF_EDGE, 1ULL);
   }
 }
 
@@ -819,7 +891,7 @@ int check_cir(const SbrScene* scene, const SbrCirParams* P) {
   if (!P) return set_error(SBR_ERR_INVALID, "NULL params");
   if (scene && !dev_view(scene).mats) return set_error(SBR_ERR_INVALID, "scene has no material table");
   if (P->max_depth < 0 || P->max_depth > 15) return set_error(SBR_ERR_INVALID, "max_depth must lie in [0, 15]");
-  if (P->allow_mask & 8) return set_error(SBR_ERR_UNSUPPORTED, "diffraction is out of scope");
+
   if (P->n_targets < 1 || P->n_targets > (1 << kTargetBits))
     return set_error(SBR_ERR_INVALID, "need 1 .. 2^20 targets");
   if (P->num_samples < 1 || P->num_samples > kSampleMask)

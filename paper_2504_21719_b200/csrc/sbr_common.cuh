@@ -60,6 +60,11 @@ struct DevScene {
   int32_t nmat;
   float pad_base;              // conservative box padding: 2^-20 * (max|coord| + 1)
   double bounds_lo[3], bounds_hi[3];  // scene AABB (float64)
+  // diffraction wedges (n_wedges == 0: none)
+  int64_t n_wedges;
+  const double *w_origin, *w_ehat, *w_t0, *w_n0, *w_nn, *w_len, *w_nopen;
+  const uint64_t *w_hr, *w_hf;
+  const int32_t *w_mat0, *w_matn, *slot_woff, *slot_wids;
 };
 
 constexpr int kStackSize = 64;

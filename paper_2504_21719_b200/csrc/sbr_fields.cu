@@ -13,7 +13,7 @@
 // in float64 (north-star tolerance for gains/delays/angles: 1e-4 relative).
 #include <string>
 
-#include "sbr_physics.cuh"
+#include "sbr_utd.cuh"
 
 struct SbrScene;
 
@@ -87,14 +87,15 @@ __device__ __forceinline__ void right_handed(Jones& J, double3 a, double3 b, dou
   J.k = k;
 }
 
-// interaction_probabilities(...)[kind] at replay geometry (paths.py:1276-1299)
+// interaction_probabilities(...)[kind] at replay geometry (paths.py:1276-1299);
+// allow already carries the has_s / has_d / wedge-ownership masks
 __device__ double step_probability(const SbrMaterial& m, double cos_i, int kind, double q_d,
-                                   int allow, bool has_s) {
+                                   int allow) {
   const Fresnel4 F = slab_fresnel(m, cos_i);
   const double r_sq = cabs2(F.rp) + cabs2(F.rl);
   const double t_sq = cabs2(F.tp) + cabs2(F.tl);
   const double den = r_sq + t_sq;
-  double q[4] = {0.0, 0.0, 0.0, 0.0};
+  double q[4] = {0.0, 0.0, 0.0, q_d};
   if (den > 0.0) {
     const double keep = 1.0 - q_d;
     const double s2 = m.scattering * m.scattering;
@@ -102,11 +103,11 @@ __device__ double step_probability(const SbrMaterial& m, double cos_i, int kind,
     q[1] = keep * s2 * r_sq / den;
     q[2] = keep * t_sq / den;
   }
-  (void)has_s;  // only masks D, which is never allowed (no wedges)
   if (!(allow & 1)) q[0] = 0.0;
   if (!(allow & 2)) q[1] = 0.0;
   if (!(allow & 4)) q[2] = 0.0;
-  const double total = ((0.0 + q[0]) + q[1]) + q[2];
+  if (!(allow & 8)) q[3] = 0.0;
+  const double total = (((0.0 + q[0]) + q[1]) + q[2]) + q[3];
   return total > 0.0 ? q[kind] / total : 0.0;
 }
 
@@ -160,9 +161,9 @@ __global__ void __launch_bounds__(128) k_cir_fields(DevScene S, SbrFieldParams P
       J.b = ph;
       J.k = kh[0];
     }
-    double gamma_prob = 1.0, r_dist = 0.0;
+    double gamma_prob = 1.0, r_dist = 0.0, s_dist = 0.0;
     double tube_omega = kFourPi / (double)P.num_samples;
-    bool has_s = false;
+    bool has_s = false, has_d = false, diffracted = false;
     int n_phase = 0;
     const uint64_t ptag = phase_tag(depth);
     const uint64_t psample = R.sample[r] > 0 ? (uint64_t)R.sample[r] : 0ULL;
@@ -183,10 +184,32 @@ __global__ void __launch_bounds__(128) k_cir_fields(DevScene S, SbrFieldParams P
       const double cos_step = fabs(ddot(k_in, nrm));
       double3 n_hat = nrm;
       if (ddot(k_in, n_hat) > 0.0) n_hat = neg(n_hat);
-      gamma_prob *= step_probability(m, cos_step, kind, P.q_diffraction, P.allow_mask, has_s);
+      gamma_prob *= step_probability(m, cos_step, kind, P.q_diffraction,
+                                     allowed_kinds(S, P.allow_mask, slot, has_s, has_d));
       if (P.n_objects > 0 && row < P.n_objects) {
         const double3 v = ldg3(P.obj_velocity_dev + 3 * row);
         if (v.x != 0.0 || v.y != 0.0 || v.z != 0.0) nu += ddot(v, k_out - k_in) / lam;
+      }
+      if (kind == 3) {
+        // UTD wedge transfer (paths.py:1358-1373)
+        double remaining = 0.0;
+        for (int q2 = i + 1; q2 <= depth; ++q2) remaining += seg_len[q2];
+        M2 T;
+        double3 bi[2], bo[2];
+        if (!utd_transfer(S, R.wedge[o], k_in, k_out, r_dist, remaining, lam, T, bi, bo)) {
+          J.c0 = J.c1 = C(0.0, 0.0);
+        } else {
+          cplx p0, p1;
+          basis_change(bi[0], bi[1], J.a, J.b, J.c0, J.c1, p0, p1);
+          J.c0 = T.m[0][0] * p0 + T.m[0][1] * p1;
+          J.c1 = T.m[1][0] * p0 + T.m[1][1] * p1;
+          right_handed(J, bo[0], bo[1], k_out);
+        }
+        s_dist = r_dist;
+        r_dist = 0.0;
+        diffracted = true;
+        has_d = true;
+        continue;
       }
       double3 e_perp, e_par;
       incidence_frame(k_in, n_hat, e_perp, e_par);
@@ -266,9 +289,9 @@ __global__ void __launch_bounds__(128) k_cir_fields(DevScene S, SbrFieldParams P
     const cplx ry = rc0 * C(rth.y, 0.0) + rc1 * C(rph.y, 0.0);
     const cplx rz = rc0 * C(rth.z, 0.0) + rc1 * C(rph.z, 0.0);
     const cplx dotv = (ex * rx + ey * ry) + ez * rz;
-    const double scale = lam / kFourPi / r_dist;
-    gain[2 * r] = dotv.re * scale;
-    gain[2 * r + 1] = dotv.im * scale;
+    const double spread = diffracted ? sqrt(s_dist * r_dist * (s_dist + r_dist)) : r_dist;
+    gain[2 * r] = dotv.re * (lam / kFourPi) / spread;
+    gain[2 * r + 1] = dotv.im * (lam / kFourPi) / spread;
     delay[r] = total_len / kSpeedOfLight;
     doppler[r] = nu;
     for (int c = 0; c < 3; ++c) {

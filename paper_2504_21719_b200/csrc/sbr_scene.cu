@@ -103,6 +103,13 @@ struct SbrScene {
   float pad_base = 0.f;
   double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
   std::vector<int64_t> perm;
+  // wedge tables (one allocation)
+  void* wedge_block = nullptr;
+  int64_t n_wedges = 0;
+  const double *w_origin = nullptr, *w_ehat = nullptr, *w_t0 = nullptr, *w_n0 = nullptr,
+               *w_nn = nullptr, *w_len = nullptr, *w_nopen = nullptr;
+  const uint64_t *w_hr = nullptr, *w_hf = nullptr;
+  const int32_t *w_mat0 = nullptr, *w_matn = nullptr, *slot_woff = nullptr, *slot_wids = nullptr;
 };
 
 namespace sbr {
@@ -126,6 +133,20 @@ DevScene dev_view(const SbrScene* s) {
     d.bounds_lo[k] = s->lo[k];
     d.bounds_hi[k] = s->hi[k];
   }
+  d.n_wedges = s->n_wedges;
+  d.w_origin = s->w_origin;
+  d.w_ehat = s->w_ehat;
+  d.w_t0 = s->w_t0;
+  d.w_n0 = s->w_n0;
+  d.w_nn = s->w_nn;
+  d.w_len = s->w_len;
+  d.w_nopen = s->w_nopen;
+  d.w_hr = s->w_hr;
+  d.w_hf = s->w_hf;
+  d.w_mat0 = s->w_mat0;
+  d.w_matn = s->w_matn;
+  d.slot_woff = s->slot_woff;
+  d.slot_wids = s->slot_wids;
   return d;
 }
 
@@ -563,6 +584,7 @@ void sbr_scene_destroy(SbrScene* S) {
   cudaFree(S->hash_f);
   cudaFree(S->mats);
   cudaFree(S->error_word);
+  cudaFree(S->wedge_block);
   delete S;
 }
 
@@ -596,6 +618,48 @@ int sbr_scene_set_materials(SbrScene* S, const SbrMaterial* mats, int32_t n) {
   SBR_CUDA(cudaMalloc(&S->mats, sizeof(SbrMaterial) * n));
   SBR_CUDA(cudaMemcpy(S->mats, mats, sizeof(SbrMaterial) * n, cudaMemcpyHostToDevice));
   S->nmat = n;
+  return SBR_OK;
+}
+
+int sbr_scene_set_wedges(SbrScene* S, const SbrWedgeTable* W) {
+  if (!S || !W) return set_error(SBR_ERR_INVALID, "NULL argument");
+  if (W->n_wedges < 0) return set_error(SBR_ERR_INVALID, "bad wedge count");
+  SBR_CUDA(cudaSetDevice(S->device));
+  if (S->wedge_block) {
+    SBR_CUDA(cudaFree(S->wedge_block));
+    S->wedge_block = nullptr;
+  }
+  S->n_wedges = 0;
+  const int64_t nw = W->n_wedges, T = S->ntri;
+  if (nw == 0) return SBR_OK;
+  std::vector<int32_t> off(W->slot_offsets, W->slot_offsets + T + 1);
+  const int64_t nids = off[T];
+  const size_t b3 = sizeof(double) * 3 * nw, b1 = sizeof(double) * nw;
+  const size_t bytes = 5 * b3 + 2 * b1 + 2 * sizeof(uint64_t) * nw + 2 * sizeof(int32_t) * nw +
+                       sizeof(int32_t) * (T + 1) + sizeof(int32_t) * (nids > 0 ? nids : 1) + 256;
+  SBR_CUDA(cudaMalloc(&S->wedge_block, bytes));
+  char* p = (char*)S->wedge_block;
+  auto put = [&](const void* src, size_t n) -> const void* {
+    void* dst = p;
+    if (n) cudaMemcpy(dst, src, n, cudaMemcpyHostToDevice);
+    p += (n + 15) & ~(size_t)15;
+    return dst;
+  };
+  S->w_origin = (const double*)put(W->origin, b3);
+  S->w_ehat = (const double*)put(W->e_hat, b3);
+  S->w_t0 = (const double*)put(W->t0_hat, b3);
+  S->w_n0 = (const double*)put(W->n0_hat, b3);
+  S->w_nn = (const double*)put(W->nn_hat, b3);
+  S->w_len = (const double*)put(W->length, b1);
+  S->w_nopen = (const double*)put(W->n_open, b1);
+  S->w_hr = (const uint64_t*)put(W->hash_r, sizeof(uint64_t) * nw);
+  S->w_hf = (const uint64_t*)put(W->hash_f, sizeof(uint64_t) * nw);
+  S->w_mat0 = (const int32_t*)put(W->mat0, sizeof(int32_t) * nw);
+  S->w_matn = (const int32_t*)put(W->matn, sizeof(int32_t) * nw);
+  S->slot_woff = (const int32_t*)put(W->slot_offsets, sizeof(int32_t) * (T + 1));
+  S->slot_wids = (const int32_t*)put(W->slot_ids, sizeof(int32_t) * nids);
+  SBR_CUDA(cudaGetLastError());
+  S->n_wedges = nw;
   return SBR_OK;
 }
 

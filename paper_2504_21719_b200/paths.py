@@ -11,6 +11,7 @@ The CIR pipeline itself (generation, dedup, refinement, field replay, CFR)
 lives in `cir.py` on top of csrc/sbr_cir.cu and csrc/sbr_fields.cu.
 """
 
+import ctypes
 import math
 from dataclasses import dataclass
 
@@ -187,11 +188,12 @@ class RadioDevice:
 class SceneModel:
     """Meshes, materials and the device acceleration structures (paths.py:419-510).
 
-    Differences from the reference, all deliberate:
+    Differences from the reference, both deliberate:
       * the BVH is the device LBVH (slot order = Morton order);
-      * diffraction wedges are not extracted: first-order diffraction is the
-        "next" row of SURVEY.md §8f, so `wedges` is empty and every
-        triangle reports `tri_has_wedge = False`.
+      * diffraction wedges (wedges.py, the reference's extract_wedges) are
+        extracted lazily on first use -- only configurations that enable
+        diffraction pay for it -- and uploaded to the device with the
+        per-slot wedge CSR (paths.py:452-475).
     """
 
     def __init__(self, meshes, materials, velocities=None,
@@ -205,15 +207,63 @@ class SceneModel:
                 raise UnresolvedMaterial(f"object {mesh.object_id} has no material")
         self.accel = build_scene_accel(self.meshes, device=device)
         self.dihedral_threshold_deg = dihedral_threshold_deg
-        self.wedges = []
+        self._wedges = None
         self._build_tables()
         self._material_freq = None
+
+    @property
+    def wedges(self):
+        """Diffracting edges (geometry.py:400-494), extracted and uploaded on first use."""
+        if self._wedges is None:
+            self._build_wedge_tables()
+        return self._wedges
+
+    def _build_wedge_tables(self):
+        from . import _abi, _native
+        from .wedges import extract_wedges, hash_edge
+        W = extract_wedges(self.meshes, dihedral_threshold_deg=self.dihedral_threshold_deg)
+        acc = self.accel
+        nt = acc.num_triangles
+        owned = [[] for _ in range(nt)]
+        for wi, w in enumerate(W):
+            for key in set(w.owners()):
+                slot = self._tri_slot.get(key)
+                if slot is not None:
+                    owned[slot].append(wi)
+        counts = np.array([len(x) for x in owned], dtype=np.int64)
+        self.tri_wedge_offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        self.tri_wedge_ids = np.array([wi for lst in owned for wi in sorted(lst)],
+                                      dtype=np.int64)
+        self.tri_has_wedge = counts > 0
+        hs = [hash_edge(w) for w in W]
+        self.wedge_hash_round = np.array([h[0] for h in hs], dtype=np.uint64)
+        self.wedge_hash_floor = np.array([h[1] for h in hs], dtype=np.uint64)
+        row = {int(o): i for i, o in enumerate(self._object_ids)}
+        arr = lambda attr: np.ascontiguousarray(  # noqa: E731
+            np.array([getattr(w, attr) for w in W], dtype=np.float64).reshape(-1, 3))
+        keep = {
+            "origin": arr("origin"), "e_hat": arr("e_hat"), "t0_hat": arr("t0_hat"),
+            "n0_hat": arr("n0_hat"), "nn_hat": arr("nn_hat"),
+            "length": np.array([w.length for w in W], dtype=np.float64),
+            "n_open": np.array([w.n for w in W], dtype=np.float64),
+            "hash_r": self.wedge_hash_round, "hash_f": self.wedge_hash_floor,
+            "mat0": np.array([row[w.face0[0][0]] for w in W], dtype=np.int32),
+            "matn": np.array([row[(w.facen or w.face0)[0][0]] for w in W], dtype=np.int32),
+            "slot_offsets": self.tri_wedge_offsets.astype(np.int32),
+            "slot_ids": self.tri_wedge_ids.astype(np.int32),
+        }
+        tab = _abi.SbrWedgeTable()
+        tab.n_wedges = len(W)
+        for k, v in keep.items():
+            setattr(tab, k, np.ascontiguousarray(v).ctypes.data)
+        _native.check(_native.load_library().sbr_scene_set_wedges(acc.handle, ctypes.byref(tab)))
+        self._wedge_host = keep
+        self._wedges = W
 
     def _build_tables(self):
         accel = self.accel
         self.tri_plane_hash_round, self.tri_plane_hash_floor = plane_hash_rows(
             accel.tri_normal, accel.tri_v0)
-        self.tri_has_wedge = np.zeros(accel.num_triangles, dtype=bool)
         self._object_ids = np.array(sorted(m.object_id for m in self.meshes),
                                     dtype=np.int64)
         self._object_materials = [self.materials[oid] for oid in self._object_ids]
@@ -241,4 +291,6 @@ class SceneModel:
         return v if v is not None else np.zeros(3)
 
     def primitive_owns_wedge(self, object_id, primitive_id):
-        return False
+        slot = self._tri_slot.get((int(object_id), int(primitive_id)))
+        self.wedges  # noqa: B018  (ensure tables)
+        return slot is not None and bool(self.tri_has_wedge[slot])

@@ -107,7 +107,11 @@ D_CASES = {
     "screen_d": dict(scene="screen", mat=CONCRETE, kinds="RSTD",
                      cfg=dict(num_samples=150_000, max_depth=1, q_diffraction=0.3, seed=0),
                      tx=[dict(pos=[0.0, -3.0, 2.0])], rx=[dict(pos=[0.0, 3.0, 2.5])]),
-    "cfg1_default": dict(scene="cfg1", mat=dict(CONCRETE_BENCH, scattering=0.2), kinds="RSTD",
+    # no T here: a transmitted ray crossing the wall box reaches z = 0 where the
+    # box bottom and the ground overlap coplanar -- an exact t-tie decided at
+    # the last ulp of the launch direction (CUDA vs glibc sin/cos), i.e. inside
+    # the north star's epsilon exclusion; blocks_rtd covers T with D
+    "cfg1_default": dict(scene="cfg1", mat=dict(CONCRETE_BENCH, scattering=0.2), kinds="RSD",
                          cfg=dict(num_samples=60_000, max_depth=3, q_diffraction=0.2, seed=1),
                          tx=[dict(pos=[0.0, 0.0, 10.0])],
                          rx=[dict(pos=[5.0, 8.0, 1.5]), dict(pos=[20.0, 3.0, 2.0])]),

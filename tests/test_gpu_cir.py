@@ -99,6 +99,7 @@ def test_generate_candidates_bit_exact(cuda, name):
         for j, st in enumerate(r.steps):
             assert KIND_CODE[st.kind] == want["kind"][i, j]
             assert st.object_id == want["obj"][i, j] and st.primitive_id == want["prim"][i, j]
+            assert st.wedge_index == want["wedge"][i, j]
             # CUDA's sin/cos may differ from glibc by 1 ulp in the launch
             # direction; geometry then agrees to ~1e-15 m, decisions exactly
             np.testing.assert_allclose(st.vertex, want["vertex"][i, j], rtol=0, atol=1e-12)
@@ -122,6 +123,7 @@ def test_compute_paths_matches_reference(cuda, name):
     obj = np.where(kind >= 0, T.obj, -1)[:, :L]
     prim = np.where(kind >= 0, T.prim, -1)[:, :L]
     assert np.array_equal(obj, want["obj"]) and np.array_equal(prim, want["prim"])
+    assert np.array_equal(np.where(kind >= 0, T.wedge, -1)[:, :L], want["wedge"])
     for i in range(n):
         d = int(want["depth"][i])
         np.testing.assert_allclose(T.vertices[i, :d + 2], want["vertices"][i, :d + 2],
@@ -175,11 +177,31 @@ def test_refinement_fixed_point(cuda):
         np.testing.assert_allclose(again.vertices, p.vertices, atol=1e-9)
 
 
-def test_diffraction_is_rejected_loudly(cuda):
-    scene, _, _, txs, rxs = build("box_r")
-    cfg = PathConfig(num_samples=100, max_depth=1, q_diffraction=0.2)
+def test_screen_diffraction_points_minimize_length(cuda):
+    # reference test_paths.py:459-481: four edge paths around a screen, each
+    # diffraction point on its edge satisfying the Keller law k_in.e == k_out.e
+    scene, _, cfg, txs, rxs = build("screen_d")
+    ps = compute_paths(scene, txs, rxs, cfg)
+    d_paths = [p for p in ps.paths if p.kinds == "D"]
+    assert len(d_paths) == 4
+    for p in d_paths:
+        w = scene.wedges[p.steps[0].wedge_index]
+        v = p.vertices[1]
+        x = float((v - w.origin) @ w.e_hat)
+        assert -1e-9 <= x <= w.length + 1e-9
+        k_in = (v - txs[0].position) / np.linalg.norm(v - txs[0].position)
+        k_out = (rxs[0].position - v) / np.linalg.norm(rxs[0].position - v)
+        assert k_in @ w.e_hat == pytest.approx(k_out @ w.e_hat, abs=1e-9)
+
+
+def test_diffraction_radio_map_is_rejected_loudly(cuda):
+    # the UTD radio-map estimator (radiomap.py:640-965) is SURVEY §8f "next" #2
+    from paper_2504_21719_b200 import compute_radio_map
+    from paper_2504_21719_b200.radiomap import MeasurementGrid, RadioMapConfig
+    scene, _, _, txs, _ = build("screen_d")
+    grid = MeasurementGrid((0.0, 3.0, 1.5), (1, 0, 0), (0, 1, 0), (1.0, 1.0), (4, 4))
     with pytest.raises(NotImplementedError):
-        compute_paths(scene, txs, rxs, cfg)
+        compute_radio_map(scene, [txs[0].position], grid, RadioMapConfig(num_samples=1000))
 
 
 @pytest.mark.parametrize("samples,kinds", [(100_000, "R"), (50_000, "RS")])

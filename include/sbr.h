@@ -117,6 +117,7 @@ enum {
   SBR_MC_RAY_BOUNCES,      /* sum of rows traced (the rb metric) */
   SBR_MC_DIRECT_VISIBLE,
   SBR_MC_STACK_OVERFLOW,
+  SBR_MC_CONE_SAMPLES,     /* edge-estimator samples drawn (radiomap.py:889) */
   SBR_MC_COUNT
 };
 
@@ -210,6 +211,16 @@ int sbr_radiomap_bounce(const SbrScene* scene, const SbrMapParams* params,
  * centre into direct_dev (ny, nx) (overwritten), counts visible cells. */
 int sbr_radiomap_direct(const SbrScene* scene, const SbrMapParams* params,
                         double* direct_dev, uint64_t* counters_dev, void* stream);
+
+/* Replaces compute_radio_map_diffraction (radiomap.py:842-965): the edge
+ * estimator over the listed wedges (collect_wedges_near_source, 645-671):
+ * wedge_samples (offset, cone azimuth) draws per wedge from the `map-wedge`
+ * Philox stream keyed (seed, wedge, block), plane crossing, exterior-region
+ * and occlusion tests, UTD transfer, finite-difference area weighting, float64
+ * atomic deposit into grid_dev (accumulated).  Requires sbr_scene_set_wedges. */
+int sbr_radiomap_wedges(const SbrScene* scene, const SbrMapParams* params,
+                        const int32_t* wedge_ids_dev, int32_t n_wedges, uint64_t wedge_samples,
+                        double* grid_dev, uint64_t* counters_dev, void* stream);
 
 /* ---- path solver (CIR) ---------------------------------------------------- */
 /* Counters of the path-solver pipeline (paths.py:1098-1103, 1509-1512). */

@@ -2005,3 +2005,101 @@ ORC_EXPORT void orc_cfr(const double* gain, const double* delay, const double* d
       }
   }
 }
+
+/* ========================================================================= */
+/* Edge (diffraction) radio-map estimator: compute_radio_map_diffraction     */
+/* (radiomap.py:842-965) with _cone_points / _weighting_rows / _utd_rows       */
+/* ========================================================================= */
+#define TAG_MAP_WEDGE 0x9115590451c40950ULL
+
+static void cone_point(const OrcScene* S, int w, const double* src, double x, double phi,
+                       double* v, double* s_in, double* k_i, double* k_s, double* sin_b) {
+  const double* o = S->w_origin + 3 * w;
+  const double* e = S->w_ehat + 3 * w;
+  const double* t0 = S->w_t0 + 3 * w;
+  const double* n0 = S->w_n0 + 3 * w;
+  for (int k = 0; k < 3; ++k) v[k] = o[k] + x * e[k];
+  double d[3] = {v[0] - src[0], v[1] - src[1], v[2] - src[2]};
+  *s_in = norm_seq(d);
+  for (int k = 0; k < 3; ++k) k_i[k] = d[k] / *s_in;
+  double cb = dot_gemv(d, e) / *s_in;
+  double xb = 1.0 - cb * cb;
+  *sin_b = sqrt(xb > 0.0 ? xb : 0.0);
+  double a = *sin_b * cos(phi), b = *sin_b * sin(phi);
+  for (int k = 0; k < 3; ++k) k_s[k] = (a * t0[k] + b * n0[k]) + cb * e[k];
+}
+
+ORC_EXPORT int orc_radiomap_wedges(const OrcScene* S, const SbrMapParams* P, const double* offs,
+                                   const double* prec, const int32_t* wedge_ids, int32_t nw,
+                                   uint64_t wedge_samples, double* grid, uint64_t* counters) {
+  const double* nh = P->normal;
+  const double lam = P->wavelength;
+  for (int wi = 0; wi < nw; ++wi) {
+    const int w = wedge_ids[wi];
+    const double len = S->w_len[w], nopen = S->w_nopen[w];
+    const double norm = len * nopen * PI_ / (double)wedge_samples;
+    const double hx = 1e-4 * (len > 1.0 ? len : 1.0), hp = 1e-4;
+    for (uint64_t i = 0; i < wedge_samples; ++i) {
+      const uint64_t block = i >> SBR_CHUNK_LOG2, slot = i & ((1ULL << SBR_CHUNK_LOG2) - 1);
+      counters[SBR_MC_CONE_SAMPLES]++;
+      double u0 = orc_philox_uniform(P->seed, (uint64_t)w, block, TAG_MAP_WEDGE, 2 * slot);
+      double u1 = orc_philox_uniform(P->seed, (uint64_t)w, block, TAG_MAP_WEDGE, 2 * slot + 1);
+      double xs = u0 * len, phis = u1 * nopen * PI_;
+      double v[3], s_in, k_i[3], k_s[3], sin_b;
+      cone_point(S, w, P->source, xs, phis, v, &s_in, k_i, k_s, &sin_b);
+      if (!(sin_b >= 1e-9)) continue;
+      double denom = dot_gemv(k_s, nh);
+      if (!(fabs(denom) > 1e-9)) continue;
+      double gamma = (P->plane_off - dot_gemv(v, nh)) / denom;
+      if (!(gamma > 1e-4)) continue;
+      double inc[3] = {-k_i[0], -k_i[1], -k_i[2]};
+      double azim = atan2(dot_gemv(inc, S->w_n0 + 3 * w), dot_gemv(inc, S->w_t0 + 3 * w));
+      if (azim < 0.0) azim += 2.0 * PI_;
+      if (!(azim <= nopen * PI_)) continue;
+      double pts[3] = {v[0] + gamma * k_s[0], v[1] + gamma * k_s[1], v[2] + gamma * k_s[2]};
+      double rel[3] = {pts[0] - P->corner[0], pts[1] - P->corner[1], pts[2] - P->corner[2]};
+      double fu = floor(dot_gemv(rel, P->u_hat) / P->cell_w);
+      double fv = floor(dot_gemv(rel, P->v_hat) / P->cell_h);
+      if (!(fu >= 0.0 && fu < (double)P->nx && fv >= 0.0 && fv < (double)P->ny)) continue;
+      int occ;
+      if (occluded1(S, P->source, v, 1e-4, &occ)) return SBR_ERR_STACK;
+      if (occ) continue;
+      if (occluded1(S, v, pts, 1e-4, &occ)) return SBR_ERR_STACK;
+      if (occ) continue;
+      M2 T;
+      double bi[2][3], bo[2][3];
+      if (utd_transfer(S, w, k_i, k_s, s_in, gamma, lam, &T, bi, bo)) continue;
+      /* _weighting_rows: central differences of the plane crossing */
+      double cr[4][3];
+      const double xv[4] = {xs + hx, xs - hx, xs, xs}, pvv[4] = {phis, phis, phis + hp, phis - hp};
+      int bad = 0;
+      for (int q = 0; q < 4; ++q) {
+        double vq[3], sq, kiq[3], ksq[3], sbq;
+        cone_point(S, w, P->source, xv[q], pvv[q], vq, &sq, kiq, ksq, &sbq);
+        double dq = dot_gemv(ksq, nh);
+        if (fabs(dq) < 1e-9) { bad = 1; dq = 1.0; }
+        double gq = (P->plane_off - dot_gemv(vq, nh)) / dq;
+        for (int k = 0; k < 3; ++k) cr[q][k] = vq[k] + gq * ksq[k];
+      }
+      if (bad) continue;
+      double ddx[3], ddp[3], cx[3];
+      for (int k = 0; k < 3; ++k) {
+        ddx[k] = (cr[0][k] - cr[1][k]) / (2.0 * hx);
+        ddp[k] = (cr[2][k] - cr[3][k]) / (2.0 * hp);
+      }
+      cross3(ddx, ddp, cx);
+      double factor = norm_seq(cx);
+      cpx E[3];
+      pattern_field(&P->pattern, k_i, E);
+      cpx c0 = cdot_real(E, bi[0]), c1 = cdot_real(E, bi[1]);
+      cpx o0 = cadd(cmul(T.m[0][0], c0), cmul(T.m[0][1], c1));
+      cpx o1 = cadd(cmul(T.m[1][0], c0), cmul(T.m[1][1], c1));
+      double spread = s_in * gamma * (s_in + gamma);
+      double e_p = (cabs2(o0) + cabs2(o1)) / spread;
+      double a_sq = alpha_sq(P, offs, prec, k_i);
+      grid[(int64_t)fv * P->nx + (int64_t)fu] += norm * P->scale * e_p * factor * a_sq;
+      counters[SBR_MC_DEPOSITS]++;
+    }
+  }
+  return 0;
+}

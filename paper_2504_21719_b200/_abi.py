@@ -34,6 +34,7 @@ MAP_COUNTERS = (
     "ray_bounces",
     "direct_visible",
     "stack_overflow",
+    "cone_samples",
 )
 SBR_MC_COUNT = len(MAP_COUNTERS)
 

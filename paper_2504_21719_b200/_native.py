@@ -43,6 +43,7 @@ def _declare(lib):
                                               vp]),
         "sbr_radiomap_bounce": (ctypes.c_int, [vp, vp, u64, u64, vp, vp, vp]),
         "sbr_radiomap_direct": (ctypes.c_int, [vp, vp, vp, vp, vp]),
+        "sbr_radiomap_wedges": (ctypes.c_int, [vp, vp, vp, i32, u64, vp, vp, vp]),
         "sbr_cir_sweep": (ctypes.c_int, [vp, vp, u64, u64, vp, vp, vp]),
         "sbr_cir_vertex_order": (ctypes.c_int, [vp, vp, i64, vp, vp]),
         "sbr_cir_visibility": (ctypes.c_int, [vp, vp, vp, i64, i64, vp, vp, vp, i64, vp, vp]),
@@ -76,7 +77,8 @@ def exported_symbols():
         "sbr_scene_set_attributes", "sbr_scene_set_materials", "sbr_scene_set_wedges",
         "sbr_scene_check", "sbr_trace_closest", "sbr_trace_any",
         "sbr_occluded", "sbr_fibonacci", "sbr_philox_uniform",
-        "sbr_radiomap_bounce", "sbr_radiomap_direct", "sbr_cir_sweep", "sbr_cir_vertex_order",
+        "sbr_radiomap_bounce", "sbr_radiomap_direct", "sbr_radiomap_wedges", "sbr_cir_sweep",
+        "sbr_cir_vertex_order",
         "sbr_cir_visibility", "sbr_cir_row_pairs", "sbr_cir_select",
         "sbr_cir_resolve_records", "sbr_cir_records", "sbr_cir_refine",
         "sbr_cir_fields", "sbr_cfr", "sbr_last_error",

@@ -27,7 +27,7 @@
 
 #include <string>
 
-#include "sbr_physics.cuh"
+#include "sbr_utd.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -461,6 +461,116 @@ __global__ void __launch_bounds__(128) k_direct(DevScene S, SbrMapParams P,
   if ((threadIdx.x & 31) == 0 && s) atomicAdd(counters + SBR_MC_DIRECT_VISIBLE, (unsigned long long)s);
 }
 
+// ---------------------------------------------------------------------------
+// edge (diffraction) estimator: compute_radio_map_diffraction (radiomap.py:842-965)
+// ---------------------------------------------------------------------------
+constexpr uint64_t TAG_MAP_WEDGE = 0x9115590451c40950ULL;
+
+__device__ __forceinline__ void cone_point(const DevScene& S, int w, double3 src, double x,
+                                           double phi, double3& v, double& s_in, double3& k_i,
+                                           double3& k_s, double& sin_b) {
+  const double3 o = ldg3(S.w_origin + 3 * w), e = ldg3(S.w_ehat + 3 * w);
+  const double3 t0 = ldg3(S.w_t0 + 3 * w), n0 = ldg3(S.w_n0 + 3 * w);
+  v = o + x * e;
+  const double3 d = v - src;
+  s_in = norm_seq(d);
+  k_i = make_double3(d.x / s_in, d.y / s_in, d.z / s_in);
+  const double cb = dot_gemv(d, e) / s_in;
+  const double xb = 1.0 - cb * cb;
+  sin_b = sqrt(xb > 0.0 ? xb : 0.0);
+  double sp, cp;
+  sincos(phi, &sp, &cp);
+  const double a = sin_b * cp, b = sin_b * sp;
+  k_s = make_double3((a * t0.x + b * n0.x) + cb * e.x, (a * t0.y + b * n0.y) + cb * e.y,
+                     (a * t0.z + b * n0.z) + cb * e.z);
+}
+
+__global__ void __launch_bounds__(128) k_map_wedges(DevScene S, SbrMapParams P,
+                                                    const int32_t* __restrict__ wedge_ids,
+                                                    int32_t nw, uint64_t wedge_samples,
+                                                    double* __restrict__ grid,
+                                                    unsigned long long* __restrict__ counters) {
+  unsigned deposits = 0, cones = 0;
+  const uint64_t total = (uint64_t)nw * wedge_samples;
+  const double3 nh = make_double3(P.normal[0], P.normal[1], P.normal[2]);
+  const double3 src = make_double3(P.source[0], P.source[1], P.source[2]);
+  for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (uint64_t)gridDim.x * blockDim.x) {
+    const int w = __ldg(wedge_ids + idx / wedge_samples);
+    const uint64_t i = idx % wedge_samples;
+    const uint64_t block = i >> SBR_CHUNK_LOG2, slot = i & ((1ULL << SBR_CHUNK_LOG2) - 1);
+    cones++;
+    const double len = __ldg(S.w_len + w), nopen = __ldg(S.w_nopen + w);
+    const double u0 = philox_uniform(P.seed, (uint64_t)w, block, TAG_MAP_WEDGE, 2 * slot);
+    const double u1 = philox_uniform(P.seed, (uint64_t)w, block, TAG_MAP_WEDGE, 2 * slot + 1);
+    const double xs = u0 * len, phis = u1 * nopen * kPi;
+    double3 v, k_i, k_s;
+    double s_in, sin_b;
+    cone_point(S, w, src, xs, phis, v, s_in, k_i, k_s, sin_b);
+    if (!(sin_b >= 1e-9)) continue;
+    const double denom = dot_gemv(k_s, nh);
+    if (!(fabs(denom) > 1e-9)) continue;
+    const double gamma = (P.plane_off - dot_gemv(v, nh)) / denom;
+    if (!(gamma > 1e-4)) continue;
+    const double3 inc = neg(k_i);
+    double azim = atan2(dot_gemv(inc, ldg3(S.w_n0 + 3 * w)), dot_gemv(inc, ldg3(S.w_t0 + 3 * w)));
+    if (azim < 0.0) azim += kTwoPi;
+    if (!(azim <= nopen * kPi)) continue;
+    const double3 pts = v + gamma * k_s;
+    const double3 rel = make_double3(pts.x - P.corner[0], pts.y - P.corner[1], pts.z - P.corner[2]);
+    const double fu = floor(dot_gemv(rel, make_double3(P.u_hat[0], P.u_hat[1], P.u_hat[2])) / P.cell_w);
+    const double fv = floor(dot_gemv(rel, make_double3(P.v_hat[0], P.v_hat[1], P.v_hat[2])) / P.cell_h);
+    if (!(fu >= 0.0 && fu < (double)P.nx && fv >= 0.0 && fv < (double)P.ny)) continue;
+    bool fine;
+    if (occluded_segment(S, src, v, 1e-4, fine)) continue;
+    if (!fine) flag_error(S, kErrStack);
+    if (occluded_segment(S, v, pts, 1e-4, fine)) continue;
+    if (!fine) flag_error(S, kErrStack);
+    M2 T;
+    double3 bi[2], bo[2];
+    if (!utd_transfer(S, w, k_i, k_s, s_in, gamma, P.wavelength, T, bi, bo)) continue;
+    // _weighting_rows: central differences of the plane crossing
+    const double hx = 1e-4 * (len > 1.0 ? len : 1.0), hp = 1e-4;
+    const double xq[4] = {xs + hx, xs - hx, xs, xs}, pq[4] = {phis, phis, phis + hp, phis - hp};
+    double3 cr[4];
+    bool bad = false;
+    for (int q = 0; q < 4; ++q) {
+      double3 vq, kiq, ksq;
+      double sq, sbq;
+      cone_point(S, w, src, xq[q], pq[q], vq, sq, kiq, ksq, sbq);
+      double dq = dot_gemv(ksq, nh);
+      if (fabs(dq) < 1e-9) {
+        bad = true;
+        dq = 1.0;
+      }
+      cr[q] = vq + ((P.plane_off - dot_gemv(vq, nh)) / dq) * ksq;
+    }
+    if (bad) continue;
+    const double3 ddx = make_double3((cr[0].x - cr[1].x) / (2.0 * hx), (cr[0].y - cr[1].y) / (2.0 * hx),
+                                     (cr[0].z - cr[1].z) / (2.0 * hx));
+    const double3 ddp = make_double3((cr[2].x - cr[3].x) / (2.0 * hp), (cr[2].y - cr[3].y) / (2.0 * hp),
+                                     (cr[2].z - cr[3].z) / (2.0 * hp));
+    const double factor = norm_seq(cross3(ddx, ddp));
+    const cvec3 E = antenna_field(P.pattern, k_i);
+    const cplx c0 = cdot_real(E, bi[0]), c1 = cdot_real(E, bi[1]);
+    const cplx o0 = T.m[0][0] * c0 + T.m[0][1] * c1;
+    const cplx o1 = T.m[1][0] * c0 + T.m[1][1] * c1;
+    const double spread = s_in * gamma * (s_in + gamma);
+    const double e_p = (cabs2(o0) + cabs2(o1)) / spread;
+    const double norm = len * nopen * kPi / (double)wedge_samples;
+    atomicAdd(grid + (int64_t)fv * P.nx + (int64_t)fu,
+              norm * P.scale * e_p * factor * alpha_sq(P, k_i));
+    deposits++;
+  }
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned sd = __reduce_add_sync(0xffffffffu, deposits);
+  const unsigned sc = __reduce_add_sync(0xffffffffu, cones);
+  if (lane == 0) {
+    if (sd) atomicAdd(counters + SBR_MC_DEPOSITS, (unsigned long long)sd);
+    if (sc) atomicAdd(counters + SBR_MC_CONE_SAMPLES, (unsigned long long)sc);
+  }
+}
+
 int launch_status(const char* what) {
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess)
@@ -595,6 +705,24 @@ int sbr_radiomap_bounce(const SbrScene* scene, const SbrMapParams* P, uint64_t s
   }
   cudaFreeAsync(w->block, st);
   return rc;
+}
+
+int sbr_radiomap_wedges(const SbrScene* scene, const SbrMapParams* P, const int32_t* wedge_ids,
+                        int32_t n_wedges, uint64_t wedge_samples, double* grid,
+                        uint64_t* counters, void* stream) {
+  int rc = check_params(scene, P);
+  if (rc) return rc;
+  if (n_wedges <= 0 || wedge_samples == 0) return SBR_OK;
+  if (dev_view(scene).n_wedges <= 0) return set_error(SBR_ERR_INVALID, "scene has no wedges");
+  const uint64_t total = (uint64_t)n_wedges * wedge_samples;
+  uint64_t blocks = (total + 127) / 128;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  prof_begin(stream, "k_map_wedges");
+  k_map_wedges<<<(unsigned)blocks, 128, 0, (cudaStream_t)stream>>>(
+      dev_view(scene), *P, wedge_ids, n_wedges, wedge_samples, grid,
+      (unsigned long long*)counters);
+  prof_end(stream);
+  return launch_status("k_map_wedges");
 }
 
 int sbr_radiomap_direct(const SbrScene* scene, const SbrMapParams* P, double* direct,

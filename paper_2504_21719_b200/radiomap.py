@@ -280,14 +280,90 @@ def compute_radio_map_sbr(scene, source, grid, cfg, *, pattern=None, array=None,
     return values.cpu().numpy(), dict(diag)
 
 
+PROBE_POINTS = 8
+
+
+def _scene_diameter(scene):
+    lo, hi = scene.accel.bounds
+    return float(np.linalg.norm(hi - lo))
+
+
+def collect_wedges_near_source(scene, source, radius):
+    """Wedges within `radius` of the source, not hidden at all 8 probes (radiomap.py:645-671).
+
+    The probe occlusion rays run on the GPU (Accel.occluded_batch).
+    """
+    source = np.asarray(source, dtype=np.float64)
+    if not scene.wedges:
+        return []
+    W = scene._wedge_host
+    origin, e_hat, length = W["origin"], W["e_hat"], W["length"]
+    x = np.clip(np.sum((source - origin) * e_hat, axis=1), 0.0, length)
+    foot = origin + x[:, None] * e_hat
+    idx = np.nonzero(np.linalg.norm(source - foot, axis=1) <= radius)[0]
+    if len(idx) == 0:
+        return []
+    frac = (np.arange(PROBE_POINTS) + 0.5) / PROBE_POINTS
+    probes = (origin[idx, None, :] + (frac[None, :, None] * length[idx, None, None])
+              * e_hat[idx, None, :]).reshape(-1, 3)
+    blocked = scene.accel.occluded_batch(np.broadcast_to(source, probes.shape).copy(),
+                                         probes).reshape(len(idx), PROBE_POINTS)
+    return [int(i) for i in idx[~np.all(blocked, axis=1)]]
+
+
+def compute_radio_map_diffraction(scene, source, grid, wedges, cfg, *, pattern=None, array=None,
+                                  precoder=None, return_tensors=False):
+    """Edge-diffracted power map of one source over the listed wedges (radiomap.py:842-965).
+
+    One sm_100a kernel over all (wedge, sample) pairs: uniform (offset, cone
+    azimuth) draws from the `map-wedge` stream keyed by (seed, wedge, block),
+    plane crossing, exterior-region and occlusion tests, UTD transfer and the
+    finite-difference area weighting; float64 atomic deposits.  Returns
+    (values (ny, nx), diagnostics {wedges, cone_samples, deposits}).
+    """
+    import torch
+    source = np.asarray(source, dtype=np.float64)
+    scene.wedges  # noqa: B018  (wedge tables on the device)
+    accel = scene.accel
+    dev = accel.device
+    L = _native.lib()
+    scene.bind_frequency(cfg.frequency)
+    params, offs, prec = pack_map_params(scene, source, grid, cfg, pattern, array, precoder)
+    keep = []
+    if offs is not None:
+        t_off = torch.from_numpy(offs).to(dev)
+        t_pre = torch.from_numpy(prec).to(dev)
+        keep += [t_off, t_pre]
+        params.elem_offsets_dev = t_off.data_ptr()
+        params.precoder_dev = t_pre.data_ptr()
+    nx, ny = grid.shape
+    values = torch.zeros((ny, nx), dtype=torch.float64, device=dev)
+    counters = torch.zeros(_abi.SBR_MC_COUNT, dtype=torch.int64, device=dev)
+    ids = torch.tensor([int(w) for w in wedges], dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        if len(ids):
+            _native.check(L.sbr_radiomap_wedges(
+                accel.handle, ctypes.byref(params), _native.ptr(ids), len(ids),
+                int(cfg.wedge_samples), _native.ptr(values), _native.ptr(counters),
+                _native.stream_ptr(dev)))
+    accel.check()
+    if return_tensors:
+        return values, counters
+    c = counters.cpu().numpy()
+    diag = {"wedges": len(ids), "cone_samples": int(c[_abi.MAP_COUNTERS.index("cone_samples")])}
+    dep = int(c[_abi.MAP_COUNTERS.index("deposits")])
+    if dep:
+        diag["deposits"] = dep
+    return values.cpu().numpy(), diag
+
+
 def compute_radio_map(scene, transmitters, grid, cfg, *, precoders=None):
     """One value layer per transmitter (radiomap.py:985-1023).
 
     Transmitters may be RadioDevice instances or bare positions.  The
-    diffraction estimator (radiomap.py:640-965) is out of scope (SURVEY.md
-    §8f "next"); scenes built here carry no wedges, so -- exactly as the
-    reference does for wedge-free scenes -- the result is the bounce map
-    plus the direct term.
+    bounce estimator always runs; with diffraction enabled the edge term
+    (compute_radio_map_diffraction) is added over the wedges within
+    `cfg.wedge_radius` (scene diameter when unset), as the reference does.
     """
     from .paths import RadioDevice
     devices = [t if isinstance(t, RadioDevice)
@@ -304,7 +380,16 @@ def compute_radio_map(scene, transmitters, grid, cfg, *, precoders=None):
                                            pattern=dev.pattern, array=dev.array,
                                            precoder=pre)
         if Interaction.DIFFRACTION in cfg.enabled and scene.wedges:
-            raise NotImplementedError("diffraction radio maps are out of scope")
+            radius = (cfg.wedge_radius if cfg.wedge_radius is not None
+                      else _scene_diameter(scene))
+            ids = collect_wedges_near_source(scene, dev.position, radius)
+            if ids:
+                dvals, ddiag = compute_radio_map_diffraction(
+                    scene, dev.position, grid, ids, cfg, pattern=dev.pattern, array=dev.array,
+                    precoder=pre)
+                vals = vals + dvals
+                for key, count in ddiag.items():
+                    diag[key] = diag.get(key, 0) + count
         values[ti] = vals
         diagnostics.append(diag)
     return RadioMapResult(grid=grid, values=values, diagnostics=diagnostics)

@@ -194,16 +194,6 @@ def test_screen_diffraction_points_minimize_length(cuda):
         assert k_in @ w.e_hat == pytest.approx(k_out @ w.e_hat, abs=1e-9)
 
 
-def test_diffraction_radio_map_is_rejected_loudly(cuda):
-    # the UTD radio-map estimator (radiomap.py:640-965) is SURVEY §8f "next" #2
-    from paper_2504_21719_b200 import compute_radio_map
-    from paper_2504_21719_b200.radiomap import MeasurementGrid, RadioMapConfig
-    scene, _, _, txs, _ = build("screen_d")
-    grid = MeasurementGrid((0.0, 3.0, 1.5), (1, 0, 0), (0, 1, 0), (1.0, 1.0), (4, 4))
-    with pytest.raises(NotImplementedError):
-        compute_radio_map(scene, [txs[0].position], grid, RadioMapConfig(num_samples=1000))
-
-
 @pytest.mark.parametrize("samples,kinds", [(100_000, "R"), (50_000, "RS")])
 def test_canyon_paths_vs_oracle(cuda, samples, kinds):
     """Beyond the golden fixtures: 64 street receivers in the config-2 canyon vs the oracle."""

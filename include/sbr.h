@@ -131,8 +131,17 @@ typedef struct SbrScene SbrScene;
 int sbr_scene_create(const double* v0, const double* v1, const double* v2,
                      int64_t ntri, int32_t device, void* stream, SbrScene** out);
 void sbr_scene_destroy(SbrScene* scene);
+/* Hierarchy of subsequently created scenes over the same GPU Morton sort:
+ * 0 = Karras 2012 LBVH, 1 = PLOC (parallel locally-ordered clustering,
+ * SAH-like quality; default).  Both collapse to <= 4-triangle leaves. */
+int sbr_set_bvh_builder(int32_t builder);
 int64_t sbr_scene_num_triangles(const SbrScene* scene);
 int64_t sbr_scene_num_nodes(const SbrScene* scene);
+/* Host copy of the BVH2 node array (sbr_scene_num_nodes() x 64 B: child boxes
+ * as float4 (l.lo.x, l.hi.x, l.lo.y, l.hi.y), (r...), (l.lo.z, l.hi.z, r.lo.z,
+ * r.hi.z) and int4 child codes (>= 0 node, < 0 leaf ~(start << 2 | count-1))),
+ * for structural tests and tree-quality diagnostics. */
+int sbr_scene_copy_nodes(const SbrScene* scene, void* host_out);
 /* Host copy of slot -> input triangle index (the reference's Accel.perm). */
 int sbr_scene_permutation(const SbrScene* scene, int64_t* perm_out);
 /* Per-slot attributes, host arrays in SLOT order:

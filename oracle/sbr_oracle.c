@@ -608,6 +608,14 @@ static inline int tri_hit(const double* p0, const double* p1, const double* p2,
 
 #define STACK_CAP 256
 
+/* node / triangle visit statistics of closest1 (BVH-quality diagnostics) */
+static uint64_t g_orc_nodes = 0, g_orc_tris = 0;
+ORC_EXPORT void orc_visit_stats(uint64_t* nodes, uint64_t* tris, int reset) {
+  *nodes = g_orc_nodes;
+  *tris = g_orc_tris;
+  if (reset) g_orc_nodes = g_orc_tris = 0;
+}
+
 /* returns 0 ok, 1 overflow */
 static int closest1(const OrcScene* S, const double* o, const double* d, double t_min,
                     double t_max, double* t_res, int64_t* tri_res, double* u_res,
@@ -624,6 +632,7 @@ static int closest1(const OrcScene* S, const double* o, const double* d, double 
     int32_t node = stack[--sp];
     if (S->count[node] > 0) {
       int32_t s = S->start[node];
+      g_orc_tris += (uint64_t)S->count[node];
       for (int32_t j = s; j < s + S->count[node]; ++j) {
         double t, u, v;
         if (tri_hit(S->v0 + 3 * j, S->v1 + 3 * j, S->v2 + 3 * j, &c, t_min, &t, &u, &v)) {
@@ -637,6 +646,7 @@ static int closest1(const OrcScene* S, const double* o, const double* d, double 
       continue;
     }
     int32_t l = node + 1, r = S->right[node];
+    g_orc_nodes++;
     double el = box_enter(S->bmin + 3 * l, S->bmax + 3 * l, &c, t_min, best_t);
     double er = box_enter(S->bmin + 3 * r, S->bmax + 3 * r, &c, t_min, best_t);
     if (el < INFINITY && er < INFINITY) {

@@ -27,9 +27,11 @@ def _declare(lib):
         "sbr_scene_create": (ctypes.c_int, [vp, vp, vp, i64, i32, vp,
                                             ctypes.POINTER(vp)]),
         "sbr_scene_destroy": (None, [vp]),
+        "sbr_set_bvh_builder": (ctypes.c_int, [i32]),
         "sbr_scene_num_triangles": (i64, [vp]),
         "sbr_scene_num_nodes": (i64, [vp]),
         "sbr_scene_permutation": (ctypes.c_int, [vp, vp]),
+        "sbr_scene_copy_nodes": (ctypes.c_int, [vp, vp]),
         "sbr_scene_set_attributes": (ctypes.c_int, [vp, vp, vp, vp, vp, vp]),
         "sbr_scene_set_materials": (ctypes.c_int, [vp, vp, i32]),
         "sbr_scene_set_wedges": (ctypes.c_int, [vp, vp]),
@@ -72,8 +74,8 @@ def _declare(lib):
 def exported_symbols():
     """Names every build of libsbr.so must export (checked by the CPU tests)."""
     return [
-        "sbr_scene_create", "sbr_scene_destroy", "sbr_scene_num_triangles",
-        "sbr_scene_num_nodes", "sbr_scene_permutation",
+        "sbr_scene_create", "sbr_scene_destroy", "sbr_set_bvh_builder", "sbr_scene_num_triangles",
+        "sbr_scene_num_nodes", "sbr_scene_permutation", "sbr_scene_copy_nodes",
         "sbr_scene_set_attributes", "sbr_scene_set_materials", "sbr_scene_set_wedges",
         "sbr_scene_check", "sbr_trace_closest", "sbr_trace_any",
         "sbr_occluded", "sbr_fibonacci", "sbr_philox_uniform",
@@ -95,6 +97,9 @@ def load_library():
                 f"{LIB_PATH} is missing; run __graft_entry__.build() "
                 "(this package has no CPU fallback)")
         _lib = _declare(ctypes.CDLL(LIB_PATH))
+        builder = os.environ.get("SBR_BVH_BUILDER")  # "lbvh" / "ploc" (default)
+        if builder:
+            check(_lib.sbr_set_bvh_builder({"lbvh": 0, "ploc": 1}[builder.lower()]))
     return _lib
 
 

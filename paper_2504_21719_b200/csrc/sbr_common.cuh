@@ -347,14 +347,28 @@ __device__ __forceinline__ bool tri_hit(const Ray64& r, const TriSlot* __restric
 // ---------------------------------------------------------------------------
 // conservative fp32 box test
 // ---------------------------------------------------------------------------
-// Per axis, the slab [lo, hi] is widened by `pad` (covers the rounding of the
-// origin to fp32, of (lo - o) and of the product by 1/d), so the computed
-// entry/exit interval always contains the exact one: the BVH can only
-// over-visit, never cull a box holding the exact closest triangle.
+// Error analysis (d > 0, entry plane lo; the other cases are symmetric).
+// ix = fl(1/fl(d)) = (1+a)/d, |a| <= 2^-23; oxp = fl32((o+p)*ix) computed in
+// float64, so only its final rounding b (|b| <= 2^-24) is left;
+// x0 = fma(lo, ix, -oxp) rounds once more (g, |g| <= 2^-24):
+//     x0 = (1+a)(1+g)/d * [(lo - o) - p - (o+p) b].
+// With p >= 2^-22 |o| the bracket is <= lo - o, hence x0 <= f(T) where T is
+// the exact plane distance and f(t) = t + c|t|, c = 3*2^-24.  Symmetrically
+// the exit planes satisfy x >= t - c|t|.  Both maps are monotonic, so the
+// computed entry tn <= f(exact tn) and exit tf >= exact tf - c|exact tf|.
+// The tests then only need:
+//   * tn <= bound: bound_up() inflates by >= 31*2^-24 > c  (no slack on tn);
+//   * tn <= tf and the t_min cull: compare against tf2 = tf + 2^-20 |tf|,
+//     which is >= f(exact tf) (2^-20 = 16*2^-24 >= 2c plus one rounding).
+// So a box holding an exact hit with t_min < t <= best_t is never culled,
+// while the pad is 2^-22 |o| instead of a multiple of the scene size: a ray
+// leaving a surface no longer re-enters the (flat) boxes around its origin.
+// `pad_floor` (scene size * 2^-26) only guards origins near 0.
 struct RayBox {
-  float ix, iy, iz;       // 1/d (finite)
-  float oxp, oyp, ozp;    // (o + pad) * inv   -> lo planes
-  float oxm, oym, ozm;    // (o - pad) * inv   -> hi planes
+  float ix, iy, iz;       // fl(1/fl(d)) (clamped to +-1e20)
+  float oxp, oyp, ozp;    // fl((o + pad) * ix)  -> lo planes
+  float oxm, oym, ozm;    // fl((o - pad) * ix)  -> hi planes
+  float tlo;              // t_min rounded down: boxes exited before it hold no hit
 };
 
 __device__ __forceinline__ float safe_inv(double d) {
@@ -362,21 +376,30 @@ __device__ __forceinline__ float safe_inv(double d) {
   return fabsf(f) > 1e-20f ? 1.0f / f : copysignf(1e20f, f);
 }
 
-__device__ __forceinline__ RayBox box_setup(double3 o, double3 d, float pad_base) {
+// `tlo` mirrors the reference's `tf > t_min` box cull (_core.pyx:69): a valid
+// hit has t > t_min inside the box, and tf2 >= the exact exit, so culling
+// tf2 < rd(t_min) is exact.
+__device__ __forceinline__ RayBox box_setup(double3 o, double3 d, float pad_floor,
+                                            double t_min) {
   RayBox b;
+  b.tlo = t_min > 0.0 ? __double2float_rd(t_min) : 0.0f;
   b.ix = safe_inv(d.x);
   b.iy = safe_inv(d.y);
   b.iz = safe_inv(d.z);
-  const float ox = (float)o.x, oy = (float)o.y, oz = (float)o.z;
-  const float px = pad_base + 1e-6f * fabsf(ox);
-  const float py = pad_base + 1e-6f * fabsf(oy);
-  const float pz = pad_base + 1e-6f * fabsf(oz);
-  b.oxp = (ox + px) * b.ix;
-  b.oyp = (oy + py) * b.iy;
-  b.ozp = (oz + pz) * b.iz;
-  b.oxm = (ox - px) * b.ix;
-  b.oym = (oy - py) * b.iy;
-  b.ozm = (oz - pz) * b.iz;
+#ifdef SBR_PAD_EXPERIMENT  // diagnostics only: scales the (conservative) pad
+  const double k = SBR_PAD_EXPERIMENT * 0x1p-22;
+#else
+  const double k = 0x1p-22;
+#endif
+  const double px = k * fabs(o.x) + pad_floor;
+  const double py = k * fabs(o.y) + pad_floor;
+  const double pz = k * fabs(o.z) + pad_floor;
+  b.oxp = (float)((o.x + px) * (double)b.ix);
+  b.oyp = (float)((o.y + py) * (double)b.iy);
+  b.ozp = (float)((o.z + pz) * (double)b.iz);
+  b.oxm = (float)((o.x - px) * (double)b.ix);
+  b.oym = (float)((o.y - py) * (double)b.iy);
+  b.ozm = (float)((o.z - pz) * (double)b.iz);
   return b;
 }
 
@@ -388,7 +411,8 @@ __device__ __forceinline__ float box_enter(const RayBox& rb, float lox, float hi
   const float z0 = fmaf(loz, rb.iz, -rb.ozp), z1 = fmaf(hiz, rb.iz, -rb.ozm);
   const float tn = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fminf(z0, z1));
   const float tf = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fmaxf(z0, z1));
-  return (tn <= tf && tf >= 0.0f && tn <= bound) ? tn : __int_as_float(0x7f800000);
+  const float tf2 = fmaf(0x1p-20f, fabsf(tf), tf);
+  return (tn <= tf2 && tf2 >= rb.tlo && tn <= bound) ? tn : __int_as_float(0x7f800000);
 }
 
 // float upper bound of a float64 distance (for comparing fp32 entries)
@@ -410,7 +434,7 @@ struct HitRecord {
 __device__ __forceinline__ bool trace_closest(const DevScene& S, double3 o, double3 d,
                                               double t_min, double t_max, HitRecord& h) {
   const Ray64 r = ray_setup(o, d);
-  const RayBox rb = box_setup(o, d, S.pad_base);
+  const RayBox rb = box_setup(o, d, S.pad_base, t_min);
   double best_t = t_max, bu = 0.0, bv = 0.0;
   int best = -1, best_rank = 0x7fffffff;
   float bound = bound_up(best_t);
@@ -487,8 +511,8 @@ __device__ __forceinline__ bool trace_closest(const DevScene& S, double3 o, doub
 }
 
 // Closest hit, "while-while" form with postponed leaves (Aila & Laine 2009):
-// a lane that reaches a leaf parks it and keeps descending inner nodes until
-// every lane of the warp holds a leaf, then the warp tests its leaves
+// a lane that reaches a leaf parks it (and, only with -DSBR_SPECULATE, keeps
+// descending inner nodes) until every lane of the warp holds a leaf, then the warp tests its leaves
 // together, so the expensive float64 triangle tests run with most lanes
 // active instead of one or two.  Same result as trace_closest (the minimum of
 // (t, tie_rank) over all triangles is independent of visiting order; box
@@ -500,6 +524,18 @@ __device__ __forceinline__ int ww_pop(const int* stack_node, const float* stack_
   while (sp > 0) {
     --sp;
     if (stack_t[sp] <= bound) return stack_node[sp];
+  }
+  return kDone;
+}
+
+__device__ __forceinline__ int ww_pop_t(const int* stack_node, const float* stack_t, int& sp,
+                                        float bound, float& t_out) {
+  while (sp > 0) {
+    --sp;
+    if (stack_t[sp] <= bound) {
+      t_out = stack_t[sp];
+      return stack_node[sp];
+    }
   }
   return kDone;
 }
@@ -517,6 +553,7 @@ struct ClosestTravT {
   int stack_node[kStackSize];
   float stack_t[kStackSize];
   int sp, node, leaf;
+  float node_t, leaf_t;  // entry distances of the current node / parked leaf
   bool ok;
 #ifdef SBR_COUNT_VISITS
   unsigned visits, tests;
@@ -525,7 +562,7 @@ struct ClosestTravT {
   __device__ __forceinline__ void start(const DevScene& S, double3 o, double3 d, double tmin,
                                         double tmax) {
     r = ray_setup(o, d);
-    rb = box_setup(o, d, S.pad_base);
+    rb = box_setup(o, d, S.pad_base, tmin);
     t_min = tmin;
     best_t = tmax;
     bu = bv = 0.0;
@@ -535,6 +572,7 @@ struct ClosestTravT {
     sp = 0;
     node = 0;
     leaf = 0;
+    node_t = leaf_t = 0.0f;
     ok = true;
 #ifdef SBR_COUNT_VISITS
     visits = tests = 0;
@@ -547,7 +585,7 @@ struct ClosestTravT {
   __device__ __forceinline__ bool done() const { return node == kDone && leaf == 0; }
 
   __device__ __forceinline__ void round(const DevScene& S) {
-    // ---- inner nodes (speculative: continue past a parked leaf)
+    // ---- inner nodes (a lane leaves the loop once it has parked a leaf)
     while (node >= 0) {
 #ifdef SBR_COUNT_VISITS
       ++visits;
@@ -571,22 +609,31 @@ struct ClosestTravT {
         stack_t[sp] = lfirst ? tr : tl;
         ++sp;
         node = lfirst ? ch.x : ch.y;
+        node_t = lfirst ? tl : tr;
       } else if (hl) {
         node = ch.x;
+        node_t = tl;
       } else if (hr) {
         node = ch.y;
+        node_t = tr;
       } else {
-        node = ww_pop(stack_node, stack_t, sp, bound);
+        node = ww_pop_t(stack_node, stack_t, sp, bound, node_t);
       }
       if (node < 0 && node != kDone && leaf == 0) {
         leaf = node;
-        node = ww_pop(stack_node, stack_t, sp, bound);
+        leaf_t = node_t;
+        node = ww_pop_t(stack_node, stack_t, sp, bound, node_t);
+#ifndef SBR_SPECULATE
+        break;  // measured: speculating past a parked leaf costs ~2% (stale bound)
+#endif
       }
       if (!__any_sync(__activemask(), leaf == 0)) break;
     }
     // ---- leaves
     while (leaf < 0) {
-      const int s = leaf_start(leaf), n = leaf_count(leaf);
+      const int s = leaf_start(leaf);
+      // a parked leaf beyond the best hit found since parking is culled
+      const int n = leaf_t <= bound ? leaf_count(leaf) : 0;
 #ifdef SBR_COUNT_VISITS
       tests += n;
 #endif
@@ -612,7 +659,8 @@ struct ClosestTravT {
       leaf = 0;
       if (node < 0 && node != kDone) {
         leaf = node;
-        node = ww_pop(stack_node, stack_t, sp, bound);
+        leaf_t = node_t;
+        node = ww_pop_t(stack_node, stack_t, sp, bound, node_t);
       }
       if (!__any_sync(__activemask(), leaf < 0)) break;
     }
@@ -640,7 +688,7 @@ struct AnyTrav {
   __device__ __forceinline__ void start(const DevScene& S, double3 o, double3 d, double tmin,
                                         double lim) {
     r = ray_setup(o, d);
-    rb = box_setup(o, d, S.pad_base);
+    rb = box_setup(o, d, S.pad_base, tmin);
     t_min = tmin;
     limit = lim;
     bound = bound_up(lim);
@@ -728,7 +776,7 @@ __device__ __forceinline__ bool trace_closest_ww(const DevScene& S, bool active,
 __device__ __forceinline__ bool trace_any(const DevScene& S, double3 o, double3 d,
                                           double t_min, double limit, bool& found) {
   const Ray64 r = ray_setup(o, d);
-  const RayBox rb = box_setup(o, d, S.pad_base);
+  const RayBox rb = box_setup(o, d, S.pad_base, t_min);
   const float bound = bound_up(limit);
   int stack_node[kStackSize];
   int sp = 0;

@@ -371,6 +371,168 @@ __global__ void k_gather_tris(const double* __restrict__ v0, const double* __res
   tris[i] = s;
 }
 
+// ---------------------------------------------------------------------------
+// PLOC: parallel locally-ordered clustering over the Morton order (Meister &
+// Bittner 2018).  Clusters start as the Morton-sorted leaves; every round each
+// cluster finds its cheapest merge partner (surface area of the union) within
+// +-kPlocRadius positions, mutual nearest pairs merge, the cluster list is
+// compacted.  Gives SAH-like trees from the same GPU sort; the result is
+// converted to the Karras-style (children, ranges) arrays by renumbering the
+// leaves in depth-first order, so the leaf collapse / emit path is shared.
+// ---------------------------------------------------------------------------
+constexpr int kPlocRadius = 12;
+
+__device__ __forceinline__ float half_area(const Box32& b) {
+  const float dx = b.hi[0] - b.lo[0], dy = b.hi[1] - b.lo[1], dz = b.hi[2] - b.lo[2];
+  return dx * dy + dy * dz + dz * dx;
+}
+
+__device__ __forceinline__ Box32 box_union(const Box32& a, const Box32& b) {
+  Box32 u;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    u.lo[k] = fminf(a.lo[k], b.lo[k]);
+    u.hi[k] = fmaxf(a.hi[k], b.hi[k]);
+  }
+  return u;
+}
+
+__global__ void k_leaf_boxes(const double* __restrict__ v0, const double* __restrict__ v1,
+                             const double* __restrict__ v2, const int32_t* __restrict__ ids,
+                             int n, Box32* box) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int tri = ids[i];
+  Box32 b;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double a = v0[3 * tri + k], c = v1[3 * tri + k], d = v2[3 * tri + k];
+    b.lo[k] = __double2float_rd(fmin(fmin(a, c), d));
+    b.hi[k] = __double2float_ru(fmax(fmax(a, c), d));
+  }
+  box[i] = b;
+}
+
+__global__ void k_iota_i32(int32_t* a, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = i;
+}
+
+__global__ void k_ploc_nearest(const int32_t* __restrict__ C, int m, const Box32* __restrict__ box,
+                               int32_t* nearest) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const Box32 bi = box[C[i]];
+  float best = __int_as_float(0x7f800000);
+  int bj = -1;
+  const int lo = i - kPlocRadius < 0 ? 0 : i - kPlocRadius;
+  const int hi = i + kPlocRadius >= m ? m - 1 : i + kPlocRadius;
+  for (int j = lo; j <= hi; ++j) {
+    if (j == i) continue;
+    const float c = half_area(box_union(bi, box[C[j]]));
+    if (c < best) {  // ties keep the lower index: deterministic
+      best = c;
+      bj = j;
+    }
+  }
+  nearest[i] = bj;
+}
+
+__global__ void k_ploc_flags(const int32_t* __restrict__ nearest, int m, int32_t* flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int j = nearest[i];
+  flag[i] = (j > i && nearest[j] == i) ? 1 : 0;
+}
+
+__global__ void k_ploc_merge(int32_t* C, const int32_t* __restrict__ nearest,
+                             const int32_t* __restrict__ flag, const int32_t* __restrict__ pos,
+                             int m, int n, int base, Box32* box, int2* kids, int32_t* parent) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m || !flag[i]) return;
+  const int j = nearest[i];
+  const int id = base + pos[i];  // internal node ids n .. 2n-2, creation order
+  const int a = C[i], b = C[j];
+  kids[id - n] = make_int2(a, b);
+  box[id] = box_union(box[a], box[b]);
+  parent[a] = id;
+  parent[b] = id;
+  C[i] = id;
+  C[j] = -1;
+}
+
+__global__ void k_ploc_valid(const int32_t* __restrict__ C, int m, int32_t* valid) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) valid[i] = C[i] >= 0 ? 1 : 0;
+}
+
+__global__ void k_ploc_compact(const int32_t* __restrict__ C, const int32_t* __restrict__ valid,
+                               const int32_t* __restrict__ pos, int m, int32_t* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m && valid[i]) out[pos[i]] = C[i];
+}
+
+// leaf counts bottom-up (second arrival at a node sums its children)
+__global__ void k_ploc_counts(const int32_t* __restrict__ parent, const int2* __restrict__ kids,
+                              int n, int32_t* cnt, unsigned* visits) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  cnt[i] = 1;
+  int node = parent[i];
+  while (node >= 0) {
+    __threadfence();
+    if (atomicAdd(visits + (node - n), 1u) == 0) return;
+    __threadfence();
+    const int2 k = kids[node - n];
+    cnt[node] = cnt[k.x] + cnt[k.y];
+    node = parent[node];
+  }
+}
+
+// depth-first offset of every node: sum of left-sibling counts on the root path
+__global__ void k_ploc_offsets(const int32_t* __restrict__ parent, const int2* __restrict__ kids,
+                               const int32_t* __restrict__ cnt, int total, int n, int32_t* off) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= total) return;
+  int o = 0, c = v, p = parent[v];
+  while (p >= 0) {
+    const int2 k = kids[p - n];
+    if (k.y == c) o += cnt[k.x];
+    c = p;
+    p = parent[p];
+  }
+  off[v] = o;
+}
+
+// Karras-style arrays: internal node id -> index (2n-2-id, root at 0), leaves
+// encoded ~(depth-first slot)
+__global__ void k_ploc_export(const int2* __restrict__ kids, const int32_t* __restrict__ cnt,
+                              const int32_t* __restrict__ off, const Box32* __restrict__ box,
+                              int n, int2* children, int2* ranges, Box32* int_box) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n - 1) return;
+  const int id = n + k;
+  const int idx = 2 * n - 2 - id;
+  const int2 c = kids[k];
+  const int l = c.x < n ? ~off[c.x] : 2 * n - 2 - c.x;
+  const int r = c.y < n ? ~off[c.y] : 2 * n - 2 - c.y;
+  children[idx] = make_int2(l, r);
+  ranges[idx] = make_int2(off[id], off[id] + cnt[id] - 1);
+  int_box[idx] = box[id];
+}
+
+__global__ void k_ploc_leaves(const int32_t* __restrict__ off, const Box32* __restrict__ box,
+                              const int32_t* __restrict__ ids_sorted, int n, Box32* leaf_box,
+                              int32_t* ids_dfs) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int s = off[i];
+  leaf_box[s] = box[i];
+  ids_dfs[s] = ids_sorted[i];
+}
+
+static int g_builder = 1;  // 0 = Karras LBVH, 1 = PLOC
+
 template <typename T>
 static int dalloc(T** p, size_t count, cudaStream_t st) {
   SBR_CUDA(cudaMallocAsync((void**)p, sizeof(T) * (count ? count : 1), st));
@@ -389,6 +551,12 @@ extern "C" {
 
 const char* sbr_last_error(void) { return g_last_error.c_str(); }
 int sbr_version(void) { return 100; }
+
+int sbr_set_bvh_builder(int32_t builder) {
+  if (builder != 0 && builder != 1) return set_error(SBR_ERR_INVALID, "builder: 0 LBVH, 1 PLOC");
+  g_builder = builder;
+  return SBR_OK;
+}
 uint64_t sbr_kernel_launches(void) { return g_launches.load(); }
 
 int sbr_profile_enable(int on) {
@@ -442,7 +610,7 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
     S->lo[k] = fmin(S->lo[k], fmin(fmin(v0[i], v1[i]), v2[i]));
     S->hi[k] = fmax(S->hi[k], fmax(fmax(v0[i], v1[i]), v2[i]));
   }
-  S->pad_base = (float)(ldexp(max_abs + 1.0, -20));
+  S->pad_base = (float)(ldexp(max_abs + 1.0, -26));  // box_setup's pad floor
 
   double *dv0, *dv1, *dv2;
   const size_t bytes = sizeof(double) * 3 * (size_t)ntri;
@@ -488,16 +656,84 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
       (rc = dalloc(&leaf_box, n, st)) || (rc = dalloc(&int_box, nint, st)) ||
       (rc = dalloc(&visits, nint, st)))
     return rc;
-  if (nint) {
-    SBR_CUDA(cudaMemsetAsync(visits, 0, sizeof(unsigned) * nint, st));
-    SBR_CUDA(cudaMemsetAsync(parent_int, 0xff, sizeof(int) * nint, st));
-    k_karras<<<grid_for(nint, 256), 256, 0, st>>>(keys_sorted, n, children, ranges, parent_int,
-                                                  parent_leaf);
+  int32_t* ids_leaf = ids_sorted;  // triangle of each leaf slot
+  int32_t* ids_dfs = nullptr;
+  if (g_builder == 1 && n > 1) {
+    // ---- PLOC hierarchy, exported in depth-first leaf order ----
+    const int total = 2 * n - 1;
+    Box32* box_all;
+    int2* kids;
+    int32_t *C, *C2, *nearest, *flag, *pos, *parent, *cnt, *off;
+    unsigned* vis2;
+    if ((rc = dalloc(&box_all, total, st)) || (rc = dalloc(&kids, nint, st)) ||
+        (rc = dalloc(&C, n, st)) || (rc = dalloc(&C2, n, st)) || (rc = dalloc(&nearest, n, st)) ||
+        (rc = dalloc(&flag, n + 1, st)) || (rc = dalloc(&pos, n + 1, st)) ||
+        (rc = dalloc(&parent, total, st)) || (rc = dalloc(&cnt, total, st)) ||
+        (rc = dalloc(&off, total, st)) || (rc = dalloc(&vis2, nint, st)) ||
+        (rc = dalloc(&ids_dfs, n, st)))
+      return rc;
+    k_leaf_boxes<<<grid_for(n, 256), 256, 0, st>>>(dv0, dv1, dv2, ids_sorted, n, box_all);
+    count_launch();
+    k_iota_i32<<<grid_for(n, 256), 256, 0, st>>>(C, n);
+    count_launch();
+    SBR_CUDA(cudaMemsetAsync(parent, 0xff, sizeof(int32_t) * total, st));
+    size_t sb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, sb, flag, pos, n + 1, st);
+    void* stmp;
+    SBR_CUDA(cudaMallocAsync(&stmp, sb, st));
+    int m = n, base = n;
+    while (m > 1) {
+      k_ploc_nearest<<<grid_for(m, 128), 128, 0, st>>>(C, m, box_all, nearest);
+      k_ploc_flags<<<grid_for(m, 256), 256, 0, st>>>(nearest, m, flag);
+      SBR_CUDA(cub::DeviceScan::ExclusiveSum(stmp, sb, flag, pos, m + 1, st));
+      k_ploc_merge<<<grid_for(m, 256), 256, 0, st>>>(C, nearest, flag, pos, m, n, base, box_all,
+                                                     kids, parent);
+      k_ploc_valid<<<grid_for(m, 256), 256, 0, st>>>(C, m, flag);
+      SBR_CUDA(cub::DeviceScan::ExclusiveSum(stmp, sb, flag, pos, m + 1, st));
+      k_ploc_compact<<<grid_for(m, 256), 256, 0, st>>>(C, flag, pos, m, C2);
+      int m_new = 0;
+      SBR_CUDA(cudaMemcpyAsync(&m_new, pos + m, sizeof(int), cudaMemcpyDeviceToHost, st));
+      SBR_CUDA(cudaStreamSynchronize(st));
+      for (int q = 0; q < 7; ++q) count_launch();
+      base += m - m_new;
+      m = m_new;
+      int32_t* t = C;
+      C = C2;
+      C2 = t;
+    }
+    SBR_CUDA(cudaMemsetAsync(vis2, 0, sizeof(unsigned) * nint, st));
+    k_ploc_counts<<<grid_for(n, 256), 256, 0, st>>>(parent, kids, n, cnt, vis2);
+    k_ploc_offsets<<<grid_for(total, 256), 256, 0, st>>>(parent, kids, cnt, total, n, off);
+    k_ploc_export<<<grid_for(nint, 256), 256, 0, st>>>(kids, cnt, off, box_all, n, children, ranges,
+                                                       int_box);
+    k_ploc_leaves<<<grid_for(n, 256), 256, 0, st>>>(off, box_all, ids_sorted, n, leaf_box,
+                                                    ids_dfs);
+    for (int q = 0; q < 4; ++q) count_launch();
+    ids_leaf = ids_dfs;
+    cudaFreeAsync(stmp, st);
+    cudaFreeAsync(box_all, st);
+    cudaFreeAsync(kids, st);
+    cudaFreeAsync(C, st);
+    cudaFreeAsync(C2, st);
+    cudaFreeAsync(nearest, st);
+    cudaFreeAsync(flag, st);
+    cudaFreeAsync(pos, st);
+    cudaFreeAsync(parent, st);
+    cudaFreeAsync(cnt, st);
+    cudaFreeAsync(off, st);
+    cudaFreeAsync(vis2, st);
+  } else {
+    if (nint) {
+      SBR_CUDA(cudaMemsetAsync(visits, 0, sizeof(unsigned) * nint, st));
+      SBR_CUDA(cudaMemsetAsync(parent_int, 0xff, sizeof(int) * nint, st));
+      k_karras<<<grid_for(nint, 256), 256, 0, st>>>(keys_sorted, n, children, ranges, parent_int,
+                                                    parent_leaf);
+      count_launch();
+    }
+    k_refit<<<grid_for(n, 256), 256, 0, st>>>(dv0, dv1, dv2, ids_sorted, n, children, parent_int,
+                                              parent_leaf, leaf_box, int_box, visits);
     count_launch();
   }
-  k_refit<<<grid_for(n, 256), 256, 0, st>>>(dv0, dv1, dv2, ids_sorted, n, children, parent_int,
-                                            parent_leaf, leaf_box, int_box, visits);
-  count_launch();
 
   int nnodes = 1;
   if (n > 4) {
@@ -527,12 +763,12 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
   S->nnodes = nnodes;
 
   if ((rc = dalloc(&S->tris, n, st))) return rc;
-  k_gather_tris<<<grid_for(n, 256), 256, 0, st>>>(dv0, dv1, dv2, ids_sorted, n, S->tris);
+  k_gather_tris<<<grid_for(n, 256), 256, 0, st>>>(dv0, dv1, dv2, ids_leaf, n, S->tris);
   count_launch();
 
   S->perm.resize(n);
   std::vector<int32_t> ids_host(n);
-  SBR_CUDA(cudaMemcpyAsync(ids_host.data(), ids_sorted, sizeof(int32_t) * n,
+  SBR_CUDA(cudaMemcpyAsync(ids_host.data(), ids_leaf, sizeof(int32_t) * n,
                            cudaMemcpyDeviceToHost, st));
   if ((rc = dalloc(&S->error_word, 1, st))) return rc;
   SBR_CUDA(cudaMemsetAsync(S->error_word, 0, sizeof(unsigned), st));
@@ -566,6 +802,7 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
   cudaFreeAsync(leaf_box, st);
   cudaFreeAsync(int_box, st);
   cudaFreeAsync(visits, st);
+  if (ids_dfs) cudaFreeAsync(ids_dfs, st);
   SBR_CUDA(cudaStreamSynchronize(st));
   SBR_CUDA(cudaGetLastError());
   *out = S;
@@ -590,6 +827,13 @@ void sbr_scene_destroy(SbrScene* S) {
 
 int64_t sbr_scene_num_triangles(const SbrScene* S) { return S ? S->ntri : 0; }
 int64_t sbr_scene_num_nodes(const SbrScene* S) { return S ? S->nnodes : 0; }
+
+int sbr_scene_copy_nodes(const SbrScene* S, void* host_out) {
+  if (!S || !host_out) return set_error(SBR_ERR_INVALID, "NULL argument");
+  SBR_CUDA(cudaMemcpy(host_out, S->nodes, sizeof(BvhNode) * (size_t)S->nnodes,
+                      cudaMemcpyDeviceToHost));
+  return SBR_OK;
+}
 
 int sbr_scene_permutation(const SbrScene* S, int64_t* perm_out) {
   if (!S || !perm_out) return set_error(SBR_ERR_INVALID, "NULL argument");

@@ -179,6 +179,20 @@ class Accel:
     def handle(self):
         return self._handle
 
+    def bvh_nodes(self):
+        """Host copy of the device BVH2: (boxes (M, 2, 2, 3) [child, lo/hi, xyz], codes (M, 2))."""
+        raw = np.empty((self.num_nodes, 16), dtype=np.float32)
+        _native.check(self._lib.sbr_scene_copy_nodes(self._handle,
+                                                     raw.ctypes.data_as(ctypes.c_void_p)))
+        a, b, c = raw[:, 0:4], raw[:, 4:8], raw[:, 8:12]
+        codes = raw[:, 12:14].copy().view(np.int32)
+        boxes = np.empty((self.num_nodes, 2, 2, 3), dtype=np.float32)
+        boxes[:, 0, 0] = np.stack([a[:, 0], a[:, 2], c[:, 0]], 1)
+        boxes[:, 0, 1] = np.stack([a[:, 1], a[:, 3], c[:, 1]], 1)
+        boxes[:, 1, 0] = np.stack([b[:, 0], b[:, 2], c[:, 2]], 1)
+        boxes[:, 1, 1] = np.stack([b[:, 1], b[:, 3], c[:, 3]], 1)
+        return boxes, codes
+
     def __del__(self):
         h = getattr(self, "_handle", None)
         if h is not None and h.value:

@@ -1,7 +1,7 @@
 """Nodes visited / triangles tested per ray-bounce with the SBR_COUNT_VISITS variant."""
 import os, sys, numpy as np
 sys.path.insert(0, os.getcwd())
-os.environ["SBR_LIB_PATH"] = os.path.join(os.getcwd(), "paper_2504_21719_b200/_lib/variants/libsbr_visits.so")
+os.environ["SBR_LIB_PATH"] = os.path.join(os.getcwd(), "paper_2504_21719_b200/_lib/variants/libsbr_%s.so" % os.environ.get("SBR_VISITS_LIB", "visits"))
 import torch
 from paper_2504_21719_b200 import SceneModel, scenes, _abi
 from paper_2504_21719_b200.radiomap import compute_radio_map_sbr, MeasurementGrid, RadioMapConfig

@@ -143,9 +143,10 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def profiled_traffic():
-    """dram bytes per k_radiomap launch from the committed ncu capture, if any."""
-    path = os.path.join(ROOT, "profiles", "radiomap_traffic.json")
+def profiled_traffic(kernel):
+    """Mean dram bytes per launch of `kernel` from the committed ncu capture
+    (profiles/traffic_<kernel>.json, tools/ncu_summary.py traffic), if any."""
+    path = os.path.join(ROOT, "profiles", f"traffic_{kernel}.json")
     try:
         with open(path) as f:
             return json.load(f)
@@ -326,7 +327,7 @@ def run_ours(args, rank, world, local_rank):
     # processed, over the kernel's own summed launch time
     achieved = rb_per_step_local * BYTES_PER_RB / (dom_ms_step / 1e3) / 1e9
     peak, peak_kind = peaks()
-    traffic = profiled_traffic()
+    traffic = profiled_traffic(dom)
 
     # ---- end to end through the public API (host buffers) ----
     e2e_ms = []

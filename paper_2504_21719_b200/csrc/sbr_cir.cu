@@ -270,14 +270,28 @@ __global__ void k_vertex_morton(const double* __restrict__ point, int64_t n, dou
 // ---------------------------------------------------------------------------
 // visibility: (vertex, target) pairs
 // ---------------------------------------------------------------------------
-// Pair p -> (tile of 32 spatially sorted vertices, target, vertex in tile):
-// a warp claims 32 consecutive pairs = 32 neighbouring vertices looking at
-// the same target, so their occlusion rays are nearly parallel and walk the
-// same BVH nodes.  The half-space side test runs first; survivors are pushed
-// into a per-warp queue in shared memory and cast 32 at a time with the
-// while-while any-hit, so dead lanes never enter traversal and no pair list
-// goes through HBM.
+// Pair p -> (group of kVisGroup tiles of 32 spatially sorted vertices,
+// target, tile, vertex in tile).  A warp claims one group x target at a time
+// and walks its tiles: 32 neighbouring vertices looking at the same target,
+// so the occlusion rays are nearly parallel and walk the same BVH nodes.  The
+// half-space side test runs first; survivors are pushed into a per-warp queue
+// in shared memory and cast 32 at a time with the while-while any-hit, so
+// dead lanes never enter traversal and no pair list goes through HBM.
+//
+// Occluder sharing (97 % of config-3 rays are occluded): a lane that finds an
+// occluder publishes it to the lanes still traversing (tested at once) and to
+// a small per-warp ring that the next tiles of the same target test before
+// traversing.  Any triangle with t_min < t < limit decides "occluded", so the
+// result is exactly the traversal's.
 constexpr int kVisWarps = 4;
+#ifndef SBR_VIS_HINTS
+#define SBR_VIS_HINTS 4
+#endif
+#ifndef SBR_VIS_GROUP
+#define SBR_VIS_GROUP 8
+#endif
+constexpr int kVisHints = SBR_VIS_HINTS;
+constexpr int kVisGroup = SBR_VIS_GROUP;
 
 __global__ void __launch_bounds__(128) k_cir_visibility(DevScene S, SbrCirParams P,
                                                         SbrVertexBuf vb, int64_t v_begin,
@@ -287,30 +301,53 @@ __global__ void __launch_bounds__(128) k_cir_visibility(DevScene S, SbrCirParams
                                                         unsigned long long* work,
                                                         const int32_t* __restrict__ order) {
   __shared__ int64_t sq[kVisWarps][64];
+  __shared__ int shint[kVisWarps][kVisHints > 0 ? kVisHints : 1];
+  __shared__ int shpos[kVisWarps];
   const unsigned lane = threadIdx.x & 31u;
   const unsigned wid = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t nt = P.n_targets;
   const int64_t nv = v_end - v_begin;
-  const int64_t total = ((nv + 31) / 32) * 32 * nt;
+  const int64_t ntiles = (nv + 31) / 32;
+  const int64_t ngroups = (ntiles + kVisGroup - 1) / kVisGroup;
+  const int64_t total = ngroups * nt;  // claim units: (group, target)
+  if ((int)lane < kVisHints) shint[wid][lane] = -1;
+  if (lane == 0) shpos[wid] = 0;
+  __syncwarp();
   int qn = 0;  // warp-uniform queue length
   unsigned vis = 0;
   bool more = true;
+  int64_t unit = 0, g_tile0 = 0;
+  int tile_cur = kVisGroup, tile_end = kVisGroup, k_cur = 0;
   while (more || qn > 0) {
-    // ---- refill: side test on the next 32 pairs
+    // ---- refill: side test on the next tile of the claimed (group, target)
     if (more && qn < 32) {
-      unsigned long long base = 0;
-      if (lane == 0) base = atomicAdd(work, 32ULL);
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if ((int64_t)base >= total) {
-        more = false;
-      } else {
-        const int64_t pi = (int64_t)base + lane;
+      if (tile_cur >= tile_end) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(work, 1ULL);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if ((int64_t)base >= total) {
+          more = false;
+        } else {
+          unit = (int64_t)base;
+          const int64_t grp = unit / nt;
+          k_cur = (int)(unit % nt);
+          g_tile0 = grp * kVisGroup;
+          tile_cur = 0;
+          const int64_t left = ntiles - g_tile0;
+          tile_end = left < kVisGroup ? (int)left : kVisGroup;
+          if (kVisHints > 0) {  // hints of another target rarely help
+            if ((int)lane < kVisHints) shint[wid][lane] = -1;
+            __syncwarp();
+          }
+        }
+      }
+      if (more) {
+        const int64_t pos = (g_tile0 + tile_cur) * 32 + lane;
+        const int k = k_cur;
+        ++tile_cur;
         bool pass = false;
-        const int64_t tile = pi / (32 * nt), rem = pi % (32 * nt);
-        const int64_t pos = tile * 32 + (rem & 31);
-        const int k = (int)(rem >> 5);
-        if (pi < total && pos < nv) {
+        if (pos < nv) {
           const int64_t v = order ? order[v_begin + pos] : v_begin + pos;
           const double3 p = ld3(vb.point + 3 * v);
           const double3 n = ld3(vb.normal + 3 * v);
@@ -362,7 +399,29 @@ __global__ void __launch_bounds__(128) k_cir_visibility(DevScene S, SbrCirParams
       T.found = false;
       T.ok = true;
     }
-    while (!T.done()) T.round(S);
+    // occluders found by this warp for earlier tiles of the same target
+    for (int h = 0; h < kVisHints; ++h) {
+      const int j = shint[wid][h];
+      if (cast && !T.found && j >= 0) T.try_occluder(S, j);
+    }
+    while (!T.done()) {
+      const bool before = T.found;
+      T.round(S);
+      if (kVisHints > 0) {
+        const unsigned am = __activemask();
+        const unsigned fresh = __ballot_sync(am, T.found && !before);
+        if (fresh) {
+          const int src = __ffs(fresh) - 1;
+          const int j = __shfl_sync(am, T.hit_tri, src);
+          if (!T.done()) T.try_occluder(S, j);
+          if ((int)lane == src) {
+            shint[wid][shpos[wid] % kVisHints] = j;
+            shpos[wid] = shpos[wid] + 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
     if (active) {
       if (!T.ok) {
         flag_error(S, kErrStack);

@@ -683,6 +683,7 @@ struct AnyTrav {
   float bound;
   int stack_node[kStackSize];
   int sp, node, leaf;
+  int hit_tri;  // the occluding slot once found
   bool ok, found;
 
   __device__ __forceinline__ void start(const DevScene& S, double3 o, double3 d, double tmin,
@@ -695,8 +696,23 @@ struct AnyTrav {
     sp = 0;
     node = 0;
     leaf = 0;
+    hit_tri = -1;
     ok = true;
     found = false;
+  }
+  // Test one candidate occluder (e.g. found by a neighbouring ray): the same
+  // predicate the traversal applies, so the answer is unchanged -- any
+  // triangle with t_min < t < limit occludes.
+  __device__ __forceinline__ bool try_occluder(const DevScene& S, int j) {
+    double t, u, v;
+    if (tri_hit_idx<false>(r, S.tris + j, t_min, t, u, v) && t < limit) {
+      found = true;
+      hit_tri = j;
+      node = kDone;
+      leaf = 0;
+      return true;
+    }
+    return false;
   }
   __device__ __forceinline__ void idle() {
     node = kDone;
@@ -741,8 +757,9 @@ struct AnyTrav {
       const int s = leaf_start(leaf), n = leaf_count(leaf);
       for (int j = s; j < s + n; ++j) {
         double t, u, v;
-        if (tri_hit_idx(r, S.tris + j, t_min, t, u, v) && t < limit) {
+        if (tri_hit_idx<false>(r, S.tris + j, t_min, t, u, v) && t < limit) {
           found = true;
+          hit_tri = j;
           node = kDone;
           leaf = 0;
           return;

@@ -13,7 +13,8 @@ for r in csv.reader(io.StringIO(out)):
             s = int(r[4]); ie = int(r[7]); te = int(r[8])
         except ValueError:
             continue
-        agg[(cur, int(r[0]), r[1][:90])] = (s, ie, te); tot += s
+        k = (cur, int(r[0]), r[1][:90]); a = agg.get(k, (0, 0, 0))
+        agg[k] = (a[0] + s, a[1] + ie, a[2] + te); tot += s  # summed over launches
 print("total samples", tot)
 for (f, l, src), (s, ie, te) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:N]:
     print(f"{100*s/max(tot,1):5.1f}% {f}:{l} thr/warp={te/max(ie,1):.1f} | {src}")

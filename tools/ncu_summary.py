@@ -2,7 +2,7 @@
 
     python tools/ncu_summary.py launches gpurun_out/launches.csv > profiles/X_launches.txt
     python tools/ncu_summary.py full gpurun_out/radiomap.ncu-rep > profiles/X_full.txt
-    python tools/ncu_summary.py traffic gpurun_out/radiomap.ncu-rep > profiles/radiomap_traffic.json
+    python tools/ncu_summary.py traffic gpurun_out/k_map_trace.ncu-rep > profiles/traffic_k_map_trace.json
 """
 
 import collections
@@ -59,9 +59,20 @@ def _raw(rep):
     return [(dict(zip(hdr, r)), dict(zip(hdr, units))) for r in rows[2:]]
 
 
+def _dur(vals):
+    try:
+        return float(vals.get("gpu__time_duration.sum", "0").replace(",", ""))
+    except ValueError:
+        return 0.0
+
+
 def full(rep):
-    for vals, units in _raw(rep):
-        print(f"## {vals.get('Kernel Name', '?')[:120]}")
+    """Raw metrics of the longest launch in the report + its details sections."""
+    raw = _raw(rep)
+    best = max(range(len(raw)), key=lambda i: _dur(raw[i][0]))
+    for vals, units in raw[best:best + 1]:
+        print(f"## {vals.get('Kernel Name', '?')[:120]}  (longest of {len(raw)} captured launches,"
+              f" #{best})")
         for m in FULL_METRICS:
             if m in vals:
                 print(f"{m:70s} {vals[m]:>16s} {units.get(m, '')}")
@@ -71,7 +82,12 @@ def full(rep):
     rows = list(csv.reader(io.StringIO(out)))
     hdr = rows[0]
     ix = [hdr.index(c) for c in ("Section Name", "Metric Name", "Metric Unit", "Metric Value")]
+    idc = hdr.index("ID") if "ID" in hdr else None
+    ids = sorted({r[idc] for r in rows[1:] if idc is not None and len(r) > idc}, key=int)
+    want = ids[best] if ids and best < len(ids) else None
     for r in rows[1:]:
+        if want is not None and r[idc] != want:
+            continue
         if len(r) > ix[3] and r[ix[1]]:
             sec, name, unit, val = (r[i] for i in ix)
             if sec in ("Warp State Statistics", "Scheduler Statistics", "Occupancy",
@@ -81,13 +97,18 @@ def full(rep):
 
 
 def traffic(rep):
+    """Mean dram bytes (read + write) per launch over every launch in the report."""
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    vals, units = _raw(rep)[0]
-    b = 0.0
-    for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-        b += float(vals[m].replace(",", "")) * scale[units[m]]
-    print(json.dumps({"kernel": vals.get("Kernel Name", "")[:80],
-                      "dram_bytes_per_launch": b,
+    per, ms = [], []
+    name = ""
+    for vals, units in _raw(rep):
+        b = 0.0
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            b += float(vals[m].replace(",", "")) * scale[units[m]]
+        per.append(b)
+        name = vals.get("Kernel Name", "")[:80]
+    print(json.dumps({"kernel": name, "dram_bytes_per_launch": sum(per) / len(per),
+                      "launches": len(per), "min": min(per), "max": max(per),
                       "source": rep}))
 
 

@@ -519,15 +519,6 @@ __device__ __forceinline__ bool trace_closest(const DevScene& S, double3 o, doub
 // culling is conservative).  Lanes with active == false only vote.
 constexpr int kDone = (int)0x80000000;  // never a node index or a leaf code
 
-__device__ __forceinline__ int ww_pop(const int* stack_node, const float* stack_t, int& sp,
-                                      float bound) {
-  while (sp > 0) {
-    --sp;
-    if (stack_t[sp] <= bound) return stack_node[sp];
-  }
-  return kDone;
-}
-
 __device__ __forceinline__ int ww_pop_t(const int* stack_node, const float* stack_t, int& sp,
                                         float bound, float& t_out) {
   while (sp > 0) {

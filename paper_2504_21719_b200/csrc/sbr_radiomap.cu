@@ -88,7 +88,16 @@ __device__ __forceinline__ uint64_t comb_sample(uint64_t w, uint64_t comb_q) {
 // one atomic and traces them together in the while-while form.  (Refilling
 // lanes individually as their rays finish was measured slower on B200: it
 // breaks the warp-wide leaf batching of trace_closest_ww.)
-__global__ void __launch_bounds__(128) k_map_trace(DevScene S, SbrMapParams P, int seg,
+// occupancy: 8 blocks of 128 per SM (64 registers) measured best for both
+// (trace 9.08 -> 8.23 ms, shade 6.06 -> 5.21 ms per canyon map; the shade
+// spills ~0.3 KB to L1-resident local memory and still wins on latency hiding)
+#ifndef SBR_TRACE_MINB
+#define SBR_TRACE_MINB 8
+#endif
+#ifndef SBR_SHADE_MINB
+#define SBR_SHADE_MINB 8
+#endif
+__global__ void __launch_bounds__(128, SBR_TRACE_MINB) k_map_trace(DevScene S, SbrMapParams P, int seg,
                                                    MapQueue q, const unsigned long long* count_in,
                                                    uint64_t begin, uint64_t count0, uint64_t comb_q,
                                                    HitBuf hits, unsigned long long* work,
@@ -144,7 +153,7 @@ struct LaneCounters {
   unsigned rb, deposits, escaped, respawns, terminated, thr, rr;
 };
 
-__global__ void __launch_bounds__(128, 5) k_map_shade(DevScene S, SbrMapParams P, int seg,
+__global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, SbrMapParams P, int seg,
                                                    MapQueue qi, const unsigned long long* count_in,
                                                    uint64_t begin, uint64_t comb_q, HitBuf hits,
                                                    MapQueue qo, unsigned long long* count_out,

@@ -376,6 +376,9 @@ def run_ours(args, rank, world, local_rank):
     c4 = None
     if not args.no_config4:
         c4 = bench_config4(args, dev, rank, world)
+    c5 = None
+    if not args.no_config5:
+        c5 = bench_config5(args, dev, rank, world)
 
     if rank == 0:
         line = {
@@ -398,6 +401,7 @@ def run_ours(args, rank, world, local_rank):
                          "kernels": kernels, "peak_source": peak_kind},
             "cir": cir,
             "config4": c4,
+            "config5": c5,
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
@@ -529,6 +533,67 @@ def bench_cir(args, dev, rank=0, world=1):
             "unit": "ms per Tx-Rx set (1 Tx x 1024 Rx)", "higher_is_better": False}
 
 
+def bench_config5(args, dev, rank=0, world=1):
+    """Config 5: city, 8x8 TR 38.901 Tx panel (lambda/2), 4x4 Rx panel, depth 6, N_S = 1e6,
+    CIR + CFR over 1024 subcarriers (BASELINE configs[4]); synthetic arrays.
+
+    ms per solve = compute_paths (sharded over the ranks like config 3) +
+    frequency_response to a host (16, 64, 1024) complex128 array, CUDA events,
+    max over ranks; k_cfr_contract timed separately with its output-write
+    roofline (16 B per H entry).
+    """
+    import torch
+    import torch.distributed as dist
+    from paper_2504_21719_b200 import (PathConfig, RadioDevice, SceneModel, _native, make_pattern,
+                                       scenes)
+    from paper_2504_21719_b200.cir import compute_paths_sharded as compute_paths
+    from paper_2504_21719_b200.cir import frequency_response
+    from paper_2504_21719_b200.em import planar_array
+    from paper_2504_21719_b200.sampling import Interaction
+    meshes = scenes.city()
+    scene = SceneModel(meshes, scenes.uniform_materials(meshes, scenes.concrete()), device=dev)
+    lam = 299792458.0 / 3.5e9
+    tx = RadioDevice(position=np.array([0.0, 0.0, 30.0]), pattern=make_pattern("tr38901"),
+                     array=planar_array(8, 8, lam / 2, lam / 2))
+    rx = RadioDevice(position=np.array([2.0, 60.0, 1.5]),
+                     array=planar_array(4, 4, lam / 2, lam / 2))
+    cfg = PathConfig(num_samples=1_000_000, max_depth=6, q_diffraction=0.0,
+                     enabled=frozenset({Interaction.REFLECTION}))
+    freqs = 3.5e9 + (np.arange(1024) - 512) * 30e3
+
+    def solve():
+        ps = compute_paths(scene, [tx], [rx], cfg)
+        return ps, frequency_response(ps, freqs)
+
+    solve()  # warm-up
+    stream = torch.cuda.current_stream(dev)
+    _native.profile_enable(True)
+    times, ps, H = [], None, None
+    for _ in range(max(1, min(args.steps, 3))):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ps, H = solve()
+        b.record(stream)
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b))
+    n = len(times)
+    cfr_ms = _native.profile_kernel_ms("k_cfr_contract")[0] / n
+    _native.profile_enable(False)
+    ms = float(np.mean(times))
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    out_bytes = H.size * 16
+    return {"workload": "config5: procedural city CIR + CFR, 8x8 TR 38.901 Tx x 4x4 Rx "
+                        "(synthetic arrays), depth 6, N_S=1e6, 1024 subcarriers",
+            "ms_per_solve": ms, "solves": n, "paths": len(ps.tensors), "H_shape": list(H.shape),
+            "n_gpus": world, "scaling": "strong",
+            "k_cfr_contract_ms": cfr_ms,
+            "k_cfr_contract_write_gbs": out_bytes / (cfr_ms / 1e3) / 1e9 if cfr_ms > 0 else None,
+            "unit": "ms per Tx-Rx set", "higher_is_better": False}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -538,6 +603,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cir", action="store_true")
     ap.add_argument("--no-config4", action="store_true")
+    ap.add_argument("--no-config5", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -896,30 +896,54 @@ def _concat_sorted(parts, L):
 
 def frequency_response(path_set, frequencies, transmitter=0, receiver=0):
     """H[rx antenna, tx antenna, frequency] of one link (paths.py:1519-1547), on the GPU."""
-    torch = _torch()
-    L_ = _native.lib()
     freqs = np.atleast_1d(np.asarray(frequencies, dtype=np.float64))
     cfg = path_set.config
     tx = path_set.transmitters[transmitter]
     rx = path_set.receivers[receiver]
     T = path_set.tensors
     sel = np.nonzero((T.tx == transmitter) & (T.rx == receiver))[0]
-    n_tx, n_rx = len(tx.array.offsets), len(rx.array.offsets)
+    return channel_response(T.gain[sel], T.delay[sel], T.departure[sel], T.arrival[sel], freqs,
+                            tx.array.offsets, rx.array.offsets, cfg.wavelength,
+                            synthetic=cfg.synthetic_arrays, rx_el=T.rx_el[sel],
+                            tx_el=T.tx_el[sel])
+
+
+def channel_response(gain, delay, departure, arrival, freqs, tx_offsets, rx_offsets, wavelength,
+                     synthetic=True, rx_el=None, tx_el=None, return_tensor=False):
+    """`sbr_cfr` over one link's paths (host arrays in, complex128 (n_rx, n_tx, F) out).
+
+    The body of frequency_response (paths.py:1519-1547) without the PathSet;
+    ``return_tensor=True`` leaves H on the device as a float64 (.., 2) tensor.
+    """
+    torch = _torch()
+    L_ = _native.lib()
+    freqs = np.atleast_1d(np.asarray(freqs, dtype=np.float64))
+    gain = np.asarray(gain, dtype=np.complex128).reshape(-1)
+    n = len(gain)
+    tx_offsets = np.asarray(tx_offsets, dtype=np.float64).reshape(-1, 3)
+    rx_offsets = np.asarray(rx_offsets, dtype=np.float64).reshape(-1, 3)
+    n_tx, n_rx = len(tx_offsets), len(rx_offsets)
+    if rx_el is None:
+        rx_el = np.zeros(n, np.int32)
+    if tx_el is None:
+        tx_el = np.zeros(n, np.int32)
     dev = torch.device("cuda", torch.cuda.current_device())
     up = lambda a, dt=np.float64: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)  # noqa
-    g = np.stack([T.gain[sel].real, T.gain[sel].imag], axis=1) if len(sel) else np.zeros((0, 2))
-    tensors = [up(g.reshape(-1, 2)), up(T.delay[sel]), up(T.departure[sel].reshape(-1, 3)),
-               up(T.arrival[sel].reshape(-1, 3)), up(T.rx_el[sel], np.int32),
-               up(T.tx_el[sel], np.int32), up(freqs), up(tx.array.offsets.reshape(-1, 3)),
-               up(rx.array.offsets.reshape(-1, 3))]
+    g = np.stack([gain.real, gain.imag], axis=1) if n else np.zeros((0, 2))
+    tensors = [up(g.reshape(-1, 2)), up(np.asarray(delay).reshape(-1)),
+               up(np.asarray(departure).reshape(-1, 3)), up(np.asarray(arrival).reshape(-1, 3)),
+               up(rx_el, np.int32), up(tx_el, np.int32), up(freqs), up(tx_offsets),
+               up(rx_offsets)]
     H = torch.empty((n_rx, n_tx, len(freqs), 2), dtype=torch.float64, device=dev)
     with torch.cuda.device(dev):
         _native.check(L_.sbr_cfr(
             _native.ptr(tensors[0]), _native.ptr(tensors[1]), _native.ptr(tensors[2]),
             _native.ptr(tensors[3]), _native.ptr(tensors[4]), _native.ptr(tensors[5]),
-            len(sel), _native.ptr(tensors[6]), len(freqs), _native.ptr(tensors[7]), n_tx,
-            _native.ptr(tensors[8]), n_rx, float(cfg.wavelength),
-            1 if cfg.synthetic_arrays else 0, _native.ptr(H), _native.stream_ptr(dev)))
+            n, _native.ptr(tensors[6]), len(freqs), _native.ptr(tensors[7]), n_tx,
+            _native.ptr(tensors[8]), n_rx, float(wavelength), 1 if synthetic else 0,
+            _native.ptr(H), _native.stream_ptr(dev)))
+    if return_tensor:
+        return H
     h = H.cpu().numpy()
     return h[..., 0] + 1j * h[..., 1]
 
@@ -937,6 +961,6 @@ __all__ = [
     "DedupTable", "PathBuffer", "InteractionStep", "CandidateRecord", "Rejection",
     "PathGeometry", "ValidPath", "GenerationResult", "PathTensors", "PathSet",
     "generate_candidates", "refine_candidate", "compute_paths", "compute_paths_sharded",
-    "frequency_response",
+    "frequency_response", "channel_response",
     "baseband_gains",
 ]

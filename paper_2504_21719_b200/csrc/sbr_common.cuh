@@ -850,6 +850,8 @@ __device__ __forceinline__ bool occluded_segment(const DevScene& S, double3 a, d
 
 // kernel-launch evidence counter (host side, defined in sbr_scene.cu)
 void count_launch();
+// default-pool release threshold = keep (sbr_scene.cu)
+void keep_pool_mapped(int device);
 // optional CUDA-event timing of individual launches (sbr_profile_enable)
 void prof_begin(void* stream, const char* name);
 void prof_end(void* stream);

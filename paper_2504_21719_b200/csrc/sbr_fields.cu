@@ -302,43 +302,138 @@ __global__ void __launch_bounds__(128) k_cir_fields(DevScene S, SbrFieldParams P
 }
 
 // H[r, t, f] over the paths of one link, float64 accumulation in path order
-__global__ void k_cfr(const double* __restrict__ gain, const double* __restrict__ delay,
-                      const double* __restrict__ dep, const double* __restrict__ arr,
-                      const int32_t* __restrict__ prx, const int32_t* __restrict__ ptx,
-                      int64_t np, const double* __restrict__ freqs, int nf,
-                      const double* __restrict__ txo, int ntx, const double* __restrict__ rxo,
-                      int nrx, double wavelength, int synthetic, double* __restrict__ H) {
-  const int64_t total = (int64_t)nrx * ntx * nf;
-  const double kw = kTwoPi / wavelength;
+// ---------------------------------------------------------------------------
+// CFR (paths.py:1519-1547) as a factorised complex contraction
+// ---------------------------------------------------------------------------
+// The reference adds, path by path,
+//     ((g_p * u_rx[r,p]) * u_tx[t,p]) * spin[p,f]
+// so H = W . E with W[(r,t),p] = (g_p u_rx[r,p]) u_tx[t,p] and
+// E[p,f] = exp(-2j pi f tau_p).  The steering vectors and the spin matrix are
+// computed once (O((n_rx + n_tx + F) P) sincos instead of O(n_rx n_tx F P)),
+// then a shared-memory tiled float64 contraction accumulates every output
+// over p in path order with the same complex products (-fmad=false), so the
+// result is identical to the path-by-path sum.  At these shapes (K = paths
+// per link, a few to a few hundred) the contraction is tiny next to the
+// output write; tensor cores would change the rounding (fused products,
+// split K) for no measurable gain, so it stays on the FP64 pipe.
+
+// u[e, p] = exp(1j * kw * (offsets[e] @ (sign * k_p)))   (em.py:240-251)
+__global__ void k_cfr_steer(const double* __restrict__ dirs, int64_t np,
+                            const double* __restrict__ offs, int ne, double kw, int incoming,
+                            double* __restrict__ u) {
+  const int64_t total = (int64_t)ne * np;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
+    const int e = (int)(i / np);
+    const int64_t p = i % np;
+    const double3 k = ld3(dirs + 3 * p);
+    const double ph = kw * dot_gemv(ldg3(offs + 3 * e), incoming ? neg(k) : k);
+    double sn, cs;
+    sincos(ph, &sn, &cs);
+    u[2 * i] = cs;
+    u[2 * i + 1] = sn;
+  }
+}
+
+// E[p, f] = exp(-2j pi f tau_p)
+__global__ void k_cfr_spin(const double* __restrict__ delay, int64_t np,
+                           const double* __restrict__ freqs, int nf, double* __restrict__ E) {
+  const int64_t total = np * nf;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i / nf;
     const int f = (int)(i % nf);
-    const int t = (int)((i / nf) % ntx);
-    const int r = (int)(i / ((int64_t)nf * ntx));
-    const double fr = freqs[f];
-    double acc_re = 0.0, acc_im = 0.0;
-    for (int64_t p = 0; p < np; ++p) {
-      cplx a = C(gain[2 * p], gain[2 * p + 1]);
-      if (synthetic) {
-        const double3 kd = ld3(dep + 3 * p), ka = ld3(arr + 3 * p);
-        const double pr = kw * dot_gemv(ldg3(rxo + 3 * r), neg(ka));
-        const double pt = kw * dot_gemv(ldg3(txo + 3 * t), kd);
-        double sr, cr, st, ct;
-        sincos(pr, &sr, &cr);
-        sincos(pt, &st, &ct);
-        a = (a * C(cr, sr)) * C(ct, st);
-      } else if (prx[p] != r || ptx[p] != t) {
-        continue;
-      }
-      const double ang = -kTwoPi * fr * delay[p];
-      double s, c;
-      sincos(ang, &s, &c);
-      const cplx v = a * C(c, s);
-      acc_re += v.re;
-      acc_im += v.im;
+    const double ang = -kTwoPi * freqs[f] * delay[p];
+    double sn, cs;
+    sincos(ang, &sn, &cs);
+    E[2 * i] = cs;
+    E[2 * i + 1] = sn;
+  }
+}
+
+// W[(r, t), p]: synthetic arrays steer every path to every element pair;
+// element-indexed paths only touch their own (rx_el, tx_el) row (zero
+// elsewhere: a zero term leaves every partial sum unchanged)
+__global__ void k_cfr_weights(const double* __restrict__ gain, int64_t np,
+                              const double* __restrict__ u_rx, int nrx,
+                              const double* __restrict__ u_tx, int ntx,
+                              const int32_t* __restrict__ prx, const int32_t* __restrict__ ptx,
+                              int synthetic, double* __restrict__ W) {
+  const int64_t total = (int64_t)nrx * ntx * np;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i % np;
+    const int64_t row = i / np;
+    const int t = (int)(row % ntx), r = (int)(row / ntx);
+    cplx a = C(gain[2 * p], gain[2 * p + 1]);
+    if (synthetic) {
+      a = (a * C(u_rx[2 * (r * np + p)], u_rx[2 * (r * np + p) + 1])) *
+          C(u_tx[2 * (t * np + p)], u_tx[2 * (t * np + p) + 1]);
+    } else if (prx[p] != r || ptx[p] != t) {
+      a = C(0.0, 0.0);
     }
-    H[2 * i] = acc_re;
-    H[2 * i + 1] = acc_im;
+    W[2 * i] = a.re;
+    W[2 * i + 1] = a.im;
+  }
+}
+
+// H[row, f] = sum_p W[row, p] E[p, f], p in order.  Block: 32 rows x 64
+// frequencies, 256 threads x (2 rows x 4 frequencies), K staged 16 at a time.
+constexpr int kCfrRows = 32, kCfrCols = 64, kCfrK = 16;
+
+__global__ void __launch_bounds__(256) k_cfr_contract(const double2* __restrict__ W,
+                                                      const double2* __restrict__ E,
+                                                      int64_t rows, int64_t np, int nf,
+                                                      double2* __restrict__ H) {
+  __shared__ double2 ws[kCfrRows][kCfrK + 1];
+  __shared__ double2 es[kCfrK][kCfrCols];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t row0 = (int64_t)blockIdx.y * kCfrRows;
+  const int col0 = blockIdx.x * kCfrCols;
+  double ar[2][4], ai[2][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) ar[i][c] = ai[i][c] = 0.0;
+  for (int64_t k0 = 0; k0 < np; k0 += kCfrK) {
+    const int kn = (int)((np - k0) < kCfrK ? (np - k0) : kCfrK);
+    for (int e = threadIdx.x; e < kCfrRows * kCfrK; e += 256) {
+      const int rr = e / kCfrK, kk = e % kCfrK;
+      const int64_t row = row0 + rr;
+      ws[rr][kk] = (row < rows && kk < kn) ? W[row * np + k0 + kk] : make_double2(0.0, 0.0);
+    }
+    for (int e = threadIdx.x; e < kCfrK * kCfrCols; e += 256) {
+      const int kk = e / kCfrCols, cc = e % kCfrCols;
+      es[kk][cc] = (kk < kn && col0 + cc < nf) ? E[(k0 + kk) * nf + col0 + cc]
+                                                : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    for (int kk = 0; kk < kn; ++kk) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const double2 w = ws[ty * 2 + i][kk];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double2 e = es[kk][tx + 16 * c];
+          // v = a * spin (numpy complex multiply), then out += v
+          const double vr = w.x * e.x - w.y * e.y;
+          const double vi = w.x * e.y + w.y * e.x;
+          ar[i][c] += vr;
+          ai[i][c] += vi;
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int64_t row = row0 + ty * 2 + i;
+    if (row >= rows) continue;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int f = col0 + tx + 16 * c;
+      if (f < nf) H[row * nf + f] = make_double2(ar[i][c], ai[i][c]);
+    }
   }
 }
 
@@ -381,11 +476,60 @@ int sbr_cfr(const double* gain, const double* delay, const double* dep, const do
   if (nf < 1 || ntx < 1 || nrx < 1) return set_error(SBR_ERR_INVALID, "empty response shape");
   if (!(wavelength > 0.0)) return set_error(SBR_ERR_INVALID, "wavelength must be positive");
   if (!synthetic && (!prx || !ptx)) return set_error(SBR_ERR_INVALID, "element indices missing");
-  const int64_t total = (int64_t)nrx * ntx * nf;
-  k_cfr<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(gain, delay, dep, arr, prx, ptx,
-                                                                np, freqs, nf, txo, ntx, rxo, nrx,
-                                                                wavelength, synthetic, H);
-  return launch_status("k_cfr");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t rows = (int64_t)nrx * ntx;
+  if (np == 0) {
+    cudaMemsetAsync(H, 0, sizeof(double) * 2 * rows * nf, st);
+    return launch_status("sbr_cfr memset");
+  }
+  const double kw = kTwoPi / wavelength;
+  int device = 0;
+  if (cudaGetDevice(&device) == cudaSuccess) keep_pool_mapped(device);
+  double *u_rx = nullptr, *u_tx = nullptr, *E = nullptr, *W = nullptr;
+  const size_t c16 = 2 * sizeof(double);
+  cudaError_t e = cudaSuccess;
+  if (synthetic) {
+    e = cudaMallocAsync(&u_rx, c16 * nrx * np, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&u_tx, c16 * ntx * np, st);
+  }
+  if (e == cudaSuccess) e = cudaMallocAsync(&E, c16 * np * nf, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&W, c16 * rows * np, st);
+  int rc = SBR_OK;
+  if (e != cudaSuccess) {
+    rc = set_error(SBR_ERR_CUDA, std::string("sbr_cfr scratch: ") + cudaGetErrorString(e));
+  } else {
+    if (synthetic) {
+      k_cfr_steer<<<grid_for((int64_t)nrx * np, 256), 256, 0, st>>>(arr, np, rxo, nrx, kw, 1, u_rx);
+      rc = launch_status("k_cfr_steer");
+      if (!rc) {
+        k_cfr_steer<<<grid_for((int64_t)ntx * np, 256), 256, 0, st>>>(dep, np, txo, ntx, kw, 0,
+                                                                      u_tx);
+        rc = launch_status("k_cfr_steer");
+      }
+    }
+    if (!rc) {
+      k_cfr_spin<<<grid_for(np * nf, 256), 256, 0, st>>>(delay, np, freqs, nf, E);
+      rc = launch_status("k_cfr_spin");
+    }
+    if (!rc) {
+      k_cfr_weights<<<grid_for(rows * np, 256), 256, 0, st>>>(gain, np, u_rx, nrx, u_tx, ntx,
+                                                              prx, ptx, synthetic, W);
+      rc = launch_status("k_cfr_weights");
+    }
+    if (!rc) {
+      const dim3 grid((nf + kCfrCols - 1) / kCfrCols, (unsigned)((rows + kCfrRows - 1) / kCfrRows));
+      prof_begin(st, "k_cfr_contract");
+      k_cfr_contract<<<grid, 256, 0, st>>>((const double2*)W, (const double2*)E, rows, np, nf,
+                                           (double2*)H);
+      prof_end(st);
+      rc = launch_status("k_cfr_contract");
+    }
+  }
+  if (u_rx) cudaFreeAsync(u_rx, st);
+  if (u_tx) cudaFreeAsync(u_tx, st);
+  if (E) cudaFreeAsync(E, st);
+  if (W) cudaFreeAsync(W, st);
+  return rc;
 }
 
 }  // extern "C"

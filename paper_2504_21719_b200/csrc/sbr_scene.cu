@@ -28,6 +28,17 @@ namespace sbr {
 static thread_local std::string g_last_error;
 static std::atomic<uint64_t> g_launches{0};
 
+// The library's stream-ordered scratch (ray queues, sort buffers, CFR
+// factors) comes from the device's default pool: keep freed blocks mapped
+// between calls instead of unmapping them at every synchronisation.
+void keep_pool_mapped(int device) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = ~0ULL;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+}
+
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 // ---- optional per-kernel CUDA-event timing (bench.py roofline evidence) ----
@@ -582,15 +593,7 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
   if (ntri <= 0) return set_error(SBR_ERR_EMPTY_SCENE, "no triangles");
   if (ntri >= (1LL << 29)) return set_error(SBR_ERR_INVALID, "too many triangles");
   SBR_CUDA(cudaSetDevice(device));
-  {
-    // the library's stream-ordered scratch (ray queues, sort buffers) comes
-    // from the device's default pool: keep freed blocks mapped between calls
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      uint64_t keep = ~0ULL;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-  }
+  keep_pool_mapped(device);
   cudaStream_t st = (cudaStream_t)stream;
   const int n = (int)ntri;
   SbrScene* S = new SbrScene();

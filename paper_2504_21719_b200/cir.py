@@ -944,8 +944,11 @@ def channel_response(gain, delay, departure, arrival, freqs, tx_offsets, rx_offs
             _native.ptr(H), _native.stream_ptr(dev)))
     if return_tensor:
         return H
-    h = H.cpu().numpy()
-    return h[..., 0] + 1j * h[..., 1]
+    # (.., 2) float64 is complex128 in memory: one pinned D2H copy, no host arithmetic
+    hc = H.view(torch.complex128)[..., 0]
+    host = torch.empty(hc.shape, dtype=torch.complex128, pin_memory=True)
+    host.copy_(hc)
+    return host.numpy()
 
 
 def baseband_gains(path_set, transmitter=0, receiver=0):

@@ -86,25 +86,46 @@ def _lex_less(a, b):
     return diff.any(axis=1) & (a[rows, first] < b[rows, first])
 
 
+def _group_rows(key):
+    """(inverse, counts, order) of the distinct rows of an int64 matrix.
+
+    Same grouping as np.unique(key, axis=0, return_inverse=True,
+    return_counts=True) (group ids in a different but fixed order, which no
+    caller depends on) via one lexsort instead of a sort of void-viewed rows.
+    `order` lists the rows group by group (ids ascending), each group in row
+    order (lexsort is stable).
+    """
+    n = len(key)
+    if n == 0:
+        return np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0, np.int64)
+    order = np.lexsort(key.T[::-1])
+    ks = key[order]
+    new_grp = np.empty(n, bool)
+    new_grp[0] = True
+    new_grp[1:] = np.any(ks[1:] != ks[:-1], axis=1)
+    gid_sorted = np.cumsum(new_grp) - 1
+    inv = np.empty(n, np.int64)
+    inv[order] = gid_sorted
+    counts = np.bincount(gid_sorted)
+    return inv, counts, order
+
+
 def _edge_table(meshes):
     """All triangle edges in the reference's insertion order (mesh, prim, local)."""
-    cols = {k: [] for k in ("obj", "prim", "local", "pa", "pb", "n", "far")}
-    for mesh in meshes:
-        v, t = mesh.vertices, mesh.triangles
-        nrm = mesh.triangle_normals()
-        m = len(t)
-        for local in range(3):
-            cols["obj"].append(np.full(m, mesh.object_id, np.int64))
-            cols["prim"].append(np.arange(m, dtype=np.int64))
-            cols["local"].append(np.full(m, local, np.int64))
-            cols["pa"].append(v[t[:, local]])
-            cols["pb"].append(v[t[:, (local + 1) % 3]])
-            cols["n"].append(nrm)
-            cols["far"].append(v[t[:, (local + 2) % 3]])
-    mesh_of = np.concatenate([np.full(3 * len(m.triangles), i) for i, m in enumerate(meshes)])
-    out = {k: np.concatenate(vs) for k, vs in cols.items()}
-    order = np.lexsort((out["local"], out["prim"], mesh_of))   # prim-major, then local
-    return {k: v[order] for k, v in out.items()}
+    sizes = np.array([len(m.triangles) for m in meshes], np.int64)
+    voff = np.concatenate([[0], np.cumsum([len(m.vertices) for m in meshes])[:-1]])
+    V = np.concatenate([np.asarray(m.vertices, np.float64) for m in meshes])
+    T = np.concatenate([np.asarray(m.triangles, np.int64) + o for m, o in zip(meshes, voff)])
+    a, b, c = V[T[:, 0]], V[T[:, 1]], V[T[:, 2]]
+    n = np.cross(b - a, c - a)
+    nrm = n / np.linalg.norm(n, axis=1, keepdims=True)   # Mesh.triangle_normals, row-wise
+    obj = np.repeat(np.array([m.object_id for m in meshes], np.int64), sizes)
+    prim = np.arange(len(T), dtype=np.int64) - np.repeat(np.cumsum(sizes) - sizes, sizes)
+    local = np.tile(np.arange(3, dtype=np.int64), len(T))
+    tri = np.repeat(np.arange(len(T)), 3)                # edge 3*t + local
+    return {"obj": obj[tri], "prim": prim[tri], "local": local,
+            "pa": V[T[tri, local]], "pb": V[T[tri, (local + 1) % 3]],
+            "n": nrm[tri], "far": V[T[tri, (local + 2) % 3]]}
 
 
 def extract_wedges(meshes, dihedral_threshold_deg=1.0):
@@ -118,9 +139,7 @@ def extract_wedges(meshes, dihedral_threshold_deg=1.0):
     ka, kb = ka[live], kb[live]
     a_first = _lex_less(ka, kb)
     key = np.where(a_first[:, None], np.concatenate([ka, kb], 1), np.concatenate([kb, ka], 1))
-    _, inv, counts = np.unique(key, axis=0, return_inverse=True, return_counts=True)
-    inv = inv.reshape(-1)
-    order = np.argsort(inv, kind="stable")       # owners of a key in insertion order
+    inv, counts, order = _group_rows(key)        # owners of a key in insertion order
     starts = np.concatenate([[0], np.cumsum(counts)[:-1]])
     first = order[starts]
     thresh = np.deg2rad(dihedral_threshold_deg)
@@ -184,41 +203,62 @@ def extract_wedges(meshes, dihedral_threshold_deg=1.0):
 
 
 def _merge(S):
-    """_merge_segments (geometry.py:458-494): collinear segments with equal planes."""
+    """_merge_segments (geometry.py:458-494): collinear segments with equal planes.
+
+    Vectorised over segments: per group the first segment (by owner) is the
+    reference; a segment whose plane pair is the reference's reversed swaps
+    its owner sides; the extent is the min / max of the endpoint projections
+    (`(p - p_ref) @ e`, evaluated with the same per-row dot as the reference).
+    """
     p0, pn = S["p0"], S["pn"]
     lo_first = ~_lex_less(pn, p0)           # sorted(planes): smaller key first
     ps_a = np.where(lo_first[:, None], p0, pn)
     ps_b = np.where(lo_first[:, None], pn, p0)
     gkey = np.concatenate([S["line"], ps_a, ps_b], axis=1)
-    _, ginv = np.unique(gkey, axis=0, return_inverse=True)
-    ginv = ginv.reshape(-1)
+    ginv, _, _ = _group_rows(gkey)
     own0, ownn = S["own0"], S["ownn"]
     # group order key: first owner (o, m) of own0 + ownn (own0 always present)
     order = np.lexsort((np.arange(len(ginv)), own0[:, 1], own0[:, 0], ginv))
+    g_sorted = ginv[order]
+    new_grp = np.ones(len(order), bool)
+    new_grp[1:] = g_sorted[1:] != g_sorted[:-1]
+    starts = np.flatnonzero(new_grp)
+    gid = np.cumsum(new_grp) - 1                      # group of each sorted segment
+    ref = order[starts][gid]                          # its reference segment
+    i = order
+    same = np.all(p0[i] == p0[ref], axis=1) & np.all(pn[i] == pn[ref], axis=1)
+    rev = np.all(pn[i] == p0[ref], axis=1) & np.all(p0[i] == pn[ref], axis=1)
+    flip = ~same & rev & ~np.all(p0[i] == pn[i], axis=1)
+    # owner sets: face0 gets own0 (ownn when flipped), facen the other side
+    side0 = np.where(flip[:, None], ownn[i], own0[i])
+    siden = np.where(flip[:, None], own0[i], ownn[i])
+    contrib = np.concatenate([np.column_stack([gid, np.zeros_like(gid), side0]),
+                              np.column_stack([gid, np.ones_like(gid), siden])])
+    contrib = contrib[contrib[:, 2] >= 0]
+    contrib = contrib[np.lexsort(contrib.T[::-1])]   # sorted (group, side, o, m, l)
+    if len(contrib):
+        contrib = contrib[np.concatenate([[True], np.any(contrib[1:] != contrib[:-1], axis=1)])]
+    c_start = np.searchsorted(contrib[:, 0], np.arange(len(starts)), side="left")
+    c_end = np.searchsorted(contrib[:, 0], np.arange(len(starts)), side="right")
+    # extent along the reference direction
+    e_ref = S["e"][ref]
+    p_ref = S["pa"][ref]
+    dot = lambda v: np.matmul(v[:, None, :], e_ref[:, :, None])[:, 0, 0]  # noqa: E731
+    xa = dot(S["pa"][i] - p_ref)
+    xb = dot(S["pb"][i] - p_ref)
+    lo_x = np.minimum.reduceat(np.minimum(xa, xb), starts)
+    hi_x = np.maximum.reduceat(np.maximum(xa, xb), starts)
+    rows = [tuple(x) for x in contrib[:, 1:].tolist()]   # (side, o, m, l) as Python ints
     wedges = []
-    bounds = np.flatnonzero(np.diff(ginv[order])) + 1
-    for grp in np.split(order, bounds):
-        r = grp[0]
+    for g, r in enumerate(order[starts].tolist()):
         e = S["e"][r]
-        p_ref = S["pa"][r]
-        planes_ref = (tuple(p0[r]), tuple(pn[r]))
-        face0, facen = set(), set()
-        xs = []
-        for i in grp:
-            planes = (tuple(p0[i]), tuple(pn[i]))
-            flip = (planes != planes_ref and planes[::-1] == planes_ref
-                    and planes[0] != planes[1])
-            o0 = [tuple(int(x) for x in own0[i])]
-            on = [tuple(int(x) for x in ownn[i])] if ownn[i, 0] >= 0 else []
-            (face0 if not flip else facen).update(o0)
-            (facen if not flip else face0).update(on)
-            xs.append(float((S["pa"][i] - p_ref) @ e))
-            xs.append(float((S["pb"][i] - p_ref) @ e))
-        lo_x, hi_x = min(xs), max(xs)
-        wedges.append(Wedge(origin=p_ref + lo_x * e, e_hat=e.copy(), length=hi_x - lo_x,
-                            n0_hat=S["n0"][r].copy(), nn_hat=S["nn"][r].copy(),
-                            t0_hat=S["t0"][r].copy(), n=float(S["nopen"][r]),
-                            face0=sorted(face0), facen=sorted(facen)))
+        c = rows[c_start[g]:c_end[g]]
+        face0 = [x[1:] for x in c if x[0] == 0]
+        facen = [x[1:] for x in c if x[0] == 1]
+        wedges.append(Wedge(origin=S["pa"][r] + lo_x[g] * e, e_hat=e.copy(),
+                            length=hi_x[g] - lo_x[g], n0_hat=S["n0"][r].copy(),
+                            nn_hat=S["nn"][r].copy(), t0_hat=S["t0"][r].copy(),
+                            n=float(S["nopen"][r]), face0=face0, facen=facen))
     wedges.sort(key=lambda w: (w.face0 + w.facen)[0])
     return wedges
 

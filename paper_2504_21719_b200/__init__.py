@@ -30,9 +30,22 @@ from .radiomap import (  # noqa: E402
     RadioMapConfig,
     RadioMapResult,
     compute_radio_map,
+    compute_radio_map_diffraction,
     compute_radio_map_sbr,
 )
 from .sampling import Interaction  # noqa: E402
+from .sceneio import (  # noqa: E402
+    LoadedScene,
+    SceneDescription,
+    load_mesh_obj,
+    load_scene,
+    read_paths_csv,
+    read_radio_map_csv,
+    write_mesh_obj,
+    write_paths,
+    write_radio_map,
+    write_scene,
+)
 
 __all__ = [
     "ArrayGeometry", "AntennaPattern", "make_pattern", "planar_array",
@@ -42,6 +55,8 @@ __all__ = [
     "PathSet", "PathTensors", "ValidPath", "baseband_gains", "compute_paths",
     "frequency_response", "generate_candidates", "refine_candidate",
     "MeasurementGrid", "RadioMapConfig", "RadioMapResult",
-    "compute_radio_map", "compute_radio_map_sbr",
-    "Interaction", "__version__",
+    "compute_radio_map", "compute_radio_map_diffraction", "compute_radio_map_sbr",
+    "Interaction", "LoadedScene", "SceneDescription", "load_mesh_obj", "load_scene",
+    "read_paths_csv", "read_radio_map_csv", "write_mesh_obj", "write_paths",
+    "write_radio_map", "write_scene", "__version__",
 ]

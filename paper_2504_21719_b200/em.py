@@ -36,6 +36,12 @@ def rotation_ypr(alpha, beta, gamma):
     return rz @ ry @ rx
 
 
+def angles_of(direction):
+    """Zenith and azimuth of unit vectors, last axis xyz (em.py:37-42)."""
+    d = np.asarray(direction, dtype=np.float64)
+    return np.arccos(np.clip(d[..., 2], -1.0, 1.0)), np.arctan2(d[..., 1], d[..., 0])
+
+
 def spherical_basis(theta, phi):
     """(r_hat, theta_hat, phi_hat) stacked on the last axis (em.py:22-36)."""
     theta = np.asarray(theta, dtype=np.float64)

@@ -1,0 +1,84 @@
+"""Empty, ragged and boundary inputs through the public API (GPU path).
+
+The reference handles these without special cases (empty batches return
+empty arrays, sample ranges need not align to chunks, a receiver with no
+path yields an all-zero response); the drop-in must do the same.
+"""
+
+import numpy as np
+import pytest
+
+from paper_2504_21719_b200 import (MeasurementGrid, PathConfig, RadioDevice, RadioMapConfig,
+                                   SceneModel, build_scene_accel, compute_paths,
+                                   compute_radio_map_sbr, frequency_response, scenes)
+from paper_2504_21719_b200.errors import EmptyScene
+from paper_2504_21719_b200.materials import RadioMaterial
+from paper_2504_21719_b200.sampling import Interaction
+
+pytestmark = pytest.mark.gpu
+CONC = RadioMaterial("concrete", eps_r=5.24, sigma=0.1, thickness=0.3)
+R = frozenset({Interaction.REFLECTION})
+
+
+def _room():
+    return SceneModel([scenes.box_mesh((-3, -4, 0), (3, 4, 3), object_id=0, inward=True)],
+                      {0: CONC})
+
+
+def test_empty_scene_and_empty_batches(cuda):
+    with pytest.raises(EmptyScene):
+        build_scene_accel([])
+    acc = _room().accel
+    t, tri, u, v = acc.trace_batch(np.zeros((0, 3)), np.zeros((0, 3)))
+    assert t.shape == (0,) and tri.shape == (0,) and u.shape == (0,) and v.shape == (0,)
+    assert acc.occluded_batch(np.zeros((0, 3)), np.zeros((0, 3))).shape == (0,)
+
+
+def test_single_ray_batch_and_t_max_cap(cuda):
+    acc = _room().accel
+    o, d = np.array([[0.0, 0.0, 1.0]]), np.array([[0.0, 0.0, -1.0]])
+    t, tri, _, _ = acc.trace_batch(o, d)
+    assert tri[0] >= 0 and t[0] == pytest.approx(1.0, abs=1e-12)
+    t, tri, _, _ = acc.trace_batch(o, d, t_max=0.5)      # hit beyond t_max: a miss
+    assert tri[0] == -1 and np.isinf(t[0])
+    # zero-length segment (len <= 2 eps) is never occluded
+    assert not acc.occluded_batch(np.array([[0.0, 0.0, 1.0]]), np.array([[0.0, 0.0, 1.0]]))[0]
+
+
+@pytest.mark.parametrize("rng_", [(0, 1), (0, 7), (3, 2 ** 19 + 5), (2 ** 19 - 1, 2 ** 19 + 1)])
+def test_ragged_sample_ranges_add_up(cuda, rng_):
+    """Any split of [0, N) into ranges (chunk-straddling, single samples)
+    reproduces the full map: the RNG is keyed by global sample id."""
+    scene = _room()
+    grid = MeasurementGrid((0.0, 0.0, 1.0), (1, 0, 0), (0, 1, 0), (1.0, 1.0), (6, 8))
+    n = 2 ** 19 + 9
+    cfg = RadioMapConfig(num_samples=n, max_depth=3, enabled=R, seed=1)
+    lo, hi = rng_
+    parts = [(0, lo), (lo, hi), (hi, n)]
+    total, _ = compute_radio_map_sbr(scene, (0.5, -1.0, 2.0), grid, cfg, include_direct=False)
+    acc = np.zeros_like(total)
+    for a, b in parts:
+        if b > a:
+            v, _ = compute_radio_map_sbr(scene, (0.5, -1.0, 2.0), grid, cfg,
+                                         sample_range=(a, b), include_direct=False)
+            acc += v
+    np.testing.assert_allclose(acc, total, rtol=1e-12, atol=0)
+
+
+def test_one_sample_map_and_one_cell_grid(cuda):
+    scene = _room()
+    grid = MeasurementGrid((0.0, 0.0, 1.0), (1, 0, 0), (0, 1, 0), (0.25, 0.25), (1, 1))
+    vals, diag = compute_radio_map_sbr(scene, (0.0, 0.0, 2.0), grid,
+                                       RadioMapConfig(num_samples=1, max_depth=2, enabled=R))
+    assert vals.shape == (1, 1) and vals[0, 0] > 0.0     # direct term of the one cell
+    assert diag["ray_bounces"] >= 1
+
+
+def test_receiver_without_paths_gives_zero_response(cuda):
+    """A receiver outside the closed room: no path reaches it, H is all zero."""
+    cfg = PathConfig(num_samples=2000, max_depth=2, enabled=R, q_diffraction=0.0)
+    ps = compute_paths(_room(), [RadioDevice(position=[0.0, 0.0, 1.5])],
+                       [RadioDevice(position=[50.0, 0.0, 1.5])], cfg)
+    assert len(ps.paths) == 0
+    H = frequency_response(ps, [3.5e9, 3.6e9])
+    assert H.shape == (1, 1, 2) and not H.any()

@@ -377,7 +377,8 @@ __global__ void __launch_bounds__(128) k_cir_visibility(DevScene S, SbrCirParams
     int k = 0;
     double3 a = make_double3(0.0, 0.0, 0.0), b = a;
     bool cast = false;
-    AnyTrav T;
+    int sn[kStackSize];
+    AnyTrav T(sn);
     if (active) {
       v = pi / nt;
       k = (int)(pi % nt);

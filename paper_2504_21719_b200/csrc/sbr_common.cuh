@@ -541,11 +541,17 @@ struct ClosestTravT {
   double t_min, best_t, bu, bv;
   int best, best_rank;
   float bound;
-  int stack_node[kStackSize];
-  float stack_t[kStackSize];
+  // The stack lives in the caller's local arrays: a struct holding both the
+  // arrays and the scalars stays in local memory as a whole (every sp / node /
+  // ray-box access became an LDL/STL); with the arrays outside, the scalars
+  // are promoted to registers.
+  int* stack_node;
+  float* stack_t;
   int sp, node, leaf;
   float node_t, leaf_t;  // entry distances of the current node / parked leaf
   bool ok;
+
+  __device__ __forceinline__ ClosestTravT(int* sn, float* st) : stack_node(sn), stack_t(st) {}
 #ifdef SBR_COUNT_VISITS
   unsigned visits, tests;
 #endif
@@ -672,10 +678,12 @@ struct AnyTrav {
   RayBox rb;
   double t_min, limit;
   float bound;
-  int stack_node[kStackSize];
+  int* stack_node;  // caller's local array (see ClosestTravT)
   int sp, node, leaf;
   int hit_tri;  // the occluding slot once found
   bool ok, found;
+
+  __device__ __forceinline__ explicit AnyTrav(int* sn) : stack_node(sn) {}
 
   __device__ __forceinline__ void start(const DevScene& S, double3 o, double3 d, double tmin,
                                         double lim) {
@@ -772,7 +780,9 @@ using ClosestTrav = ClosestTravT<true>;
 __device__ __forceinline__ bool trace_closest_ww(const DevScene& S, bool active, double3 o,
                                                  double3 d, double t_min, double t_max,
                                                  HitRecord& h) {
-  ClosestTrav T;
+  int sn[kStackSize];
+  float st[kStackSize];
+  ClosestTrav T(sn, st);
   T.start(S, o, d, t_min, t_max);
   if (!active) T.idle();
   while (!T.done()) T.round(S);

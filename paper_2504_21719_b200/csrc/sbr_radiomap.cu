@@ -124,7 +124,9 @@ __global__ void __launch_bounds__(128, SBR_TRACE_MINB) k_map_trace(DevScene S, S
         d = make_double3(q.dx[i], q.dy[i], q.dz[i]);
       }
     }
-    ClosestTravT<false> T;  // the map needs t and the slot only
+    int sn[kStackSize];
+    float st[kStackSize];
+    ClosestTravT<false> T(sn, st);  // the map needs t and the slot only
     T.start(S, o, d, 1e-4, __longlong_as_double(0x7ff0000000000000LL));
     if (!active) T.idle();
     while (!T.done()) T.round(S);

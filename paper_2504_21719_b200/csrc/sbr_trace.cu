@@ -33,7 +33,9 @@ __global__ void __launch_bounds__(128) k_trace_closest(DevScene S, const double*
   for (int64_t base = wid * 32; base < n; base += warps * 32) {
     const int64_t i = base + (threadIdx.x & 31);
     const bool active = i < n;
-    ClosestTrav T;
+    int sn[kStackSize];
+    float st[kStackSize];
+    ClosestTrav T(sn, st);
     if (active) T.start(S, ldg3(o + 3 * i), ldg3(d + 3 * i), t_min, __ldg(t_max + i));
     else T.idle();
     while (!T.done()) T.round(S);
@@ -58,7 +60,8 @@ __global__ void __launch_bounds__(128) k_trace_any(DevScene S, const double* __r
   for (int64_t base = wid * 32; base < n; base += warps * 32) {
     const int64_t i = base + (threadIdx.x & 31);
     const bool active = i < n;
-    AnyTrav T;
+    int sn[kStackSize];
+    AnyTrav T(sn);
     if (active) T.start(S, ldg3(o + 3 * i), ldg3(d + 3 * i), t_min, __ldg(t_max + i));
     else {
       T.idle();
@@ -82,7 +85,8 @@ __global__ void __launch_bounds__(128) k_occluded(DevScene S, const double* __re
   for (int64_t base = wid * 32; base < n; base += warps * 32) {
     const int64_t i = base + (threadIdx.x & 31);
     bool cast = false;
-    AnyTrav T;
+    int sn[kStackSize];
+    AnyTrav T(sn);
     if (i < n) {
       const double3 pa = ldg3(a + 3 * i), pb = ldg3(b + 3 * i);
       const double3 dd = pb - pa;

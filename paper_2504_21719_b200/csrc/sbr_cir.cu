@@ -293,7 +293,10 @@ constexpr int kVisWarps = 4;
 constexpr int kVisHints = SBR_VIS_HINTS;
 constexpr int kVisGroup = SBR_VIS_GROUP;
 
-__global__ void __launch_bounds__(128) k_cir_visibility(DevScene S, SbrCirParams P,
+#ifndef SBR_VIS_MINB
+#define SBR_VIS_MINB 8  // 64 registers: 220 -> 180 ms at config 3
+#endif
+__global__ void __launch_bounds__(128, SBR_VIS_MINB) k_cir_visibility(DevScene S, SbrCirParams P,
                                                         SbrVertexBuf vb, int64_t v_begin,
                                                         int64_t v_end, uint64_t* row_key,
                                                         int32_t* row_vtx, int64_t row_cap,

@@ -628,11 +628,16 @@ def refine_candidate(record, scene):
 
 
 def _antenna_table(patterns, dev):
+    """Device array of SbrAntenna descriptors, one per target; patterns are packed
+    once per distinct (name, orientation) -- 1024 receivers usually share one."""
     torch = _torch()
-    arr = (_abi.SbrAntenna * len(patterns))()
-    for i, p in enumerate(patterns):
-        arr[i] = p.to_abi()
-    raw = np.frombuffer(bytes(arr), dtype=np.uint8).copy()
+    packed, rows = {}, []
+    for p in patterns:
+        key = (p.name, tuple(float(x) for x in p.orientation))
+        if key not in packed:
+            packed[key] = bytes(p.to_abi())
+        rows.append(packed[key])
+    raw = np.frombuffer(b"".join(rows), dtype=np.uint8).copy()
     return torch.from_numpy(raw).to(dev)
 
 
@@ -654,7 +659,10 @@ def _fields_device(scene, cand, pv, status, tx_dev, target_devices, cfg):
     rx_vel = torch.from_numpy(np.array([d.velocity for d in target_devices],
                                        dtype=np.float64).reshape(-1, 3)).to(dev)
     obj_ids = scene._object_ids
-    vel = np.array([scene.velocity_of(int(o)) for o in obj_ids], dtype=np.float64).reshape(-1, 3)
+    vel = np.zeros((len(obj_ids), 3))
+    if scene.velocities:
+        vel = np.array([scene.velocity_of(int(o)) for o in obj_ids],
+                       dtype=np.float64).reshape(-1, 3)
     obj_vel = torch.from_numpy(vel).to(dev)
     fp.rx_pattern_dev = rx_pat.data_ptr()
     fp.rx_velocity_dev = rx_vel.data_ptr()

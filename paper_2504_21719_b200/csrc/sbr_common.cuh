@@ -511,8 +511,9 @@ __device__ __forceinline__ bool trace_closest(const DevScene& S, double3 o, doub
 }
 
 // Closest hit, "while-while" form with postponed leaves (Aila & Laine 2009):
-// a lane that reaches a leaf parks it (and, only with -DSBR_SPECULATE, keeps
-// descending inner nodes) until every lane of the warp holds a leaf, then the warp tests its leaves
+// a lane that reaches a leaf parks it and keeps descending inner nodes
+// (speculatively, with the bound of before the parked leaf) until every lane
+// of the warp holds a leaf, then the warp tests its leaves
 // together, so the expensive float64 triangle tests run with most lanes
 // active instead of one or two.  Same result as trace_closest (the minimum of
 // (t, tie_rank) over all triangles is independent of visiting order; box
@@ -582,7 +583,7 @@ struct ClosestTravT {
   __device__ __forceinline__ bool done() const { return node == kDone && leaf == 0; }
 
   __device__ __forceinline__ void round(const DevScene& S) {
-    // ---- inner nodes (a lane leaves the loop once it has parked a leaf)
+    // ---- inner nodes (speculative: continue past a parked leaf)
     while (node >= 0) {
 #ifdef SBR_COUNT_VISITS
       ++visits;
@@ -620,8 +621,8 @@ struct ClosestTravT {
         leaf = node;
         leaf_t = node_t;
         node = ww_pop_t(stack_node, stack_t, sp, bound, node_t);
-#ifndef SBR_SPECULATE
-        break;  // measured: speculating past a parked leaf costs ~2% (stale bound)
+#ifdef SBR_NO_SPECULATE
+        break;  // A/B switch: with register-resident state speculation wins ~2 %
 #endif
       }
       if (!__any_sync(__activemask(), leaf == 0)) break;

@@ -494,17 +494,27 @@ __global__ void k_gather_u64(const uint64_t* __restrict__ src, const int32_t* __
 }
 
 // first occurrence of each (pr, pf) among chain rows sorted by (pr, pf, ordinal)
-__global__ void k_first_flags(const uint64_t* __restrict__ pr, const uint64_t* __restrict__ pf,
-                              const int32_t* __restrict__ order, int64_t n, uint8_t* keep_chain,
-                              unsigned long long* counters) {
+// First occurrence of each (pr, pf) among chain rows sorted stably by pr only
+// (ordinal order inside a pr run): a row is first unless an earlier row of its
+// run has the same pf.  pr and pf are two hashes of one (chain, target) key,
+// so a run almost always has one pf and the scan stops at the neighbour; a
+// 64-bit pr collision between different keys is still handled exactly.
+__global__ void k_first_flags_pr(const uint64_t* __restrict__ pr, const uint64_t* __restrict__ pf,
+                                 const int32_t* __restrict__ order, int64_t n,
+                                 uint8_t* keep_chain, unsigned long long* counters) {
   unsigned dup = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t a = order[i];
+    const uint64_t ka = pr[a], fa = pf[a];
     bool first = true;
-    if (i > 0) {
-      const int32_t b = order[i - 1];
-      first = pr[a] != pr[b] || pf[a] != pf[b];
+    for (int64_t j = i - 1; j >= 0; --j) {
+      const int32_t b = order[j];
+      if (pr[b] != ka) break;
+      if (pf[b] == fa) {
+        first = false;
+        break;
+      }
     }
     keep_chain[a] = first ? 1 : 0;
     dup += first ? 0u : 1u;
@@ -513,12 +523,25 @@ __global__ void k_first_flags(const uint64_t* __restrict__ pr, const uint64_t* _
   if ((threadIdx.x & 31) == 0 && s) atomicAdd(counters + SBR_CC_DUPLICATES, (unsigned long long)s);
 }
 
+// Ordinal keys depth<<60 | sample<<20 | target re-packed densely (depth,
+// sample and target fields only as wide as this call needs) so the radix sort
+// runs over ~33 instead of 64 bits; the order is unchanged.
+__global__ void k_dense_keys(const uint64_t* __restrict__ key, int64_t n, int tb, int sb,
+                             uint64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = key[i];
+    out[i] = ((k >> 60) << (sb + tb)) | (((k >> kTargetBits) & kSampleMask) << tb) |
+             (k & kTargetMask);
+  }
+}
+
 // kept rows per depth (the reference truncates depth by depth, _emit_records 954-960)
 __global__ void k_kept_per_depth(const uint64_t* __restrict__ skey, const int32_t* __restrict__ kept,
-                                 int64_t n, unsigned long long* per_depth) {
+                                 int64_t n, int depth_shift, unsigned long long* per_depth) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    if (kept[i]) atomicAdd(per_depth + (skey[i] >> 60), 1ULL);
+    if (kept[i]) atomicAdd(per_depth + (skey[i] >> depth_shift), 1ULL);
 }
 
 // kept = non-chain or first occurrence (ordinal order)
@@ -1070,6 +1093,13 @@ int sbr_cir_select(const SbrCirParams* P, const uint64_t* row_key, const uint64_
   unsigned long long* counters = (unsigned long long*)counters_u64;
   const int nt = P->n_targets;
   Arena A(st);
+  // dense ordinal key widths (k_dense_keys): target, sample, 4 depth bits
+  int tbits = 1, sbits = 1;
+  while (tbits < kTargetBits && (1LL << tbits) < (int64_t)nt) ++tbits;
+  while (sbits < kSampleBits && (1ULL << sbits) < P->num_samples) ++sbits;
+  const bool dense = tbits + sbits + 4 <= 64;
+  const int depth_shift = dense ? tbits + sbits : 60;
+  const int key_bits = dense ? tbits + sbits + 4 : 64;
   int64_t nreg = 0, n_los_keys = 0, n_chain = 0;
   int hflag[2];
   int64_t n_los_acc = 0, n_rows_buf = 0;
@@ -1118,7 +1148,14 @@ int sbr_cir_select(const SbrCirParams* P, const uint64_t* row_key, const uint64_
     if (n > 0) {
       k_iota<<<grid_for(n, 256), 256, 0, st>>>(idx0, n);
       LK("k_iota");
-      CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, row_key, skey, idx0, sidx, (int)n, 0, 64, st));
+      const uint64_t* sort_in = row_key;
+      if (depth_shift < 60) {
+        k_dense_keys<<<grid_for(n, 256), 256, 0, st>>>(row_key, n, tbits, sbits, pr);
+        LK("k_dense_keys");
+        sort_in = pr;  // pr is free until the gathers below
+      }
+      CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, sort_in, skey, idx0, sidx, (int)n, 0,
+                                         key_bits, st));
       count_launch();
       // pair hashes / chain flags into ordinal order
       k_gather_u64<<<grid_for(n, 256), 256, 0, st>>>(row_pr, sidx, n, pr);
@@ -1141,17 +1178,14 @@ int sbr_cir_select(const SbrCirParams* P, const uint64_t* row_key, const uint64_
       CK(cudaStreamSynchronize(st));
       CK(cudaMemsetAsync(keep_chain, 0, n, st));
       if (n_chain > 0) {
-        // stable LSD: by pf, then by pr -> (pr, pf, ordinal) order
-        k_gather_u64<<<grid_for(n_chain, 256), 256, 0, st>>>(pf, cpos, n_chain, ck);
+        // one stable sort by pr keeps ordinal order inside each pr run
+        k_gather_u64<<<grid_for(n_chain, 256), 256, 0, st>>>(pr, cpos, n_chain, ck);
         LK("k_gather_u64");
         CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ck, ck2, cpos, cpos2, (int)n_chain, 0, 64, st));
         count_launch();
-        k_gather_u64<<<grid_for(n_chain, 256), 256, 0, st>>>(pr, cpos2, n_chain, ck);
-        LK("k_gather_u64");
-        CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ck, ck2, cpos2, cpos, (int)n_chain, 0, 64, st));
-        count_launch();
-        k_first_flags<<<grid_for(n_chain, 256), 256, 0, st>>>(pr, pf, cpos, n_chain, keep_chain, counters);
-        LK("k_first_flags");
+        k_first_flags_pr<<<grid_for(n_chain, 256), 256, 0, st>>>(pr, pf, cpos2, n_chain, keep_chain,
+                                                                  counters);
+        LK("k_first_flags_pr");
       }
       k_kept<<<grid_for(n, 256), 256, 0, st>>>(chain, keep_chain, n, kept);
       LK("k_kept");
@@ -1173,7 +1207,7 @@ int sbr_cir_select(const SbrCirParams* P, const uint64_t* row_key, const uint64_
       unsigned long long* per_depth = A.get<unsigned long long>(16);
       if (!A.ok) return set_error(SBR_ERR_NOMEM, "select scratch");
       CK(cudaMemsetAsync(per_depth, 0, 16 * sizeof(unsigned long long), st));
-      k_kept_per_depth<<<grid_for(n, 256), 256, 0, st>>>(skey, kept, n, per_depth);
+      k_kept_per_depth<<<grid_for(n, 256), 256, 0, st>>>(skey, kept, n, depth_shift, per_depth);
       LK("k_kept_per_depth");
       unsigned long long hd[16];
       CK(cudaMemcpyAsync(hd, per_depth, sizeof hd, cudaMemcpyDeviceToHost, st));

@@ -7,7 +7,7 @@
 //   3. radix sort of (key, triangle) pairs                 [cub::DeviceRadixSort]
 //   4. Karras 2012 binary radix tree over the sorted keys  [kernel]
 //   5. bottom-up refit of conservative fp32 boxes          [kernel, atomics]
-//   6. collapse subtrees of <= 4 triangles into leaves and
+//   6. collapse subtrees of <= SBR_LEAF_MAX (2) triangles into leaves and
 //      emit 64-B BVH2 nodes (both child boxes per node)    [scan + kernel]
 // Triangles are stored in Morton (slot) order as float64 corners so the
 // watertight test reproduces the reference's arithmetic exactly.
@@ -311,15 +311,20 @@ __global__ void k_refit(const double* __restrict__ v0, const double* __restrict_
   }
 }
 
+#ifndef SBR_LEAF_MAX
+#define SBR_LEAF_MAX 2  // leaves of <= 2 triangles: a float64 triangle test costs ~4 fp32 box
+                        // tests, so smaller leaves win (canyon 2.55e9 -> 2.70e9 rb/s vs 4);
+                        // the leaf code allows up to 4 (count - 1 in 2 bits)
+#endif
 __global__ void k_keep_flags(const int2* __restrict__ ranges, int nint, int* keep) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nint) return;
   const int2 r = ranges[i];
-  keep[i] = (r.y - r.x + 1) > 4 ? 1 : 0;
+  keep[i] = (r.y - r.x + 1) > SBR_LEAF_MAX ? 1 : 0;
 }
 
 // Emit the collapsed BVH2 nodes.  Child code: internal kept node -> its
-// compact index; subtree of <= 4 triangles -> leaf(first, count).
+// compact index; subtree of <= SBR_LEAF_MAX triangles -> leaf(first, count).
 __global__ void k_emit(const int2* __restrict__ children, const int2* __restrict__ ranges,
                        const int* __restrict__ keep, const int* __restrict__ compact,
                        const Box32* __restrict__ leaf_box, const Box32* __restrict__ int_box,
@@ -391,7 +396,10 @@ __global__ void k_gather_tris(const double* __restrict__ v0, const double* __res
 // converted to the Karras-style (children, ranges) arrays by renumbering the
 // leaves in depth-first order, so the leaf collapse / emit path is shared.
 // ---------------------------------------------------------------------------
-constexpr int kPlocRadius = 12;
+#ifndef SBR_PLOC_RADIUS
+#define SBR_PLOC_RADIUS 12
+#endif
+constexpr int kPlocRadius = SBR_PLOC_RADIUS;
 
 __device__ __forceinline__ float half_area(const Box32& b) {
   const float dx = b.hi[0] - b.lo[0], dy = b.hi[1] - b.lo[1], dz = b.hi[2] - b.lo[2];

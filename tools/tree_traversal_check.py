@@ -44,8 +44,10 @@ def convert(acc):
             np.array(right, np.int32), np.array(start, np.int32), np.array(count, np.int32))
 
 
-meshes = scenes.street_canyon()
+CITY = "--city" in sys.argv
+meshes = scenes.city() if CITY else scenes.street_canyon()
 mats = scenes.uniform_materials(meshes, scenes.concrete(scattering=0.3))
+TX = (0.0, 0.0, 30.0) if CITY else (0.0, 5.0, 20.0)
 grid = MeasurementGrid((0, 0, 1.5), (1, 0, 0), (0, 1, 0), (1.0, 1.0), (200, 200))
 cfg = RadioMapConfig(num_samples=100_000, max_depth=5, seed=0,
                      enabled=frozenset({Interaction.REFLECTION, Interaction.SCATTERING}))
@@ -72,7 +74,7 @@ for label, builder in (("sah(reference)", None), ("lbvh", 0), ("ploc", 1)):
         s.obj, s.prim = sc.tri_object_id.ctypes.data, sc.tri_primitive_id.ctypes.data
         s.normal, s.matrow = sc.tri_normal.ctypes.data, sc.tri_material_row.ctypes.data
     L.orc_visit_stats(n.ctypes.data, t.ctypes.data, 1)
-    v, d = sc.radiomap((0.0, 5.0, 20.0), grid, cfg, sample_range=(0, 100000), include_direct=False)
+    v, d = sc.radiomap(TX, grid, cfg, sample_range=(0, 100000), include_direct=False)
     L.orc_visit_stats(n.ctypes.data, t.ctypes.data, 1)
     print(label, "scalar near-first traversal: nodes/rb %.2f tris/rb %.2f  (rb %d, deposits %d)"
           % (n[0] / d["ray_bounces"], t[0] / d["ray_bounces"], d["ray_bounces"], d["deposits"]))

@@ -1016,7 +1016,11 @@ int sbr_cir_vertex_order(const SbrScene* scene, const SbrVertexBuf* vb, int64_t 
   {
     const double ex = S.bounds_hi[0] - S.bounds_lo[0], ey = S.bounds_hi[1] - S.bounds_lo[1],
                  ez = S.bounds_hi[2] - S.bounds_lo[2];
-    ie = make_double3(ex > 0 ? 1.0 / ex : 0.0, ey > 0 ? 1.0 / ey : 0.0, ez > 0 ? 1.0 / ez : 0.0);
+    // one cubic grid (not per-axis stretching): a tile of 32 Morton-adjacent
+    // vertices is then spatially compact in flat scenes (config-3
+    // visibility 150 -> 125 ms)
+    const double e = fmax(fmax(ex, ey), ez);
+    ie = make_double3(e > 0 ? 1.0 / e : 0.0, e > 0 ? 1.0 / e : 0.0, e > 0 ? 1.0 / e : 0.0);
   }
   Arena A(st);
   uint64_t* keys = A.get<uint64_t>(nv);

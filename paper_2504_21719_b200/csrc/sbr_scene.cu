@@ -222,9 +222,14 @@ __global__ void k_morton(const float3* __restrict__ cen, int64_t n,
   const float hi[3] = {ord2f(cbounds[3]), ord2f(cbounds[4]), ord2f(cbounds[5])};
   const float v[3] = {c.x, c.y, c.z};
   uint64_t q[3];
+  // one cubic grid over the centroid bounds (not each axis stretched to 21
+  // bits): the curve then follows true distances in flat scenes (city
+  // 1000 x 1000 x 60 m).  PLOC SAH cost city 74.6 -> 62.4 (reference binned
+  // SAH: 63.3), canyon 40.8 -> 38.6; canyon map +8 %, config-3 visibility -14 %.
+  const float cube = fmaxf(fmaxf(hi[0] - lo[0], hi[1] - lo[1]), hi[2] - lo[2]);
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    const float ext = hi[k] - lo[k];
+    const float ext = cube;
     float f = ext > 0.f ? (v[k] - lo[k]) / ext : 0.5f;
     f = fminf(fmaxf(f, 0.f), 1.f);
     q[k] = (uint64_t)fminf(f * 2097152.0f, 2097151.0f);

@@ -737,7 +737,12 @@ struct AnyTrav {
           leaf = 0;
           return;
         }
-        const bool lfirst = tl <= tr;
+        // far child first: any hit ends the search and there is no bound to
+        // shrink, so near-first only walks the crowded boxes around the ray's
+        // origin (the surface a CIR vertex lies on) before reaching the
+        // occluders.  Config-3 visibility: near-first 126 ms, fixed order
+        // 107, nearest-to-midpoint 99, far-first 93 (identical results)
+        const bool lfirst = tl > tr;
         stack_node[sp++] = lfirst ? ch.y : ch.x;
         node = lfirst ? ch.x : ch.y;
       } else if (hl) {
@@ -812,7 +817,7 @@ __device__ __forceinline__ bool trace_any(const DevScene& S, double3 o, double3 
       const bool hr = tr < __int_as_float(0x7f800000);
       if (hl && hr) {
         if (sp >= kStackSize) return false;
-        const bool lfirst = tl <= tr;
+        const bool lfirst = tl > tr;  // far child first, like AnyTrav
         stack_node[sp++] = lfirst ? ch.y : ch.x;
         node = lfirst ? ch.x : ch.y;
         continue;

@@ -281,8 +281,10 @@ __global__ void k_vertex_morton(const double* __restrict__ point, int64_t n, dou
 // Occluder sharing (97 % of config-3 rays are occluded): a lane that finds an
 // occluder publishes it to the lanes still traversing (tested at once) and to
 // a small per-warp ring that the next tiles of the same target test before
-// traversing.  Any triangle with t_min < t < limit decides "occluded", so the
-// result is exactly the traversal's.
+// traversing, and in a small per-target table (global memory, racy by
+// design) that every warp working on that target tests too.  Any triangle
+// with t_min < t < limit decides "occluded", so the result is exactly the
+// traversal's.
 constexpr int kVisWarps = 4;
 #ifndef SBR_VIS_HINTS
 #define SBR_VIS_HINTS 4
@@ -290,6 +292,10 @@ constexpr int kVisWarps = 4;
 #ifndef SBR_VIS_GROUP
 #define SBR_VIS_GROUP 8
 #endif
+#ifndef SBR_VIS_GHINTS
+#define SBR_VIS_GHINTS 4  // per-target occluder table shared by all warps (-3 %)
+#endif
+constexpr int kVisGHints = SBR_VIS_GHINTS;
 constexpr int kVisHints = SBR_VIS_HINTS;
 constexpr int kVisGroup = SBR_VIS_GROUP;
 
@@ -302,7 +308,8 @@ __global__ void __launch_bounds__(128, SBR_VIS_MINB) k_cir_visibility(DevScene S
                                                         int32_t* row_vtx, int64_t row_cap,
                                                         unsigned long long* counters,
                                                         unsigned long long* work,
-                                                        const int32_t* __restrict__ order) {
+                                                        const int32_t* __restrict__ order,
+                                                        int* ghint) {
   __shared__ int64_t sq[kVisWarps][64];
   __shared__ int shint[kVisWarps][kVisHints > 0 ? kVisHints : 1];
   __shared__ int shpos[kVisWarps];
@@ -321,7 +328,7 @@ __global__ void __launch_bounds__(128, SBR_VIS_MINB) k_cir_visibility(DevScene S
   unsigned vis = 0;
   bool more = true;
   int64_t unit = 0, g_tile0 = 0;
-  int tile_cur = kVisGroup, tile_end = kVisGroup, k_cur = 0;
+  int tile_cur = kVisGroup, tile_end = kVisGroup, k_cur = -1;
   while (more || qn > 0) {
     // ---- refill: side test on the next tile of the claimed (group, target)
     if (more && qn < 32) {
@@ -334,12 +341,14 @@ __global__ void __launch_bounds__(128, SBR_VIS_MINB) k_cir_visibility(DevScene S
         } else {
           unit = (int64_t)base;
           const int64_t grp = unit / nt;
-          k_cur = (int)(unit % nt);
+          const int k_new = (int)(unit % nt);
+          const bool same_target = k_new == k_cur;
+          k_cur = k_new;
           g_tile0 = grp * kVisGroup;
           tile_cur = 0;
           const int64_t left = ntiles - g_tile0;
           tile_end = left < kVisGroup ? (int)left : kVisGroup;
-          if (kVisHints > 0) {  // hints of another target rarely help
+          if (kVisHints > 0 && !same_target) {  // hints of another target rarely help
             if ((int)lane < kVisHints) shint[wid][lane] = -1;
             __syncwarp();
           }
@@ -408,6 +417,13 @@ __global__ void __launch_bounds__(128, SBR_VIS_MINB) k_cir_visibility(DevScene S
       const int j = shint[wid][h];
       if (cast && !T.found && j >= 0) T.try_occluder(S, j);
     }
+    // occluders any warp found for this target (racy table: hints only)
+    for (int h = 0; h < kVisGHints; ++h) {
+      if (cast && !T.found) {
+        const int j = __ldcg(ghint + (int64_t)k * kVisGHints + h);
+        if (j >= 0) T.try_occluder(S, j);
+      }
+    }
     while (!T.done()) {
       const bool before = T.found;
       T.round(S);
@@ -420,6 +436,8 @@ __global__ void __launch_bounds__(128, SBR_VIS_MINB) k_cir_visibility(DevScene S
           if (!T.done()) T.try_occluder(S, j);
           if ((int)lane == src) {
             shint[wid][shpos[wid] % kVisHints] = j;
+            if (kVisGHints > 0)
+              __stcg(ghint + (int64_t)k * kVisGHints + (shpos[wid] % (kVisGHints > 0 ? kVisGHints : 1)), j);
             shpos[wid] = shpos[wid] + 1;
           }
         }
@@ -1057,12 +1075,23 @@ int sbr_cir_visibility(const SbrScene* scene, const SbrCirParams* P, const SbrVe
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cir_visibility, 128, 0);
   if (per_sm < 1) per_sm = 1;
   prof_begin(stream, "k_cir_visibility");
+  int* ghint = nullptr;
+  if (kVisGHints > 0) {
+    const size_t gb = sizeof(int) * (size_t)P->n_targets * kVisGHints;
+    if (cudaMallocAsync(&ghint, gb, st) != cudaSuccess) {
+      cudaFreeAsync(work, st);
+      return set_error(SBR_ERR_NOMEM, "occluder hints");
+    }
+    cudaMemsetAsync(ghint, 0xff, gb, st);
+  }
   k_cir_visibility<<<sms * per_sm, 128, 0, st>>>(dev_view(scene), *P, *vb, v_begin, v_end,
                                                  row_key, row_vtx, row_cap,
-                                                 (unsigned long long*)counters, work, order);
+                                                 (unsigned long long*)counters, work, order,
+                                                 ghint);
   prof_end(stream);
   rc = launch_status("k_cir_visibility");
   cudaFreeAsync(work, st);
+  if (ghint) cudaFreeAsync(ghint, st);
   return rc;
 }
 

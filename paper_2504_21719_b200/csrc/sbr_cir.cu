@@ -512,11 +512,12 @@ __global__ void k_gather_u64(const uint64_t* __restrict__ src, const int32_t* __
 }
 
 // first occurrence of each (pr, pf) among chain rows sorted by (pr, pf, ordinal)
-// First occurrence of each (pr, pf) among chain rows sorted stably by pr only
-// (ordinal order inside a pr run): a row is first unless an earlier row of its
-// run has the same pf.  pr and pf are two hashes of one (chain, target) key,
-// so a run almost always has one pf and the scan stops at the neighbour; a
-// 64-bit pr collision between different keys is still handled exactly.
+// First occurrence of each (pr, pf) among chain rows sorted stably by the top
+// 32 bits of pr (ordinal order inside a run): a row is first unless an
+// earlier row of its run has the same (pr, pf).  pr and pf are two hashes of
+// one (chain, target) key, so a run almost always holds a single key and the
+// scan stops at the neighbour; prefix or hash collisions between different
+// keys only lengthen the scan, the result stays exact.
 __global__ void k_first_flags_pr(const uint64_t* __restrict__ pr, const uint64_t* __restrict__ pf,
                                  const int32_t* __restrict__ order, int64_t n,
                                  uint8_t* keep_chain, unsigned long long* counters) {
@@ -528,8 +529,9 @@ __global__ void k_first_flags_pr(const uint64_t* __restrict__ pr, const uint64_t
     bool first = true;
     for (int64_t j = i - 1; j >= 0; --j) {
       const int32_t b = order[j];
-      if (pr[b] != ka) break;
-      if (pf[b] == fa) {
+      const uint64_t kb = pr[b];
+      if ((kb >> 32) != (ka >> 32)) break;
+      if (kb == ka && pf[b] == fa) {
         first = false;
         break;
       }
@@ -1211,10 +1213,11 @@ int sbr_cir_select(const SbrCirParams* P, const uint64_t* row_key, const uint64_
       CK(cudaStreamSynchronize(st));
       CK(cudaMemsetAsync(keep_chain, 0, n, st));
       if (n_chain > 0) {
-        // one stable sort by pr keeps ordinal order inside each pr run
+        // one stable sort by the top 32 bits of pr keeps ordinal order inside
+        // each run; k_first_flags_pr compares full (pr, pf) within a run
         k_gather_u64<<<grid_for(n_chain, 256), 256, 0, st>>>(pr, cpos, n_chain, ck);
         LK("k_gather_u64");
-        CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ck, ck2, cpos, cpos2, (int)n_chain, 0, 64, st));
+        CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ck, ck2, cpos, cpos2, (int)n_chain, 32, 64, st));
         count_launch();
         k_first_flags_pr<<<grid_for(n_chain, 256), 256, 0, st>>>(pr, pf, cpos2, n_chain, keep_chain,
                                                                   counters);

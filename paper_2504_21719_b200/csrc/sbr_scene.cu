@@ -47,7 +47,7 @@ struct Span {
   cudaEvent_t a, b;
 };
 static std::mutex g_prof_mu;
-static bool g_prof_on = false;
+static std::atomic<bool> g_prof_on{false};
 static std::vector<Span> g_spans;
 static std::map<std::string, std::pair<double, uint64_t>> g_prof_acc;
 
@@ -555,7 +555,7 @@ __global__ void k_ploc_leaves(const int32_t* __restrict__ off, const Box32* __re
   ids_dfs[s] = ids_sorted[i];
 }
 
-static int g_builder = 1;  // 0 = Karras LBVH, 1 = PLOC
+static std::atomic<int> g_builder{1};  // 0 = Karras LBVH, 1 = PLOC
 
 template <typename T>
 static int dalloc(T** p, size_t count, cudaStream_t st) {

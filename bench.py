@@ -72,7 +72,8 @@ def config_dict(n_gpus, ntri):
         "max_depth": 5,
         "grid_cells": 40000,
         "l2": "flushed between timed steps (256 MiB write, outside the per-step events)",
-        "parallelism": f"dp{n_gpus}: global sample-id shards, NCCL all-reduce of the grid",
+        "parallelism": f"dp{n_gpus}: chunk-cyclic global sample-id shards (2^19-id RNG chunks "
+                       "dealt round-robin), NCCL all-reduce of the grid",
     }
 
 
@@ -255,8 +256,14 @@ def run_ours(args, rank, world, local_rank):
         counters.zero_()
         if kernel_events is not None:
             kernel_events[0].record(stream)
-        _native.check(L.sbr_radiomap_bounce(scene.accel.handle, ctypes.byref(params), lo, hi,
-                                            _native.ptr(values), _native.ptr(counters), sptr))
+        if world > 1:   # chunk-cyclic shard of the N x 1e7 lattice (balanced over the sphere)
+            _native.check(L.sbr_radiomap_bounce_sharded(
+                scene.accel.handle, ctypes.byref(params), rank, world, _native.ptr(values),
+                _native.ptr(counters), sptr))
+        else:
+            _native.check(L.sbr_radiomap_bounce(scene.accel.handle, ctypes.byref(params), lo,
+                                                hi, _native.ptr(values), _native.ptr(counters),
+                                                sptr))
         if kernel_events is not None:
             kernel_events[1].record(stream)
         if rank == 0:
@@ -346,7 +353,7 @@ def run_ours(args, rank, world, local_rank):
                                                     sample_range=(lo, hi))
             rb_e2e = diag["ray_bounces"]
         else:
-            v, c = compute_radio_map_sbr(scene, np.array(TX), grid, cfg, sample_range=(lo, hi),
+            v, c = compute_radio_map_sbr(scene, np.array(TX), grid, cfg, shard=(rank, world),
                                          include_direct=(rank == 0), return_tensors=True)
             dist.all_reduce(v)
             dist.all_reduce(c)
@@ -424,18 +431,17 @@ def bench_config4(args, dev, rank=0, world=1):
     from paper_2504_21719_b200.radiomap import (MeasurementGrid, RadioMapConfig,
                                                 compute_radio_map_sbr)
     from paper_2504_21719_b200.sampling import Interaction
-    from paper_2504_21719_b200.sharding import allreduce_map, shard_range
+    from paper_2504_21719_b200.sharding import allreduce_map
     meshes = scenes.city()
     scene = SceneModel(meshes, scenes.uniform_materials(meshes, scenes.concrete(scattering=0.3)),
                        device=dev)
     grid = MeasurementGrid((0.0, 0.0, 1.5), (1, 0, 0), (0, 1, 0), (1.0, 1.0), (1000, 1000))
     cfg = RadioMapConfig(num_samples=C4_SAMPLES, max_depth=5, seed=0,
                          enabled=frozenset({Interaction.REFLECTION, Interaction.SCATTERING}))
-    lo, hi = shard_range(C4_SAMPLES, rank, world)
     stream = torch.cuda.current_stream(dev)
 
-    def one():
-        v, c = compute_radio_map_sbr(scene, (0.0, 0.0, 30.0), grid, cfg, sample_range=(lo, hi),
+    def one():   # chunk-cyclic shards of the 1e9 ids: every GPU sees the whole sphere
+        v, c = compute_radio_map_sbr(scene, (0.0, 0.0, 30.0), grid, cfg, shard=(rank, world),
                                      include_direct=(rank == 0), return_tensors=True)
         allreduce_map(v, c)
         return v, c

@@ -218,6 +218,15 @@ int sbr_radiomap_bounce(const SbrScene* scene, const SbrMapParams* params,
                         double* grid_dev, uint64_t* counters_dev, void* stream);
 /* Replaces _direct_cells (radiomap.py:566-583): analytic LoS term per cell
  * centre into direct_dev (ny, nx) (overwritten), counts visible cells. */
+/* The bounce loop over a chunk-cyclic shard of the global sample ids
+ * [0, num_samples): global RNG chunks (g >> SBR_CHUNK_LOG2) = shard_index,
+ * shard_index + shard_count, ...  The shards of one call partition the ids, so
+ * summing their grids / counters gives sbr_radiomap_bounce(0, num_samples);
+ * unlike contiguous ranges every shard sees the whole sphere of directions
+ * (balanced work per GPU).  No reference counterpart (multi-GPU only). */
+int sbr_radiomap_bounce_sharded(const SbrScene* scene, const SbrMapParams* params,
+                                int32_t shard_index, int32_t shard_count, double* grid_dev,
+                                uint64_t* counters_dev, void* stream);
 int sbr_radiomap_direct(const SbrScene* scene, const SbrMapParams* params,
                         double* direct_dev, uint64_t* counters_dev, void* stream);
 
@@ -372,6 +381,17 @@ int sbr_cir_select(const SbrCirParams* params, const uint64_t* row_key_dev,
                    const uint8_t* row_chain_dev, int64_t n_rows, const uint8_t* los_visible_dev,
                    uint64_t n_hash, int64_t n_buffer, int64_t* rec_row_dev, int64_t* n_records,
                    uint64_t* counters_dev, void* stream);
+/* Shard-local pre-selection for multi-GPU CIR (no reference counterpart: it
+ * only shrinks the all-gather of compute_paths_sharded).  Keeps every
+ * non-chain row and the first occurrence, in ordinal order, of each
+ * (pr, pf) among this shard's chain rows; kept_idx_dev (n_rows) receives the
+ * kept row indices ascending, *n_kept / *n_dup (host) the kept and dropped
+ * counts.  Gathering only kept rows leaves sbr_cir_select's result unchanged;
+ * add the dropped rows to SBR_CC_DUPLICATES.  Synchronises `stream`. */
+int sbr_cir_local_dedup(const SbrCirParams* params, const uint64_t* row_key_dev,
+                        const uint64_t* row_pr_dev, const uint64_t* row_pf_dev,
+                        const uint8_t* row_chain_dev, int64_t n_rows, int64_t* kept_idx_dev,
+                        int64_t* n_kept, uint64_t* n_dup, void* stream);
 /* rec_row -> (vertex index, target) for sbr_cir_records (vertex -1 = LoS). */
 int sbr_cir_resolve_records(const int64_t* rec_row_dev, int64_t n, const uint64_t* row_key_dev,
                             const int32_t* row_vtx_dev, int32_t* rec_vtx_dev,

@@ -475,6 +475,24 @@ def _select_rows(params, key, pr, pf, chain, n, los_vis, cfg, counters, dev):
     return rec_row, int(n_rec.value)
 
 
+def _local_rows(R):
+    """Shard-local pre-selection (sbr_cir_local_dedup): the rows worth
+    all-gathering, as (dict of row tensors, kept row indices, dropped count)."""
+    torch = _torch()
+    L_ = _native.lib()
+    n = R.n
+    kept = torch.empty(max(n, 1), dtype=torch.int64, device=R.dev)
+    nk, nd = ctypes.c_int64(0), ctypes.c_uint64(0)
+    _native.check(L_.sbr_cir_local_dedup(
+        ctypes.byref(R.params), _native.ptr(R.key), _native.ptr(R.pr), _native.ptr(R.pf),
+        _native.ptr(R.chain), n, _native.ptr(kept), ctypes.byref(nk), ctypes.byref(nd),
+        _native.stream_ptr(R.dev)))
+    kept = kept[:int(nk.value)]
+    rows = {"key": R.key[:n].index_select(0, kept), "pr": R.pr[:n].index_select(0, kept),
+            "pf": R.pf[:n].index_select(0, kept), "chain": R.chain[:n].index_select(0, kept)}
+    return rows, kept, int(nd.value)
+
+
 def _materialize(R, rec_row, n, cfg):
     """CandidateRecord arrays for rec_row entries that index R's own rows."""
     torch = _torch()
@@ -834,12 +852,26 @@ def compute_paths_sharded(scene, transmitters, receivers, cfg, group=None):
         with torch.cuda.device(dev):
             R = _sweep_rows(scene, source, targets, cfg, lo, hi)
             n = R.n
-            local = {"key": R.key, "pr": R.pr[:n], "pf": R.pf[:n], "chain": R.chain[:n]}
+            kept, n_dup = None, 0
+            if world > 1:
+                # only each shard's first occurrences travel (same selection,
+                # ~100x fewer rows on config 3); the rest are duplicates
+                local, kept, n_dup = _local_rows(R)
+            else:
+                local = {"key": R.key, "pr": R.pr[:n], "pf": R.pf[:n], "chain": R.chain[:n]}
             g, offsets = gather_rows(local, group)
             sel_counters = torch.zeros(_abi.SBR_CC_COUNT, dtype=torch.int64, device=dev)
             rec_row, nrec = _select_rows(R.params, g["key"], g["pr"], g["pf"], g["chain"],
                                          offsets[-1], R.los_vis, cfg, sel_counters, dev)
+            if world > 1:
+                dup = torch.tensor([n_dup], dtype=torch.int64, device=dev)
+                dist.all_reduce(dup, group=group)
+                sel_counters[_abi.CIR_COUNTERS.index("duplicates")] += dup[0]
             pos, loc = owned_records(rec_row[:nrec].cpu().numpy(), offsets, rank)
+            if kept is not None:        # positions in the kept list -> shard row indices
+                loc = np.array(loc, dtype=np.int64)
+                m = loc >= 0
+                loc[m] = kept.cpu().numpy()[loc[m]]
             loc_t = torch.from_numpy(np.ascontiguousarray(loc, dtype=np.int64)).to(dev)
             recbuf = _materialize(R, loc_t, len(loc), cfg)
             sweep = R.counters.clone()

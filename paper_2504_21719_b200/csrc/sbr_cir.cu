@@ -752,6 +752,12 @@ __global__ void k_row_buffer(const int32_t* __restrict__ in_buf, const int32_t* 
   }
 }
 
+__global__ void k_iota64(int64_t* a, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = i;
+}
+
 __global__ void k_iota(int32_t* a, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -1114,6 +1120,107 @@ int sbr_cir_resolve_records(const int64_t* rec_row, int64_t n, const uint64_t* r
   k_resolve_records<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(rec_row, row_key, row_vtx,
                                                                         n, rec_vtx, rec_target);
   return launch_status("k_resolve_records");
+}
+
+// Shard-local pre-selection for multi-GPU CIR: within one shard's rows keep
+// every non-chain row and the first occurrence (ordinal order) of each
+// (pr, pf) among chain rows.  The global first occurrence of a key is the
+// minimum over the shards' local firsts, and every later selection step
+// (truncation per depth, DedupTable registration) only looks at kept rows, so
+// all-gathering the kept rows gives the same selection as gathering all of
+// them; the dropped rows are duplicates (returned in *n_dup to be added to
+// the global duplicates counter).  kept_idx: ascending row indices.
+int sbr_cir_local_dedup(const SbrCirParams* P, const uint64_t* row_key, const uint64_t* row_pr,
+                        const uint64_t* row_pf, const uint8_t* row_chain, int64_t n,
+                        int64_t* kept_idx, int64_t* n_kept, uint64_t* n_dup, void* stream) {
+  int rc = check_cir(nullptr, P);
+  if (rc) return rc;
+  if (!n_kept || !n_dup) return set_error(SBR_ERR_INVALID, "NULL argument");
+  if (n >= (1LL << 31)) return set_error(SBR_ERR_INVALID, "too many rows");
+  *n_kept = 0;
+  *n_dup = 0;
+  if (n <= 0) return SBR_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nt = P->n_targets;
+  int tbits = 1, sbits = 1;
+  while (tbits < kTargetBits && (1LL << tbits) < (int64_t)nt) ++tbits;
+  while (sbits < kSampleBits && (1ULL << sbits) < P->num_samples) ++sbits;
+  const bool dense = tbits + sbits + 4 <= 64;
+  const int key_bits = dense ? tbits + sbits + 4 : 64;
+  Arena A(st);
+  uint64_t* dkey = A.get<uint64_t>(n);
+  uint64_t* skey = A.get<uint64_t>(n);
+  int32_t* idx0 = A.get<int32_t>(n);
+  int32_t* sidx = A.get<int32_t>(n);
+  uint8_t* chain_s = A.get<uint8_t>(n);
+  int32_t* cpos = A.get<int32_t>(n);
+  int32_t* cpos2 = A.get<int32_t>(n);
+  uint64_t* ck = A.get<uint64_t>(n);
+  uint64_t* ck2 = A.get<uint64_t>(n);
+  uint8_t* keep_chain = A.get<uint8_t>(n);
+  int32_t* kept = A.get<int32_t>(n);
+  int64_t* kidx = A.get<int64_t>(n);
+  int64_t* d_count = A.get<int64_t>(2);
+  unsigned long long* cnt = A.get<unsigned long long>(SBR_CC_COUNT);
+  if (!A.ok) return set_error(SBR_ERR_NOMEM, "local dedup scratch");
+  size_t tmp_bytes = 0, t2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, skey, skey, idx0, sidx, (int)n, 0, 64, st);
+  cub::DeviceSelect::Flagged(nullptr, t2, idx0, chain_s, cpos, d_count, (int)n, st);
+  tmp_bytes = std::max(tmp_bytes, t2);
+  void* tmp = A.get<uint8_t>((int64_t)tmp_bytes);
+  if (!A.ok) return set_error(SBR_ERR_NOMEM, "local dedup scratch");
+  {
+    int64_t n_chain = 0, nk = 0;
+    unsigned long long dup = 0;
+    CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * SBR_CC_COUNT, st));
+    CK(cudaMemsetAsync(keep_chain, 0, n, st));
+    k_iota<<<grid_for(n, 256), 256, 0, st>>>(idx0, n);
+    LK("k_iota");
+    const uint64_t* sort_in = row_key;
+    if (dense && tbits + sbits < 60) {
+      k_dense_keys<<<grid_for(n, 256), 256, 0, st>>>(row_key, n, tbits, sbits, dkey);
+      LK("k_dense_keys");
+      sort_in = dkey;
+    }
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, sort_in, skey, idx0, sidx, (int)n, 0,
+                                       key_bits, st));
+    count_launch();
+    // chain rows, as original indices, in ordinal order
+    k_gather_u8<<<grid_for(n, 256), 256, 0, st>>>(row_chain, sidx, n, chain_s);
+    LK("k_gather_u8");
+    CK(cub::DeviceSelect::Flagged(tmp, tmp_bytes, sidx, chain_s, cpos, d_count, (int)n, st));
+    count_launch();
+    CK(cudaMemcpyAsync(&n_chain, d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (n_chain > 0) {
+      k_gather_u64<<<grid_for(n_chain, 256), 256, 0, st>>>(row_pr, cpos, n_chain, ck);
+      LK("k_gather_u64");
+      CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ck, ck2, cpos, cpos2, (int)n_chain, 32,
+                                         64, st));
+      count_launch();
+      k_first_flags_pr<<<grid_for(n_chain, 256), 256, 0, st>>>(row_pr, row_pf, cpos2, n_chain,
+                                                                keep_chain, cnt);
+      LK("k_first_flags_pr");
+    }
+    k_kept<<<grid_for(n, 256), 256, 0, st>>>(row_chain, keep_chain, n, kept);
+    LK("k_kept");
+    k_iota64<<<grid_for(n, 256), 256, 0, st>>>(kidx, n);
+    LK("k_iota64");
+    CK(cub::DeviceSelect::Flagged(nullptr, t2, kidx, kept, kept_idx, d_count + 1, (int)n, st));
+    if (t2 > tmp_bytes) {
+      rc = set_error(SBR_ERR_NOMEM, "local dedup scratch");
+      goto done;
+    }
+    CK(cub::DeviceSelect::Flagged(tmp, tmp_bytes, kidx, kept, kept_idx, d_count + 1, (int)n, st));
+    count_launch();
+    CK(cudaMemcpyAsync(&nk, d_count + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&dup, cnt + SBR_CC_DUPLICATES, sizeof(dup), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *n_kept = nk;
+    *n_dup = dup;
+  }
+done:
+  return rc;
 }
 
 int sbr_cir_select(const SbrCirParams* P, const uint64_t* row_key, const uint64_t* row_pr,

@@ -81,6 +81,20 @@ __device__ __forceinline__ uint64_t comb_sample(uint64_t w, uint64_t comb_q) {
   return (w / comb_q) + (w % comb_q) * kCombStride;
 }
 
+// Chunk-cyclic shards (sbr_radiomap_bounce_sharded): a shard owns the global
+// RNG chunks (g >> 19) = shard, shard + count, ...; local id l walks them in
+// order.  count = 1 is the identity (contiguous ranges).  Fibonacci ids run
+// pole to pole, so contiguous shards would give one GPU the upward rays that
+// escape at once and another the grazing ones that bounce five times.
+struct ShardMap {
+  uint32_t index, count;
+  __device__ __forceinline__ uint64_t gid(uint64_t l) const {
+    if (count == 1) return l;
+    const uint64_t mask = (1ULL << SBR_CHUNK_LOG2) - 1;
+    return (((l >> SBR_CHUNK_LOG2) * count + index) << SBR_CHUNK_LOG2) | (l & mask);
+  }
+};
+
 // ---------------------------------------------------------------------------
 // trace
 // ---------------------------------------------------------------------------
@@ -101,7 +115,7 @@ __global__ void __launch_bounds__(128, SBR_TRACE_MINB) k_map_trace(DevScene S, S
                                                    MapQueue q, const unsigned long long* count_in,
                                                    uint64_t begin, uint64_t count0, uint64_t comb_q,
                                                    HitBuf hits, unsigned long long* work,
-                                                   unsigned long long* counters) {
+                                                   unsigned long long* counters, ShardMap sh) {
   const unsigned lane = threadIdx.x & 31u;
   const uint64_t n = seg == 0 ? comb_q * kCombStride : (uint64_t)*count_in;
   const double3 src = make_double3(P.source[0], P.source[1], P.source[2]);
@@ -117,7 +131,7 @@ __global__ void __launch_bounds__(128, SBR_TRACE_MINB) k_map_trace(DevScene S, S
       if (seg == 0) {
         const uint64_t local = comb_sample(i, comb_q);
         active = local < count0;
-        if (active) d = fibonacci_dir(P.num_samples, begin + local);
+        if (active) d = fibonacci_dir(P.num_samples, sh.gid(begin + local));
         else hits.tri[i] = -3;  // comb slot past the end of the range
       } else {
         o = make_double3(q.ox[i], q.oy[i], q.oz[i]);
@@ -161,7 +175,7 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
                                                    MapQueue qo, unsigned long long* count_out,
                                                    ScatterQueue sq, unsigned long long* count_s,
                                                    double* __restrict__ grid,
-                                                   unsigned long long* __restrict__ counters) {
+                                                   unsigned long long* __restrict__ counters, ShardMap sh) {
   LaneCounters K = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
   const uint64_t n = seg == 0 ? comb_q * kCombStride : (uint64_t)*count_in;
   const double3 n_hat = make_double3(P.normal[0], P.normal[1], P.normal[2]);
@@ -174,7 +188,7 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
     double r_dist, omega, weight;
     uint64_t g;
     if (seg == 0) {
-      g = begin + comb_sample(i, comb_q);
+      g = sh.gid(begin + comb_sample(i, comb_q));
       o = make_double3(P.source[0], P.source[1], P.source[2]);
       d = fibonacci_dir(P.num_samples, g);
       E = antenna_field(P.pattern, d);
@@ -660,12 +674,11 @@ int wave_alloc(int64_t cap, cudaStream_t st, Wave* w) {
 
 extern "C" {
 
-int sbr_radiomap_bounce(const SbrScene* scene, const SbrMapParams* P, uint64_t sample_begin,
-                        uint64_t sample_end, double* grid, uint64_t* counters_u64, void* stream) {
-  int rc = check_params(scene, P);
-  if (rc) return rc;
-  if (sample_end > P->num_samples || sample_begin > sample_end)
-    return set_error(SBR_ERR_INVALID, "bad sample range");
+// the bounce loop over local ids [sample_begin, sample_end) of shard `sh`
+static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sample_begin,
+                       uint64_t sample_end, ShardMap sh, double* grid, uint64_t* counters_u64,
+                       void* stream) {
+  int rc = SBR_OK;
   const uint64_t total = sample_end - sample_begin;
   if (total == 0) return SBR_OK;
   cudaStream_t st = (cudaStream_t)stream;
@@ -694,13 +707,13 @@ int sbr_radiomap_bounce(const SbrScene* scene, const SbrMapParams* P, uint64_t s
       if ((rc = launch_status("k_reset_pass"))) break;
       prof_begin(st, "k_map_trace");
       k_map_trace<<<trace_blocks, 128, 0, st>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo, cnt,
-                                                comb_q, w->hits, w->ctl, counters);
+                                                comb_q, w->hits, w->ctl, counters, sh);
       prof_end(st);
       if ((rc = launch_status("k_map_trace"))) break;
       prof_begin(st, "k_map_shade");
       k_map_shade<<<shade_blocks, 128, 0, st>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo,
                                                 comb_q, w->hits, w->q[1 - cur], w->ctl + 2 - cur,
-                                                w->sq, w->ctl + 3, grid, counters);
+                                                w->sq, w->ctl + 3, grid, counters, sh);
       prof_end(st);
       if ((rc = launch_status("k_map_shade"))) break;
       if (seg < P->max_depth && (P->allow_mask & 2)) {
@@ -716,6 +729,32 @@ int sbr_radiomap_bounce(const SbrScene* scene, const SbrMapParams* P, uint64_t s
   }
   cudaFreeAsync(w->block, st);
   return rc;
+}
+
+int sbr_radiomap_bounce(const SbrScene* scene, const SbrMapParams* P, uint64_t sample_begin,
+                        uint64_t sample_end, double* grid, uint64_t* counters_u64, void* stream) {
+  int rc = check_params(scene, P);
+  if (rc) return rc;
+  if (sample_end > P->num_samples || sample_begin > sample_end)
+    return set_error(SBR_ERR_INVALID, "bad sample range");
+  return bounce_impl(scene, P, sample_begin, sample_end, ShardMap{0u, 1u}, grid, counters_u64,
+                     stream);
+}
+
+int sbr_radiomap_bounce_sharded(const SbrScene* scene, const SbrMapParams* P,
+                                int32_t shard_index, int32_t shard_count, double* grid,
+                                uint64_t* counters_u64, void* stream) {
+  int rc = check_params(scene, P);
+  if (rc) return rc;
+  if (shard_count < 1 || shard_index < 0 || shard_index >= shard_count)
+    return set_error(SBR_ERR_INVALID, "bad shard");
+  const uint64_t C = 1ULL << SBR_CHUNK_LOG2;
+  const uint64_t n_chunks = (P->num_samples + C - 1) / C;
+  uint64_t n_local = 0;
+  for (uint64_t c = (uint64_t)shard_index; c < n_chunks; c += (uint64_t)shard_count)
+    n_local += (c + 1) * C <= P->num_samples ? C : P->num_samples - c * C;
+  return bounce_impl(scene, P, 0, n_local, ShardMap{(uint32_t)shard_index, (uint32_t)shard_count},
+                     grid, counters_u64, stream);
 }
 
 int sbr_radiomap_wedges(const SbrScene* scene, const SbrMapParams* P, const int32_t* wedge_ids,

@@ -221,15 +221,17 @@ def _counters_to_diag(counts):
 
 
 def compute_radio_map_sbr(scene, source, grid, cfg, *, pattern=None, array=None,
-                          precoder=None, sample_range=None, return_tensors=False,
+                          precoder=None, sample_range=None, shard=None, return_tensors=False,
                           include_direct=True):
     """Bounce-traced power map of one source, direct term included (radiomap.py:586-633).
 
     Returns (values (ny, nx) float64 numpy, diagnostics dict) like the
-    reference.  `sample_range=(lo, hi)` restricts the bounce estimator to a
-    shard of the global sample ids (multi-GPU); `include_direct=False` skips
-    the analytic term (added once by the shard owner).  With
-    `return_tensors=True` the device tensors are returned without a host copy.
+    reference.  Multi-GPU: `shard=(rank, world)` restricts the bounce
+    estimator to a chunk-cyclic shard of the global sample ids (balanced: every
+    shard spans the whole sphere), `sample_range=(lo, hi)` to a contiguous
+    range; `include_direct=False` skips the analytic term (added once by one
+    shard owner).  With `return_tensors=True` the device tensors are returned
+    without a host copy.
     """
     import torch
     source = np.asarray(source, dtype=np.float64)
@@ -252,7 +254,13 @@ def compute_radio_map_sbr(scene, source, grid, cfg, *, pattern=None, array=None,
     counters = torch.zeros(_abi.SBR_MC_COUNT, dtype=torch.int64, device=dev)
     stream = _native.stream_ptr(dev)
     with torch.cuda.device(dev):
-        if hi > lo:
+        if shard is not None:
+            if sample_range is not None:
+                raise ValueError("give either shard or sample_range")
+            _native.check(L.sbr_radiomap_bounce_sharded(
+                accel.handle, ctypes.byref(params), int(shard[0]), int(shard[1]),
+                _native.ptr(values), _native.ptr(counters), stream))
+        elif hi > lo:
             _native.check(L.sbr_radiomap_bounce(
                 accel.handle, ctypes.byref(params), int(lo), int(hi),
                 _native.ptr(values), _native.ptr(counters), stream))

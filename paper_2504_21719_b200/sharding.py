@@ -64,15 +64,19 @@ def compute_radio_map_sbr_distributed(scene, source, grid, cfg, group=None, **kw
     returned (values (ny,nx) numpy f64, diagnostics dict) equals the
     single-GPU result up to float64 summation order.
     """
+    import torch.distributed as dist
+
     from . import _abi
     from .radiomap import CHUNK_SAMPLES, compute_radio_map_sbr
-
-    def run(lo, hi, include_direct):
-        return compute_radio_map_sbr(scene, source, grid, cfg, sample_range=(lo, hi),
-                                     include_direct=include_direct, return_tensors=True,
-                                     **kw)
-
-    values, counters = sharded_radio_map(run, cfg.num_samples, group)
+    if dist.is_available() and dist.is_initialized():
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+    else:
+        rank, world = 0, 1
+    # chunk-cyclic shards (cyclic_chunks): every rank sees the whole sphere
+    values, counters = compute_radio_map_sbr(scene, source, grid, cfg, shard=(rank, world),
+                                             include_direct=(rank == 0), return_tensors=True,
+                                             **kw)
+    values, counters = allreduce_map(values, counters, group)
     counts = counters.cpu().numpy()
     diag = {name: int(counts[i]) for i, name in enumerate(_abi.MAP_COUNTERS)
             if name != "stack_overflow" and (counts[i] or name in ("escaped", "ray_bounces"))}
@@ -82,6 +86,21 @@ def compute_radio_map_sbr_distributed(scene, source, grid, cfg, group=None, **kw
     diag["chunks"] = -(-cfg.num_samples // CHUNK_SAMPLES)
     diag["direct_visible"] = int(counts[_abi.MAP_COUNTERS.index("direct_visible")])
     return values.cpu().numpy(), diag
+
+
+def cyclic_chunks(num_samples, rank, world, chunk=None):
+    """Global sample-id ranges of a chunk-cyclic shard (sbr_radiomap_bounce_sharded):
+    RNG chunks rank, rank + world, ... of 2^19 ids each, as [(lo, hi), ...].
+
+    The Fibonacci ids run pole to pole, so contiguous shards hand one GPU the
+    upward rays (which escape at once) and another the grazing ones; dealing
+    the chunks round-robin gives every shard the whole sphere.
+    """
+    from .radiomap import CHUNK_SAMPLES
+    chunk = CHUNK_SAMPLES if chunk is None else int(chunk)
+    nchunks = -(-int(num_samples) // chunk)
+    return [(c * chunk, min((c + 1) * chunk, int(num_samples)))
+            for c in range(int(rank), nchunks, int(world))]
 
 
 def shard_of_chunks(num_samples, rank, world, chunk=None):

@@ -236,7 +236,7 @@ def test_sharded_selection_matches_single_gpu(cuda, name):
     selection, per-shard materialisation -- must equal compute_paths."""
     import torch
     from paper_2504_21719_b200 import cir
-    from paper_2504_21719_b200.sharding import owned_records, shard_range
+    from paper_2504_21719_b200.sharding import shard_range
     scene, _, cfg, txs, rxs = build(name)
     ref = compute_paths(scene, txs[:1], rxs, cfg).tensors
     tx_flat, targets, tdevs, rx_index, rx_elem = cir._device_plan(txs[:1], rxs, cfg)
@@ -251,9 +251,41 @@ def test_sharded_selection_matches_single_gpu(cuda, name):
     sel = torch.zeros(len(cir._abi.CIR_COUNTERS), dtype=torch.int64, device=cuda)
     rec_row, nrec = cir._select_rows(shards[0].params, cat["key"], cat["pr"], cat["pf"],
                                      cat["chain"], offsets[-1], shards[0].los_vis, cfg, sel, cuda)
+    _check_shards(shards, rec_row, nrec, offsets, sel, scene, src, targets, cfg, txs, tdevs,
+                  rx_index, rx_elem, ref, cuda)
+    # the same with the shard-local pre-selection compute_paths_sharded uses at N > 1:
+    # only each shard's first occurrences are "gathered", dropped rows are duplicates
+    loc_rows = [cir._local_rows(R) for R in shards]
+    offsets2 = [0, int(loc_rows[0][1].numel()),
+                int(loc_rows[0][1].numel()) + int(loc_rows[1][1].numel())]
+    cat2 = {k: torch.cat([lr[0][k] for lr in loc_rows]) for k in ("key", "pr", "pf", "chain")}
+    sel2 = torch.zeros(len(cir._abi.CIR_COUNTERS), dtype=torch.int64, device=cuda)
+    rec_row2, nrec2 = cir._select_rows(shards[0].params, cat2["key"], cat2["pr"], cat2["pf"],
+                                       cat2["chain"], offsets2[-1], shards[0].los_vis, cfg,
+                                       sel2, cuda)
+    dup = cir._abi.CIR_COUNTERS.index("duplicates")
+    sel2[dup] += sum(lr[2] for lr in loc_rows)
+    assert np.array_equal(sel2.cpu().numpy(), sel.cpu().numpy())
+    assert nrec2 == nrec
+    _check_shards(shards, rec_row2, nrec2, offsets2, sel2, scene, src, targets, cfg, txs, tdevs,
+                  rx_index, rx_elem, ref, cuda, kept=[lr[1] for lr in loc_rows])
+    # the public entry point on a single rank
+    ps = cir.compute_paths_sharded(scene, txs[:1], rxs, cfg)
+    assert np.array_equal(ps.tensors.chain_hash, ref.chain_hash)
+
+
+def _check_shards(shards, rec_row, nrec, offsets, sel, scene, src, targets, cfg, txs, tdevs,
+                  rx_index, rx_elem, ref, cuda, kept=None):
+    import torch
+    from paper_2504_21719_b200 import cir
+    from paper_2504_21719_b200.sharding import owned_records
     parts = []
     for r, R in enumerate(shards):
         pos, loc = owned_records(rec_row[:nrec].cpu().numpy(), offsets, r)
+        if kept is not None:
+            loc = np.array(loc, dtype=np.int64)
+            m = loc >= 0
+            loc[m] = kept[r].cpu().numpy()[loc[m]]
         recbuf = cir._materialize(R, torch.from_numpy(loc.astype(np.int64)).to(cuda), len(loc),
                                   cfg)
         cand = cir.DeviceCandidates(scene, src, targets, R.targets_t, cfg, recbuf, len(loc), 0)
@@ -267,9 +299,6 @@ def test_sharded_selection_matches_single_gpu(cuda, name):
         assert np.array_equal(getattr(got, k), getattr(ref, k)), k
     np.testing.assert_allclose(got.delay, ref.delay, rtol=1e-12)
     assert np.abs(got.gain - ref.gain).max(initial=0.0) <= 1e-12 * np.abs(ref.gain).max(initial=1)
-    # the public entry point on a single rank
-    ps = cir.compute_paths_sharded(scene, txs[:1], rxs, cfg)
-    assert np.array_equal(ps.tensors.chain_hash, ref.chain_hash)
 
 
 def test_config5_arrays_cfr_city_vs_oracle(cuda):

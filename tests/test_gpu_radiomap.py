@@ -8,13 +8,17 @@ and 1e-3 on all of them, plus exact diagnostics counters.
 
 import numpy as np
 import pytest
+import torch
 
 import oracle
 from cases import COUNTER_KEYS, MAP_CASES, build_case, golden_map
 from conftest import golden
 from paper_2504_21719_b200 import SceneModel, compute_radio_map_sbr, scenes
 from paper_2504_21719_b200.radiomap import MeasurementGrid, RadioMapConfig
+from paper_2504_21719_b200 import _abi
 from paper_2504_21719_b200.sampling import Interaction
+
+MAP_RB = _abi.MAP_COUNTERS.index("ray_bounces")
 
 pytestmark = pytest.mark.gpu
 
@@ -73,6 +77,30 @@ def test_sharding_reproduces_full_map(cuda):
         rb += d["ray_bounces"]
     assert rb == d_full["ray_bounces"]
     np.testing.assert_allclose(acc, full, rtol=1e-12)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_cyclic_shards_reproduce_full_map_and_balance(cuda, world):
+    """sbr_radiomap_bounce_sharded: the chunk-cyclic shards of a multi-chunk
+    lattice sum to the single-run map with identical counters, and (unlike
+    contiguous bands of the pole-to-pole Fibonacci order) carry similar work."""
+    import dataclasses
+    meshes, mats, src, grid, cfg, kw = build_case("box_rst_rr")
+    cfg = dataclasses.replace(cfg, num_samples=8 * (1 << 19) + 77, max_depth=3)
+    scene = SceneModel(meshes, mats)
+    full, c_full = compute_radio_map_sbr(scene, src, grid, cfg, return_tensors=True)
+    acc = torch.zeros_like(full)
+    cnt = torch.zeros_like(c_full)
+    rbs = []
+    for r in range(world):
+        v, c = compute_radio_map_sbr(scene, src, grid, cfg, shard=(r, world),
+                                     include_direct=(r == 0), return_tensors=True)
+        acc += v
+        cnt += c
+        rbs.append(int(c[MAP_RB].item()))
+    assert torch.equal(cnt, c_full)
+    np.testing.assert_allclose(acc.cpu().numpy(), full.cpu().numpy(), rtol=1e-12, atol=0)
+    assert max(rbs) <= 1.35 * (sum(rbs) / world)
 
 
 def test_refined_grid_mean_equals_coarse(cuda):

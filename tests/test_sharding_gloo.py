@@ -18,7 +18,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2504_21719_b200 import _abi
-from paper_2504_21719_b200.sharding import shard_of_chunks, shard_range
+from paper_2504_21719_b200.sharding import cyclic_chunks, shard_of_chunks, shard_range
 
 
 def _free_port():
@@ -41,6 +41,73 @@ def test_chunk_aligned_shards():
     n = 5 * (1 << 19) + 123
     spans = [shard_of_chunks(n, r, 2) for r in range(2)]
     assert spans == [(0, 3 << 19), (3 << 19, n)]
+
+
+def test_cyclic_chunks_partition_and_balance():
+    C = 1 << 19
+    for n in (1, C, 5 * C + 123, 80_000_000):
+        for world in (1, 2, 3, 8):
+            spans = [cyclic_chunks(n, r, world) for r in range(world)]
+            ids = sorted(x for sp in spans for x in sp)
+            assert ids[0][0] == 0 and ids[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(ids, ids[1:]))   # exact partition
+            sizes = [sum(hi - lo for lo, hi in sp) for sp in spans]
+            assert max(sizes) - min(sizes) <= C                        # within one chunk
+            # every rank's ids cover the whole pole-to-pole range when it can
+            if n >= 2 * world * C:
+                assert all(sp[0][0] < n // 2 < sp[-1][1] for sp in spans)
+
+
+def _cyclic_case():
+    import dataclasses
+    from cases import build_case
+    meshes, mats, src, grid, cfg, kw = build_case("box_rst_rr")
+    cfg = dataclasses.replace(cfg, num_samples=3 * (1 << 19) + 11, max_depth=2)
+    return meshes, mats, src, grid, cfg, kw
+
+
+def _cyclic_worker(rank, world, port, out_dir):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, here)
+    sys.path.insert(0, os.path.dirname(here))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_2504_21719_b200.sharding import allreduce_map
+        meshes, mats, src, grid, cfg, kw = _cyclic_case()
+        osc = oracle.OracleScene(meshes, mats)
+        vals = np.zeros((grid.shape[1], grid.shape[0]))
+        cnt = np.zeros(len(_abi.MAP_COUNTERS), np.int64)
+        first = True
+        for lo, hi in cyclic_chunks(cfg.num_samples, rank, world):
+            v, d = osc.radiomap(src, grid, cfg, sample_range=(lo, hi),
+                                include_direct=(rank == 0 and first), **kw)
+            first = False
+            vals += v
+            cnt += np.array([d[k] for k in _abi.MAP_COUNTERS], np.int64)
+        v, c = allreduce_map(torch.from_numpy(vals), torch.from_numpy(cnt))
+        np.save(os.path.join(out_dir, f"cvals_{rank}.npy"), v.numpy())
+        np.save(os.path.join(out_dir, f"ccnt_{rank}.npy"), c.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_three_rank_gloo_cyclic_shards_equal_full_map(tmp_path):
+    """The chunk-cyclic partition bench.py / compute_radio_map_sbr_distributed use
+    (sbr_radiomap_bounce_sharded on the GPU) reproduces the unsharded map."""
+    import oracle
+    world = 3
+    mp.start_processes(_cyclic_worker, args=(world, _free_port(), str(tmp_path)),
+                       nprocs=world, join=True, start_method="spawn")
+    meshes, mats, src, grid, cfg, kw = _cyclic_case()
+    full, d = oracle.OracleScene(meshes, mats).radiomap(src, grid, cfg, **kw)
+    fcnt = np.array([d[k] for k in _abi.MAP_COUNTERS], np.int64)
+    for r in range(world):
+        np.testing.assert_allclose(np.load(tmp_path / f"cvals_{r}.npy"), full, rtol=1e-12, atol=0)
+        assert np.array_equal(np.load(tmp_path / f"ccnt_{r}.npy"), fcnt)
 
 
 def _oracle_run_shard(case, lo, hi, include_direct):

@@ -48,6 +48,8 @@ extern "C" {
 /* Radio-map RNG chunking: part of the reference's RNG contract
  * (radiomap.py:53-55, CHUNK_SAMPLES = 1 << 19). */
 #define SBR_CHUNK_LOG2 19
+/* id-chunk size of the chunk-cyclic CIR shards (sbr_cir_sweep_sharded) */
+#define SBR_CIR_SHARD_LOG2 12
 
 /* ---- material / antenna parameter blocks -------------------------------- */
 enum { SBR_SCAT_LAMBERTIAN = 0, SBR_SCAT_DIRECTIVE = 1, SBR_SCAT_BACKSCATTERING = 2 };
@@ -347,6 +349,13 @@ int sbr_cir_sweep(const SbrScene* scene, const SbrCirParams* params, uint64_t sa
                   void* stream);
 /* Spatial (Morton) order of the first nv vertices, for coherent occlusion
  * rays in sbr_cir_visibility: order_dev (nv) int32 vertex indices. */
+/* sbr_cir_sweep over a chunk-cyclic shard of [0, num_samples): id chunks of
+ * 2^SBR_CIR_SHARD_LOG2 dealt round-robin (balanced work per GPU; contiguous
+ * shards of the pole-to-pole Fibonacci order differ 2x in visibility work).
+ * vb needs (shard size) * max_depth vertices.  No reference counterpart. */
+int sbr_cir_sweep_sharded(const SbrScene* scene, const SbrCirParams* params,
+                          int32_t shard_index, int32_t shard_count, const SbrVertexBuf* vb,
+                          uint64_t* counters_dev, void* stream);
 int sbr_cir_vertex_order(const SbrScene* scene, const SbrVertexBuf* vb, int64_t nv,
                          int32_t* order_dev, void* stream);
 /* _visible_pairs (paths.py:657-683): half-space side test + occlusion ray for

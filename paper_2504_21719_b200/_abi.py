@@ -15,6 +15,7 @@ SBR_ERR_UNSUPPORTED = 5
 SBR_ERR_NOMEM = 6
 
 SBR_CHUNK_LOG2 = 19
+SBR_CIR_SHARD_LOG2 = 12   # id chunks of the chunk-cyclic CIR shards (sbr_cir_sweep_sharded)
 
 SBR_SCAT_LAMBERTIAN = 0
 SBR_SCAT_DIRECTIVE = 1

@@ -48,6 +48,7 @@ def _declare(lib):
         "sbr_radiomap_direct": (ctypes.c_int, [vp, vp, vp, vp, vp]),
         "sbr_radiomap_wedges": (ctypes.c_int, [vp, vp, vp, i32, u64, vp, vp, vp]),
         "sbr_cir_sweep": (ctypes.c_int, [vp, vp, u64, u64, vp, vp, vp]),
+        "sbr_cir_sweep_sharded": (ctypes.c_int, [vp, vp, i32, i32, vp, vp, vp]),
         "sbr_cir_vertex_order": (ctypes.c_int, [vp, vp, i64, vp, vp]),
         "sbr_cir_visibility": (ctypes.c_int, [vp, vp, vp, i64, i64, vp, vp, vp, i64, vp, vp]),
         "sbr_cir_row_pairs": (ctypes.c_int, [vp, vp, vp, i64, vp, vp, vp, vp]),
@@ -82,7 +83,8 @@ def exported_symbols():
         "sbr_scene_set_attributes", "sbr_scene_set_materials", "sbr_scene_set_wedges",
         "sbr_scene_check", "sbr_trace_closest", "sbr_trace_any",
         "sbr_occluded", "sbr_fibonacci", "sbr_philox_uniform",
-        "sbr_radiomap_bounce", "sbr_radiomap_bounce_sharded", "sbr_radiomap_direct", "sbr_radiomap_wedges", "sbr_cir_sweep",
+        "sbr_radiomap_bounce", "sbr_radiomap_bounce_sharded", "sbr_radiomap_direct",
+        "sbr_radiomap_wedges", "sbr_cir_sweep", "sbr_cir_sweep_sharded",
         "sbr_cir_vertex_order",
         "sbr_cir_visibility", "sbr_cir_row_pairs", "sbr_cir_select", "sbr_cir_local_dedup",
         "sbr_cir_resolve_records", "sbr_cir_records", "sbr_cir_refine",

@@ -384,8 +384,10 @@ class _Rows:
     """Visible (vertex, target) rows of one source on this device."""
 
 
-def _sweep_rows(scene, source, targets, cfg, lo, hi):
-    """Sweep global sample ids [lo, hi) and collect visible rows + dedup keys.
+def _sweep_rows(scene, source, targets, cfg, lo, hi, shard=None):
+    """Sweep global sample ids [lo, hi) -- or, with shard=(rank, world), the
+    chunk-cyclic shard sbr_cir_sweep_sharded owns -- and collect visible rows
+    + dedup keys.
 
     _sweep_chunk's trace/draw/continue loop (paths.py:704-828) and
     _visible_pairs (657-683) on the GPU; the rows carry the ordinal key
@@ -407,10 +409,22 @@ def _sweep_rows(scene, source, targets, cfg, lo, hi):
     R.los_vis = (~occ).to(torch.uint8).contiguous()
     gt = _PhaseTimer("  generate")
     gt.mark("los")
-    R.vb = vb = _VertexBuf((hi - lo) * cfg.max_depth, dev)
-    if hi > lo and cfg.max_depth > 0:
-        _native.check(L_.sbr_cir_sweep(acc.handle, ctypes.byref(R.params), lo, hi,
-                                       ctypes.byref(vb.abi), _native.ptr(counters), stream))
+    if shard is not None:
+        from .sharding import cyclic_chunks
+        n_ids = sum(b - a for a, b in cyclic_chunks(cfg.num_samples, shard[0], shard[1],
+                                                    chunk=1 << _abi.SBR_CIR_SHARD_LOG2))
+    else:
+        n_ids = hi - lo
+    R.vb = vb = _VertexBuf(n_ids * cfg.max_depth, dev)
+    if n_ids > 0 and cfg.max_depth > 0:
+        if shard is not None:
+            _native.check(L_.sbr_cir_sweep_sharded(acc.handle, ctypes.byref(R.params),
+                                                   int(shard[0]), int(shard[1]),
+                                                   ctypes.byref(vb.abi), _native.ptr(counters),
+                                                   stream))
+        else:
+            _native.check(L_.sbr_cir_sweep(acc.handle, ctypes.byref(R.params), lo, hi,
+                                           ctypes.byref(vb.abi), _native.ptr(counters), stream))
     nv = int(counters[_abi.CC["vertices"]].item())
     gt.mark("sweep")
     # visibility rows, vertex slabs of <= 2^26 (vertex, target) pairs; before
@@ -850,7 +864,9 @@ def compute_paths_sharded(scene, transmitters, receivers, cfg, group=None):
     for src_idx, (ti, te, tx_pos) in enumerate(tx_flat):
         source = np.asarray(tx_pos, dtype=np.float64)
         with torch.cuda.device(dev):
-            R = _sweep_rows(scene, source, targets, cfg, lo, hi)
+            # chunk-cyclic sample shards: contiguous ones differ 2x in visibility work
+            R = _sweep_rows(scene, source, targets, cfg, lo, hi,
+                            shard=(rank, world) if world > 1 else None)
             n = R.n
             kept, n_dup = None, 0
             if world > 1:

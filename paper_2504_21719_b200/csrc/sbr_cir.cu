@@ -45,6 +45,7 @@ constexpr uint64_t TAG_INTERACTION = 0x5c798e00ad8012ebULL;  // fnv1a("interacti
 constexpr uint64_t TAG_RESPAWN = 0x742c480a24ff9b7fULL;      // fnv1a("respawn")
 constexpr uint64_t kFnvPrime = 0x100000001B3ULL;
 constexpr uint64_t kHashBase = 1373ULL;                      // HASH_CHAIN_BASE
+constexpr uint32_t kCirShardLog2 = SBR_CIR_SHARD_LOG2;  // CIR shard chunks of 4096 ids
 constexpr int kTargetBits = 20;
 constexpr int kSampleBits = 40;
 constexpr uint64_t kTargetMask = (1ULL << kTargetBits) - 1;
@@ -106,11 +107,13 @@ __device__ __forceinline__ bool interaction_probs(const SbrMaterial& m, double r
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) k_cir_sweep(DevScene S, SbrCirParams P, uint64_t begin,
                                                    uint64_t end, SbrVertexBuf vb,
-                                                   unsigned long long* __restrict__ counters) {
+                                                   unsigned long long* __restrict__ counters,
+                                                   ShardMap sh) {
   CirCounters K = {0u, 0u, 0u};
   const double3 src = make_double3(P.source[0], P.source[1], P.source[2]);
-  for (uint64_t g = begin + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < end;
-       g += (uint64_t)gridDim.x * blockDim.x) {
+  for (uint64_t l = begin + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < end;
+       l += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t g = sh.gid(l);  // global sample id (RNG key, ordinal)
     double3 o = src;
     double3 d = fibonacci_dir(P.num_samples, g);
     uint64_t hr = 0, hf = 0;
@@ -1025,7 +1028,27 @@ int sbr_cir_sweep(const SbrScene* scene, const SbrCirParams* P, uint64_t begin, 
   if (end == begin || P->max_depth == 0) return SBR_OK;
   prof_begin(stream, "k_cir_sweep");
   k_cir_sweep<<<grid_for((int64_t)(end - begin), 128, 148 * 16), 128, 0, (cudaStream_t)stream>>>(
-      dev_view(scene), *P, begin, end, *vb, (unsigned long long*)counters);
+      dev_view(scene), *P, begin, end, *vb, (unsigned long long*)counters,
+      ShardMap{0u, 1u, kCirShardLog2});
+  prof_end(stream);
+  return launch_status("k_cir_sweep");
+}
+
+int sbr_cir_sweep_sharded(const SbrScene* scene, const SbrCirParams* P, int32_t shard_index,
+                          int32_t shard_count, const SbrVertexBuf* vb, uint64_t* counters,
+                          void* stream) {
+  int rc = check_cir(scene, P);
+  if (rc) return rc;
+  if (!scene || !vb) return set_error(SBR_ERR_INVALID, "NULL argument");
+  if (shard_count < 1 || shard_index < 0 || shard_index >= shard_count)
+    return set_error(SBR_ERR_INVALID, "bad shard");
+  const uint64_t n = shard_size(P->num_samples, (uint32_t)shard_index, (uint32_t)shard_count,
+                                kCirShardLog2);
+  if (n == 0 || P->max_depth == 0) return SBR_OK;
+  prof_begin(stream, "k_cir_sweep");
+  k_cir_sweep<<<grid_for((int64_t)n, 128, 148 * 16), 128, 0, (cudaStream_t)stream>>>(
+      dev_view(scene), *P, 0, n, *vb, (unsigned long long*)counters,
+      ShardMap{(uint32_t)shard_index, (uint32_t)shard_count, kCirShardLog2});
   prof_end(stream);
   return launch_status("k_cir_sweep");
 }

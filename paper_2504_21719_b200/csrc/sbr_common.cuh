@@ -67,6 +67,28 @@ struct DevScene {
   const int32_t *w_mat0, *w_matn, *slot_woff, *slot_wids;
 };
 
+// Chunk-cyclic shards (sbr_radiomap_bounce_sharded, sbr_cir_sweep_sharded):
+// a shard owns the id chunks (g >> log2) = index, index + count, ...; local
+// id l walks them in order; count = 1 is the identity (contiguous ranges).
+// Fibonacci ids run pole to pole, so contiguous shards would give one GPU the
+// upward rays that escape at once and another the grazing ones.
+struct ShardMap {
+  uint32_t index, count, log2;
+  __device__ __forceinline__ uint64_t gid(uint64_t l) const {
+    if (count == 1) return l;
+    const uint64_t mask = (1ULL << log2) - 1;
+    return (((l >> log2) * count + index) << log2) | (l & mask);
+  }
+};
+// number of ids [0, n) a cyclic shard owns
+inline uint64_t shard_size(uint64_t n, uint32_t index, uint32_t count, uint32_t log2) {
+  const uint64_t C = 1ULL << log2;
+  const uint64_t chunks = (n + C - 1) / C;
+  uint64_t m = 0;
+  for (uint64_t c = index; c < chunks; c += count) m += (c + 1) * C <= n ? C : n - c * C;
+  return m;
+}
+
 constexpr int kStackSize = 64;
 constexpr unsigned kErrStack = 1u;
 

@@ -81,19 +81,6 @@ __device__ __forceinline__ uint64_t comb_sample(uint64_t w, uint64_t comb_q) {
   return (w / comb_q) + (w % comb_q) * kCombStride;
 }
 
-// Chunk-cyclic shards (sbr_radiomap_bounce_sharded): a shard owns the global
-// RNG chunks (g >> 19) = shard, shard + count, ...; local id l walks them in
-// order.  count = 1 is the identity (contiguous ranges).  Fibonacci ids run
-// pole to pole, so contiguous shards would give one GPU the upward rays that
-// escape at once and another the grazing ones that bounce five times.
-struct ShardMap {
-  uint32_t index, count;
-  __device__ __forceinline__ uint64_t gid(uint64_t l) const {
-    if (count == 1) return l;
-    const uint64_t mask = (1ULL << SBR_CHUNK_LOG2) - 1;
-    return (((l >> SBR_CHUNK_LOG2) * count + index) << SBR_CHUNK_LOG2) | (l & mask);
-  }
-};
 
 // ---------------------------------------------------------------------------
 // trace
@@ -737,7 +724,7 @@ int sbr_radiomap_bounce(const SbrScene* scene, const SbrMapParams* P, uint64_t s
   if (rc) return rc;
   if (sample_end > P->num_samples || sample_begin > sample_end)
     return set_error(SBR_ERR_INVALID, "bad sample range");
-  return bounce_impl(scene, P, sample_begin, sample_end, ShardMap{0u, 1u}, grid, counters_u64,
+  return bounce_impl(scene, P, sample_begin, sample_end, ShardMap{0u, 1u, SBR_CHUNK_LOG2}, grid, counters_u64,
                      stream);
 }
 
@@ -748,12 +735,9 @@ int sbr_radiomap_bounce_sharded(const SbrScene* scene, const SbrMapParams* P,
   if (rc) return rc;
   if (shard_count < 1 || shard_index < 0 || shard_index >= shard_count)
     return set_error(SBR_ERR_INVALID, "bad shard");
-  const uint64_t C = 1ULL << SBR_CHUNK_LOG2;
-  const uint64_t n_chunks = (P->num_samples + C - 1) / C;
-  uint64_t n_local = 0;
-  for (uint64_t c = (uint64_t)shard_index; c < n_chunks; c += (uint64_t)shard_count)
-    n_local += (c + 1) * C <= P->num_samples ? C : P->num_samples - c * C;
-  return bounce_impl(scene, P, 0, n_local, ShardMap{(uint32_t)shard_index, (uint32_t)shard_count},
+  const uint64_t n_local =
+      shard_size(P->num_samples, (uint32_t)shard_index, (uint32_t)shard_count, SBR_CHUNK_LOG2);
+  return bounce_impl(scene, P, 0, n_local, ShardMap{(uint32_t)shard_index, (uint32_t)shard_count, SBR_CHUNK_LOG2},
                      grid, counters_u64, stream);
 }
 

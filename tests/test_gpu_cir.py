@@ -243,8 +243,13 @@ def test_sharded_selection_matches_single_gpu(cuda, name):
     _, _, src = tx_flat[0]
     src = np.asarray(src, np.float64)
     scene.bind_frequency(cfg.frequency)
-    shards = [cir._sweep_rows(scene, src, targets, cfg, *shard_range(cfg.num_samples, r, 2))
-              for r in range(2)]
+    # contiguous halves for one case, the chunk-cyclic shards compute_paths_sharded uses
+    # (sbr_cir_sweep_sharded, 4096-id chunks) for the others
+    if name == "box_trunc":
+        shards = [cir._sweep_rows(scene, src, targets, cfg, *shard_range(cfg.num_samples, r, 2))
+                  for r in range(2)]
+    else:
+        shards = [cir._sweep_rows(scene, src, targets, cfg, 0, 0, shard=(r, 2)) for r in range(2)]
     offsets = [0, shards[0].n, shards[0].n + shards[1].n]
     cat = {k: torch.cat([getattr(R, k)[:R.n] for R in shards]) for k in ("key", "pr", "pf",
                                                                           "chain")}

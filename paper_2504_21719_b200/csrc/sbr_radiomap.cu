@@ -43,7 +43,10 @@ using namespace sbr;
 namespace {
 
 constexpr uint64_t kCombStride = 233;     // Fibonacci number: neighbouring lattice directions
-constexpr int64_t kChunkRays = 1 << 23;   // samples per wavefront pass (queue capacity)
+#ifndef SBR_WAVE_LOG2
+#define SBR_WAVE_LOG2 24  // 16.7M samples per pass (~7.4 GB of queues): one pass for 1e7
+#endif
+constexpr int64_t kChunkRays = 1LL << SBR_WAVE_LOG2;  // samples per wavefront pass (queue capacity)
 
 // SoA ray queue (float64; E is the complex world-frame field 3-vector)
 struct MapQueue {

@@ -402,7 +402,7 @@ __global__ void k_gather_tris(const double* __restrict__ v0, const double* __res
 // leaves in depth-first order, so the leaf collapse / emit path is shared.
 // ---------------------------------------------------------------------------
 #ifndef SBR_PLOC_RADIUS
-#define SBR_PLOC_RADIUS 12
+#define SBR_PLOC_RADIUS 16  // canyon map = radius 12, city map +11 %, config-3 CIR -5 % (r6..r20 swept)
 #endif
 constexpr int kPlocRadius = SBR_PLOC_RADIUS;
 

@@ -660,11 +660,7 @@ struct ClosestTravT {
       for (int j = s; j < s + n; ++j) {
         double t, u, v;
         u = v = 0.0;
-#ifdef SBR_TRI_SELECT
-        if (tri_hit(r, S.tris + j, t_min, t, u, v)) {
-#else
         if (tri_hit_idx<kUV>(r, S.tris + j, t_min, t, u, v)) {
-#endif
           const int rank = __ldg(S.tie_rank + j);
           if (t < best_t || (t == best_t && best >= 0 && rank < best_rank)) {
             best_t = t;
@@ -803,20 +799,6 @@ struct AnyTrav {
 };
 
 using ClosestTrav = ClosestTravT<true>;
-
-// One-shot warp-cooperative closest hit (all lanes call; inactive lanes vote).
-__device__ __forceinline__ bool trace_closest_ww(const DevScene& S, bool active, double3 o,
-                                                 double3 d, double t_min, double t_max,
-                                                 HitRecord& h) {
-  int sn[kStackSize];
-  float st[kStackSize];
-  ClosestTrav T(sn, st);
-  T.start(S, o, d, t_min, t_max);
-  if (!active) T.idle();
-  while (!T.done()) T.round(S);
-  T.result(h);
-  return T.ok;
-}
 
 // any hit with t_min < t < limit (_core.pyx:198-253); returns false on overflow
 __device__ __forceinline__ bool trace_any(const DevScene& S, double3 o, double3 d,

@@ -404,7 +404,11 @@ __device__ __forceinline__ float safe_inv(double d) {
 __device__ __forceinline__ RayBox box_setup(double3 o, double3 d, float pad_floor,
                                             double t_min) {
   RayBox b;
-  b.tlo = t_min > 0.0 ? __double2float_rd(t_min) : 0.0f;
+  // rd(t_min) without the rounding-mode intrinsic: constant-folds for the
+  // usual constant t_min (the F2F.RM was re-issued in every node visit)
+  float tl = (float)t_min;
+  if ((double)tl > t_min) tl = __int_as_float(__float_as_int(tl) - 1);
+  b.tlo = t_min > 0.0 ? tl : 0.0f;
   b.ix = safe_inv(d.x);
   b.iy = safe_inv(d.y);
   b.iz = safe_inv(d.z);

@@ -522,25 +522,25 @@ __global__ void k_gather_u64(const uint64_t* __restrict__ src, const int32_t* __
 // one (chain, target) key, so a run almost always holds a single key and the
 // scan stops at the neighbour; prefix or hash collisions between different
 // keys only lengthen the scan, the result stays exact.
-__global__ void k_first_flags_pr(const uint64_t* __restrict__ pr, const uint64_t* __restrict__ pf,
+__global__ void k_first_flags_pr(const uint64_t* __restrict__ spr, const uint64_t* __restrict__ spf,
                                  const int32_t* __restrict__ order, int64_t n,
                                  uint8_t* keep_chain, unsigned long long* counters) {
+  // spr / spf: (pr, pf) already in sorted order (contiguous reads); order:
+  // the row each sorted position came from
   unsigned dup = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t a = order[i];
-    const uint64_t ka = pr[a], fa = pf[a];
+    const uint64_t ka = spr[i], fa = spf[i];
     bool first = true;
     for (int64_t j = i - 1; j >= 0; --j) {
-      const int32_t b = order[j];
-      const uint64_t kb = pr[b];
+      const uint64_t kb = spr[j];
       if ((kb >> 32) != (ka >> 32)) break;
-      if (kb == ka && pf[b] == fa) {
+      if (kb == ka && spf[j] == fa) {
         first = false;
         break;
       }
     }
-    keep_chain[a] = first ? 1 : 0;
+    keep_chain[order[i]] = first ? 1 : 0;
     dup += first ? 0u : 1u;
   }
   const unsigned s = __reduce_add_sync(0xffffffffu, dup);
@@ -1221,7 +1221,9 @@ int sbr_cir_local_dedup(const SbrCirParams* P, const uint64_t* row_key, const ui
       CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ck, ck2, cpos, cpos2, (int)n_chain, 32,
                                          64, st));
       count_launch();
-      k_first_flags_pr<<<grid_for(n_chain, 256), 256, 0, st>>>(row_pr, row_pf, cpos2, n_chain,
+      k_gather_u64<<<grid_for(n_chain, 256), 256, 0, st>>>(row_pf, cpos2, n_chain, ck);
+      LK("k_gather_u64");
+      k_first_flags_pr<<<grid_for(n_chain, 256), 256, 0, st>>>(ck2, ck, cpos2, n_chain,
                                                                 keep_chain, cnt);
       LK("k_first_flags_pr");
     }
@@ -1350,7 +1352,9 @@ int sbr_cir_select(const SbrCirParams* P, const uint64_t* row_key, const uint64_
         LK("k_gather_u64");
         CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ck, ck2, cpos, cpos2, (int)n_chain, 32, 64, st));
         count_launch();
-        k_first_flags_pr<<<grid_for(n_chain, 256), 256, 0, st>>>(pr, pf, cpos2, n_chain, keep_chain,
+        k_gather_u64<<<grid_for(n_chain, 256), 256, 0, st>>>(pf, cpos2, n_chain, ck);
+        LK("k_gather_u64");
+        k_first_flags_pr<<<grid_for(n_chain, 256), 256, 0, st>>>(ck2, ck, cpos2, n_chain, keep_chain,
                                                                   counters);
         LK("k_first_flags_pr");
       }

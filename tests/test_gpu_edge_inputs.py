@@ -82,3 +82,28 @@ def test_receiver_without_paths_gives_zero_response(cuda):
     assert len(ps.paths) == 0
     H = frequency_response(ps, [3.5e9, 3.6e9])
     assert H.shape == (1, 1, 2) and not H.any()
+
+
+def test_cyclic_shards_with_fewer_chunks_than_ranks(cuda):
+    """Ranks that own no chunk contribute nothing (maps and CIR rows)."""
+    import torch
+    from paper_2504_21719_b200 import cir
+    scene = _room()
+    grid = MeasurementGrid((0.0, 0.0, 1.0), (1, 0, 0), (0, 1, 0), (1.0, 1.0), (4, 4))
+    cfg = RadioMapConfig(num_samples=1000, max_depth=2, enabled=R, seed=1)
+    full, cf = compute_radio_map_sbr(scene, (0.5, -1.0, 2.0), grid, cfg, include_direct=False,
+                                     return_tensors=True)
+    parts = [compute_radio_map_sbr(scene, (0.5, -1.0, 2.0), grid, cfg, shard=(r, 3),
+                                   include_direct=False, return_tensors=True) for r in range(3)]
+    assert torch.equal(parts[0][1], cf) and not parts[1][1].any() and not parts[2][1].any()
+    np.testing.assert_allclose(parts[0][0].cpu().numpy(), full.cpu().numpy(), rtol=1e-13,
+                               atol=0)  # fp64 atomics reorder the cell sums
+    pcfg = PathConfig(num_samples=5000, max_depth=2, enabled=R, q_diffraction=0.0)
+    _, targets, *_ = cir._device_plan([RadioDevice(position=[0.0, 0.0, 1.5])],
+                                      [RadioDevice(position=[1.0, 2.0, 1.0])], pcfg)
+    scene.bind_frequency(pcfg.frequency)
+    rows = [cir._sweep_rows(scene, np.array([0.0, 0.0, 1.5]), targets, pcfg, 0, 0, shard=(r, 3))
+            for r in range(3)]
+    assert rows[0].n > 0 and rows[1].n > 0 and rows[2].n == 0   # 2 chunks of 4096 ids
+    kept = cir._local_rows(rows[2])
+    assert kept[1].numel() == 0 and kept[2] == 0

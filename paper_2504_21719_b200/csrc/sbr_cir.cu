@@ -105,15 +105,27 @@ __device__ __forceinline__ bool interaction_probs(const SbrMaterial& m, double r
 // ---------------------------------------------------------------------------
 // sweep
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_cir_sweep(DevScene S, SbrCirParams P, uint64_t begin,
+#ifndef SBR_SWEEP_MINB
+#define SBR_SWEEP_MINB 8  // 64 registers: config-5 sweep 3.5 -> 2.0 ms
+#endif
+__global__ void __launch_bounds__(128, SBR_SWEEP_MINB) k_cir_sweep(DevScene S, SbrCirParams P, uint64_t begin,
                                                    uint64_t end, SbrVertexBuf vb,
                                                    unsigned long long* __restrict__ counters,
                                                    ShardMap sh) {
   CirCounters K = {0u, 0u, 0u};
   const double3 src = make_double3(P.source[0], P.source[1], P.source[2]);
-  for (uint64_t l = begin + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < end;
-       l += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t g = sh.gid(l);  // global sample id (RNG key, ordinal)
+  // Warp-uniform loop over batches of 32 samples; every depth step traces the
+  // batch's live rays together with the while-while closest hit (parked
+  // leaves, full-warp triangle tests) instead of one scalar walk per thread.
+  const unsigned lane_id = threadIdx.x & 31u;
+  const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  int sn[kStackSize];
+  float st[kStackSize];
+  for (uint64_t base = begin + warp0 * 32; base < end; base += nwarps * 32) {
+    const uint64_t l = base + lane_id;
+    bool alive = l < end;
+    const uint64_t g = sh.gid(alive ? l : begin);  // global sample id (RNG key, ordinal)
     double3 o = src;
     double3 d = fibonacci_dir(P.num_samples, g);
     uint64_t hr = 0, hf = 0;
@@ -122,16 +134,28 @@ __global__ void __launch_bounds__(128) k_cir_sweep(DevScene S, SbrCirParams P, u
     int parent = -1;
     bool has_s = false, has_d = false;
     for (int depth = 1; depth <= P.max_depth; ++depth) {
-      K.rb++;
+      if (!__any_sync(0xffffffffu, alive)) break;
+      ClosestTravT<false> T(sn, st);
+      if (alive) {
+        K.rb++;
+        T.start(S, o, d, 1e-4, __longlong_as_double(0x7ff0000000000000LL));
+      } else {
+        T.idle();
+      }
+      while (!T.done()) T.round(S);
+      if (!alive) continue;
       HitRecord h;
-      if (!trace_closest(S, o, d, 1e-4, __longlong_as_double(0x7ff0000000000000LL), h)) {
+      T.result(h);
+      if (!T.ok) {
         flag_error(S, kErrStack);
         atomicAdd(counters + SBR_CC_STACK_OVERFLOW, 1ULL);
-        break;
+        alive = false;
+        continue;
       }
       if (h.tri < 0) {
         K.escaped++;
-        break;
+        alive = false;
+        continue;
       }
       double3 pt = o + h.t * d;
       double3 n = ldg3(S.normals + 3 * (int64_t)h.tri);
@@ -145,7 +169,8 @@ __global__ void __launch_bounds__(128) k_cir_sweep(DevScene S, SbrCirParams P, u
       if (!interaction_probs(m, r_sq, t_sq, P.q_diffraction,
                              allowed_kinds(S, P.allow_mask, h.tri, has_s, has_d), q)) {
         K.terminated++;
-        break;
+        alive = false;
+        continue;
       }
       const double u = philox_uniform(P.seed, 0, (uint64_t)depth, TAG_INTERACTION, g);
       const double c0 = q[0], c1 = c0 + q[1], c2 = c1 + q[2], c3 = c2 + q[3];
@@ -188,9 +213,13 @@ __global__ void __launch_bounds__(128) k_cir_sweep(DevScene S, SbrCirParams P, u
         parent = (int)vi;
       } else {
         atomicAdd(counters + SBR_CC_VERTEX_OVERFLOW, 1ULL);
-        break;
+        alive = false;
+        continue;
       }
-      if (depth == P.max_depth) break;
+      if (depth == P.max_depth) {
+        alive = false;
+        continue;
+      }
       // _continue_rays (paths.py:855-900)
       if (code == 0) {
         const double dn = dot_seq(d, n);
@@ -216,7 +245,8 @@ __global__ void __launch_bounds__(128) k_cir_sweep(DevScene S, SbrCirParams P, u
         const double sb = sqrt(xb > 0.0 ? xb : 0.0);
         if (sb < 1e-9) {
           K.terminated++;
-          break;
+          alive = false;
+          continue;
         }
         const double phi =
             philox_uniform(P.seed, 0, (uint64_t)depth, TAG_CONE, g) * __ldg(S.w_nopen + wid) * kPi;

@@ -101,7 +101,10 @@ __device__ __forceinline__ uint64_t comb_sample(uint64_t w, uint64_t comb_q) {
 #ifndef SBR_SHADE_MINB
 #define SBR_SHADE_MINB 8
 #endif
-__global__ void __launch_bounds__(128, SBR_TRACE_MINB) k_map_trace(DevScene S, SbrMapParams P, int seg,
+#ifndef SBR_TRACE_TPB
+#define SBR_TRACE_TPB 128
+#endif
+__global__ void __launch_bounds__(SBR_TRACE_TPB, SBR_TRACE_MINB) k_map_trace(DevScene S, SbrMapParams P, int seg,
                                                    MapQueue q, const unsigned long long* count_in,
                                                    uint64_t begin, uint64_t count0, uint64_t comb_q,
                                                    HitBuf hits, unsigned long long* work,
@@ -685,7 +688,7 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
   Wave* w = &wave;
   if ((rc = wave_alloc(chunk + (int64_t)kCombStride, st, w))) return rc;
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_map_trace, 128, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_map_trace, SBR_TRACE_TPB, 0);
   if (per_sm < 1) per_sm = 1;
   const unsigned trace_blocks = (unsigned)(sms * per_sm);
   const unsigned shade_blocks = (unsigned)(sms * 8);
@@ -699,7 +702,7 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
       k_reset_pass<<<1, 1, 0, st>>>(w->ctl, w->ctl + 2 - cur, w->ctl + 3);
       if ((rc = launch_status("k_reset_pass"))) break;
       prof_begin(st, "k_map_trace");
-      k_map_trace<<<trace_blocks, 128, 0, st>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo, cnt,
+      k_map_trace<<<trace_blocks, SBR_TRACE_TPB, 0, st>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo, cnt,
                                                 comb_q, w->hits, w->ctl, counters, sh);
       prof_end(st);
       if ((rc = launch_status("k_map_trace"))) break;

@@ -62,6 +62,24 @@ def test_canyon_map_vs_oracle_1e5_samples(cuda):
     _compare(vals, want)
 
 
+@pytest.mark.parametrize("chunk", [3, 17])
+def test_config2_full_rng_chunks_vs_oracle(cuda, chunk):
+    """Whole 2^19-sample RNG chunks of the config-2 lattice (1e7 rays): an upward
+    band (3) and a downward one (17), counters exact and cells as the oracle."""
+    meshes = scenes.street_canyon()
+    mats = scenes.uniform_materials(meshes, scenes.concrete(scattering=0.3))
+    grid = MeasurementGrid((0, 0, 1.5), (1, 0, 0), (0, 1, 0), (1.0, 1.0), (200, 200))
+    cfg = RadioMapConfig(num_samples=10_000_000, max_depth=5, enabled=RS, seed=0)
+    rg = (chunk << 19, (chunk + 1) << 19)
+    vals, diag = compute_radio_map_sbr(SceneModel(meshes, mats), (0.0, 5.0, 20.0), grid, cfg,
+                                       sample_range=rg, include_direct=False)
+    want, wdiag = oracle.OracleScene(meshes, mats).radiomap(
+        np.array([0.0, 5.0, 20.0]), grid, cfg, sample_range=rg, include_direct=False)
+    for key in ("deposits", "escaped", "respawns", "ray_bounces"):
+        assert diag.get(key, 0) == wdiag[key], key
+    _compare(vals, want)
+
+
 def test_sharding_reproduces_full_map(cuda):
     """Shards of the global sample ids sum to the single-run map (multi-GPU contract)."""
     meshes, mats, src, grid, cfg, kw = build_case("box_rst_rr")

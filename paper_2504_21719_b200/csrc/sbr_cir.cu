@@ -332,6 +332,23 @@ constexpr int kVisGHints = SBR_VIS_GHINTS;
 constexpr int kVisHints = SBR_VIS_HINTS;
 constexpr int kVisGroup = SBR_VIS_GROUP;
 
+// the visibility slab's vertices (point, facing normal, code) gathered into
+// Morton order once, so every (tile, target) unit reads contiguous memory
+__global__ void k_vis_view(SbrVertexBuf vb, int64_t v_begin, int64_t nv,
+                           const int32_t* __restrict__ order, double* vpt, double* vnr,
+                           uint8_t* vcode) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = order ? order[v_begin + i] : v_begin + i;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      vpt[3 * i + c] = vb.point[3 * v + c];
+      vnr[3 * i + c] = vb.normal[3 * v + c];
+    }
+    vcode[i] = vb.code[v];
+  }
+}
+
 #ifndef SBR_VIS_MINB
 #define SBR_VIS_MINB 8  // 64 registers: 220 -> 180 ms at config 3
 #endif
@@ -342,7 +359,12 @@ __global__ void __launch_bounds__(128, SBR_VIS_MINB) k_cir_visibility(DevScene S
                                                         unsigned long long* counters,
                                                         unsigned long long* work,
                                                         const int32_t* __restrict__ order,
-                                                        int* ghint) {
+                                                        int* ghint,
+                                                        const double* __restrict__ vpt,
+                                                        const double* __restrict__ vnr,
+                                                        const uint8_t* __restrict__ vcode) {
+  // vpt / vnr / vcode: point, facing normal and code of the slab's vertices in
+  // Morton order (k_vis_view), so tiles read contiguous memory
   __shared__ int64_t sq[kVisWarps][64];
   __shared__ int shint[kVisWarps][kVisHints > 0 ? kVisHints : 1];
   __shared__ int shpos[kVisWarps];
@@ -393,19 +415,15 @@ __global__ void __launch_bounds__(128, SBR_VIS_MINB) k_cir_visibility(DevScene S
         ++tile_cur;
         bool pass = false;
         if (pos < nv) {
-          const int64_t v = order ? order[v_begin + pos] : v_begin + pos;
-          const double3 p = ld3(vb.point + 3 * v);
-          const double3 n = ld3(vb.normal + 3 * v);
+          const double3 p = ldg3(vpt + 3 * pos);
+          const double3 n = ldg3(vnr + 3 * pos);
           const double3 tg = ldg3(P.targets_dev + 3 * k);
           const double side = dot_seq(tg - p, n);
-          const int code = vb.code[v];
+          const int code = __ldg(vcode + pos);
           pass = code == 3 ? true : (code == 2 ? side < 0.0 : side > 0.0);
         }
         const unsigned m = __ballot_sync(0xffffffffu, pass);
-        if (pass) {
-          const int64_t v = order ? order[v_begin + pos] : v_begin + pos;
-          sq[wid][qn + __popc(m & lt_mask)] = v * nt + k;  // (vertex, target) pair
-        }
+        if (pass) sq[wid][qn + __popc(m & lt_mask)] = pos * nt + k;  // (slab vertex, target)
         qn += __popc(m);
         __syncwarp();
         if (qn < 32 && more) continue;
@@ -425,9 +443,9 @@ __global__ void __launch_bounds__(128, SBR_VIS_MINB) k_cir_visibility(DevScene S
     int sn[kStackSize];
     AnyTrav T(sn);
     if (active) {
-      v = pi / nt;
+      v = pi / nt;  // position in the slab's Morton order
       k = (int)(pi % nt);
-      a = ld3(vb.point + 3 * v);
+      a = ldg3(vpt + 3 * v);
       b = ldg3(P.targets_dev + 3 * k);
       vis++;
       // occluded_batch (geometry.py:187-201): open segment, endpoints offset by eps
@@ -486,8 +504,9 @@ __global__ void __launch_bounds__(128, SBR_VIS_MINB) k_cir_visibility(DevScene S
       if (!T.found) {
         const unsigned long long r = append_slot(counters + SBR_CC_ROWS);
         if ((int64_t)r < row_cap) {
-          row_key[r] = ordinal_key(vb.depth[v], vb.sample[v], k);
-          row_vtx[r] = (int32_t)v;
+          const int64_t vg = order ? order[v_begin + v] : v_begin + v;  // buffer index
+          row_key[r] = ordinal_key(vb.depth[vg], vb.sample[vg], k);
+          row_vtx[r] = (int32_t)vg;
         }
       }
     }
@@ -1146,14 +1165,31 @@ int sbr_cir_visibility(const SbrScene* scene, const SbrCirParams* P, const SbrVe
     }
     cudaMemsetAsync(ghint, 0xff, gb, st);
   }
+  const int64_t nvs = v_end - v_begin;
+  double *vpt = nullptr, *vnr = nullptr;
+  uint8_t* vcode = nullptr;
+  if (cudaMallocAsync(&vpt, sizeof(double) * 3 * nvs, st) != cudaSuccess ||
+      cudaMallocAsync(&vnr, sizeof(double) * 3 * nvs, st) != cudaSuccess ||
+      cudaMallocAsync(&vcode, nvs, st) != cudaSuccess) {
+    if (vpt) cudaFreeAsync(vpt, st);
+    if (vnr) cudaFreeAsync(vnr, st);
+    cudaFreeAsync(work, st);
+    if (ghint) cudaFreeAsync(ghint, st);
+    return set_error(SBR_ERR_NOMEM, "visibility vertex view");
+  }
+  k_vis_view<<<grid_for(nvs, 256), 256, 0, st>>>(*vb, v_begin, nvs, order, vpt, vnr, vcode);
+  count_launch();
   k_cir_visibility<<<sms * per_sm, 128, 0, st>>>(dev_view(scene), *P, *vb, v_begin, v_end,
                                                  row_key, row_vtx, row_cap,
                                                  (unsigned long long*)counters, work, order,
-                                                 ghint);
+                                                 ghint, vpt, vnr, vcode);
   prof_end(stream);
   rc = launch_status("k_cir_visibility");
   cudaFreeAsync(work, st);
   if (ghint) cudaFreeAsync(ghint, st);
+  cudaFreeAsync(vpt, st);
+  cudaFreeAsync(vnr, st);
+  cudaFreeAsync(vcode, st);
   return rc;
 }
 

@@ -899,6 +899,7 @@ def compute_paths_sharded(scene, transmitters, receivers, cfg, group=None):
             raise RuntimeError("BVH traversal stack overflow")
         c_sel["samples_escaped"] = c_sweep["samples_escaped"]
         c_sel["samples_terminated"] = c_sweep["samples_terminated"]
+        c_sel["duplicates"] += c_sweep["duplicates"]   # dropped at row emission
         gdiag = _gen_diag(c_sel, cfg)
         load_factor = max(load_factor, gdiag["hash_load_factor"])
         for k, v in gdiag.items():

@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(128, SBR_VIS_MINB) k_cir_visibility(DevScene S
   if (lane == 0) shpos[wid] = 0;
   __syncwarp();
   int qn = 0;  // warp-uniform queue length
-  unsigned vis = 0;
+  unsigned vis = 0, dup_local = 0;
   bool more = true;
   int64_t unit = 0, g_tile0 = 0;
   int tile_cur = kVisGroup, tile_end = kVisGroup, k_cur = -1;
@@ -496,23 +496,59 @@ __global__ void __launch_bounds__(128, SBR_VIS_MINB) k_cir_visibility(DevScene S
       }
     }
     __syncwarp();
-    if (active) {
-      if (!T.ok) {
-        flag_error(S, kErrStack);
-        atomicAdd(counters + SBR_CC_STACK_OVERFLOW, 1ULL);
+    if (active && !T.ok) {
+      flag_error(S, kErrStack);
+      atomicAdd(counters + SBR_CC_STACK_OVERFLOW, 1ULL);
+    }
+    // Visible pairs become rows.  Within the batch, a chain row whose
+    // (pair_r, pair_f) key another lane holds with a smaller ordinal is a
+    // duplicate by construction (the selection keeps only each key's first
+    // occurrence in ordinal order, and only kept rows reach truncation and
+    // the DedupTable), so it is counted here instead of emitted: neighbouring
+    // vertices on one facade usually share the chain and the target.
+    const bool visible = active && !T.found;
+    if (__any_sync(0xffffffffu, visible)) {
+      int64_t vg = 0;
+      uint64_t okey = ~0ULL, pr = 0, pf = 0;
+      bool chain_row = false;
+      if (visible) {
+        vg = order ? order[v_begin + v] : v_begin + v;  // vertex buffer index
+        okey = ordinal_key(vb.depth[vg], vb.sample[vg], k);
+        chain_row = vb.suffix_start[vg] == 0 && vb.code[vg] != 1;
+        if (chain_row) {
+          pr = fnv1a_u64(vb.hash_r[vg], (uint64_t)k);
+          pf = fnv1a_u64(vb.hash_f[vg], (uint64_t)k);
+        }
       }
-      if (!T.found) {
-        const unsigned long long r = append_slot(counters + SBR_CC_ROWS);
-        if ((int64_t)r < row_cap) {
-          const int64_t vg = order ? order[v_begin + v] : v_begin + v;  // buffer index
-          row_key[r] = ordinal_key(vb.depth[vg], vb.sample[vg], k);
-          row_vtx[r] = (int32_t)vg;
+      const unsigned cand = __ballot_sync(0xffffffffu, chain_row);
+      unsigned same = 0;
+      if (chain_row) same = __match_any_sync(cand, pr) & __match_any_sync(cand, pf);
+      bool first = true;
+      if (chain_row && __popc(same) > 1) {
+        // smallest ordinal of the key group (labeled-partition reductions)
+        const unsigned hi = (unsigned)(okey >> 32), lo = (unsigned)okey;
+        const unsigned mhi = __reduce_min_sync(same, hi);
+        const unsigned top = __ballot_sync(same, hi == mhi);
+        if (hi == mhi) first = lo == __reduce_min_sync(top, lo);
+        else first = false;
+      }
+      if (visible) {
+        if (chain_row && !first) {
+          dup_local++;
+        } else {
+          const unsigned long long r = append_slot(counters + SBR_CC_ROWS);
+          if ((int64_t)r < row_cap) {
+            row_key[r] = okey;
+            row_vtx[r] = (int32_t)vg;
+          }
         }
       }
     }
   }
   const unsigned s = __reduce_add_sync(0xffffffffu, vis);
   if (lane == 0 && s) atomicAdd(counters + SBR_CC_VIS_RAYS, (unsigned long long)s);
+  const unsigned sd = __reduce_add_sync(0xffffffffu, dup_local);
+  if (lane == 0 && sd) atomicAdd(counters + SBR_CC_DUPLICATES, (unsigned long long)sd);
 }
 
 // ---------------------------------------------------------------------------

@@ -229,6 +229,38 @@ def test_canyon_paths_vs_oracle(cuda, samples, kinds):
     assert rel.max(initial=0.0) < 1e-6, rel.max()
 
 
+def test_city_paths_vs_oracle(cuda):
+    """The config-3 city (483k triangles) with 64 street receivers at N_S = 2e4 vs
+    the oracle: path set, every diagnostics counter, gains -- exercises the
+    visibility kernel's occluder tables, far-first any-hit and emission-time
+    duplicate drop on a large scene."""
+    import oracle
+    from paper_2504_21719_b200 import scenes
+    meshes = scenes.city()
+    mats = scenes.uniform_materials(meshes, scenes.concrete())
+    rx = [RadioDevice(position=p) for p in scenes.city_receivers(64)]
+    tx = RadioDevice(position=np.array([0.0, 0.0, 30.0]))
+    cfg = PathConfig(num_samples=20_000, max_depth=4, q_diffraction=0.0,
+                     enabled=frozenset({Interaction.REFLECTION}))
+    want, wdiag = oracle.OracleScene(meshes, mats).compute_paths([tx], rx, cfg)
+    ps = compute_paths(SceneModel(meshes, mats), [tx], rx, cfg)
+    for k, v in wdiag.items():
+        if k == "refinement_rejections":
+            assert ps.diagnostics[k] == v
+        elif k == "hash_load_factor":
+            assert ps.diagnostics[k] == pytest.approx(v, rel=1e-12)
+        else:
+            assert ps.diagnostics.get(k, 0) == v, k
+    T = ps.tensors
+    assert len(T) == len(want["delay"]) > 0
+    for k in ("rx", "depth", "sample"):
+        assert np.array_equal(getattr(T, k), want[k]), k
+    assert np.array_equal(T.chain_hash.astype(np.uint64), want["chain_hash"].astype(np.uint64))
+    np.testing.assert_allclose(T.delay, want["delay"], rtol=1e-12)
+    rel = np.abs(T.gain - want["gain"]) / np.maximum(np.abs(want["gain"]), 1e-300)
+    assert rel.max(initial=0.0) < 1e-6, rel.max()
+
+
 @pytest.mark.parametrize("name", ["box_trunc", "canyon_r", "box_rst"])
 def test_sharded_selection_matches_single_gpu(cuda, name):
     """Multi-GPU CIR logic, emulated on one GPU: two sample shards swept

@@ -42,7 +42,7 @@ using namespace sbr;
 
 namespace {
 
-constexpr uint64_t kCombStride = 233;     // Fibonacci number: neighbouring lattice directions
+
 #ifndef SBR_WAVE_LOG2
 #define SBR_WAVE_LOG2 24  // 16.7M samples per pass (~7.4 GB of queues): one pass for 1e7
 #endif
@@ -79,9 +79,30 @@ __device__ __forceinline__ unsigned long long append_slot(unsigned long long* co
   return base + grp.thread_rank();
 }
 
-// comb order of segment 0: item w -> sample offset c + k*F (k = w % Q, c = w / Q)
-__device__ __forceinline__ uint64_t comb_sample(uint64_t w, uint64_t comb_q) {
-  return (w / comb_q) + (w % comb_q) * kCombStride;
+// Comb order of segment 0: item w -> sample offset c + k*F (k = w % Q,
+// c = w / Q) with F the Fibonacci number nearest sqrt(N): on the Fibonacci
+// lattice ids i and i + F are neighbouring directions, so the 32 rays of a
+// warp (and, through the queue order, their later bounces) stay coherent.
+// Measured on the canyon (N = 1e7): F = 89 / 233 / 987 / 2584 / 4181 ->
+// trace 5.9 / 5.2 / 4.5 / 4.2 / 4.2 ms per map.
+struct CombMap {
+  uint64_t q, stride;  // Q = ceil(count / F) columns, F
+  __device__ __forceinline__ uint64_t sample(uint64_t w) const {
+    return (w / q) + (w % q) * stride;
+  }
+  __device__ __forceinline__ uint64_t slots() const { return q * stride; }
+};
+
+static uint64_t comb_stride(uint64_t num_samples) {
+  uint64_t a = 1, b = 2, best = 1;
+  const double target = sqrt((double)num_samples);
+  while (b < (1ULL << 40)) {
+    if (fabs((double)b - target) < fabs((double)best - target)) best = b;
+    const uint64_t c = a + b;
+    a = b;
+    b = c;
+  }
+  return best;
 }
 
 
@@ -106,11 +127,11 @@ __device__ __forceinline__ uint64_t comb_sample(uint64_t w, uint64_t comb_q) {
 #endif
 __global__ void __launch_bounds__(SBR_TRACE_TPB, SBR_TRACE_MINB) k_map_trace(DevScene S, SbrMapParams P, int seg,
                                                    MapQueue q, const unsigned long long* count_in,
-                                                   uint64_t begin, uint64_t count0, uint64_t comb_q,
+                                                   uint64_t begin, uint64_t count0, CombMap comb,
                                                    HitBuf hits, unsigned long long* work,
                                                    unsigned long long* counters, ShardMap sh) {
   const unsigned lane = threadIdx.x & 31u;
-  const uint64_t n = seg == 0 ? comb_q * kCombStride : (uint64_t)*count_in;
+  const uint64_t n = seg == 0 ? comb.slots() : (uint64_t)*count_in;
   const double3 src = make_double3(P.source[0], P.source[1], P.source[2]);
   while (true) {
     unsigned long long base = 0;
@@ -122,7 +143,7 @@ __global__ void __launch_bounds__(SBR_TRACE_TPB, SBR_TRACE_MINB) k_map_trace(Dev
     double3 o = src, d = make_double3(0.0, 0.0, 1.0);
     if (active) {
       if (seg == 0) {
-        const uint64_t local = comb_sample(i, comb_q);
+        const uint64_t local = comb.sample(i);
         active = local < count0;
         if (active) d = fibonacci_dir(P.num_samples, sh.gid(begin + local));
         else hits.tri[i] = -3;  // comb slot past the end of the range
@@ -164,13 +185,13 @@ struct LaneCounters {
 
 __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, SbrMapParams P, int seg,
                                                    MapQueue qi, const unsigned long long* count_in,
-                                                   uint64_t begin, uint64_t comb_q, HitBuf hits,
+                                                   uint64_t begin, CombMap comb, HitBuf hits,
                                                    MapQueue qo, unsigned long long* count_out,
                                                    ScatterQueue sq, unsigned long long* count_s,
                                                    double* __restrict__ grid,
                                                    unsigned long long* __restrict__ counters, ShardMap sh) {
   LaneCounters K = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
-  const uint64_t n = seg == 0 ? comb_q * kCombStride : (uint64_t)*count_in;
+  const uint64_t n = seg == 0 ? comb.slots() : (uint64_t)*count_in;
   const double3 n_hat = make_double3(P.normal[0], P.normal[1], P.normal[2]);
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
@@ -181,7 +202,7 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
     double r_dist, omega, weight;
     uint64_t g;
     if (seg == 0) {
-      g = sh.gid(begin + comb_sample(i, comb_q));
+      g = sh.gid(begin + comb.sample(i));
       o = make_double3(P.source[0], P.source[1], P.source[2]);
       d = fibonacci_dir(P.num_samples, g);
       E = antenna_field(P.pattern, d);
@@ -683,10 +704,11 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t chunk = total < (uint64_t)kChunkRays ? (int64_t)total : kChunkRays;
-  // segment 0 runs over comb slots: up to chunk + kCombStride items
+  // segment 0 runs over comb slots: up to chunk + F items
+  const uint64_t F = comb_stride(P->num_samples);
   Wave wave;
   Wave* w = &wave;
-  if ((rc = wave_alloc(chunk + (int64_t)kCombStride, st, w))) return rc;
+  if ((rc = wave_alloc(chunk + (int64_t)F, st, w))) return rc;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_map_trace, SBR_TRACE_TPB, 0);
   if (per_sm < 1) per_sm = 1;
@@ -695,7 +717,7 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
   const DevScene S = dev_view(scene);
   for (uint64_t lo = sample_begin; lo < sample_end; lo += (uint64_t)chunk) {
     const uint64_t cnt = (sample_end - lo) < (uint64_t)chunk ? (sample_end - lo) : (uint64_t)chunk;
-    const uint64_t comb_q = (cnt + kCombStride - 1) / kCombStride;
+    const CombMap comb{(cnt + F - 1) / F, F};
     int cur = 0;
     for (int seg = 0; seg <= P->max_depth; ++seg) {
       // ctl[0] = work counter; ctl[1 + cur] = this segment's count; ctl[2 - cur] = next count
@@ -703,12 +725,12 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
       if ((rc = launch_status("k_reset_pass"))) break;
       prof_begin(st, "k_map_trace");
       k_map_trace<<<trace_blocks, SBR_TRACE_TPB, 0, st>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo, cnt,
-                                                comb_q, w->hits, w->ctl, counters, sh);
+                                                comb, w->hits, w->ctl, counters, sh);
       prof_end(st);
       if ((rc = launch_status("k_map_trace"))) break;
       prof_begin(st, "k_map_shade");
       k_map_shade<<<shade_blocks, 128, 0, st>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo,
-                                                comb_q, w->hits, w->q[1 - cur], w->ctl + 2 - cur,
+                                                comb, w->hits, w->q[1 - cur], w->ctl + 2 - cur,
                                                 w->sq, w->ctl + 3, grid, counters, sh);
       prof_end(st);
       if ((rc = launch_status("k_map_shade"))) break;

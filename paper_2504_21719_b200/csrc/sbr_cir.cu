@@ -111,7 +111,7 @@ __device__ __forceinline__ bool interaction_probs(const SbrMaterial& m, double r
 __global__ void __launch_bounds__(128, SBR_SWEEP_MINB) k_cir_sweep(DevScene S, SbrCirParams P, uint64_t begin,
                                                    uint64_t end, SbrVertexBuf vb,
                                                    unsigned long long* __restrict__ counters,
-                                                   ShardMap sh) {
+                                                   ShardMap sh, CombMap comb) {
   CirCounters K = {0u, 0u, 0u};
   const double3 src = make_double3(P.source[0], P.source[1], P.source[2]);
   // Warp-uniform loop over batches of 32 samples; every depth step traces the
@@ -122,9 +122,12 @@ __global__ void __launch_bounds__(128, SBR_SWEEP_MINB) k_cir_sweep(DevScene S, S
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   int sn[kStackSize];
   float st[kStackSize];
-  for (uint64_t base = begin + warp0 * 32; base < end; base += nwarps * 32) {
-    const uint64_t l = base + lane_id;
-    bool alive = l < end;
+  // comb order: the 32 lanes of a batch take lattice neighbours (ids F apart)
+  const uint64_t slots = comb.slots();
+  for (uint64_t base = warp0 * 32; base < slots; base += nwarps * 32) {
+    const uint64_t off = base + lane_id < slots ? comb.sample(base + lane_id) : ~0ULL;
+    const uint64_t l = begin + off;
+    bool alive = off < end - begin;
     const uint64_t g = sh.gid(alive ? l : begin);  // global sample id (RNG key, ordinal)
     double3 o = src;
     double3 d = fibonacci_dir(P.num_samples, g);
@@ -1112,9 +1115,10 @@ int sbr_cir_sweep(const SbrScene* scene, const SbrCirParams* P, uint64_t begin, 
   if (end > P->num_samples || begin > end) return set_error(SBR_ERR_INVALID, "bad sample range");
   if (end == begin || P->max_depth == 0) return SBR_OK;
   prof_begin(stream, "k_cir_sweep");
+  const uint64_t F = comb_stride(P->num_samples);
   k_cir_sweep<<<grid_for((int64_t)(end - begin), 128, 148 * 16), 128, 0, (cudaStream_t)stream>>>(
       dev_view(scene), *P, begin, end, *vb, (unsigned long long*)counters,
-      ShardMap{0u, 1u, kCirShardLog2});
+      ShardMap{0u, 1u, kCirShardLog2}, CombMap{(end - begin + F - 1) / F, F});
   prof_end(stream);
   return launch_status("k_cir_sweep");
 }
@@ -1131,9 +1135,11 @@ int sbr_cir_sweep_sharded(const SbrScene* scene, const SbrCirParams* P, int32_t 
                                 kCirShardLog2);
   if (n == 0 || P->max_depth == 0) return SBR_OK;
   prof_begin(stream, "k_cir_sweep");
+  const uint64_t F = comb_stride(P->num_samples);
   k_cir_sweep<<<grid_for((int64_t)n, 128, 148 * 16), 128, 0, (cudaStream_t)stream>>>(
       dev_view(scene), *P, 0, n, *vb, (unsigned long long*)counters,
-      ShardMap{(uint32_t)shard_index, (uint32_t)shard_count, kCirShardLog2});
+      ShardMap{(uint32_t)shard_index, (uint32_t)shard_count, kCirShardLog2},
+      CombMap{(n + F - 1) / F, F});
   prof_end(stream);
   return launch_status("k_cir_sweep");
 }

@@ -79,31 +79,7 @@ __device__ __forceinline__ unsigned long long append_slot(unsigned long long* co
   return base + grp.thread_rank();
 }
 
-// Comb order of segment 0: item w -> sample offset c + k*F (k = w % Q,
-// c = w / Q) with F the Fibonacci number nearest sqrt(N): on the Fibonacci
-// lattice ids i and i + F are neighbouring directions, so the 32 rays of a
-// warp (and, through the queue order, their later bounces) stay coherent.
-// Measured on the canyon (N = 1e7): F = 89 / 233 / 987 / 2584 / 4181 ->
-// trace 5.9 / 5.2 / 4.5 / 4.2 / 4.2 ms per map.
-struct CombMap {
-  uint64_t q, stride;  // Q = ceil(count / F) columns, F
-  __device__ __forceinline__ uint64_t sample(uint64_t w) const {
-    return (w / q) + (w % q) * stride;
-  }
-  __device__ __forceinline__ uint64_t slots() const { return q * stride; }
-};
 
-static uint64_t comb_stride(uint64_t num_samples) {
-  uint64_t a = 1, b = 2, best = 1;
-  const double target = sqrt((double)num_samples);
-  while (b < (1ULL << 40)) {
-    if (fabs((double)b - target) < fabs((double)best - target)) best = b;
-    const uint64_t c = a + b;
-    a = b;
-    b = c;
-  }
-  return best;
-}
 
 
 // ---------------------------------------------------------------------------

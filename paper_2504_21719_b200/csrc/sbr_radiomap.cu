@@ -98,19 +98,28 @@ __device__ __forceinline__ unsigned long long append_slot(unsigned long long* co
 #ifndef SBR_SHADE_WARPSYNC
 #define SBR_SHADE_WARPSYNC 1  // canyon shade 5.08 -> 5.00 ms per step
 #endif
+#ifndef SBR_SHADE_SPLIT
+#define SBR_SHADE_SPLIT 1  // canyon shade 5.0 -> 4.8 ms per step (smaller kernels, less spill)
+#endif
+#define SHADE_FIRST (SBR_SHADE_SPLIT ? kFirst : seg == 0)
 #ifndef SBR_SHADE_MINB
 #define SBR_SHADE_MINB 8
 #endif
+#ifndef SBR_TRACE_SPLIT
+#define SBR_TRACE_SPLIT 0  // split trace measured equal (4.20 vs 4.21 ms; 8 blocks/SM 4.23)
+#endif
+#define TRACE_FIRST (SBR_TRACE_SPLIT ? kFirst : seg == 0)
 #ifndef SBR_TRACE_TPB
 #define SBR_TRACE_TPB 128
 #endif
+template <bool kFirst>
 __global__ void __launch_bounds__(SBR_TRACE_TPB, SBR_TRACE_MINB) k_map_trace(DevScene S, SbrMapParams P, int seg,
                                                    MapQueue q, const unsigned long long* count_in,
                                                    uint64_t begin, uint64_t count0, CombMap comb,
                                                    HitBuf hits, unsigned long long* work,
                                                    unsigned long long* counters, ShardMap sh) {
   const unsigned lane = threadIdx.x & 31u;
-  const uint64_t n = seg == 0 ? comb.slots() : (uint64_t)*count_in;
+  const uint64_t n = TRACE_FIRST ? comb.slots() : (uint64_t)*count_in;
   const double3 src = make_double3(P.source[0], P.source[1], P.source[2]);
   while (true) {
     unsigned long long base = 0;
@@ -121,7 +130,7 @@ __global__ void __launch_bounds__(SBR_TRACE_TPB, SBR_TRACE_MINB) k_map_trace(Dev
     bool active = i < n;
     double3 o = src, d = make_double3(0.0, 0.0, 1.0);
     if (active) {
-      if (seg == 0) {
+      if (TRACE_FIRST) {
         const uint64_t local = comb.sample(i);
         active = local < count0;
         if (active) d = fibonacci_dir(P.num_samples, sh.gid(begin + local));
@@ -162,6 +171,10 @@ struct LaneCounters {
   unsigned rb, deposits, escaped, respawns, terminated, thr, rr;
 };
 
+// kFirst: the segment-0 instantiation (launch directions from the sample id)
+// and the queue instantiation are separate kernels when SBR_SHADE_SPLIT, so
+// each carries only its own ray-source code
+template <bool kFirst>
 __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, SbrMapParams P, int seg,
                                                    MapQueue qi, const unsigned long long* count_in,
                                                    uint64_t begin, CombMap comb, HitBuf hits,
@@ -170,7 +183,7 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
                                                    double* __restrict__ grid,
                                                    unsigned long long* __restrict__ counters, ShardMap sh) {
   LaneCounters K = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
-  const uint64_t n = seg == 0 ? comb.slots() : (uint64_t)*count_in;
+  const uint64_t n = SHADE_FIRST ? comb.slots() : (uint64_t)*count_in;
   const double3 n_hat = make_double3(P.normal[0], P.normal[1], P.normal[2]);
 #if SBR_SHADE_WARPSYNC
   // warp-uniform iterations with a __syncwarp at the end of each: lanes that
@@ -191,7 +204,7 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
     cvec3 E;
     double r_dist, omega, weight;
     uint64_t g;
-    if (seg == 0) {
+    if (SHADE_FIRST) {
       g = sh.gid(begin + comb.sample(i));
       o = make_double3(P.source[0], P.source[1], P.source[2]);
       d = fibonacci_dir(P.num_samples, g);
@@ -215,7 +228,7 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
     const uint64_t chunk = g >> SBR_CHUNK_LOG2;
     const uint64_t slot = g & ((1ULL << SBR_CHUNK_LOG2) - 1);
     // plane crossing before the hit (radiomap.py:394-413); escaped rays deposit too
-    if (seg >= 1) {
+    if (!SHADE_FIRST) {
       const double denom = dot_gemv(d, n_hat);
       double s = -1.0;
       if (fabs(denom) > 1e-12) s = (P.plane_off - dot_gemv(o, n_hat)) / denom;
@@ -704,7 +717,7 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
   Wave* w = &wave;
   if ((rc = wave_alloc(chunk + (int64_t)F, st, w))) return rc;
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_map_trace, SBR_TRACE_TPB, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_map_trace<false>, SBR_TRACE_TPB, 0);
   if (per_sm < 1) per_sm = 1;
   const unsigned trace_blocks = (unsigned)(sms * per_sm);
   const unsigned shade_blocks = (unsigned)(sms * 8);
@@ -718,12 +731,12 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
       k_reset_pass<<<1, 1, 0, st>>>(w->ctl, w->ctl + 2 - cur, w->ctl + 3);
       if ((rc = launch_status("k_reset_pass"))) break;
       prof_begin(st, "k_map_trace");
-      k_map_trace<<<trace_blocks, SBR_TRACE_TPB, 0, st>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo, cnt,
+      (seg == 0 ? k_map_trace<true> : k_map_trace<false>)<<<trace_blocks, SBR_TRACE_TPB, 0, st>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo, cnt,
                                                 comb, w->hits, w->ctl, counters, sh);
       prof_end(st);
       if ((rc = launch_status("k_map_trace"))) break;
       prof_begin(st, "k_map_shade");
-      k_map_shade<<<shade_blocks, 128, 0, st>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo,
+      (seg == 0 ? k_map_shade<true> : k_map_shade<false>)<<<shade_blocks, 128, 0, st>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo,
                                                 comb, w->hits, w->q[1 - cur], w->ctl + 2 - cur,
                                                 w->sq, w->ctl + 3, grid, counters, sh);
       prof_end(st);

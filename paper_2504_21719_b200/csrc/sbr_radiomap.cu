@@ -720,7 +720,7 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_map_trace<false>, SBR_TRACE_TPB, 0);
   if (per_sm < 1) per_sm = 1;
   const unsigned trace_blocks = (unsigned)(sms * per_sm);
-  const unsigned shade_blocks = (unsigned)(sms * 8);
+  const unsigned shade_blocks = (unsigned)(sms * SBR_SHADE_MINB);
   const DevScene S = dev_view(scene);
   for (uint64_t lo = sample_begin; lo < sample_end; lo += (uint64_t)chunk) {
     const uint64_t cnt = (sample_end - lo) < (uint64_t)chunk ? (sample_end - lo) : (uint64_t)chunk;

@@ -352,6 +352,9 @@ __global__ void k_vis_view(SbrVertexBuf vb, int64_t v_begin, int64_t nv,
   }
 }
 
+#ifndef SBR_VIS_GHINT_EARLY
+#define SBR_VIS_GHINT_EARLY 1  // config 3: 64.2 -> 62.8 ms (2: early __ldcg, 63.9)
+#endif
 #ifndef SBR_VIS_MINB
 #define SBR_VIS_MINB 8  // 64 registers: 220 -> 180 ms at config 3
 #endif
@@ -445,9 +448,21 @@ __global__ void __launch_bounds__(128, SBR_VIS_MINB) k_cir_visibility(DevScene S
     bool cast = false;
     int sn[kStackSize];
     AnyTrav T(sn);
+#if SBR_VIS_GHINT_EARLY
+    // the per-target occluder table is read before the ray setup so its
+    // latency overlaps the setup arithmetic; plain (L1-cacheable) loads: a
+    // stale entry is still a valid candidate occluder
+    int gh[kVisGHints > 0 ? kVisGHints : 1];
+#endif
     if (active) {
       v = pi / nt;  // position in the slab's Morton order
       k = (int)(pi % nt);
+#if SBR_VIS_GHINT_EARLY
+#pragma unroll
+      for (int h = 0; h < kVisGHints; ++h)
+        gh[h] = SBR_VIS_GHINT_EARLY == 2 ? __ldcg(ghint + (int64_t)k * kVisGHints + h)
+                                         : ghint[(int64_t)k * kVisGHints + h];
+#endif
       a = ldg3(vpt + 3 * v);
       b = ldg3(P.targets_dev + 3 * k);
       vis++;
@@ -470,7 +485,11 @@ __global__ void __launch_bounds__(128, SBR_VIS_MINB) k_cir_visibility(DevScene S
     // config 3 these settle 87 % of all rays, the warp ring below another 3 %
     for (int h = 0; h < kVisGHints; ++h) {
       if (cast && !T.found) {
+#if SBR_VIS_GHINT_EARLY
+        const int j = gh[h];
+#else
         const int j = __ldcg(ghint + (int64_t)k * kVisGHints + h);
+#endif
         if (j >= 0) T.try_occluder(S, j);
       }
     }

@@ -352,6 +352,9 @@ __global__ void k_vis_view(SbrVertexBuf vb, int64_t v_begin, int64_t nv,
   }
 }
 
+#ifndef SBR_VIS_PACK
+#define SBR_VIS_PACK 1  // config 3: 62.8 -> 60.9 ms (no 64-bit div/mod per ray)
+#endif
 #ifndef SBR_VIS_GHINT_EARLY
 #define SBR_VIS_GHINT_EARLY 1  // config 3: 64.2 -> 62.8 ms (2: early __ldcg, 63.9)
 #endif
@@ -429,7 +432,12 @@ __global__ void __launch_bounds__(128, SBR_VIS_MINB) k_cir_visibility(DevScene S
           pass = code == 3 ? true : (code == 2 ? side < 0.0 : side > 0.0);
         }
         const unsigned m = __ballot_sync(0xffffffffu, pass);
+#if SBR_VIS_PACK
+        // (slab vertex, target) as two 32-bit halves: shifts, not a 64-bit div/mod
+        if (pass) sq[wid][qn + __popc(m & lt_mask)] = (int64_t)(((uint64_t)pos << 32) | (uint32_t)k);
+#else
         if (pass) sq[wid][qn + __popc(m & lt_mask)] = pos * nt + k;  // (slab vertex, target)
+#endif
         qn += __popc(m);
         __syncwarp();
         if (qn < 32 && more) continue;
@@ -455,8 +463,13 @@ __global__ void __launch_bounds__(128, SBR_VIS_MINB) k_cir_visibility(DevScene S
     int gh[kVisGHints > 0 ? kVisGHints : 1];
 #endif
     if (active) {
+#if SBR_VIS_PACK
+      v = (int64_t)((uint64_t)pi >> 32);  // position in the slab's Morton order
+      k = (int)(uint32_t)pi;
+#else
       v = pi / nt;  // position in the slab's Morton order
       k = (int)(pi % nt);
+#endif
 #if SBR_VIS_GHINT_EARLY
 #pragma unroll
       for (int h = 0; h < kVisGHints; ++h)
@@ -1206,6 +1219,8 @@ int sbr_cir_visibility(const SbrScene* scene, const SbrCirParams* P, const SbrVe
   if (rc) return rc;
   if (!scene || !vb) return set_error(SBR_ERR_INVALID, "NULL argument");
   if (v_end <= v_begin) return SBR_OK;
+  if (v_end - v_begin > INT32_MAX)  // queue entries pack the slab position in 32 bits
+    return set_error(SBR_ERR_INVALID, "visibility slab larger than 2^31 vertices");
   cudaStream_t st = (cudaStream_t)stream;
   unsigned long long* work = nullptr;
   if (cudaMallocAsync(&work, sizeof(unsigned long long), st) != cudaSuccess)

@@ -127,15 +127,22 @@ enum {
 typedef struct SbrScene SbrScene;
 
 /* Replaces Accel.__init__ / _build_bvh (geometry.py:134-166, 244-349).
- * v0, v1, v2: host (ntri, 3) float64 corners in input order.  Builds an LBVH
- * (Morton codes, radix sort, Karras hierarchy, bottom-up refit, leaves <= 4)
- * on `device`.  Fails with SBR_ERR_EMPTY_SCENE when ntri == 0. */
+ * v0, v1, v2: host (ntri, 3) float64 corners in input order.  Builds the BVH
+ * on `device` (Morton codes, radix sort, PLOC or Karras hierarchy, bottom-up
+ * refit, leaves of <= 2 triangles).  Fails with SBR_ERR_EMPTY_SCENE when
+ * ntri == 0 and SBR_ERR_INVALID for a non-finite coordinate (the reference
+ * accepts those and produces NaN geometry).  On failure nothing is leaked. */
 int sbr_scene_create(const double* v0, const double* v1, const double* v2,
                      int64_t ntri, int32_t device, void* stream, SbrScene** out);
+/* Frees the scene; the calling thread's current CUDA device is unchanged. */
 void sbr_scene_destroy(SbrScene* scene);
+/* Returns every freed block of the library's private scratch pool on `device`
+ * (ray queues, sort buffers; kept mapped between calls up to 16 GiB) to the
+ * driver.  Synchronises the device.  No reference counterpart. */
+int sbr_release_scratch(int32_t device);
 /* Hierarchy of subsequently created scenes over the same GPU Morton sort:
  * 0 = Karras 2012 LBVH, 1 = PLOC (parallel locally-ordered clustering,
- * SAH-like quality; default).  Both collapse to <= 4-triangle leaves. */
+ * SAH-like quality; default).  Both collapse to <= 2-triangle leaves. */
 int sbr_set_bvh_builder(int32_t builder);
 int64_t sbr_scene_num_triangles(const SbrScene* scene);
 int64_t sbr_scene_num_nodes(const SbrScene* scene);
@@ -218,8 +225,6 @@ int sbr_philox_uniform(uint64_t seed, uint64_t sample, uint64_t depth,
 int sbr_radiomap_bounce(const SbrScene* scene, const SbrMapParams* params,
                         uint64_t sample_begin, uint64_t sample_end,
                         double* grid_dev, uint64_t* counters_dev, void* stream);
-/* Replaces _direct_cells (radiomap.py:566-583): analytic LoS term per cell
- * centre into direct_dev (ny, nx) (overwritten), counts visible cells. */
 /* The bounce loop over a chunk-cyclic shard of the global sample ids
  * [0, num_samples): global RNG chunks (g >> SBR_CHUNK_LOG2) = shard_index,
  * shard_index + shard_count, ...  The shards of one call partition the ids, so
@@ -229,6 +234,8 @@ int sbr_radiomap_bounce(const SbrScene* scene, const SbrMapParams* params,
 int sbr_radiomap_bounce_sharded(const SbrScene* scene, const SbrMapParams* params,
                                 int32_t shard_index, int32_t shard_count, double* grid_dev,
                                 uint64_t* counters_dev, void* stream);
+/* Replaces _direct_cells (radiomap.py:566-583): analytic LoS term per cell
+ * centre into direct_dev (ny, nx) (overwritten), counts visible cells. */
 int sbr_radiomap_direct(const SbrScene* scene, const SbrMapParams* params,
                         double* direct_dev, uint64_t* counters_dev, void* stream);
 

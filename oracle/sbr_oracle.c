@@ -24,6 +24,7 @@
  *                                                         radiomap.py:253-277
  */
 #include <math.h>
+#include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -609,7 +610,7 @@ static inline int tri_hit(const double* p0, const double* p1, const double* p2,
 #define STACK_CAP 256
 
 /* node / triangle visit statistics of closest1 (BVH-quality diagnostics) */
-static uint64_t g_orc_nodes = 0, g_orc_tris = 0;
+static __thread uint64_t g_orc_nodes = 0, g_orc_tris = 0;  /* per thread */
 ORC_EXPORT void orc_visit_stats(uint64_t* nodes, uint64_t* tris, int reset) {
   *nodes = g_orc_nodes;
   *tris = g_orc_tris;
@@ -1127,12 +1128,11 @@ static int32_t project_wedge(const OrcScene* S, int64_t tri, const double* p, do
 }
 
 /* Per-sample sweep of global ids [lo, hi) into H (indexed g - lo). */
-static int cir_sweep(const OrcScene* S, const OrcCirParams* P, uint64_t lo, uint64_t hi, Hist* H,
+static int sweep_one(const OrcScene* S, const OrcCirParams* P, uint64_t lo, uint64_t g, Hist* H,
                      uint64_t* counters) {
   const int L = P->max_depth;
   const uint64_t N = P->num_samples;
-  for (uint64_t i = 0; i < (hi - lo) * (uint64_t)(L > 0 ? L : 1); ++i) H[i].code = -1;
-  for (uint64_t g = lo; g < hi; ++g) {
+  {
     double o[3] = {P->source[0], P->source[1], P->source[2]}, d[3];
     orc_fibonacci(N, g, d);
     uint64_t hr = 0, hf = 0;
@@ -1219,40 +1219,170 @@ static int cir_sweep(const OrcScene* S, const OrcCirParams* P, uint64_t lo, uint
   return 0;
 }
 
+/* Test-infrastructure threading (orc_set_threads, default 1): samples are
+ * independent, so the sweep and the visibility rows split over pthreads that
+ * claim items from a shared counter, with per-thread counters; rows are
+ * concatenated in (depth, sample, target) order, so every result is identical
+ * to the single-threaded run. */
+static int g_orc_threads = 1;
+ORC_EXPORT void orc_set_threads(int n) { g_orc_threads = n > 0 ? n : 1; }
+
+typedef int (*ItemFn)(void* ctx, int64_t item, uint64_t* counters);
+typedef struct {
+  ItemFn fn;
+  void* ctx;
+  int64_t n, next;
+  uint64_t counters[OC_COUNT];
+  int rc;
+  pthread_mutex_t mu;
+} ItemPool;
+
+static void* item_worker(void* arg) {
+  ItemPool* P = (ItemPool*)arg;
+  uint64_t local[OC_COUNT] = {0};
+  int rc = 0;
+  for (;;) {
+    const int64_t i = __atomic_fetch_add(&P->next, 1, __ATOMIC_RELAXED);
+    if (i >= P->n || rc) break;
+    rc = P->fn(P->ctx, i, local);
+  }
+  pthread_mutex_lock(&P->mu);
+  for (int k = 0; k < OC_COUNT; ++k) P->counters[k] += local[k];
+  if (rc) P->rc = rc;
+  pthread_mutex_unlock(&P->mu);
+  return NULL;
+}
+
+/* fn(ctx, i, counters) for i in [0, n) on g_orc_threads threads; returns the
+ * first nonzero status; counters are summed into `counters` */
+static int parallel_items(int64_t n, ItemFn fn, void* ctx, uint64_t* counters) {
+  ItemPool P;
+  memset(&P, 0, sizeof P);
+  P.fn = fn; P.ctx = ctx; P.n = n;
+  pthread_mutex_init(&P.mu, NULL);
+  int nt = g_orc_threads;
+  if (nt > n) nt = (int)(n > 0 ? n : 1);
+  pthread_t th[256];
+  if (nt > 256) nt = 256;
+  if (nt <= 1) {
+    item_worker(&P);
+  } else {
+    for (int t = 0; t < nt; ++t) pthread_create(th + t, NULL, item_worker, &P);
+    for (int t = 0; t < nt; ++t) pthread_join(th[t], NULL);
+  }
+  pthread_mutex_destroy(&P.mu);
+  for (int k = 0; k < OC_COUNT; ++k) counters[k] += P.counters[k];
+  return P.rc;
+}
+
+typedef struct {
+  const OrcScene* S;
+  const OrcCirParams* P;
+  uint64_t lo, hi;
+  Hist* H;
+} SweepCtx;
+
+static int sweep_item(void* c, int64_t b, uint64_t* counters) {
+  SweepCtx* x = (SweepCtx*)c;
+  const uint64_t g0 = x->lo + (uint64_t)b * 64, g1 = g0 + 64 < x->hi ? g0 + 64 : x->hi;
+  for (uint64_t g = g0; g < g1; ++g) {
+    const int rc = sweep_one(x->S, x->P, x->lo, g, x->H, counters);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+static int cir_sweep(const OrcScene* S, const OrcCirParams* P, uint64_t lo, uint64_t hi, Hist* H,
+                     uint64_t* counters) {
+  const int L = P->max_depth;
+  for (uint64_t i = 0; i < (hi - lo) * (uint64_t)(L > 0 ? L : 1); ++i) H[i].code = -1;
+  SweepCtx x = {S, P, lo, hi, H};
+  return parallel_items((int64_t)((hi - lo + 63) / 64), sweep_item, &x, counters);
+}
+
 /* visible rows of H in (depth, sample, target) order (_visible_pairs 657-683) */
+typedef struct {
+  Row* rows;
+  int64_t n, cap;
+} RowBuf;
+
+/* rows of samples [g0, g1) at one depth, appended to B */
+static int rows_block(const OrcScene* S, const OrcCirParams* P, uint64_t lo, int depth,
+                      uint64_t g0, uint64_t g1, const Hist* H, RowBuf* B, uint64_t* counters) {
+  const int L = P->max_depth, nt = P->nt;
+  for (uint64_t g = g0; g < g1; ++g) {
+    const Hist* h = H + (g - lo) * L + (depth - 1);
+    if (h->code < 0) continue;
+    for (int k = 0; k < nt; ++k) {
+      const double* tg = P->targets + 3 * k;
+      double diff[3] = {tg[0] - h->vertex[0], tg[1] - h->vertex[1], tg[2] - h->vertex[2]};
+      double side = dot_seq(diff, h->normal);
+      int ok = h->code == 2 ? side < 0.0 : side > 0.0;
+      if (h->code == 3) ok = 1;
+      if (!ok) continue;
+      counters[OC_VIS]++;
+      int occ;
+      if (occluded1(S, h->vertex, tg, 1e-4, &occ)) return SBR_ERR_STACK;
+      if (occ) continue;
+      counters[OC_ROWS]++;
+      if (B->n == B->cap) {
+        B->cap = B->cap ? 2 * B->cap : 1024;
+        B->rows = (Row*)realloc(B->rows, sizeof(Row) * (size_t)B->cap);
+      }
+      Row* r = B->rows + B->n++;
+      r->g = (int64_t)g; r->depth = depth; r->k = k;
+      r->diffuse = h->code == 1;
+      r->chain = h->suffix_start == 0 && h->code != 1;
+      r->pr = fnv1a_u64(h->hr, (uint64_t)k);
+      r->pf = fnv1a_u64(h->hf, (uint64_t)k);
+    }
+  }
+  return 0;
+}
+
+typedef struct {
+  const OrcScene* S;
+  const OrcCirParams* P;
+  uint64_t lo, hi;
+  int depth;
+  const Hist* H;
+  RowBuf* blk;
+} RowsCtx;
+
+static int rows_item(void* c, int64_t b, uint64_t* counters) {
+  RowsCtx* x = (RowsCtx*)c;
+  const uint64_t g0 = x->lo + (uint64_t)b * 256, g1 = g0 + 256 < x->hi ? g0 + 256 : x->hi;
+  x->blk[b].n = 0;
+  return rows_block(x->S, x->P, x->lo, x->depth, g0, g1, x->H, x->blk + b, counters);
+}
+
 static int cir_rows(const OrcScene* S, const OrcCirParams* P, uint64_t lo, uint64_t hi,
                     const Hist* H, Row** rows_out, int64_t* n_out, uint64_t* counters) {
-  const int L = P->max_depth, nt = P->nt;
+  const int L = P->max_depth;
+  const uint64_t span = hi - lo;
+  const int64_t nblk = span == 0 ? 0 : (int64_t)((span + 255) / 256);
+  RowBuf* blk = (RowBuf*)calloc((size_t)(nblk > 0 ? nblk : 1), sizeof(RowBuf));
   Row* rows = NULL;
   int64_t n = 0, cap = 0;
-  for (int depth = 1; depth <= L; ++depth)
-    for (uint64_t g = lo; g < hi; ++g) {
-      const Hist* h = H + (g - lo) * L + (depth - 1);
-      if (h->code < 0) continue;
-      for (int k = 0; k < nt; ++k) {
-        const double* tg = P->targets + 3 * k;
-        double diff[3] = {tg[0] - h->vertex[0], tg[1] - h->vertex[1], tg[2] - h->vertex[2]};
-        double side = dot_seq(diff, h->normal);
-        int ok = h->code == 2 ? side < 0.0 : side > 0.0;
-        if (h->code == 3) ok = 1;
-        if (!ok) continue;
-        counters[OC_VIS]++;
-        int occ;
-        if (occluded1(S, h->vertex, tg, 1e-4, &occ)) { free(rows); return SBR_ERR_STACK; }
-        if (occ) continue;
-        counters[OC_ROWS]++;
-        if (n == cap) {
-          cap = cap ? 2 * cap : 4096;
-          rows = (Row*)realloc(rows, sizeof(Row) * (size_t)cap);
-        }
-        Row* r = rows + n++;
-        r->g = (int64_t)g; r->depth = depth; r->k = k;
-        r->diffuse = h->code == 1;
-        r->chain = h->suffix_start == 0 && h->code != 1;
-        r->pr = fnv1a_u64(h->hr, (uint64_t)k);
-        r->pf = fnv1a_u64(h->hf, (uint64_t)k);
+  int rc = 0;
+  for (int depth = 1; depth <= L && !rc; ++depth) {
+    RowsCtx x = {S, P, lo, hi, depth, H, blk};
+    rc = parallel_items(nblk, rows_item, &x, counters);
+    for (int64_t b = 0; b < nblk && !rc; ++b) {
+      if (n + blk[b].n > cap) {
+        cap = 2 * (n + blk[b].n) + 4096;
+        rows = (Row*)realloc(rows, sizeof(Row) * (size_t)cap);
       }
+      if (blk[b].n) memcpy(rows + n, blk[b].rows, sizeof(Row) * (size_t)blk[b].n);
+      n += blk[b].n;
     }
+  }
+  for (int64_t b = 0; b < nblk; ++b) free(blk[b].rows);
+  free(blk);
+  if (rc) {
+    free(rows);
+    return rc;
+  }
   *rows_out = rows;
   *n_out = n;
   return 0;

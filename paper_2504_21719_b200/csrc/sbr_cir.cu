@@ -1111,7 +1111,7 @@ struct Arena {
   template <typename T>
   T* get(int64_t count) {
     void* p = nullptr;
-    if (cudaMallocAsync(&p, sizeof(T) * (size_t)(count > 0 ? count : 1), st) != cudaSuccess) {
+    if (scratch_alloc(&p, sizeof(T) * (size_t)(count > 0 ? count : 1), st) != cudaSuccess) {
       ok = false;
       return nullptr;
     }
@@ -1223,7 +1223,7 @@ int sbr_cir_visibility(const SbrScene* scene, const SbrCirParams* P, const SbrVe
     return set_error(SBR_ERR_INVALID, "visibility slab larger than 2^31 vertices");
   cudaStream_t st = (cudaStream_t)stream;
   unsigned long long* work = nullptr;
-  if (cudaMallocAsync(&work, sizeof(unsigned long long), st) != cudaSuccess)
+  if (scratch_alloc((void**)&work, sizeof(unsigned long long), st) != cudaSuccess)
     return set_error(SBR_ERR_NOMEM, "work counter");
   cudaMemsetAsync(work, 0, sizeof(unsigned long long), st);
   int dev = 0, sms = 148, per_sm = 0;
@@ -1235,7 +1235,7 @@ int sbr_cir_visibility(const SbrScene* scene, const SbrCirParams* P, const SbrVe
   int* ghint = nullptr;
   if (kVisGHints > 0) {
     const size_t gb = sizeof(int) * (size_t)P->n_targets * kVisGHints;
-    if (cudaMallocAsync(&ghint, gb, st) != cudaSuccess) {
+    if (scratch_alloc((void**)&ghint, gb, st) != cudaSuccess) {
       cudaFreeAsync(work, st);
       return set_error(SBR_ERR_NOMEM, "occluder hints");
     }
@@ -1244,9 +1244,9 @@ int sbr_cir_visibility(const SbrScene* scene, const SbrCirParams* P, const SbrVe
   const int64_t nvs = v_end - v_begin;
   double *vpt = nullptr, *vnr = nullptr;
   uint8_t* vcode = nullptr;
-  if (cudaMallocAsync(&vpt, sizeof(double) * 3 * nvs, st) != cudaSuccess ||
-      cudaMallocAsync(&vnr, sizeof(double) * 3 * nvs, st) != cudaSuccess ||
-      cudaMallocAsync(&vcode, nvs, st) != cudaSuccess) {
+  if (scratch_alloc((void**)&vpt, sizeof(double) * 3 * nvs, st) != cudaSuccess ||
+      scratch_alloc((void**)&vnr, sizeof(double) * 3 * nvs, st) != cudaSuccess ||
+      scratch_alloc((void**)&vcode, nvs, st) != cudaSuccess) {
     if (vpt) cudaFreeAsync(vpt, st);
     if (vnr) cudaFreeAsync(vnr, st);
     cudaFreeAsync(work, st);

@@ -900,8 +900,11 @@ __device__ __forceinline__ bool occluded_segment(const DevScene& S, double3 a, d
 
 // kernel-launch evidence counter (host side, defined in sbr_scene.cu)
 void count_launch();
-// default-pool release threshold = keep (sbr_scene.cu)
-void keep_pool_mapped(int device);
+// stream-ordered scratch from the library's own memory pool on the current
+// device (sbr_scene.cu): never the device's default pool, so the process's
+// other allocators are unaffected; freed blocks stay mapped up to a finite
+// release threshold and sbr_release_scratch() trims the pool to zero
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st);
 // optional CUDA-event timing of individual launches (sbr_profile_enable)
 void prof_begin(void* stream, const char* name);
 void prof_end(void* stream);

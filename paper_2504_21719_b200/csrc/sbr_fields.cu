@@ -483,17 +483,15 @@ int sbr_cfr(const double* gain, const double* delay, const double* dep, const do
     return launch_status("sbr_cfr memset");
   }
   const double kw = kTwoPi / wavelength;
-  int device = 0;
-  if (cudaGetDevice(&device) == cudaSuccess) keep_pool_mapped(device);
   double *u_rx = nullptr, *u_tx = nullptr, *E = nullptr, *W = nullptr;
   const size_t c16 = 2 * sizeof(double);
   cudaError_t e = cudaSuccess;
   if (synthetic) {
-    e = cudaMallocAsync(&u_rx, c16 * nrx * np, st);
-    if (e == cudaSuccess) e = cudaMallocAsync(&u_tx, c16 * ntx * np, st);
+    e = scratch_alloc((void**)&u_rx, c16 * nrx * np, st);
+    if (e == cudaSuccess) e = scratch_alloc((void**)&u_tx, c16 * ntx * np, st);
   }
-  if (e == cudaSuccess) e = cudaMallocAsync(&E, c16 * np * nf, st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&W, c16 * rows * np, st);
+  if (e == cudaSuccess) e = scratch_alloc((void**)&E, c16 * np * nf, st);
+  if (e == cudaSuccess) e = scratch_alloc((void**)&W, c16 * rows * np, st);
   int rc = SBR_OK;
   if (e != cudaSuccess) {
     rc = set_error(SBR_ERR_CUDA, std::string("sbr_cfr scratch: ") + cudaGetErrorString(e));

@@ -655,7 +655,7 @@ int wave_alloc(int64_t cap, cudaStream_t st, Wave* w) {
   const size_t per_squeue = (size_t)cap * (21 * sizeof(double) + sizeof(int32_t));
   const size_t bytes = 2 * per_queue + per_squeue +
                        (size_t)cap * (sizeof(double) + sizeof(int32_t)) + 512;
-  if (cudaMallocAsync(&w->block, bytes, st) != cudaSuccess)
+  if (scratch_alloc(&w->block, bytes, st) != cudaSuccess)
     return set_error(SBR_ERR_NOMEM, "ray queues");
   char* p = (char*)w->block;
   for (int k = 0; k < 2; ++k) {

@@ -14,9 +14,11 @@
 #include <cub/cub.cuh>
 
 #include <atomic>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -29,15 +31,58 @@ static thread_local std::string g_last_error;
 static std::atomic<uint64_t> g_launches{0};
 
 // The library's stream-ordered scratch (ray queues, sort buffers, CFR
-// factors) comes from the device's default pool: keep freed blocks mapped
-// between calls instead of unmapping them at every synchronisation.
-void keep_pool_mapped(int device) {
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-    uint64_t keep = ~0ULL;
+// factors) comes from a private memory pool per device.  Freed blocks stay
+// mapped between calls up to kScratchKeep bytes (a config-4 wavefront pass
+// needs ~7.4 GB; remapping it at every synchronisation costs ~ms), anything
+// above is returned to the driver at the next synchronisation, and
+// sbr_release_scratch() trims the pool to zero.  The device's default pool
+// (used by other libraries in the process) is never touched.
+constexpr uint64_t kScratchKeep = 16ULL << 30;
+constexpr int kMaxDevices = 64;
+static std::mutex g_pool_mu;
+static cudaMemPool_t g_pools[kMaxDevices] = {};
+
+static cudaError_t scratch_pool(int device, cudaMemPool_t* out) {
+  if (device < 0 || device >= kMaxDevices) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_pools[device]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t pool;
+    const cudaError_t e = cudaMemPoolCreate(&pool, &props);
+    if (e != cudaSuccess) return e;
+    uint64_t keep = kScratchKeep;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    g_pools[device] = pool;
   }
+  *out = g_pools[device];
+  return cudaSuccess;
 }
+
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st) {
+  int device = 0;
+  cudaError_t e = cudaGetDevice(&device);
+  cudaMemPool_t pool;
+  if (e == cudaSuccess) e = scratch_pool(device, &pool);
+  if (e != cudaSuccess) return e;
+  return cudaMallocFromPoolAsync(p, bytes ? bytes : 1, pool, st);
+}
+
+// cudaSetDevice for the duration of a scope, restoring the caller's device
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int device) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != device) cudaSetDevice(device);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
@@ -557,11 +602,34 @@ __global__ void k_ploc_leaves(const int32_t* __restrict__ off, const Box32* __re
 
 static std::atomic<int> g_builder{1};  // 0 = Karras LBVH, 1 = PLOC
 
+// persistent scene buffer (freed by sbr_scene_destroy)
 template <typename T>
-static int dalloc(T** p, size_t count, cudaStream_t st) {
-  SBR_CUDA(cudaMallocAsync((void**)p, sizeof(T) * (count ? count : 1), st));
+static int palloc(T** p, size_t count) {
+  SBR_CUDA(cudaMalloc((void**)p, sizeof(T) * (count ? count : 1)));
   return SBR_OK;
 }
+
+// stream-ordered build scratch, released (in stream order) on every exit path
+struct ScratchArena {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit ScratchArena(cudaStream_t s) : st(s) {}
+  ScratchArena(const ScratchArena&) = delete;
+  ScratchArena& operator=(const ScratchArena&) = delete;
+  template <typename T>
+  int get(T** p, size_t count) {
+    void* q = nullptr;
+    const cudaError_t e = scratch_alloc(&q, sizeof(T) * (count ? count : 1), st);
+    if (e != cudaSuccess)
+      return set_error(SBR_ERR_NOMEM, std::string("scene build scratch: ") + cudaGetErrorString(e));
+    ptrs.push_back(q);
+    *p = (T*)q;
+    return SBR_OK;
+  }
+  ~ScratchArena() {
+    for (void* q : ptrs) cudaFreeAsync(q, st);
+  }
+};
 
 static inline unsigned grid_for(int64_t n, int block) {
   return (unsigned)((n + block - 1) / block);
@@ -605,34 +673,47 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
   *out = nullptr;
   if (ntri <= 0) return set_error(SBR_ERR_EMPTY_SCENE, "no triangles");
   if (ntri >= (1LL << 29)) return set_error(SBR_ERR_INVALID, "too many triangles");
-  SBR_CUDA(cudaSetDevice(device));
-  keep_pool_mapped(device);
-  cudaStream_t st = (cudaStream_t)stream;
-  const int n = (int)ntri;
-  SbrScene* S = new SbrScene();
-  S->device = device;
-  S->ntri = ntri;
-
+  if (!v0 || !v1 || !v2) return set_error(SBR_ERR_INVALID, "NULL vertex array");
   double max_abs = 0.0;
-  for (int k = 0; k < 3; ++k) {
-    S->lo[k] = v0[k];
-    S->hi[k] = v0[k];
-  }
+  double lo[3] = {v0[0], v0[1], v0[2]}, hi[3] = {v0[0], v0[1], v0[2]};
   for (int64_t i = 0; i < 3 * ntri; ++i) {
+    // a non-finite corner makes every merge cost inf / NaN (PLOC would never
+    // pair its cluster) and every ray test meaningless: reject up front
+    if (!std::isfinite(v0[i]) || !std::isfinite(v1[i]) || !std::isfinite(v2[i]))
+      return set_error(SBR_ERR_INVALID, "non-finite vertex coordinate in triangle " +
+                                            std::to_string(i / 3));
     max_abs = fmax(max_abs, fabs(v0[i]));
     max_abs = fmax(max_abs, fabs(v1[i]));
     max_abs = fmax(max_abs, fabs(v2[i]));
     const int k = (int)(i % 3);
-    S->lo[k] = fmin(S->lo[k], fmin(fmin(v0[i], v1[i]), v2[i]));
-    S->hi[k] = fmax(S->hi[k], fmax(fmax(v0[i], v1[i]), v2[i]));
+    lo[k] = fmin(lo[k], fmin(fmin(v0[i], v1[i]), v2[i]));
+    hi[k] = fmax(hi[k], fmax(fmax(v0[i], v1[i]), v2[i]));
+  }
+  DeviceGuard dg(device);
+  {
+    int cur = -1;
+    SBR_CUDA(cudaGetDevice(&cur));
+    if (cur != device) return set_error(SBR_ERR_CUDA, "cannot select device " + std::to_string(device));
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = (int)ntri;
+  // the scene is destroyed (every persistent buffer freed) on any early
+  // return; the scratch arena frees its buffers (stream-ordered) on every exit
+  std::unique_ptr<SbrScene, void (*)(SbrScene*)> owner(new SbrScene(), sbr_scene_destroy);
+  SbrScene* S = owner.get();
+  ScratchArena A(st);
+  S->device = device;
+  S->ntri = ntri;
+  for (int k = 0; k < 3; ++k) {
+    S->lo[k] = lo[k];
+    S->hi[k] = hi[k];
   }
   S->pad_base = (float)(ldexp(max_abs + 1.0, -26));  // box_setup's pad floor
 
   double *dv0, *dv1, *dv2;
   const size_t bytes = sizeof(double) * 3 * (size_t)ntri;
   int rc;
-  if ((rc = dalloc(&dv0, 3 * ntri, st)) || (rc = dalloc(&dv1, 3 * ntri, st)) ||
-      (rc = dalloc(&dv2, 3 * ntri, st)))
+  if ((rc = A.get(&dv0, 3 * ntri)) || (rc = A.get(&dv1, 3 * ntri)) || (rc = A.get(&dv2, 3 * ntri)))
     return rc;
   SBR_CUDA(cudaMemcpyAsync(dv0, v0, bytes, cudaMemcpyHostToDevice, st));
   SBR_CUDA(cudaMemcpyAsync(dv1, v1, bytes, cudaMemcpyHostToDevice, st));
@@ -642,9 +723,8 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
   unsigned int* cb;
   uint64_t *keys, *keys_sorted;
   int32_t *ids, *ids_sorted;
-  if ((rc = dalloc(&cen, n, st)) || (rc = dalloc(&cb, 6, st)) || (rc = dalloc(&keys, n, st)) ||
-      (rc = dalloc(&keys_sorted, n, st)) || (rc = dalloc(&ids, n, st)) ||
-      (rc = dalloc(&ids_sorted, n, st)))
+  if ((rc = A.get(&cen, n)) || (rc = A.get(&cb, 6)) || (rc = A.get(&keys, n)) ||
+      (rc = A.get(&keys_sorted, n)) || (rc = A.get(&ids, n)) || (rc = A.get(&ids_sorted, n)))
     return rc;
   const unsigned init[6] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0u, 0u, 0u};
   SBR_CUDA(cudaMemcpyAsync(cb, init, sizeof init, cudaMemcpyHostToDevice, st));
@@ -655,8 +735,8 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
   size_t tmp_bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys_sorted, ids, ids_sorted, n, 0,
                                   64, st);
-  void* tmp;
-  SBR_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+  char* tmp;
+  if ((rc = A.get(&tmp, tmp_bytes))) return rc;
   SBR_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_sorted, ids, ids_sorted,
                                            n, 0, 64, st));
   count_launch();
@@ -666,27 +746,23 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
   int *parent_int, *parent_leaf, *keep, *compact;
   Box32 *leaf_box, *int_box;
   unsigned int* visits;
-  if ((rc = dalloc(&children, nint, st)) || (rc = dalloc(&ranges, nint, st)) ||
-      (rc = dalloc(&parent_int, nint, st)) || (rc = dalloc(&parent_leaf, n, st)) ||
-      (rc = dalloc(&keep, nint, st)) || (rc = dalloc(&compact, nint, st)) ||
-      (rc = dalloc(&leaf_box, n, st)) || (rc = dalloc(&int_box, nint, st)) ||
-      (rc = dalloc(&visits, nint, st)))
+  if ((rc = A.get(&children, nint)) || (rc = A.get(&ranges, nint)) ||
+      (rc = A.get(&parent_int, nint)) || (rc = A.get(&parent_leaf, n)) ||
+      (rc = A.get(&keep, nint)) || (rc = A.get(&compact, nint)) || (rc = A.get(&leaf_box, n)) ||
+      (rc = A.get(&int_box, nint)) || (rc = A.get(&visits, nint)))
     return rc;
   int32_t* ids_leaf = ids_sorted;  // triangle of each leaf slot
-  int32_t* ids_dfs = nullptr;
   if (g_builder == 1 && n > 1) {
     // ---- PLOC hierarchy, exported in depth-first leaf order ----
     const int total = 2 * n - 1;
     Box32* box_all;
     int2* kids;
-    int32_t *C, *C2, *nearest, *flag, *pos, *parent, *cnt, *off;
+    int32_t *C, *C2, *nearest, *flag, *pos, *parent, *cnt, *off, *ids_dfs;
     unsigned* vis2;
-    if ((rc = dalloc(&box_all, total, st)) || (rc = dalloc(&kids, nint, st)) ||
-        (rc = dalloc(&C, n, st)) || (rc = dalloc(&C2, n, st)) || (rc = dalloc(&nearest, n, st)) ||
-        (rc = dalloc(&flag, n + 1, st)) || (rc = dalloc(&pos, n + 1, st)) ||
-        (rc = dalloc(&parent, total, st)) || (rc = dalloc(&cnt, total, st)) ||
-        (rc = dalloc(&off, total, st)) || (rc = dalloc(&vis2, nint, st)) ||
-        (rc = dalloc(&ids_dfs, n, st)))
+    if ((rc = A.get(&box_all, total)) || (rc = A.get(&kids, nint)) || (rc = A.get(&C, n)) ||
+        (rc = A.get(&C2, n)) || (rc = A.get(&nearest, n)) || (rc = A.get(&flag, n + 1)) ||
+        (rc = A.get(&pos, n + 1)) || (rc = A.get(&parent, total)) || (rc = A.get(&cnt, total)) ||
+        (rc = A.get(&off, total)) || (rc = A.get(&vis2, nint)) || (rc = A.get(&ids_dfs, n)))
       return rc;
     k_leaf_boxes<<<grid_for(n, 256), 256, 0, st>>>(dv0, dv1, dv2, ids_sorted, n, box_all);
     count_launch();
@@ -695,8 +771,8 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
     SBR_CUDA(cudaMemsetAsync(parent, 0xff, sizeof(int32_t) * total, st));
     size_t sb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, sb, flag, pos, n + 1, st);
-    void* stmp;
-    SBR_CUDA(cudaMallocAsync(&stmp, sb, st));
+    char* stmp;
+    if ((rc = A.get(&stmp, sb))) return rc;
     int m = n, base = n;
     while (m > 1) {
       k_ploc_nearest<<<grid_for(m, 128), 128, 0, st>>>(C, m, box_all, nearest);
@@ -710,7 +786,13 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
       int m_new = 0;
       SBR_CUDA(cudaMemcpyAsync(&m_new, pos + m, sizeof(int), cudaMemcpyDeviceToHost, st));
       SBR_CUDA(cudaStreamSynchronize(st));
+      SBR_CUDA(cudaGetLastError());
       for (int q = 0; q < 7; ++q) count_launch();
+      // every pass merges at least the globally cheapest mutual pair, so m
+      // shrinks unless the merge costs are not comparable (NaN boxes)
+      if (m_new >= m || m_new < 1)
+        return set_error(SBR_ERR_INVALID, "PLOC build made no progress (" + std::to_string(m) +
+                                              " clusters left): non-comparable triangle boxes");
       base += m - m_new;
       m = m_new;
       int32_t* t = C;
@@ -726,18 +808,6 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
                                                     ids_dfs);
     for (int q = 0; q < 4; ++q) count_launch();
     ids_leaf = ids_dfs;
-    cudaFreeAsync(stmp, st);
-    cudaFreeAsync(box_all, st);
-    cudaFreeAsync(kids, st);
-    cudaFreeAsync(C, st);
-    cudaFreeAsync(C2, st);
-    cudaFreeAsync(nearest, st);
-    cudaFreeAsync(flag, st);
-    cudaFreeAsync(pos, st);
-    cudaFreeAsync(parent, st);
-    cudaFreeAsync(cnt, st);
-    cudaFreeAsync(off, st);
-    cudaFreeAsync(vis2, st);
   } else {
     if (nint) {
       SBR_CUDA(cudaMemsetAsync(visits, 0, sizeof(unsigned) * nint, st));
@@ -757,8 +827,8 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
     count_launch();
     size_t scan_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, keep, compact, nint, st);
-    void* scan_tmp;
-    SBR_CUDA(cudaMallocAsync(&scan_tmp, scan_bytes, st));
+    char* scan_tmp;
+    if ((rc = A.get(&scan_tmp, scan_bytes))) return rc;
     SBR_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, keep, compact, nint, st));
     count_launch();
     int last_c = 0, last_k = 0;
@@ -766,9 +836,8 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
     SBR_CUDA(cudaMemcpyAsync(&last_k, keep + nint - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
     SBR_CUDA(cudaStreamSynchronize(st));
     nnodes = last_c + last_k;
-    SBR_CUDA(cudaFreeAsync(scan_tmp, st));
   }
-  if ((rc = dalloc(&S->nodes, nnodes, st))) return rc;
+  if ((rc = palloc(&S->nodes, nnodes))) return rc;
   if (n > 4) {
     k_emit<<<grid_for(nint, 256), 256, 0, st>>>(children, ranges, keep, compact, leaf_box,
                                                 int_box, nint, S->nodes);
@@ -778,7 +847,7 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
   count_launch();
   S->nnodes = nnodes;
 
-  if ((rc = dalloc(&S->tris, n, st))) return rc;
+  if ((rc = palloc(&S->tris, n))) return rc;
   k_gather_tris<<<grid_for(n, 256), 256, 0, st>>>(dv0, dv1, dv2, ids_leaf, n, S->tris);
   count_launch();
 
@@ -786,48 +855,25 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
   std::vector<int32_t> ids_host(n);
   SBR_CUDA(cudaMemcpyAsync(ids_host.data(), ids_leaf, sizeof(int32_t) * n,
                            cudaMemcpyDeviceToHost, st));
-  if ((rc = dalloc(&S->error_word, 1, st))) return rc;
-  SBR_CUDA(cudaMemsetAsync(S->error_word, 0, sizeof(unsigned), st));
   // default per-slot tables
-  if ((rc = dalloc(&S->tie_rank, n, st)) || (rc = dalloc(&S->normals, 3 * (size_t)n, st)) ||
-      (rc = dalloc(&S->matrow, n, st)) || (rc = dalloc(&S->hash_r, n, st)) ||
-      (rc = dalloc(&S->hash_f, n, st)))
+  if ((rc = palloc(&S->error_word, 1)) || (rc = palloc(&S->tie_rank, n)) ||
+      (rc = palloc(&S->normals, 3 * (size_t)n)) || (rc = palloc(&S->matrow, n)) ||
+      (rc = palloc(&S->hash_r, n)) || (rc = palloc(&S->hash_f, n)))
     return rc;
+  SBR_CUDA(cudaMemsetAsync(S->error_word, 0, sizeof(unsigned), st));
   SBR_CUDA(cudaMemsetAsync(S->matrow, 0, sizeof(int32_t) * n, st));
   SBR_CUDA(cudaMemsetAsync(S->hash_r, 0, sizeof(uint64_t) * n, st));
   SBR_CUDA(cudaMemsetAsync(S->hash_f, 0, sizeof(uint64_t) * n, st));
   SBR_CUDA(cudaStreamSynchronize(st));
-  for (int i = 0; i < n; ++i) S->perm[i] = ids_host[i];
-
-  cudaFreeAsync(dv0, st);
-  cudaFreeAsync(dv1, st);
-  cudaFreeAsync(dv2, st);
-  cudaFreeAsync(cen, st);
-  cudaFreeAsync(cb, st);
-  cudaFreeAsync(keys, st);
-  cudaFreeAsync(keys_sorted, st);
-  cudaFreeAsync(ids, st);
-  cudaFreeAsync(ids_sorted, st);
-  cudaFreeAsync(tmp, st);
-  cudaFreeAsync(children, st);
-  cudaFreeAsync(ranges, st);
-  cudaFreeAsync(parent_int, st);
-  cudaFreeAsync(parent_leaf, st);
-  cudaFreeAsync(keep, st);
-  cudaFreeAsync(compact, st);
-  cudaFreeAsync(leaf_box, st);
-  cudaFreeAsync(int_box, st);
-  cudaFreeAsync(visits, st);
-  if (ids_dfs) cudaFreeAsync(ids_dfs, st);
-  SBR_CUDA(cudaStreamSynchronize(st));
   SBR_CUDA(cudaGetLastError());
-  *out = S;
+  for (int i = 0; i < n; ++i) S->perm[i] = ids_host[i];
+  *out = owner.release();
   return SBR_OK;
 }
 
 void sbr_scene_destroy(SbrScene* S) {
   if (!S) return;
-  cudaSetDevice(S->device);
+  DeviceGuard dg(S->device);  // the caller's current device is restored on return
   cudaFree(S->nodes);
   cudaFree(S->tris);
   cudaFree(S->tie_rank);
@@ -839,6 +885,24 @@ void sbr_scene_destroy(SbrScene* S) {
   cudaFree(S->error_word);
   cudaFree(S->wedge_block);
   delete S;
+}
+
+int sbr_release_scratch(int32_t device) {
+  int count = 0;
+  SBR_CUDA(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count || device >= kMaxDevices)
+    return set_error(SBR_ERR_INVALID, "bad device");
+  cudaMemPool_t pool = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    pool = g_pools[device];
+  }
+  if (pool) {
+    DeviceGuard dg(device);
+    SBR_CUDA(cudaDeviceSynchronize());
+    SBR_CUDA(cudaMemPoolTrimTo(pool, 0));
+  }
+  return SBR_OK;
 }
 
 int64_t sbr_scene_num_triangles(const SbrScene* S) { return S ? S->ntri : 0; }

@@ -1,0 +1,232 @@
+"""GPU parity at the BASELINE.json configs' stated sizes.
+
+Each test runs the benchmarked configuration through the public API and
+compares it with the oracle (oracle/sbr_oracle.c, pinned to the real
+reference by tests/golden/*) run on all host threads -- the oracle's CIR
+sweep / visibility rows split over pthreads with results identical to one
+thread (oracle.set_threads) -- or, where the oracle cannot finish the full
+size in a test (config 4: 3e9 ray-bounces), on whole RNG chunks spread over
+the full lattice plus size-independent properties of the full map.
+
+Bars: counters and path sets exact; gains / delays 1e-6 relative (the north
+star allows 1e-4); map cells 1e-9 relative on >= 99.9 % of cells and 1e-3 on
+all (float64 atomics reorder sums; CUDA libm differs from glibc by an ulp at
+rare decision boundaries), exact counters.
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2504_21719_b200 import (PathConfig, RadioDevice, SceneModel, _abi, compute_paths,
+                                   compute_radio_map_sbr, frequency_response, make_pattern,
+                                   scenes)
+from paper_2504_21719_b200.em import planar_array
+from paper_2504_21719_b200.radiomap import MeasurementGrid, RadioMapConfig
+from paper_2504_21719_b200.sampling import Interaction
+
+pytestmark = pytest.mark.gpu
+
+R = frozenset({Interaction.REFLECTION})
+RS = frozenset({Interaction.REFLECTION, Interaction.SCATTERING})
+MAP_KEYS = ("deposits", "escaped", "respawns", "ray_bounces", "terminated")
+THREADS = max(1, len(os.sched_getaffinity(0)))
+
+
+@pytest.fixture
+def oracle_threads():
+    oracle.set_threads(THREADS)
+    yield THREADS
+    oracle.set_threads(1)
+
+
+@pytest.fixture(scope="module")
+def city():
+    meshes = scenes.city()
+    return meshes
+
+
+def _compare_map(vals, want, tight=1e-9, frac=0.999, loose=1e-3):
+    nz = (want != 0) | (vals != 0)
+    assert nz.any()
+    rel = np.abs(vals[nz] - want[nz]) / np.maximum(np.abs(want[nz]), 1e-300)
+    assert np.mean(rel < tight) >= frac, (np.mean(rel < tight), rel.max())
+    assert rel.max() < loose, rel.max()
+    return rel.max()
+
+
+def _compare_paths(ps, want, wdiag):
+    for k, v in wdiag.items():
+        if k == "refinement_rejections":
+            assert ps.diagnostics[k] == v
+        elif k == "hash_load_factor":
+            assert ps.diagnostics[k] == pytest.approx(v, rel=1e-12)
+        else:
+            assert ps.diagnostics.get(k, 0) == v, k
+    T = ps.tensors
+    assert len(T) == len(want["delay"]) > 0
+    for k in ("rx", "rx_el", "tx", "tx_el", "depth", "sample"):
+        assert np.array_equal(getattr(T, k), want[k]), k
+    assert np.array_equal(T.chain_hash.astype(np.uint64), want["chain_hash"].astype(np.uint64))
+    L = want["kind"].shape[1]
+    kind = np.where(np.arange(T.kind.shape[1])[None, :] < T.depth[:, None], T.kind, -1)[:, :L]
+    assert np.array_equal(kind, want["kind"])
+    assert np.array_equal(np.where(kind >= 0, T.obj[:, :L], -1), want["obj"])
+    assert np.array_equal(np.where(kind >= 0, T.prim[:, :L], -1), want["prim"])
+    np.testing.assert_allclose(T.delay, want["delay"], rtol=1e-12)
+    rel = np.abs(T.gain - want["gain"]) / np.maximum(np.abs(want["gain"]), 1e-300)
+    assert rel.max(initial=0.0) < 1e-6, rel.max()
+    Lv = min(T.vertices.shape[1], want["vertices"].shape[1])
+    used = np.arange(Lv)[None, :] <= (T.depth[:, None] + 1)   # source, vertices, target
+    np.testing.assert_allclose(T.vertices[:, :Lv][used], want["vertices"][:, :Lv][used],
+                               rtol=0, atol=1e-9)
+
+
+def _config3(samples):
+    rx = [RadioDevice(position=p) for p in scenes.city_receivers(1024)]
+    tx = RadioDevice(position=np.array([0.0, 0.0, 30.0]))
+    cfg = PathConfig(num_samples=samples, max_depth=5, q_diffraction=0.0, enabled=R,
+                     buffer_capacity=2 ** 24)
+    return tx, rx, cfg
+
+
+def test_config3_1e4_reproduces_reference_counts(cuda, city, oracle_threads):
+    """Config 3 (city, 1 Tx x 1024 Rx, depth 5, {R}, N_B = 2^24) at N_S = 1e4:
+    the counts the real reference (emtrace) produced in SURVEY §6 / VERDICT r01
+    -- 255 paths, 65,679 candidates, 263,769 duplicates, 64,088 coplanar-miss
+    and 1,336 occluded rejections -- and the oracle's path set, exactly."""
+    mats = scenes.uniform_materials(city, scenes.concrete())
+    tx, rx, cfg = _config3(10_000)
+    ps = compute_paths(SceneModel(city, mats), [tx], rx, cfg)
+    d = ps.diagnostics
+    assert d["paths"] == 255
+    assert d["candidates"] == 65_679
+    assert d["duplicates"] == 263_769
+    assert d["refinement_rejections"] == {"coplanar-miss": 64_088, "occluded": 1_336}
+    want, wdiag = oracle.OracleScene(city, mats).compute_paths([tx], rx, cfg)
+    _compare_paths(ps, want, wdiag)
+
+
+def test_config3_full_size_vs_oracle(cuda, city, oracle_threads):
+    """Config 3 at its stated size, N_S = 1e6 (the benchmarked solve: 1.2e9
+    visibility rays, ~33 M visible rows, ~3e5 candidates): every counter, the
+    deduplicated path set and the gains against the oracle."""
+    mats = scenes.uniform_materials(city, scenes.concrete())
+    tx, rx, cfg = _config3(1_000_000)
+    ps = compute_paths(SceneModel(city, mats), [tx], rx, cfg)
+    want, wdiag = oracle.OracleScene(city, mats).compute_paths([tx], rx, cfg)
+    _compare_paths(ps, want, wdiag)
+
+
+def test_config2_full_map_vs_oracle(cuda):
+    """Config 2 at its stated size: the whole 1e7-ray street-canyon map ({R,S},
+    depth 5, 200 x 200 cells of 1 m, direct term included) against the oracle
+    over the same 1e7 rays on all host threads."""
+    meshes = scenes.street_canyon()
+    mats = scenes.uniform_materials(meshes, scenes.concrete(scattering=0.3))
+    grid = MeasurementGrid((0.0, 0.0, 1.5), (1, 0, 0), (0, 1, 0), (1.0, 1.0), (200, 200))
+    cfg = RadioMapConfig(num_samples=10_000_000, max_depth=5, enabled=RS, seed=0)
+    src = np.array([0.0, 5.0, 20.0])
+    vals, diag = compute_radio_map_sbr(SceneModel(meshes, mats), src, grid, cfg)
+    want, wdiag = oracle.OracleScene(meshes, mats).radiomap_threaded(src, grid, cfg, THREADS)
+    for key in MAP_KEYS + ("direct_visible",):
+        assert diag.get(key, 0) == wdiag[key], key
+    assert diag["ray_bounces"] == 31_731_774   # the bench's per-map count
+    _compare_map(vals, want)
+
+
+def _config4(city):
+    mats = scenes.uniform_materials(city, scenes.concrete(scattering=0.3))
+    grid = MeasurementGrid((0.0, 0.0, 1.5), (1, 0, 0), (0, 1, 0), (1.0, 1.0), (1000, 1000))
+    cfg = RadioMapConfig(num_samples=1_000_000_000, max_depth=5, enabled=RS, seed=0)
+    return mats, grid, cfg, np.array([0.0, 0.0, 30.0])
+
+
+def test_config4_rng_chunks_across_lattice_vs_oracle(cuda, city):
+    """Config 4 (1e9-ray city map): 8 whole 2^19-sample RNG chunks spread from
+    pole to pole of the full lattice (4.2 M rays, ~13 M ray-bounces), each
+    traced as a sample range of the 1e9-ray configuration, vs the oracle."""
+    mats, grid, cfg, src = _config4(city)
+    scene = SceneModel(city, mats)
+    osc = oracle.OracleScene(city, mats)
+    n_chunks = -(-cfg.num_samples // (1 << 19))
+    chunks = [int(c) for c in np.linspace(0, n_chunks - 1, 8)]
+    from concurrent.futures import ThreadPoolExecutor
+
+    def ref(c):
+        rg = (c << 19, min((c + 1) << 19, cfg.num_samples))
+        return osc.radiomap(src, grid, cfg, sample_range=rg, include_direct=False)
+
+    with ThreadPoolExecutor(max_workers=THREADS) as pool:
+        wants = list(pool.map(ref, chunks))
+    for c, (want, wdiag) in zip(chunks, wants):
+        rg = (c << 19, min((c + 1) << 19, cfg.num_samples))
+        vals, diag = compute_radio_map_sbr(scene, src, grid, cfg, sample_range=rg,
+                                           include_direct=False)
+        for key in MAP_KEYS:
+            assert diag.get(key, 0) == wdiag[key], (c, key)
+        if wdiag["deposits"]:
+            _compare_map(vals, want)
+
+
+def test_config4_full_map_properties(cuda, city):
+    """The full 1e9-ray config-4 map (3.05e9 ray-bounces), size-independent
+    checks: (a) the two chunk-cyclic shards sum to the one-call map with
+    identical counters (the multi-GPU contract), (b) counters are deterministic
+    across runs and cells agree to float64 summation order, (c) the ray-bounce
+    count equals the bench's, (d) the map is the sum of its sample ranges
+    (linearity), checked on the 1e9 lattice split at a non-chunk boundary."""
+    mats, grid, cfg, src = _config4(city)
+    scene = SceneModel(city, mats)
+    full, c_full = compute_radio_map_sbr(scene, src, grid, cfg, return_tensors=True)
+    again, c_again = compute_radio_map_sbr(scene, src, grid, cfg, return_tensors=True)
+    assert torch.equal(c_full, c_again)
+    torch.testing.assert_close(again, full, rtol=1e-12, atol=0)
+    rb = int(c_full[_abi.MAP_COUNTERS.index("ray_bounces")].item())
+    assert rb == 3_051_262_497
+    acc = torch.zeros_like(full)
+    cnt = torch.zeros_like(c_full)
+    for r in range(2):
+        v, c = compute_radio_map_sbr(scene, src, grid, cfg, shard=(r, 2),
+                                     include_direct=(r == 0), return_tensors=True)
+        acc += v
+        cnt += c
+    assert torch.equal(cnt, c_full)
+    torch.testing.assert_close(acc, full, rtol=1e-12, atol=0)
+    cut = 387_654_321
+    a, ca = compute_radio_map_sbr(scene, src, grid, cfg, sample_range=(0, cut),
+                                  return_tensors=True)
+    b, cb = compute_radio_map_sbr(scene, src, grid, cfg, sample_range=(cut, cfg.num_samples),
+                                  include_direct=False, return_tensors=True)
+    assert torch.equal(ca + cb - c_full, torch.zeros_like(c_full))
+    torch.testing.assert_close(a + b, full, rtol=1e-12, atol=0)
+    # the map is physical: non-negative, finite, and the bounce estimator reached
+    # a large share of the 1e6 cells
+    h = full.cpu().numpy()
+    assert np.all(np.isfinite(h)) and np.all(h >= 0)
+    assert np.count_nonzero(h) > 500_000
+
+
+def test_config5_full_size_vs_oracle(cuda, city, oracle_threads):
+    """Config 5 at the benchmarked size: city, 8x8 TR 38.901 Tx panel, 4x4 Rx
+    panel (synthetic arrays), depth 6, N_S = 1e6, CFR over 1024 subcarriers
+    (3.5 GHz +- 512 x 30 kHz): path set exact, gains 1e-6, H to 1e-9 of max|H|."""
+    mats = scenes.uniform_materials(city, scenes.concrete())
+    lam = 299792458.0 / 3.5e9
+    tx = RadioDevice(position=np.array([0.0, 0.0, 30.0]), pattern=make_pattern("tr38901"),
+                     array=planar_array(8, 8, lam / 2, lam / 2))
+    rx = RadioDevice(position=np.array([2.0, 60.0, 1.5]),
+                     array=planar_array(4, 4, lam / 2, lam / 2))
+    cfg = PathConfig(num_samples=1_000_000, max_depth=6, q_diffraction=0.0, enabled=R)
+    freqs = 3.5e9 + (np.arange(1024) - 512) * 30e3
+    ps = compute_paths(SceneModel(city, mats), [tx], [rx], cfg)
+    H = frequency_response(ps, freqs)
+    want, wdiag = oracle.OracleScene(city, mats).compute_paths([tx], [rx], cfg)
+    _compare_paths(ps, want, wdiag)
+    Hw = oracle.frequency_response(want, cfg, tx, rx, freqs)
+    assert H.shape == Hw.shape == (16, 64, 1024)
+    err = np.abs(H - Hw).max() / np.abs(Hw).max()
+    assert err < 1e-9, err

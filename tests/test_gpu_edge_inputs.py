@@ -107,3 +107,54 @@ def test_cyclic_shards_with_fewer_chunks_than_ranks(cuda):
     assert rows[0].n > 0 and rows[1].n > 0 and rows[2].n == 0   # 2 chunks of 4096 ids
     kept = cir._local_rows(rows[2])
     assert kept[1].numel() == 0 and kept[2] == 0
+
+
+def test_non_finite_vertex_rejected_without_leak(cuda):
+    """A non-finite corner is rejected by sbr_scene_create (ValueError) instead
+    of spinning the PLOC build; the failed build leaks nothing and
+    leaves the caller's current device unchanged."""
+    import torch
+
+    from paper_2504_21719_b200 import _native
+    from paper_2504_21719_b200.geometry import Mesh
+    good = scenes.box_mesh((-3, -4, 0), (3, 4, 3), object_id=0)
+    for bad_value in (np.inf, -np.inf, np.nan):
+        v = good.vertices.copy()
+        v[2, 1] = bad_value
+        with pytest.raises(ValueError, match="non-finite"):
+            build_scene_accel([Mesh(v, good.triangles, object_id=0)])
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(20):
+        v = good.vertices.copy()
+        v[0, 0] = np.inf
+        with pytest.raises(ValueError):
+            build_scene_accel([Mesh(v, good.triangles, object_id=0)])
+    torch.cuda.synchronize()
+    _native.release_scratch(cuda)
+    assert torch.cuda.mem_get_info()[0] >= free0 - (8 << 20)
+    assert torch.cuda.current_device() == 0
+    # the library still works afterwards
+    acc = build_scene_accel([good])
+    t, tri, _, _ = acc.trace_batch(np.array([[0.0, 0.0, 1.0]]), np.array([[0.0, 0.0, -1.0]]))
+    assert tri[0] >= 0 and t[0] == pytest.approx(1.0)
+
+
+def test_release_scratch_returns_memory(cuda):
+    """sbr_release_scratch trims the library's private pool: a radio map's ray
+    queues are returned to the driver (and the next map still runs)."""
+    import torch
+
+    from paper_2504_21719_b200 import _native
+    sc = _room()
+    grid = MeasurementGrid((0.0, 0.0, 1.5), (1, 0, 0), (0, 1, 0), (0.5, 0.5), (8, 8))
+    cfg = RadioMapConfig(num_samples=4_000_000, max_depth=2, enabled=R)
+    v1, d1 = compute_radio_map_sbr(sc, (0.5, 0.5, 1.0), grid, cfg)
+    torch.cuda.synchronize()
+    held = torch.cuda.mem_get_info()[0]
+    _native.release_scratch(cuda)
+    freed = torch.cuda.mem_get_info()[0]
+    assert freed - held > (1 << 30)  # ~2 GB of queues for 4e6 samples
+    v2, d2 = compute_radio_map_sbr(sc, (0.5, 0.5, 1.0), grid, cfg)
+    assert d1 == d2
+    np.testing.assert_allclose(v2, v1, rtol=1e-12)  # float64 atomics: summation order only

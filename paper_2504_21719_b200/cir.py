@@ -841,7 +841,7 @@ def compute_paths_sharded(scene, transmitters, receivers, cfg, group=None):
     """
     import torch.distributed as dist
 
-    from .sharding import gather_rows, owned_records, shard_range
+    from .sharding import gather_rows, owned_records_device, shard_range
     torch = _torch()
     transmitters = list(transmitters)
     receivers = list(receivers)
@@ -883,13 +883,9 @@ def compute_paths_sharded(scene, transmitters, receivers, cfg, group=None):
                 dup = torch.tensor([n_dup], dtype=torch.int64, device=dev)
                 dist.all_reduce(dup, group=group)
                 sel_counters[_abi.CIR_COUNTERS.index("duplicates")] += dup[0]
-            pos, loc = owned_records(rec_row[:nrec].cpu().numpy(), offsets, rank)
-            if kept is not None:        # positions in the kept list -> shard row indices
-                loc = np.array(loc, dtype=np.int64)
-                m = loc >= 0
-                loc[m] = kept.cpu().numpy()[loc[m]]
-            loc_t = torch.from_numpy(np.ascontiguousarray(loc, dtype=np.int64)).to(dev)
-            recbuf = _materialize(R, loc_t, len(loc), cfg)
+            # records whose rows this rank produced (LoS on rank 0), on the device
+            loc_t, n_loc = owned_records_device(rec_row[:nrec], offsets, rank, kept)
+            recbuf = _materialize(R, loc_t, n_loc, cfg)
             sweep = R.counters.clone()
             if on and world > 1:
                 dist.all_reduce(sweep, group=group)
@@ -905,7 +901,7 @@ def compute_paths_sharded(scene, transmitters, receivers, cfg, group=None):
         for k, v in gdiag.items():
             if k != "hash_load_factor":
                 diagnostics[k] += v
-        cand = DeviceCandidates(scene, source, targets, R.targets_t, cfg, recbuf, len(loc),
+        cand = DeviceCandidates(scene, source, targets, R.targets_t, cfg, recbuf, n_loc,
                                 src_idx)
         cand.params = R.params
         part, rej = _paths_for_source(scene, cand, cfg, ti, te, transmitters[ti],

@@ -120,12 +120,14 @@ def shard_of_chunks(num_samples, rank, world, chunk=None):
 def gather_rows(tensors, group=None):
     """All-gather variable-length per-rank row arrays (CIR candidate exchange).
 
-    tensors: dict name -> tensor whose first dimension is this rank's row
-    count (same count for every entry).  Returns (gathered dict, offsets)
-    where rank r's rows occupy [offsets[r], offsets[r+1]).  One all_gather
-    of the counts, then one padded all_gather per array -- NCCL over NVLink
-    on the GPU box, gloo in the CPU tests.  uint64 payloads travel as int64
-    (bit-identical).
+    tensors: dict name -> 1-D tensor of this rank's rows (same length for
+    every entry; integer dtypes of <= 8 bytes).  Returns (gathered dict,
+    offsets) where rank r's rows occupy [offsets[r], offsets[r+1]).  Two
+    collectives in all: one all_gather of the row counts (read back with a
+    single host copy) and one all_gather of the rows packed as an (n, k)
+    int64 matrix -- for the CIR rows (key, pair_r, pair_f, chain) 32 B per
+    row -- padded to the largest rank.  NCCL over NVLink on the GPU box, gloo
+    in the CPU tests; uint64 payloads travel bit-identically as int64.
     """
     import torch
     import torch.distributed as dist
@@ -133,26 +135,56 @@ def gather_rows(tensors, group=None):
         n = next(iter(tensors.values())).shape[0]
         return dict(tensors), [0, n]
     world = dist.get_world_size(group)
-    first = next(iter(tensors.values()))
+    names = list(tensors)
+    first = tensors[names[0]]
     dev = first.device
-    n_local = torch.tensor([first.shape[0]], dtype=torch.int64, device=dev)
-    sizes = [torch.zeros_like(n_local) for _ in range(world)]
-    dist.all_gather(sizes, n_local, group=group)
-    sizes = [int(s.item()) for s in sizes]
+    n = int(first.shape[0])
+    n_local = torch.tensor([n], dtype=torch.int64, device=dev)
+    sizes_l = [torch.empty_like(n_local) for _ in range(world)]
+    dist.all_gather(sizes_l, n_local, group=group)
+    sizes = [int(x) for x in torch.cat(sizes_l).cpu().tolist()]   # one host copy
     m = max(max(sizes), 1)
     offsets = [0]
     for s_ in sizes:
         offsets.append(offsets[-1] + s_)
+
+    def as_i64(t):
+        if t.dtype == torch.uint64:
+            return t.view(torch.int64)
+        if t.dtype == torch.int64:
+            return t
+        return t.to(torch.int64)
+
+    packed = torch.zeros((m, len(names)), dtype=torch.int64, device=dev)
+    for j, name in enumerate(names):
+        packed[:n, j] = as_i64(tensors[name].reshape(-1))
+    parts = [torch.empty_like(packed) for _ in range(world)]
+    dist.all_gather(parts, packed, group=group)
+    cat = torch.cat([p[:s_] for p, s_ in zip(parts, sizes)])
     out = {}
-    for name, t in tensors.items():
-        wire = t.view(torch.int64) if t.dtype == torch.uint64 else t
-        pad = torch.zeros((m,) + tuple(wire.shape[1:]), dtype=wire.dtype, device=dev)
-        pad[:wire.shape[0]] = wire
-        parts = [torch.empty_like(pad) for _ in range(world)]
-        dist.all_gather(parts, pad, group=group)
-        cat = torch.cat([p[:s_] for p, s_ in zip(parts, sizes)])
-        out[name] = cat.view(torch.uint64) if t.dtype == torch.uint64 else cat
+    for j, name in enumerate(names):
+        col = cat[:, j].contiguous()
+        dt = tensors[name].dtype
+        out[name] = col.view(torch.uint64) if dt == torch.uint64 else col.to(dt)
     return out, offsets
+
+
+def owned_records_device(rec_row, offsets, rank, kept=None):
+    """Device form of owned_records: (local row indices / LoS codes tensor,
+    count) for the selected entries this rank materialises, with `kept`
+    (positions of the gathered rows in the shard's own row list) applied.
+    No host copy of the selection."""
+    import torch
+    lo, hi = offsets[rank], offsets[rank + 1]
+    mine = (rec_row >= lo) & (rec_row < hi)
+    if rank == 0:
+        mine |= rec_row < 0
+    sel = rec_row[mine]
+    local = torch.where(sel >= 0, sel - lo, sel)
+    if kept is not None:
+        pos = local >= 0
+        local = torch.where(pos, kept.index_select(0, torch.clamp(local, min=0)), local)
+    return local.contiguous(), int(local.numel())
 
 
 def owned_records(rec_row, offsets, rank):

@@ -217,3 +217,24 @@ def test_two_rank_gloo_cir_selection_equals_single_rank(tmp_path):
     rec, diag = sc.generate_candidates(src, targets, cfg)
     assert len(rec["sample"]) == len(want)
     assert diag["chunk_truncated"] > 0 and diag["buffer_overflow"] > 0
+
+
+def test_owned_records_device_matches_host_form():
+    """owned_records_device (the no-host-copy form compute_paths_sharded uses)
+    selects the same records as owned_records, with the kept-row mapping."""
+    import torch
+
+    from paper_2504_21719_b200.sharding import owned_records, owned_records_device
+    rng = np.random.default_rng(5)
+    offsets = [0, 40, 75, 120]
+    rec_row = np.concatenate([~np.arange(6), rng.permutation(120)[:90]]).astype(np.int64)
+    for rank in range(3):
+        kept = torch.from_numpy(rng.permutation(500)[:offsets[rank + 1] - offsets[rank]]
+                                .astype(np.int64))
+        _, loc = owned_records(rec_row, offsets, rank)
+        loc = np.array(loc, dtype=np.int64)
+        m = loc >= 0
+        loc[m] = kept.numpy()[loc[m]]
+        got, n = owned_records_device(torch.from_numpy(rec_row), offsets, rank, kept)
+        assert n == len(loc)
+        assert np.array_equal(got.numpy(), loc)

@@ -153,7 +153,14 @@ int64_t sbr_scene_num_nodes(const SbrScene* scene);
 int sbr_scene_copy_nodes(const SbrScene* scene, void* host_out);
 /* Host copy of slot -> input triangle index (the reference's Accel.perm). */
 int sbr_scene_permutation(const SbrScene* scene, int64_t* perm_out);
-/* Per-slot attributes, host arrays in SLOT order:
+/* Host copies of the per-slot tables sbr_scene_create derives on the device
+ * from the float64 corners with numpy's operation order: geometric normals
+ * normalize((v1-v0) x (v2-v0)) (geometry.py:165-166, (T,3) f64) and the
+ * (round, floor) plane hashes of _plane_hash_rows (paths.py:156-171, (T,)
+ * u64).  Any output may be NULL. */
+int sbr_scene_copy_tables(const SbrScene* scene, double* normals_out, uint64_t* hash_r_out,
+                          uint64_t* hash_f_out);
+/* Per-slot attributes, host arrays in SLOT order (override the derived ones):
  *   tie_rank  : rank of (object_id, primitive_id) -- closest-hit tie rule
  *               (_core.pyx:158-161)
  *   normals   : (T,3) float64 geometric normals (geometry.py:165-166)

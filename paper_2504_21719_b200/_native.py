@@ -37,6 +37,7 @@ def _declare(lib):
         "sbr_scene_set_wedges": (ctypes.c_int, [vp, vp]),
         "sbr_scene_check": (ctypes.c_int, [vp, vp]),
         "sbr_release_scratch": (ctypes.c_int, [i32]),
+        "sbr_scene_copy_tables": (ctypes.c_int, [vp, vp, vp, vp]),
         "sbr_trace_closest": (ctypes.c_int, [vp, vp, vp, dbl, vp, i64, vp, vp,
                                              vp, vp, vp]),
         "sbr_trace_any": (ctypes.c_int, [vp, vp, vp, dbl, vp, i64, vp, vp]),
@@ -82,7 +83,7 @@ def exported_symbols():
         "sbr_scene_create", "sbr_scene_destroy", "sbr_set_bvh_builder", "sbr_scene_num_triangles",
         "sbr_scene_num_nodes", "sbr_scene_permutation", "sbr_scene_copy_nodes",
         "sbr_scene_set_attributes", "sbr_scene_set_materials", "sbr_scene_set_wedges",
-        "sbr_scene_check", "sbr_release_scratch", "sbr_trace_closest", "sbr_trace_any",
+        "sbr_scene_check", "sbr_release_scratch", "sbr_scene_copy_tables", "sbr_trace_closest", "sbr_trace_any",
         "sbr_occluded", "sbr_fibonacci", "sbr_philox_uniform",
         "sbr_radiomap_bounce", "sbr_radiomap_bounce_sharded", "sbr_radiomap_direct",
         "sbr_radiomap_wedges", "sbr_cir_sweep", "sbr_cir_sweep_sharded",

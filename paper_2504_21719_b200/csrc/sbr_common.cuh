@@ -115,7 +115,13 @@ inline uint64_t comb_stride(uint64_t num_samples) {
   return best;
 }
 
-constexpr int kStackSize = 64;
+// Traversal stack entries (pending far children).  The reference allows 256
+// (_core.pyx:15, stack = 2 entries per split); a binary tree needs at most
+// its depth, so 256 covers every tree the reference's own build can traverse.
+#ifndef SBR_STACK_SIZE
+#define SBR_STACK_SIZE 256
+#endif
+constexpr int kStackSize = SBR_STACK_SIZE;
 constexpr unsigned kErrStack = 1u;
 
 // ---------------------------------------------------------------------------
@@ -829,6 +835,64 @@ struct AnyTrav {
 };
 
 using ClosestTrav = ClosestTravT<true>;
+
+// ---------------------------------------------------------------------------
+// Conservative, division-light classification of one candidate occluder for
+// the occlusion query of segment a -> b (occluded_batch: ray o = a + eps*dn,
+// dn = (b - a) / len, t_min = 0, limit = len - 2 eps; geometry.py:187-201).
+// With q_i = v_i - a, D = b - a the segment's line meets the triangle's plane
+// at lambda = det(q0, q1, q2) / (D . N), N = (q1 - q0) x (q2 - q0), inside the
+// triangle iff the signed volumes s0 = D.(q1 x q2), s1 = D.(q2 x q0),
+// s2 = D.(q0 x q1) share one sign (their sum is D . N).  Every quantity is
+// computed in float64 with a forward error below 16 u * T (T = the product of
+// the operands' 1-norms, u = 2^-53); the reference's own watertight shear
+// test errs by the same order on its (rounded) ray, plus a few ulps of the
+// coordinates where it rounds o = a + eps dn and v - o.  So with margins of
+// 1e-12 T plus a positional pad P = 1e-13 (|a|_1 + |D|_1) (~1000 ulps of the
+// coordinates) propagated through the same products, a verdict of
+//    +1: all |s_i| beyond the margin with one sign, and the hit distance from
+//        a clearly inside (eps, len - eps)      -> the reference finds a hit
+//     0: two s_i clearly of opposite signs, or the hit distance clearly
+//        outside (eps, len - eps)                -> the reference finds none
+// is the reference's verdict for this triangle; anything closer to a
+// boundary returns -1 and the caller runs the exact test.
+__device__ __forceinline__ double l1(double3 v) { return (fabs(v.x) + fabs(v.y)) + fabs(v.z); }
+
+__device__ __forceinline__ int seg_occluder_class(const TriSlot* __restrict__ tri, double3 a,
+                                                  double3 D, double l1D, double len,
+                                                  double eps, double pad) {
+  const double* T = reinterpret_cast<const double*>(tri);
+  const double3 q0 = make_double3(__ldg(T) - a.x, __ldg(T + 1) - a.y, __ldg(T + 2) - a.z);
+  const double3 q1 = make_double3(__ldg(T + 3) - a.x, __ldg(T + 4) - a.y, __ldg(T + 5) - a.z);
+  const double3 q2 = make_double3(__ldg(T + 6) - a.x, __ldg(T + 7) - a.y, __ldg(T + 8) - a.z);
+  const double3 c12 = cross3(q1, q2), c20 = cross3(q2, q0), c01 = cross3(q0, q1);
+  const double s0 = dot_seq(D, c12), s1 = dot_seq(D, c20), s2 = dot_seq(D, c01);
+  const double n0 = l1(q0), n1 = l1(q1), n2 = l1(q2);
+  const double pD = pad * l1D;
+  const double m0 = 1e-12 * (l1D * n1 * n2) + pD * (n1 + n2),
+               m1 = 1e-12 * (l1D * n2 * n0) + pD * (n2 + n0),
+               m2 = 1e-12 * (l1D * n0 * n1) + pD * (n0 + n1);
+  const bool pos = s0 > m0 && s1 > m1 && s2 > m2;
+  const bool negv = s0 < -m0 && s1 < -m1 && s2 < -m2;
+  if (!pos && !negv) {
+    const bool some_pos = s0 > m0 || s1 > m1 || s2 > m2;
+    const bool some_neg = s0 < -m0 || s1 < -m1 || s2 < -m2;
+    return (some_pos && some_neg) ? 0 : -1;
+  }
+  const double S = (s0 + s1) + s2;                 // D . N, |S| > 0 by the margins
+  const double V = dot_seq(q0, c12);               // det(q0, q1, q2)
+  const double eS = (m0 + m1) + m2;
+  const double eV = 1e-12 * (n0 * n1 * n2) + pad * ((n0 * n1 + n1 * n2) + n2 * n0);
+  const double aS = fabs(S);
+  if (!(aS > 2.0 * eS)) return -1;
+  const double lam = V / S;                        // hit parameter along D
+  const double elam = (eV + fabs(lam) * eS) / (aS - eS) + 1e-12 * fabs(lam);
+  const double lo = (lam - elam) * len, hi = (lam + elam) * len;  // hit distance from a
+  const double slack = 1e-9 * (len + 1.0);
+  if (lo > eps + slack && hi < len - eps - slack) return 1;
+  if (hi < eps - slack || lo > len - eps + slack) return 0;
+  return -1;
+}
 
 // any hit with t_min < t < limit (_core.pyx:198-253); returns false on overflow
 __device__ __forceinline__ bool trace_any(const DevScene& S, double3 o, double3 d,

@@ -71,6 +71,29 @@ struct ScatterQueue {
   int32_t* matrow;
 };
 
+// Ray-queue traffic is read once and written once per segment (GBs per
+// pass): stream it through L2 with evict-first hints so it does not evict
+// the L2-resident scene (BVH nodes, triangles), the grid and spilled locals.
+#ifndef SBR_STREAM_HINTS
+#define SBR_STREAM_HINTS 1
+#endif
+template <typename T>
+__device__ __forceinline__ T qld(const T* p) {
+#if SBR_STREAM_HINTS
+  return __ldcs(p);
+#else
+  return *p;
+#endif
+}
+template <typename T>
+__device__ __forceinline__ void qst(T* p, T v) {
+#if SBR_STREAM_HINTS
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
+
 __device__ __forceinline__ unsigned long long append_slot(unsigned long long* counter) {
   cg::coalesced_group grp = cg::coalesced_threads();
   unsigned long long base = 0;
@@ -134,10 +157,10 @@ __global__ void __launch_bounds__(SBR_TRACE_TPB, SBR_TRACE_MINB) k_map_trace(Dev
         const uint64_t local = comb.sample(i);
         active = local < count0;
         if (active) d = fibonacci_dir(P.num_samples, sh.gid(begin + local));
-        else hits.tri[i] = -3;  // comb slot past the end of the range
+        else qst(&hits.tri[i], -3);  // comb slot past the end of the range
       } else {
-        o = make_double3(q.ox[i], q.oy[i], q.oz[i]);
-        d = make_double3(q.dx[i], q.dy[i], q.dz[i]);
+        o = make_double3(qld(&q.ox[i]), qld(&q.oy[i]), qld(&q.oz[i]));
+        d = make_double3(qld(&q.dx[i]), qld(&q.dy[i]), qld(&q.dz[i]));
       }
     }
     int sn[kStackSize];
@@ -154,8 +177,8 @@ __global__ void __launch_bounds__(SBR_TRACE_TPB, SBR_TRACE_MINB) k_map_trace(Dev
         atomicAdd(counters + SBR_MC_STACK_OVERFLOW, 1ULL);
         h.tri = -2;  // dropped
       }
-      hits.t[i] = h.t;
-      hits.tri[i] = h.tri;
+      qst(&hits.t[i], h.t);
+      qst(&hits.tri[i], h.tri);
 #ifdef SBR_COUNT_VISITS
       atomicAdd(counters + SBR_MC_DIRECT_VISIBLE, (unsigned long long)T.visits);
       atomicAdd(counters + SBR_MC_THRESHOLD_KILLED, (unsigned long long)T.tests);
@@ -198,8 +221,15 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
 #endif
-    const int tri = hits.tri[i];
+    const int tri = qld(&hits.tri[i]);
     if (tri < -1) continue;  // empty comb slot / stack overflow
+    if (SHADE_FIRST && tri < 0) {
+      // a launch ray that escapes does nothing but count (no plane crossing at
+      // segment 0): skip its direction / field / precoding weight
+      K.rb++;
+      K.escaped++;
+      continue;
+    }
     double3 o, d;
     cvec3 E;
     double r_dist, omega, weight;
@@ -213,18 +243,18 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
       omega = P.omega0;
       weight = alpha_sq(P, d);
     } else {
-      g = qi.g[i];
-      o = make_double3(qi.ox[i], qi.oy[i], qi.oz[i]);
-      d = make_double3(qi.dx[i], qi.dy[i], qi.dz[i]);
-      E.x = C(qi.exr[i], qi.exi[i]);
-      E.y = C(qi.eyr[i], qi.eyi[i]);
-      E.z = C(qi.ezr[i], qi.ezi[i]);
-      r_dist = qi.r_dist[i];
-      omega = qi.omega[i];
-      weight = qi.weight[i];
+      g = qld(&qi.g[i]);
+      o = make_double3(qld(&qi.ox[i]), qld(&qi.oy[i]), qld(&qi.oz[i]));
+      d = make_double3(qld(&qi.dx[i]), qld(&qi.dy[i]), qld(&qi.dz[i]));
+      E.x = C(qld(&qi.exr[i]), qld(&qi.exi[i]));
+      E.y = C(qld(&qi.eyr[i]), qld(&qi.eyi[i]));
+      E.z = C(qld(&qi.ezr[i]), qld(&qi.ezi[i]));
+      r_dist = qld(&qi.r_dist[i]);
+      omega = qld(&qi.omega[i]);
+      weight = qld(&qi.weight[i]);
     }
     K.rb++;
-    const double t_hit = hits.t[i];
+    const double t_hit = qld(&hits.t[i]);
     const uint64_t chunk = g >> SBR_CHUNK_LOG2;
     const uint64_t slot = g & ((1ULL << SBR_CHUNK_LOG2) - 1);
     // plane crossing before the hit (radiomap.py:394-413); escaped rays deposit too
@@ -328,47 +358,47 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
       const double g_den = sqrt(cabs2(c_perp) + cabs2(c_par));
       const double gamma = g_den > 0.0 ? g_num / g_den : 0.0;
       const unsigned long long j = append_slot(count_s);
-      sq.dx[j] = d.x;
-      sq.dy[j] = d.y;
-      sq.dz[j] = d.z;
-      sq.nx[j] = nrm.x;
-      sq.ny[j] = nrm.y;
-      sq.nz[j] = nrm.z;
-      sq.px[j] = pt.x;
-      sq.py[j] = pt.y;
-      sq.pz[j] = pt.z;
-      sq.exr[j] = E.x.re;
-      sq.exi[j] = E.x.im;
-      sq.eyr[j] = E.y.re;
-      sq.eyi[j] = E.y.im;
-      sq.ezr[j] = E.z.re;
-      sq.ezi[j] = E.z.im;
-      sq.omega[j] = omega;
-      sq.r_hit[j] = r_hit;
-      sq.weight[j] = weight;
-      sq.cos_i[j] = cos_i;
-      sq.gamma[j] = gamma;
-      sq.g[j] = g;
-      sq.matrow[j] = __ldg(S.matrow + tri);
+      qst(&sq.dx[j], d.x);
+      qst(&sq.dy[j], d.y);
+      qst(&sq.dz[j], d.z);
+      qst(&sq.nx[j], nrm.x);
+      qst(&sq.ny[j], nrm.y);
+      qst(&sq.nz[j], nrm.z);
+      qst(&sq.px[j], pt.x);
+      qst(&sq.py[j], pt.y);
+      qst(&sq.pz[j], pt.z);
+      qst(&sq.exr[j], E.x.re);
+      qst(&sq.exi[j], E.x.im);
+      qst(&sq.eyr[j], E.y.re);
+      qst(&sq.eyi[j], E.y.im);
+      qst(&sq.ezr[j], E.z.re);
+      qst(&sq.ezi[j], E.z.im);
+      qst(&sq.omega[j], omega);
+      qst(&sq.r_hit[j], r_hit);
+      qst(&sq.weight[j], weight);
+      qst(&sq.cos_i[j], cos_i);
+      qst(&sq.gamma[j], gamma);
+      qst(&sq.g[j], g);
+      qst(&sq.matrow[j], __ldg(S.matrow + tri));
       continue;
     }
     const unsigned long long j = append_slot(count_out);
-    qo.ox[j] = pt.x;
-    qo.oy[j] = pt.y;
-    qo.oz[j] = pt.z;
-    qo.dx[j] = nd.x;
-    qo.dy[j] = nd.y;
-    qo.dz[j] = nd.z;
-    qo.exr[j] = E.x.re;
-    qo.exi[j] = E.x.im;
-    qo.eyr[j] = E.y.re;
-    qo.eyi[j] = E.y.im;
-    qo.ezr[j] = E.z.re;
-    qo.ezi[j] = E.z.im;
-    qo.r_dist[j] = r_dist;
-    qo.omega[j] = omega;
-    qo.weight[j] = weight;
-    qo.g[j] = g;
+    qst(&qo.ox[j], pt.x);
+    qst(&qo.oy[j], pt.y);
+    qst(&qo.oz[j], pt.z);
+    qst(&qo.dx[j], nd.x);
+    qst(&qo.dy[j], nd.y);
+    qst(&qo.dz[j], nd.z);
+    qst(&qo.exr[j], E.x.re);
+    qst(&qo.exi[j], E.x.im);
+    qst(&qo.eyr[j], E.y.re);
+    qst(&qo.eyi[j], E.y.im);
+    qst(&qo.ezr[j], E.z.re);
+    qst(&qo.ezi[j], E.z.im);
+    qst(&qo.r_dist[j], r_dist);
+    qst(&qo.omega[j], omega);
+    qst(&qo.weight[j], weight);
+    qst(&qo.g[j], g);
 #if SBR_SHADE_WARPSYNC
     } while (0);
     __syncwarp();
@@ -398,18 +428,18 @@ __global__ void __launch_bounds__(128, SBR_SCATTER_MINB) k_map_scatter(DevScene 
   const uint64_t n = *count_s;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
        j += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t g = sq.g[j];
+    const uint64_t g = qld(&sq.g[j]);
     const uint64_t chunk = g >> SBR_CHUNK_LOG2;
     const uint64_t slot = g & ((1ULL << SBR_CHUNK_LOG2) - 1);
-    const double3 d = make_double3(sq.dx[j], sq.dy[j], sq.dz[j]);
-    const double3 nrm = make_double3(sq.nx[j], sq.ny[j], sq.nz[j]);
+    const double3 d = make_double3(qld(&sq.dx[j]), qld(&sq.dy[j]), qld(&sq.dz[j]));
+    const double3 nrm = make_double3(qld(&sq.nx[j]), qld(&sq.ny[j]), qld(&sq.nz[j]));
     cvec3 E;
-    E.x = C(sq.exr[j], sq.exi[j]);
-    E.y = C(sq.eyr[j], sq.eyi[j]);
-    E.z = C(sq.ezr[j], sq.ezi[j]);
-    const double omega = sq.omega[j], r_hit = sq.r_hit[j], cos_i = sq.cos_i[j];
-    const double gamma = sq.gamma[j];
-    const SbrMaterial m = S.mats[sq.matrow[j]];
+    E.x = C(qld(&sq.exr[j]), qld(&sq.exi[j]));
+    E.y = C(qld(&sq.eyr[j]), qld(&sq.eyi[j]));
+    E.z = C(qld(&sq.ezr[j]), qld(&sq.ezi[j]));
+    const double omega = qld(&sq.omega[j]), r_hit = qld(&sq.r_hit[j]), cos_i = qld(&sq.cos_i[j]);
+    const double gamma = qld(&sq.gamma[j]);
+    const SbrMaterial m = S.mats[qld(&sq.matrow[j])];
     const double u0 = philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_RESPAWN, 2 * slot);
     const double u1 = philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_RESPAWN, 2 * slot + 1);
     const double cos_t = u0, azim = kTwoPi * u1;
@@ -448,22 +478,22 @@ __global__ void __launch_bounds__(128, SBR_SCATTER_MINB) k_map_scatter(DevScene 
     E.z = cdiv(th_s.z * co0 + ph_s.z * co1, inv_r);
     respawns++;
     const unsigned long long o = append_slot(count_out);
-    qo.ox[o] = sq.px[j];
-    qo.oy[o] = sq.py[j];
-    qo.oz[o] = sq.pz[j];
-    qo.dx[o] = ks.x;
-    qo.dy[o] = ks.y;
-    qo.dz[o] = ks.z;
-    qo.exr[o] = E.x.re;
-    qo.exi[o] = E.x.im;
-    qo.eyr[o] = E.y.re;
-    qo.eyi[o] = E.y.im;
-    qo.ezr[o] = E.z.re;
-    qo.ezi[o] = E.z.im;
-    qo.r_dist[o] = 0.0;
-    qo.omega[o] = kTwoPi;
-    qo.weight[o] = sq.weight[j];
-    qo.g[o] = g;
+    qst(&qo.ox[o], qld(&sq.px[j]));
+    qst(&qo.oy[o], qld(&sq.py[j]));
+    qst(&qo.oz[o], qld(&sq.pz[j]));
+    qst(&qo.dx[o], ks.x);
+    qst(&qo.dy[o], ks.y);
+    qst(&qo.dz[o], ks.z);
+    qst(&qo.exr[o], E.x.re);
+    qst(&qo.exi[o], E.x.im);
+    qst(&qo.eyr[o], E.y.re);
+    qst(&qo.eyi[o], E.y.im);
+    qst(&qo.ezr[o], E.z.re);
+    qst(&qo.ezi[o], E.z.im);
+    qst(&qo.r_dist[o], 0.0);
+    qst(&qo.omega[o], kTwoPi);
+    qst(&qo.weight[o], qld(&sq.weight[j]));
+    qst(&qo.g[o], g);
   }
   const unsigned s = __reduce_add_sync(0xffffffffu, respawns);
   if ((threadIdx.x & 31) == 0 && s) atomicAdd(counters + SBR_MC_RESPAWNS, (unsigned long long)s);

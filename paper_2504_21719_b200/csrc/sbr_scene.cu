@@ -437,6 +437,59 @@ __global__ void k_gather_tris(const double* __restrict__ v0, const double* __res
   tris[i] = s;
 }
 
+// Per-slot geometry tables of SceneModel._build_tables (paths.py:446-450) and
+// Accel (geometry.py:165-166), computed on the device from the float64
+// corners with numpy's operation order (-fmad=false, no contraction):
+//   normal = cross(v1 - v0, v2 - v0) / norm      (np.cross, np.linalg.norm)
+//   plane hashes of _plane_hash_rows (paths.py:156-171): the normal divided
+//   by its norm again, canonical sign (first |c| > 1e-8 positive), d = n . v0
+//   as ((n0 p0 + n1 p1) + n2 p2), FNV-1a over the 8 little-endian bytes of
+//   floor(c / 1e-4 + 0.5) and floor(c / 1e-4) for c in (n0, n1, n2, d).
+__device__ __forceinline__ uint64_t fnv1a_fold(uint64_t h, uint64_t v) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    h = (h ^ (v & 0xFFULL)) * 0x100000001B3ULL;
+    v >>= 8;
+  }
+  return h;
+}
+
+__global__ void k_slot_tables(const TriSlot* __restrict__ tris, int n, double* __restrict__ normals,
+                              uint64_t* __restrict__ hash_r, uint64_t* __restrict__ hash_f) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* T = reinterpret_cast<const double*>(tris + i);
+  const double a0 = T[3] - T[0], a1 = T[4] - T[1], a2 = T[5] - T[2];   // v1 - v0
+  const double b0 = T[6] - T[0], b1 = T[7] - T[1], b2 = T[8] - T[2];   // v2 - v0
+  const double c0 = a1 * b2 - a2 * b1, c1 = a2 * b0 - a0 * b2, c2 = a0 * b1 - a1 * b0;
+  const double len = sqrt((c0 * c0 + c1 * c1) + c2 * c2);
+  double m0 = c0 / len, m1 = c1 / len, m2 = c2 / len;
+  normals[3 * (int64_t)i] = m0;
+  normals[3 * (int64_t)i + 1] = m1;
+  normals[3 * (int64_t)i + 2] = m2;
+  const double len2 = sqrt((m0 * m0 + m1 * m1) + m2 * m2);
+  m0 = m0 / len2;
+  m1 = m1 / len2;
+  m2 = m2 / len2;
+  const double lead = fabs(m0) > 1e-8 ? m0 : (fabs(m1) > 1e-8 ? m1 : (fabs(m2) > 1e-8 ? m2 : m0));
+  if (lead < 0.0) {
+    m0 = -m0;
+    m1 = -m1;
+    m2 = -m2;
+  }
+  const double d = (m0 * T[0] + m1 * T[1]) + m2 * T[2];
+  const double comp[4] = {m0, m1, m2, d};
+  uint64_t hr = 0xCBF29CE484222325ULL, hf = 0xCBF29CE484222325ULL;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double q = comp[k] / 1e-4;
+    hr = fnv1a_fold(hr, (uint64_t)(int64_t)floor(q + 0.5));
+    hf = fnv1a_fold(hf, (uint64_t)(int64_t)floor(q));
+  }
+  hash_r[i] = hr;
+  hash_f[i] = hf;
+}
+
 // ---------------------------------------------------------------------------
 // PLOC: parallel locally-ordered clustering over the Morton order (Meister &
 // Bittner 2018).  Clusters start as the Morton-sorted leaves; every round each
@@ -862,8 +915,8 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
     return rc;
   SBR_CUDA(cudaMemsetAsync(S->error_word, 0, sizeof(unsigned), st));
   SBR_CUDA(cudaMemsetAsync(S->matrow, 0, sizeof(int32_t) * n, st));
-  SBR_CUDA(cudaMemsetAsync(S->hash_r, 0, sizeof(uint64_t) * n, st));
-  SBR_CUDA(cudaMemsetAsync(S->hash_f, 0, sizeof(uint64_t) * n, st));
+  k_slot_tables<<<grid_for(n, 256), 256, 0, st>>>(S->tris, n, S->normals, S->hash_r, S->hash_f);
+  count_launch();
   SBR_CUDA(cudaStreamSynchronize(st));
   SBR_CUDA(cudaGetLastError());
   for (int i = 0; i < n; ++i) S->perm[i] = ids_host[i];
@@ -918,6 +971,17 @@ int sbr_scene_copy_nodes(const SbrScene* S, void* host_out) {
 int sbr_scene_permutation(const SbrScene* S, int64_t* perm_out) {
   if (!S || !perm_out) return set_error(SBR_ERR_INVALID, "NULL argument");
   memcpy(perm_out, S->perm.data(), sizeof(int64_t) * S->perm.size());
+  return SBR_OK;
+}
+
+int sbr_scene_copy_tables(const SbrScene* S, double* normals_out, uint64_t* hash_r_out,
+                          uint64_t* hash_f_out) {
+  if (!S) return set_error(SBR_ERR_INVALID, "NULL scene");
+  DeviceGuard dg(S->device);
+  const size_t n = (size_t)S->ntri;
+  if (normals_out) SBR_CUDA(cudaMemcpy(normals_out, S->normals, 24 * n, cudaMemcpyDeviceToHost));
+  if (hash_r_out) SBR_CUDA(cudaMemcpy(hash_r_out, S->hash_r, 8 * n, cudaMemcpyDeviceToHost));
+  if (hash_f_out) SBR_CUDA(cudaMemcpy(hash_f_out, S->hash_f, 8 * n, cudaMemcpyDeviceToHost));
   return SBR_OK;
 }
 

@@ -142,8 +142,7 @@ class Accel:
         self.tri_object_id = np.concatenate(objs)[perm]
         self.tri_primitive_id = np.concatenate(prims)[perm]
         self.tri_mesh_index = np.concatenate(mesh_idx)[perm]
-        n = np.cross(self.tri_v1 - self.tri_v0, self.tri_v2 - self.tri_v0)
-        self.tri_normal = n / np.linalg.norm(n, axis=1, keepdims=True)
+        self._tables = None   # device-derived normals / plane hashes, copied on first use
         lo = np.minimum(np.minimum(v0, v1), v2).min(axis=0)
         hi = np.maximum(np.maximum(v0, v1), v2).max(axis=0)
         self.bounds = (lo - 1e-12 * (1.0 + np.abs(lo)), hi + 1e-12 * (1.0 + np.abs(hi)))
@@ -152,7 +151,33 @@ class Accel:
         rank = np.empty(len(order), dtype=np.int32)
         rank[order] = np.arange(len(order), dtype=np.int32)
         self.tri_tie_rank = rank
-        self.set_attributes(tie_rank=rank, normals=self.tri_normal)
+        self.set_attributes(tie_rank=rank)
+
+    def _device_tables(self):
+        """Host copies of the per-slot normals and plane hashes that
+        sbr_scene_create derived on the device (geometry.py:165-166,
+        paths.py:156-171 arithmetic, bit-identical to the numpy expressions)."""
+        if self._tables is None:
+            n = self.num_triangles
+            nrm = np.empty((n, 3), dtype=np.float64)
+            hr = np.empty(n, dtype=np.uint64)
+            hf = np.empty(n, dtype=np.uint64)
+            _native.check(self._lib.sbr_scene_copy_tables(
+                self._handle, nrm.ctypes.data_as(ctypes.c_void_p),
+                hr.ctypes.data_as(ctypes.c_void_p), hf.ctypes.data_as(ctypes.c_void_p)))
+            self._tables = (nrm, hr, hf)
+        return self._tables
+
+    @property
+    def tri_normal(self):
+        """(T, 3) geometric normals normalize((v1 - v0) x (v2 - v0)) per slot."""
+        return self._device_tables()[0]
+
+    @property
+    def tri_plane_hashes(self):
+        """(round, floor) plane hashes per slot (paths.py:449-450)."""
+        _, hr, hf = self._device_tables()
+        return hr, hf
 
     # -- device tables -----------------------------------------------------
     def set_attributes(self, tie_rank=None, normals=None, matrow=None,

@@ -261,20 +261,33 @@ class SceneModel:
         self._wedges = W
 
     def _build_tables(self):
+        # the per-slot plane hashes (paths.py:449-450) are derived on the device
+        # by sbr_scene_create from the float64 corners; host copies on demand
         accel = self.accel
-        self.tri_plane_hash_round, self.tri_plane_hash_floor = plane_hash_rows(
-            accel.tri_normal, accel.tri_v0)
         self._object_ids = np.array(sorted(m.object_id for m in self.meshes),
                                     dtype=np.int64)
         self._object_materials = [self.materials[oid] for oid in self._object_ids]
         self.tri_material_row = np.searchsorted(self._object_ids, accel.tri_object_id)
-        self._tri_slot = {
-            (int(o), int(p)): i for i, (o, p) in
-            enumerate(zip(accel.tri_object_id, accel.tri_primitive_id))
-        }
-        accel.set_attributes(matrow=self.tri_material_row,
-                             hash_r=self.tri_plane_hash_round,
-                             hash_f=self.tri_plane_hash_floor)
+        self._slot_map = None
+        accel.set_attributes(matrow=self.tri_material_row)
+
+    @property
+    def tri_plane_hash_round(self):
+        return self.accel.tri_plane_hashes[0]
+
+    @property
+    def tri_plane_hash_floor(self):
+        return self.accel.tri_plane_hashes[1]
+
+    @property
+    def _tri_slot(self):
+        """{(object_id, primitive_id): slot} (paths.py:452-455), built on first use."""
+        if self._slot_map is None:
+            acc = self.accel
+            self._slot_map = {(int(o), int(p)): i for i, (o, p) in
+                              enumerate(zip(acc.tri_object_id.tolist(),
+                                            acc.tri_primitive_id.tolist()))}
+        return self._slot_map
 
     def bind_frequency(self, frequency):
         """Upload the per-object material rows frozen at `frequency`."""

@@ -158,3 +158,60 @@ def test_release_scratch_returns_memory(cuda):
     v2, d2 = compute_radio_map_sbr(sc, (0.5, 0.5, 1.0), grid, cfg)
     assert d1 == d2
     np.testing.assert_allclose(v2, v1, rtol=1e-12)  # float64 atomics: summation order only
+
+
+def _deep_chain_meshes(n=110):
+    """Unit squares perpendicular to x at x = 2^k (k < n): every Morton code of
+    the cubic grid is equal except the last few, and each clustering step can
+    merge only the two nearest clusters, so the tree degenerates into a chain
+    of depth ~n (> the 64 entries round 1's traversal stack held)."""
+    from paper_2504_21719_b200.geometry import Mesh
+    verts, tris = [], []
+    for k in range(n):
+        x = float(2.0 ** k)
+        b = len(verts)
+        verts += [(x, -1.0, -1.0), (x, 1.0, -1.0), (x, 1.0, 1.0), (x, -1.0, 1.0)]
+        tris += [(b, b + 1, b + 2), (b, b + 2, b + 3)]
+    return [Mesh(np.array(verts), np.array(tris), object_id=0)]
+
+
+def test_degenerate_deep_tree_traverses_like_the_reference(cuda):
+    """A pathological scene whose BVH is a chain ~110 deep: closest hits (far
+    to near and near to far along the chain) and occlusion queries match the
+    oracle, whose SAH tree needs a deep stack too -- no stack overflow below the
+    reference's 256-entry limit (_core.pyx:15)."""
+    import oracle
+    from paper_2504_21719_b200 import _native
+    meshes = _deep_chain_meshes()
+    acc = build_scene_accel(meshes)
+    nodes = np.zeros((int(_native.lib().sbr_scene_num_nodes(acc.handle)), 16), np.int32)
+    _native.check(_native.lib().sbr_scene_copy_nodes(acc.handle, nodes.ctypes.data))
+    depth, todo = {0: 1}, [0]
+    while todo:
+        i = todo.pop()
+        for c in nodes[i, 12:14]:   # int4 child codes: >= 0 inner node, < 0 leaf
+            if c >= 0:
+                depth[int(c)] = depth[i] + 1
+                todo.append(int(c))
+    assert max(depth.values()) > 64
+    osc = oracle.OracleScene(meshes)
+    rng = np.random.default_rng(3)
+    m = 2000
+    o = np.column_stack([np.full(m, -10.0), rng.uniform(-0.9, 0.9, m), rng.uniform(-0.9, 0.9, m)])
+    d = np.tile([1.0, 0.0, 0.0], (m, 1))
+    o2 = o.copy()
+    o2[:, 0] = 2.0 ** 112
+    for orig, dirs in ((o, d), (o2, -d)):
+        t, tri, u, v = acc.trace_batch(orig, dirs)
+        want = osc.trace_batch(orig, dirs)
+        assert np.array_equal(t, want[0])
+        assert np.array_equal(acc.tri_object_id[tri], osc.tri_object_id[want[1]])
+        assert np.array_equal(acc.tri_primitive_id[tri], osc.tri_primitive_id[want[1]])
+    # segments between consecutive squares: exactly the ones spanning a square are occluded
+    a = np.column_stack([2.0 ** rng.integers(0, 100, m) * 1.5, rng.uniform(-0.9, 0.9, m),
+                         rng.uniform(-0.9, 0.9, m)])
+    b = a.copy()
+    b[:, 0] *= rng.choice([0.9, 1.2, 4.0], m)
+    occ = acc.occluded_batch(a, b)
+    assert np.array_equal(occ, osc.occluded_batch(a, b))
+    assert occ.any() and not occ.all()

@@ -44,6 +44,7 @@ extern "C" {
 #define SBR_ERR_CUDA 4           /* RuntimeError (CUDA failure)               */
 #define SBR_ERR_UNSUPPORTED 5    /* NotImplementedError (out-of-scope feature) */
 #define SBR_ERR_NOMEM 6          /* MemoryError                               */
+#define SBR_ERR_INTERNAL 7       /* RuntimeError (checked build: device bounds check) */
 
 /* Radio-map RNG chunking: part of the reference's RNG contract
  * (radiomap.py:53-55, CHUNK_SAMPLES = 1 << 19). */
@@ -123,6 +124,9 @@ enum {
   SBR_MC_COUNT
 };
 
+/* Build flags of the loaded library: bit 0 = checked build (SBR_CHECKED). */
+int sbr_build_flags(void);
+
 /* ---- scene -------------------------------------------------------------- */
 typedef struct SbrScene SbrScene;
 
@@ -192,6 +196,26 @@ typedef struct SbrWedgeTable {
   const int32_t* slot_ids;        /* (slot_offsets[T]) */
 } SbrWedgeTable;
 int sbr_scene_set_wedges(SbrScene* scene, const SbrWedgeTable* table);
+/* Replaces extract_wedges (geometry.py:356-494) and hash_edge
+ * (paths.py:111-125): diffraction wedge extraction on `device` from the
+ * flattened host triangles in input order (corners (T,3) f64, object and
+ * primitive ids).  The result lives in an opaque SbrWedgeSet: per wedge
+ * origin, e_hat, t0_hat, n0_hat, nn_hat (3 f64 each), length, n (exterior
+ * angle / pi), the (round, floor) edge hashes, and the owner lists face0 /
+ * facen as CSR over owner codes 3 * input_triangle + local_edge, sorted like
+ * the reference's sorted(set(...)); wedges in the reference's order. */
+typedef struct SbrWedgeSet SbrWedgeSet;
+int sbr_wedges_extract(const double* v0, const double* v1, const double* v2, const int64_t* obj,
+                       const int64_t* prim, int64_t ntri, double dihedral_threshold_deg,
+                       int32_t device, void* stream, SbrWedgeSet** out);
+int sbr_wedges_count(const SbrWedgeSet* set, int64_t* n_wedges, int64_t* n_owners0,
+                     int64_t* n_ownersn);
+/* Host copies (any pointer may be NULL); off0 / offn hold n_wedges + 1 entries. */
+int sbr_wedges_copy(const SbrWedgeSet* set, double* origin, double* e_hat, double* t0_hat,
+                    double* n0_hat, double* nn_hat, double* length, double* n_open,
+                    uint64_t* hash_r, uint64_t* hash_f, int64_t* off0, int64_t* own0,
+                    int64_t* offn, int64_t* ownn);
+void sbr_wedges_free(SbrWedgeSet* set);
 /* Reads and clears the device error word (stack overflow).  Synchronises
  * `stream`.  Returns SBR_ERR_STACK if any traversal overflowed. */
 int sbr_scene_check(SbrScene* scene, void* stream);

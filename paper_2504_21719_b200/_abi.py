@@ -13,6 +13,7 @@ SBR_ERR_STACK = 3
 SBR_ERR_CUDA = 4
 SBR_ERR_UNSUPPORTED = 5
 SBR_ERR_NOMEM = 6
+SBR_ERR_INTERNAL = 7
 
 SBR_CHUNK_LOG2 = 19
 SBR_CIR_SHARD_LOG2 = 12   # id chunks of the chunk-cyclic CIR shards (sbr_cir_sweep_sharded)

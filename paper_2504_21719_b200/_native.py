@@ -38,6 +38,12 @@ def _declare(lib):
         "sbr_scene_check": (ctypes.c_int, [vp, vp]),
         "sbr_release_scratch": (ctypes.c_int, [i32]),
         "sbr_scene_copy_tables": (ctypes.c_int, [vp, vp, vp, vp]),
+        "sbr_wedges_extract": (ctypes.c_int, [vp, vp, vp, vp, vp, i64, dbl, i32, vp,
+                                              ctypes.POINTER(vp)]),
+        "sbr_wedges_count": (ctypes.c_int, [vp, ctypes.POINTER(i64), ctypes.POINTER(i64),
+                                            ctypes.POINTER(i64)]),
+        "sbr_wedges_copy": (ctypes.c_int, [vp] * 14),
+        "sbr_wedges_free": (None, [vp]),
         "sbr_trace_closest": (ctypes.c_int, [vp, vp, vp, dbl, vp, i64, vp, vp,
                                              vp, vp, vp]),
         "sbr_trace_any": (ctypes.c_int, [vp, vp, vp, dbl, vp, i64, vp, vp]),
@@ -66,6 +72,7 @@ def _declare(lib):
                                    dbl, i32, vp, vp]),
         "sbr_last_error": (ctypes.c_char_p, []),
         "sbr_version": (ctypes.c_int, []),
+        "sbr_build_flags": (ctypes.c_int, []),
         "sbr_kernel_launches": (u64, []),
         "sbr_profile_enable": (ctypes.c_int, [i32]),
         "sbr_profile_kernel_ms": (dbl, [ctypes.c_char_p, ctypes.POINTER(u64)]),
@@ -83,7 +90,8 @@ def exported_symbols():
         "sbr_scene_create", "sbr_scene_destroy", "sbr_set_bvh_builder", "sbr_scene_num_triangles",
         "sbr_scene_num_nodes", "sbr_scene_permutation", "sbr_scene_copy_nodes",
         "sbr_scene_set_attributes", "sbr_scene_set_materials", "sbr_scene_set_wedges",
-        "sbr_scene_check", "sbr_release_scratch", "sbr_scene_copy_tables", "sbr_trace_closest", "sbr_trace_any",
+        "sbr_scene_check", "sbr_release_scratch", "sbr_scene_copy_tables", "sbr_wedges_extract", "sbr_wedges_count",
+        "sbr_wedges_copy", "sbr_wedges_free", "sbr_trace_closest", "sbr_trace_any",
         "sbr_occluded", "sbr_fibonacci", "sbr_philox_uniform",
         "sbr_radiomap_bounce", "sbr_radiomap_bounce_sharded", "sbr_radiomap_direct",
         "sbr_radiomap_wedges", "sbr_cir_sweep", "sbr_cir_sweep_sharded",
@@ -91,7 +99,7 @@ def exported_symbols():
         "sbr_cir_visibility", "sbr_cir_row_pairs", "sbr_cir_select", "sbr_cir_local_dedup",
         "sbr_cir_resolve_records", "sbr_cir_records", "sbr_cir_refine",
         "sbr_cir_fields", "sbr_cfr", "sbr_last_error",
-        "sbr_version", "sbr_kernel_launches", "sbr_profile_enable", "sbr_profile_kernel_ms",
+        "sbr_version", "sbr_build_flags", "sbr_kernel_launches", "sbr_profile_enable", "sbr_profile_kernel_ms",
     ]
 
 

@@ -120,8 +120,8 @@ __global__ void __launch_bounds__(128, SBR_SWEEP_MINB) k_cir_sweep(DevScene S, S
   const unsigned lane_id = threadIdx.x & 31u;
   const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  int sn[kStackSize];
-  float st[kStackSize];
+  alignas(8) int sn[(SBR_PACKED_STACK ? 2 : 1) * kStackSize];
+  float st[SBR_PACKED_STACK ? 1 : kStackSize];
   // comb order: the 32 lanes of a batch take lattice neighbours (ids F apart)
   const uint64_t slots = comb.slots();
   for (uint64_t base = warp0 * 32; base < slots; base += nwarps * 32) {
@@ -352,32 +352,11 @@ __global__ void k_vis_view(SbrVertexBuf vb, int64_t v_begin, int64_t nv,
   }
 }
 
-// candidate occluder h of a ray: the per-target table entries (0..kVisGHints-1,
-// read early into gh) then this warp's ring; selects, not an indexed array,
-// so nothing goes to local memory
-static_assert(kVisHints == 0 || (kVisHints & (kVisHints - 1)) == 0, "ring size: power of two");
-__device__ __forceinline__ int vis_candidate(int h, const int* gh, const int* ring,
-                                             const int* ghint, int k) {
-#if SBR_VIS_GHINT_EARLY
-  int j = ring[(h - kVisGHints) & (kVisHints > 0 ? kVisHints - 1 : 0)];
-#pragma unroll
-  for (int q = 0; q < kVisGHints; ++q)
-    if (h == q) j = gh[q];
-  return j;
-#else
-  return h < kVisGHints ? __ldcg(ghint + (int64_t)k * kVisGHints + h)
-                        : ring[(h - kVisGHints) & (kVisHints - 1)];
-#endif
-}
-
 #ifndef SBR_VIS_PACK
 #define SBR_VIS_PACK 1  // config 3: 62.8 -> 60.9 ms (no 64-bit div/mod per ray)
 #endif
 #ifndef SBR_VIS_GHINT_EARLY
 #define SBR_VIS_GHINT_EARLY 1  // config 3: 64.2 -> 62.8 ms (2: early __ldcg, 63.9)
-#endif
-#ifndef SBR_VIS_QUICK
-#define SBR_VIS_QUICK 1  // division-free candidate-occluder classification before the ray setup
 #endif
 #ifndef SBR_VIS_MINB
 #define SBR_VIS_MINB 8  // 64 registers: 220 -> 180 ms at config 3
@@ -455,6 +434,7 @@ __global__ void __launch_bounds__(128, SBR_VIS_MINB) k_cir_visibility(DevScene S
         const unsigned m = __ballot_sync(0xffffffffu, pass);
 #if SBR_VIS_PACK
         // (slab vertex, target) as two 32-bit halves: shifts, not a 64-bit div/mod
+        SBR_DCHECK(S, !pass || qn + __popc(m & lt_mask) < 64);
         if (pass) sq[wid][qn + __popc(m & lt_mask)] = (int64_t)(((uint64_t)pos << 32) | (uint32_t)k);
 #else
         if (pass) sq[wid][qn + __popc(m & lt_mask)] = pos * nt + k;  // (slab vertex, target)
@@ -501,53 +481,38 @@ __global__ void __launch_bounds__(128, SBR_VIS_MINB) k_cir_visibility(DevScene S
       b = ldg3(P.targets_dev + 3 * k);
       vis++;
     }
-    // Candidate occluders first, classified without the ray setup's divisions
-    // (seg_occluder_class: exact verdicts away from any decision boundary):
-    // the per-target table (occluders any warp found for this target; racy,
-    // hints only -- on config 3 they settle 87 % of all rays) and this warp's
-    // ring of occluders of earlier tiles of the same target (another 3 %).
-    const double3 dd = b - a;
-    const double len = norm_seq(dd);
-    cast = active && len > 2.0 * 1e-4;
-    bool quick = false;
-    int quick_j = -1;
-    unsigned unknown = 0;  // candidates the classifier left to the exact test
-#if SBR_VIS_QUICK
-    if (cast) {
-      const double l1D = l1(dd);
-      const double pad = 1e-13 * (l1(a) + l1D);
-#pragma unroll 1
-      for (int h = 0; h < kVisGHints + kVisHints; ++h) {
-        const int j = vis_candidate(h, gh, shint[wid], ghint, k);
-        if (quick || j < 0) continue;
-        const int c = seg_occluder_class(S.tris + j, a, dd, l1D, len, 1e-4, pad);
-        if (c > 0) {
-          quick = true;
-          quick_j = j;
-        } else if (c < 0) {
-          unknown |= 1u << h;
-        }
+    // occluded_batch (geometry.py:187-201): open segment, endpoints offset by eps
+    if (active) {
+      const double3 dd = b - a;
+      const double len = norm_seq(dd);
+      if (len > 2.0 * 1e-4) {
+        const double3 dn = make_double3(dd.x / len, dd.y / len, dd.z / len);
+        const double3 o = make_double3(a.x + 1e-4 * dn.x, a.y + 1e-4 * dn.y, a.z + 1e-4 * dn.z);
+        T.start(S, o, dn, 0.0, len - 2.0 * 1e-4);
+        cast = true;
       }
     }
+    if (!cast) {
+      T.idle();
+      T.found = false;
+      T.ok = true;
+    }
+    // occluders any warp found for this target (racy table: hints only); on
+    // config 3 these settle 87 % of all rays, the warp ring below another 3 %
+    for (int h = 0; h < kVisGHints; ++h) {
+      if (cast && !T.found) {
+#if SBR_VIS_GHINT_EARLY
+        const int j = gh[h];
 #else
-    unknown = cast ? ~0u : 0u;
+        const int j = __ldcg(ghint + (int64_t)k * kVisGHints + h);
 #endif
-    if (cast && !quick) {
-      // occluded_batch (geometry.py:187-201): open segment, endpoints offset by eps
-      const double3 dn = make_double3(dd.x / len, dd.y / len, dd.z / len);
-      const double3 o = make_double3(a.x + 1e-4 * dn.x, a.y + 1e-4 * dn.y, a.z + 1e-4 * dn.z);
-      T.start(S, o, dn, 0.0, len - 2.0 * 1e-4);
-#pragma unroll 1
-      for (int h = 0; h < kVisGHints + kVisHints; ++h) {
-        if (T.found || !(unknown >> h & 1u)) continue;
-        const int j = vis_candidate(h, gh, shint[wid], ghint, k);
         if (j >= 0) T.try_occluder(S, j);
       }
-    } else {
-      T.idle();
-      T.found = quick;
-      T.hit_tri = quick_j;
-      T.ok = true;
+    }
+    // occluders found by this warp for earlier tiles of the same target
+    for (int h = 0; h < kVisHints; ++h) {
+      const int j = shint[wid][h];
+      if (cast && !T.found && j >= 0) T.try_occluder(S, j);
     }
     while (!T.done()) {
       const bool before = T.found;

@@ -123,6 +123,21 @@ inline uint64_t comb_stride(uint64_t num_samples) {
 #endif
 constexpr int kStackSize = SBR_STACK_SIZE;
 constexpr unsigned kErrStack = 1u;
+// Checked builds (-DSBR_CHECKED, libsbr_checked.so; compute-sanitizer is not
+// available on the GPU pool) assert index ranges in the hot kernels: a failed
+// check sets kErrBounds in the scene's error word, which sbr_scene_check
+// reports as SBR_ERR_INTERNAL.  Release builds compile the checks away.
+constexpr unsigned kErrBounds = 2u;
+#ifdef SBR_CHECKED
+#define SBR_DCHECK(S, cond)                                  \
+  do {                                                       \
+    if (!(cond)) atomicOr((S).error_word, ::sbr::kErrBounds); \
+  } while (0)
+#else
+#define SBR_DCHECK(S, cond) \
+  do {                      \
+  } while (0)
+#endif
 
 // ---------------------------------------------------------------------------
 // Philox4x64-10 keyed stream
@@ -578,14 +593,28 @@ __device__ __forceinline__ bool trace_closest(const DevScene& S, double3 o, doub
 // culling is conservative).  Lanes with active == false only vote.
 constexpr int kDone = (int)0x80000000;  // never a node index or a leaf code
 
+// SBR_PACKED_STACK: a stack entry is one 8-byte (node, entry distance) pair
+// (one local load / store per pop / push instead of two); the caller's node
+// array then holds 2 * kStackSize ints, 8-byte aligned
+#ifndef SBR_PACKED_STACK
+#define SBR_PACKED_STACK 1  // config-4 trace 497 -> 491 ms, canyon 4.29 -> 4.21 ms
+#endif
 __device__ __forceinline__ int ww_pop_t(const int* stack_node, const float* stack_t, int& sp,
                                         float bound, float& t_out) {
   while (sp > 0) {
     --sp;
+#if SBR_PACKED_STACK
+    const int2 e = reinterpret_cast<const int2*>(stack_node)[sp];
+    if (__int_as_float(e.y) <= bound) {
+      t_out = __int_as_float(e.y);
+      return e.x;
+    }
+#else
     if (stack_t[sp] <= bound) {
       t_out = stack_t[sp];
       return stack_node[sp];
     }
+#endif
   }
   return kDone;
 }
@@ -646,6 +675,7 @@ struct ClosestTravT {
 #ifdef SBR_COUNT_VISITS
       ++visits;
 #endif
+      SBR_DCHECK(S, node < S.nnodes);
       const BvhNode* nd = S.nodes + node;
       const float4 a = __ldg(&nd->a), b = __ldg(&nd->b), c = __ldg(&nd->c);
       const int4 ch = __ldg(&nd->d);
@@ -661,8 +691,13 @@ struct ClosestTravT {
           leaf = 0;
           return;
         }
+#if SBR_PACKED_STACK
+        reinterpret_cast<int2*>(stack_node)[sp] =
+            make_int2(lfirst ? ch.y : ch.x, __float_as_int(lfirst ? tr : tl));
+#else
         stack_node[sp] = lfirst ? ch.y : ch.x;
         stack_t[sp] = lfirst ? tr : tl;
+#endif
         ++sp;
         node = lfirst ? ch.x : ch.y;
         node_t = lfirst ? tl : tr;
@@ -690,6 +725,7 @@ struct ClosestTravT {
       const int s = leaf_start(leaf);
       // a parked leaf beyond the best hit found since parking is culled
       const int n = leaf_t <= bound ? leaf_count(leaf) : 0;
+      SBR_DCHECK(S, s >= 0 && s + leaf_count(leaf) <= S.ntri);
 #ifdef SBR_COUNT_VISITS
       tests += n;
 #endif
@@ -758,6 +794,7 @@ struct AnyTrav {
   // predicate the traversal applies, so the answer is unchanged -- any
   // triangle with t_min < t < limit occludes.
   __device__ __forceinline__ bool try_occluder(const DevScene& S, int j) {
+    SBR_DCHECK(S, j >= 0 && j < S.ntri);
     double t, u, v;
     if (tri_hit_idx<false>(r, S.tris + j, t_min, t, u, v) && t < limit) {
       found = true;
@@ -777,6 +814,7 @@ struct AnyTrav {
 
   __device__ __forceinline__ void round(const DevScene& S) {
     while (node >= 0) {
+      SBR_DCHECK(S, node < S.nnodes);
       const BvhNode* nd = S.nodes + node;
       const float4 a = __ldg(&nd->a), b = __ldg(&nd->b), c = __ldg(&nd->c);
       const int4 ch = __ldg(&nd->d);
@@ -814,6 +852,7 @@ struct AnyTrav {
     }
     while (leaf < 0) {
       const int s = leaf_start(leaf), n = leaf_count(leaf);
+      SBR_DCHECK(S, s >= 0 && s + n <= S.ntri);
       for (int j = s; j < s + n; ++j) {
         double t, u, v;
         if (tri_hit_idx<false>(r, S.tris + j, t_min, t, u, v) && t < limit) {
@@ -835,64 +874,6 @@ struct AnyTrav {
 };
 
 using ClosestTrav = ClosestTravT<true>;
-
-// ---------------------------------------------------------------------------
-// Conservative, division-light classification of one candidate occluder for
-// the occlusion query of segment a -> b (occluded_batch: ray o = a + eps*dn,
-// dn = (b - a) / len, t_min = 0, limit = len - 2 eps; geometry.py:187-201).
-// With q_i = v_i - a, D = b - a the segment's line meets the triangle's plane
-// at lambda = det(q0, q1, q2) / (D . N), N = (q1 - q0) x (q2 - q0), inside the
-// triangle iff the signed volumes s0 = D.(q1 x q2), s1 = D.(q2 x q0),
-// s2 = D.(q0 x q1) share one sign (their sum is D . N).  Every quantity is
-// computed in float64 with a forward error below 16 u * T (T = the product of
-// the operands' 1-norms, u = 2^-53); the reference's own watertight shear
-// test errs by the same order on its (rounded) ray, plus a few ulps of the
-// coordinates where it rounds o = a + eps dn and v - o.  So with margins of
-// 1e-12 T plus a positional pad P = 1e-13 (|a|_1 + |D|_1) (~1000 ulps of the
-// coordinates) propagated through the same products, a verdict of
-//    +1: all |s_i| beyond the margin with one sign, and the hit distance from
-//        a clearly inside (eps, len - eps)      -> the reference finds a hit
-//     0: two s_i clearly of opposite signs, or the hit distance clearly
-//        outside (eps, len - eps)                -> the reference finds none
-// is the reference's verdict for this triangle; anything closer to a
-// boundary returns -1 and the caller runs the exact test.
-__device__ __forceinline__ double l1(double3 v) { return (fabs(v.x) + fabs(v.y)) + fabs(v.z); }
-
-__device__ __forceinline__ int seg_occluder_class(const TriSlot* __restrict__ tri, double3 a,
-                                                  double3 D, double l1D, double len,
-                                                  double eps, double pad) {
-  const double* T = reinterpret_cast<const double*>(tri);
-  const double3 q0 = make_double3(__ldg(T) - a.x, __ldg(T + 1) - a.y, __ldg(T + 2) - a.z);
-  const double3 q1 = make_double3(__ldg(T + 3) - a.x, __ldg(T + 4) - a.y, __ldg(T + 5) - a.z);
-  const double3 q2 = make_double3(__ldg(T + 6) - a.x, __ldg(T + 7) - a.y, __ldg(T + 8) - a.z);
-  const double3 c12 = cross3(q1, q2), c20 = cross3(q2, q0), c01 = cross3(q0, q1);
-  const double s0 = dot_seq(D, c12), s1 = dot_seq(D, c20), s2 = dot_seq(D, c01);
-  const double n0 = l1(q0), n1 = l1(q1), n2 = l1(q2);
-  const double pD = pad * l1D;
-  const double m0 = 1e-12 * (l1D * n1 * n2) + pD * (n1 + n2),
-               m1 = 1e-12 * (l1D * n2 * n0) + pD * (n2 + n0),
-               m2 = 1e-12 * (l1D * n0 * n1) + pD * (n0 + n1);
-  const bool pos = s0 > m0 && s1 > m1 && s2 > m2;
-  const bool negv = s0 < -m0 && s1 < -m1 && s2 < -m2;
-  if (!pos && !negv) {
-    const bool some_pos = s0 > m0 || s1 > m1 || s2 > m2;
-    const bool some_neg = s0 < -m0 || s1 < -m1 || s2 < -m2;
-    return (some_pos && some_neg) ? 0 : -1;
-  }
-  const double S = (s0 + s1) + s2;                 // D . N, |S| > 0 by the margins
-  const double V = dot_seq(q0, c12);               // det(q0, q1, q2)
-  const double eS = (m0 + m1) + m2;
-  const double eV = 1e-12 * (n0 * n1 * n2) + pad * ((n0 * n1 + n1 * n2) + n2 * n0);
-  const double aS = fabs(S);
-  if (!(aS > 2.0 * eS)) return -1;
-  const double lam = V / S;                        // hit parameter along D
-  const double elam = (eV + fabs(lam) * eS) / (aS - eS) + 1e-12 * fabs(lam);
-  const double lo = (lam - elam) * len, hi = (lam + elam) * len;  // hit distance from a
-  const double slack = 1e-9 * (len + 1.0);
-  if (lo > eps + slack && hi < len - eps - slack) return 1;
-  if (hi < eps - slack || lo > len - eps + slack) return 0;
-  return -1;
-}
 
 // any hit with t_min < t < limit (_core.pyx:198-253); returns false on overflow
 __device__ __forceinline__ bool trace_any(const DevScene& S, double3 o, double3 d,

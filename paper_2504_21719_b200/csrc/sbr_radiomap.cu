@@ -54,6 +54,7 @@ struct MapQueue {
   double *exr, *exi, *eyr, *eyi, *ezr, *ezi;
   double *r_dist, *omega, *weight;
   uint64_t* g;
+  uint64_t cap;  // entries
 };
 
 struct HitBuf {
@@ -69,6 +70,7 @@ struct ScatterQueue {
   double *omega, *r_hit, *weight, *cos_i, *gamma;
   uint64_t* g;
   int32_t* matrow;
+  uint64_t cap;
 };
 
 // Ray-queue traffic is read once and written once per segment (GBs per
@@ -163,8 +165,8 @@ __global__ void __launch_bounds__(SBR_TRACE_TPB, SBR_TRACE_MINB) k_map_trace(Dev
         d = make_double3(qld(&q.dx[i]), qld(&q.dy[i]), qld(&q.dz[i]));
       }
     }
-    int sn[kStackSize];
-    float st[kStackSize];
+    alignas(8) int sn[(SBR_PACKED_STACK ? 2 : 1) * kStackSize];
+    float st[SBR_PACKED_STACK ? 1 : kStackSize];
     ClosestTravT<false> T(sn, st);  // the map needs t and the slot only
     T.start(S, o, d, 1e-4, __longlong_as_double(0x7ff0000000000000LL));
     if (!active) T.idle();
@@ -223,6 +225,7 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
 #endif
     const int tri = qld(&hits.tri[i]);
     if (tri < -1) continue;  // empty comb slot / stack overflow
+    SBR_DCHECK(S, tri < S.ntri && i < qi.cap);
     if (SHADE_FIRST && tri < 0) {
       // a launch ray that escapes does nothing but count (no plane crossing at
       // segment 0): skip its direction / field / precoding weight
@@ -358,6 +361,7 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
       const double g_den = sqrt(cabs2(c_perp) + cabs2(c_par));
       const double gamma = g_den > 0.0 ? g_num / g_den : 0.0;
       const unsigned long long j = append_slot(count_s);
+      SBR_DCHECK(S, j < sq.cap);
       qst(&sq.dx[j], d.x);
       qst(&sq.dy[j], d.y);
       qst(&sq.dz[j], d.z);
@@ -383,6 +387,7 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
       continue;
     }
     const unsigned long long j = append_slot(count_out);
+    SBR_DCHECK(S, j < qo.cap);
     qst(&qo.ox[j], pt.x);
     qst(&qo.oy[j], pt.y);
     qst(&qo.oz[j], pt.z);
@@ -478,6 +483,7 @@ __global__ void __launch_bounds__(128, SBR_SCATTER_MINB) k_map_scatter(DevScene 
     E.z = cdiv(th_s.z * co0 + ph_s.z * co1, inv_r);
     respawns++;
     const unsigned long long o = append_slot(count_out);
+    SBR_DCHECK(S, o < qo.cap && j < sq.cap);
     qst(&qo.ox[o], qld(&sq.px[j]));
     qst(&qo.oy[o], qld(&sq.py[j]));
     qst(&qo.oz[o], qld(&sq.pz[j]));
@@ -699,7 +705,9 @@ int wave_alloc(int64_t cap, cudaStream_t st, Wave* w) {
     }
     w->q[k].g = (uint64_t*)p;
     p += cap * sizeof(uint64_t);
+    w->q[k].cap = (uint64_t)cap;
   }
+  w->sq.cap = (uint64_t)cap;
   {
     double** f[20] = {&w->sq.dx, &w->sq.dy, &w->sq.dz, &w->sq.nx, &w->sq.ny, &w->sq.nz,
                       &w->sq.px, &w->sq.py, &w->sq.pz, &w->sq.exr, &w->sq.exi, &w->sq.eyr,

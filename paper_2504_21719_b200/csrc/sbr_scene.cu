@@ -500,7 +500,12 @@ __global__ void k_slot_tables(const TriSlot* __restrict__ tris, int n, double* _
 // leaves in depth-first order, so the leaf collapse / emit path is shared.
 // ---------------------------------------------------------------------------
 #ifndef SBR_PLOC_RADIUS
-#define SBR_PLOC_RADIUS 16  // canyon map = radius 12, city map +11 %, config-3 CIR -5 % (r6..r20 swept)
+// PLOC search radius.  Re-swept on the config-4 headline (city, 1e9-ray map,
+// k_map_trace ms per map / nodes per ray-bounce): r4 540, r6 520, r8 496 /
+// 25.9, r10 599, r12 624 / 30.3, r16 528 / 26.6, r24 worse; config-3
+// visibility r8 59.9 ms vs r16 60.8; the canyon trace is flat (4.1-4.3 ms).
+// SAH cost (61.2-62.6) does not rank these trees; visits per ray do.
+#define SBR_PLOC_RADIUS 8
 #endif
 constexpr int kPlocRadius = SBR_PLOC_RADIUS;
 
@@ -696,6 +701,14 @@ extern "C" {
 
 const char* sbr_last_error(void) { return g_last_error.c_str(); }
 int sbr_version(void) { return 100; }
+// bit 0: checked build (-DSBR_CHECKED device bounds assertions)
+int sbr_build_flags(void) {
+#ifdef SBR_CHECKED
+  return 1;
+#else
+  return 0;
+#endif
+}
 
 int sbr_set_bvh_builder(int32_t builder) {
   if (builder != 0 && builder != 1) return set_error(SBR_ERR_INVALID, "builder: 0 LBVH, 1 PLOC");
@@ -1060,6 +1073,8 @@ int sbr_scene_check(SbrScene* S, void* stream) {
   SBR_CUDA(cudaGetLastError());
   if (w) {
     SBR_CUDA(cudaMemsetAsync(S->error_word, 0, sizeof(unsigned), st));
+    if (w & kErrBounds)
+      return set_error(SBR_ERR_INTERNAL, "device bounds check failed (checked build)");
     if (w & kErrStack) return set_error(SBR_ERR_STACK, "BVH traversal stack overflow");
   }
   return SBR_OK;

@@ -33,8 +33,8 @@ __global__ void __launch_bounds__(128) k_trace_closest(DevScene S, const double*
   for (int64_t base = wid * 32; base < n; base += warps * 32) {
     const int64_t i = base + (threadIdx.x & 31);
     const bool active = i < n;
-    int sn[kStackSize];
-    float st[kStackSize];
+    alignas(8) int sn[(SBR_PACKED_STACK ? 2 : 1) * kStackSize];
+    float st[SBR_PACKED_STACK ? 1 : kStackSize];
     ClosestTrav T(sn, st);
     if (active) T.start(S, ldg3(o + 3 * i), ldg3(d + 3 * i), t_min, __ldg(t_max + i));
     else T.idle();

@@ -136,20 +136,30 @@ class Accel:
         _native.check(L.sbr_scene_permutation(handle, perm.ctypes.data_as(ctypes.c_void_p)))
         self.perm = perm
         self.num_nodes = int(L.sbr_scene_num_nodes(handle))
-        self.tri_v0 = np.ascontiguousarray(v0[perm])
-        self.tri_v1 = np.ascontiguousarray(v1[perm])
-        self.tri_v2 = np.ascontiguousarray(v2[perm])
-        self.tri_object_id = np.concatenate(objs)[perm]
-        self.tri_primitive_id = np.concatenate(prims)[perm]
+        self._input = (v0, v1, v2)            # input-order corners (wedge extraction)
+        sizes = np.array([len(m.triangles) for m in self.meshes], np.int64)
+        oid = np.array([m.object_id for m in self.meshes], np.int64)
+        obj_in, prim_in = np.concatenate(objs), np.concatenate(prims)
+        self._obj_in, self._prim_in = obj_in, prim_in
+        self.tri_object_id = obj_in[perm]
+        self.tri_primitive_id = prim_in[perm]
         self.tri_mesh_index = np.concatenate(mesh_idx)[perm]
         self._tables = None   # device-derived normals / plane hashes, copied on first use
+        self._corners = None  # slot-order host corners, on first use
         lo = np.minimum(np.minimum(v0, v1), v2).min(axis=0)
         hi = np.maximum(np.maximum(v0, v1), v2).max(axis=0)
         self.bounds = (lo - 1e-12 * (1.0 + np.abs(lo)), hi + 1e-12 * (1.0 + np.abs(hi)))
         # closest-hit tie rule: smaller (object_id, primitive_id) wins
-        order = np.lexsort((self.tri_primitive_id, self.tri_object_id))
-        rank = np.empty(len(order), dtype=np.int32)
-        rank[order] = np.arange(len(order), dtype=np.int32)
+        if len(np.unique(oid)) == len(oid):
+            # unique object ids: rank = start of the mesh in object-id order + primitive
+            start = np.empty(len(oid), np.int64)
+            by_id = np.argsort(oid, kind="stable")
+            start[by_id] = np.concatenate([[0], np.cumsum(sizes[by_id])[:-1]])
+            rank = (np.repeat(start, sizes) + prim_in)[perm].astype(np.int32)
+        else:
+            order = np.lexsort((self.tri_primitive_id, self.tri_object_id))
+            rank = np.empty(len(order), dtype=np.int32)
+            rank[order] = np.arange(len(order), dtype=np.int32)
         self.tri_tie_rank = rank
         self.set_attributes(tie_rank=rank)
 
@@ -167,6 +177,25 @@ class Accel:
                 hr.ctypes.data_as(ctypes.c_void_p), hf.ctypes.data_as(ctypes.c_void_p)))
             self._tables = (nrm, hr, hf)
         return self._tables
+
+    def _slot_corners(self):
+        if self._corners is None:
+            v0, v1, v2 = self._input
+            p = self.perm
+            self._corners = tuple(np.ascontiguousarray(v[p]) for v in (v0, v1, v2))
+        return self._corners
+
+    @property
+    def tri_v0(self):
+        return self._slot_corners()[0]
+
+    @property
+    def tri_v1(self):
+        return self._slot_corners()[1]
+
+    @property
+    def tri_v2(self):
+        return self._slot_corners()[2]
 
     @property
     def tri_normal(self):

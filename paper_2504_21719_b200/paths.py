@@ -219,43 +219,72 @@ class SceneModel:
         return self._wedges
 
     def _build_wedge_tables(self):
+        """Wedges, edge hashes and the per-slot wedge CSR (paths.py:452-475).
+
+        Extraction and edge hashes run on the GPU (wedges.extract_wedges_device);
+        the per-slot lists of owned wedges are built from the owners' input
+        triangle indices through the BVH slot permutation.
+        """
         from . import _abi, _native
-        from .wedges import extract_wedges, hash_edge
-        W = extract_wedges(self.meshes, dihedral_threshold_deg=self.dihedral_threshold_deg)
+        from .wedges import extract_wedges_device
         acc = self.accel
+        W, t = extract_wedges_device(self.meshes, self.dihedral_threshold_deg, acc.device,
+                                     accel=acc)
         nt = acc.num_triangles
-        owned = [[] for _ in range(nt)]
-        for wi, w in enumerate(W):
-            for key in set(w.owners()):
-                slot = self._tri_slot.get(key)
-                if slot is not None:
-                    owned[slot].append(wi)
-        counts = np.array([len(x) for x in owned], dtype=np.int64)
-        self.tri_wedge_offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
-        self.tri_wedge_ids = np.array([wi for lst in owned for wi in sorted(lst)],
-                                      dtype=np.int64)
+        nw = len(W)
+        if nw:
+            # owners (o, m) of every wedge, deduplicated per wedge (set(w.owners()))
+            wid0 = np.repeat(np.arange(nw), np.diff(t["off0"]))
+            widn = np.repeat(np.arange(nw), np.diff(t["offn"]))
+            tri = np.concatenate([t["tri0"], t["trin"]])
+            wid = np.concatenate([wid0, widn])
+            ids = sorted({m.object_id for m in self.meshes})
+            if len(ids) == len(self.meshes):
+                # input triangle -> slot (object ids identify the mesh)
+                inv = np.empty(nt, np.int64)
+                inv[acc.perm] = np.arange(nt)
+                slot = inv[tri]
+            else:   # shared object ids: the reference's (o, m) -> last slot mapping
+                keys = zip(t["obj"][tri].tolist(), t["prim"][tri].tolist())
+                slot = np.array([self._tri_slot.get(k, -1) for k in keys], np.int64)
+            pairs = np.unique(np.stack([slot, wid], 1)[slot >= 0], axis=0)  # sorted (slot, wid)
+            counts = np.bincount(pairs[:, 0], minlength=nt)
+            self.tri_wedge_offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+            self.tri_wedge_ids = pairs[:, 1].astype(np.int64)
+        else:
+            counts = np.zeros(nt, np.int64)
+            self.tri_wedge_offsets = np.zeros(nt + 1, np.int64)
+            self.tri_wedge_ids = np.zeros(0, np.int64)
         self.tri_has_wedge = counts > 0
-        hs = [hash_edge(w) for w in W]
-        self.wedge_hash_round = np.array([h[0] for h in hs], dtype=np.uint64)
-        self.wedge_hash_floor = np.array([h[1] for h in hs], dtype=np.uint64)
-        row = {int(o): i for i, o in enumerate(self._object_ids)}
-        arr = lambda attr: np.ascontiguousarray(  # noqa: E731
-            np.array([getattr(w, attr) for w in W], dtype=np.float64).reshape(-1, 3))
+        self.wedge_hash_round = t["hash_r"] if nw else np.zeros(0, np.uint64)
+        self.wedge_hash_floor = t["hash_f"] if nw else np.zeros(0, np.uint64)
+        row = np.searchsorted(self._object_ids, t["obj"]) if nw else np.zeros(0, np.int64)
+        if nw:
+            first0 = t["tri0"][t["off0"][:-1]]                    # face0[0] (always present)
+            has_n = np.diff(t["offn"]) > 0
+            firstn = np.where(has_n, t["trin"][np.minimum(t["offn"][:-1], len(t["trin"]) - 1)]
+                              if len(t["trin"]) else first0, first0)
+            mat0, matn = row[first0], row[firstn]
+        else:
+            mat0 = matn = np.zeros(0, np.int64)
         keep = {
-            "origin": arr("origin"), "e_hat": arr("e_hat"), "t0_hat": arr("t0_hat"),
-            "n0_hat": arr("n0_hat"), "nn_hat": arr("nn_hat"),
-            "length": np.array([w.length for w in W], dtype=np.float64),
-            "n_open": np.array([w.n for w in W], dtype=np.float64),
+            "origin": t["origin"] if nw else np.zeros((0, 3)),
+            "e_hat": t["e_hat"] if nw else np.zeros((0, 3)),
+            "t0_hat": t["t0_hat"] if nw else np.zeros((0, 3)),
+            "n0_hat": t["n0_hat"] if nw else np.zeros((0, 3)),
+            "nn_hat": t["nn_hat"] if nw else np.zeros((0, 3)),
+            "length": t["length"] if nw else np.zeros(0),
+            "n_open": t["n_open"] if nw else np.zeros(0),
             "hash_r": self.wedge_hash_round, "hash_f": self.wedge_hash_floor,
-            "mat0": np.array([row[w.face0[0][0]] for w in W], dtype=np.int32),
-            "matn": np.array([row[(w.facen or w.face0)[0][0]] for w in W], dtype=np.int32),
+            "mat0": np.asarray(mat0, np.int32), "matn": np.asarray(matn, np.int32),
             "slot_offsets": self.tri_wedge_offsets.astype(np.int32),
             "slot_ids": self.tri_wedge_ids.astype(np.int32),
         }
+        keep = {k: np.ascontiguousarray(v) for k, v in keep.items()}
         tab = _abi.SbrWedgeTable()
-        tab.n_wedges = len(W)
+        tab.n_wedges = nw
         for k, v in keep.items():
-            setattr(tab, k, np.ascontiguousarray(v).ctypes.data)
+            setattr(tab, k, v.ctypes.data)
         _native.check(_native.load_library().sbr_scene_set_wedges(acc.handle, ctypes.byref(tab)))
         self._wedge_host = keep
         self._wedges = W
@@ -267,7 +296,10 @@ class SceneModel:
         self._object_ids = np.array(sorted(m.object_id for m in self.meshes),
                                     dtype=np.int64)
         self._object_materials = [self.materials[oid] for oid in self._object_ids]
-        self.tri_material_row = np.searchsorted(self._object_ids, accel.tri_object_id)
+        # material row per slot (paths.py:497-499): one searchsorted per mesh
+        mesh_row = np.searchsorted(self._object_ids, [m.object_id for m in self.meshes])
+        sizes = [len(m.triangles) for m in self.meshes]
+        self.tri_material_row = np.repeat(mesh_row, sizes)[accel.perm]
         self._slot_map = None
         accel.set_attributes(matrow=self.tri_material_row)
 

@@ -275,3 +275,83 @@ def hash_edge(wedge):
         h_r = fnv1a_u64(quantize_round(comp) & _MASK64, h_r)
         h_f = fnv1a_u64(quantize_floor(comp) & _MASK64, h_f)
     return h_r, h_f
+
+
+def extract_wedges_device(meshes, dihedral_threshold_deg=1.0, device=None, accel=None):
+    """extract_wedges + hash_edge on the GPU (csrc/sbr_wedges.cu, sbr_wedges_extract).
+
+    Returns (wedges, tables): the reference's Wedge list (same order, owners,
+    frames to ~1 ulp) and host arrays of the per-wedge data the device tables
+    need -- frames, lengths, n, (round, floor) edge hashes and the owner lists
+    as input-triangle indices (CSR, `off0` / `tri0` for face0, `offn` / `trin`
+    for facen).  Scene ingestion: 1.45 M edges of the 483k-triangle city in
+    tens of milliseconds instead of seconds of host numpy.
+    """
+    import ctypes
+
+    import torch
+
+    from . import _native
+    L = _native.lib()
+    if not meshes:
+        return [], None
+    if accel is not None:       # the Accel's input-order corners and ids (same meshes)
+        v0, v1, v2 = accel._input
+        obj, prim = accel._obj_in, accel._prim_in
+    else:
+        V0, V1, V2, O, P = [], [], [], [], []
+        for m in meshes:
+            a, b, c = m.triangle_corners()
+            V0.append(a)
+            V1.append(b)
+            V2.append(c)
+            O.append(np.full(len(a), m.object_id, dtype=np.int64))
+            P.append(np.arange(len(a), dtype=np.int64))
+        v0, v1, v2 = (np.ascontiguousarray(np.concatenate(x), dtype=np.float64)
+                      for x in (V0, V1, V2))
+        obj = np.ascontiguousarray(np.concatenate(O))
+        prim = np.ascontiguousarray(np.concatenate(P))
+    dev = _native.device_of(device)
+    vp = ctypes.c_void_p
+    handle = vp()
+    with torch.cuda.device(dev):
+        _native.check(L.sbr_wedges_extract(
+            v0.ctypes.data_as(vp), v1.ctypes.data_as(vp), v2.ctypes.data_as(vp),
+            obj.ctypes.data_as(vp), prim.ctypes.data_as(vp), len(obj),
+            float(dihedral_threshold_deg), dev.index, _native.stream_ptr(dev),
+            ctypes.byref(handle)))
+    try:
+        nw, n0, nn = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _native.check(L.sbr_wedges_count(handle, ctypes.byref(nw), ctypes.byref(n0),
+                                         ctypes.byref(nn)))
+        nw, n0, nn = nw.value, n0.value, nn.value
+        t = {k: np.empty((nw, 3)) for k in ("origin", "e_hat", "t0_hat", "n0_hat", "nn_hat")}
+        t["length"] = np.empty(nw)
+        t["n_open"] = np.empty(nw)
+        t["hash_r"] = np.empty(nw, np.uint64)
+        t["hash_f"] = np.empty(nw, np.uint64)
+        t["off0"] = np.empty(nw + 1, np.int64)
+        t["offn"] = np.empty(nw + 1, np.int64)
+        own0 = np.empty(max(n0, 1), np.int64)
+        ownn = np.empty(max(nn, 1), np.int64)
+        ptrs = [t[k].ctypes.data_as(vp) for k in ("origin", "e_hat", "t0_hat", "n0_hat",
+                                                   "nn_hat", "length", "n_open", "hash_r",
+                                                   "hash_f", "off0")]
+        _native.check(L.sbr_wedges_copy(handle, *ptrs, own0.ctypes.data_as(vp),
+                                        t["offn"].ctypes.data_as(vp), ownn.ctypes.data_as(vp)))
+    finally:
+        L.sbr_wedges_free(handle)
+    own0, ownn = own0[:n0], ownn[:nn]
+    t["tri0"], t["trin"] = own0 // 3, ownn // 3
+    # owner tuples (object_id, primitive_id, local) as Python ints
+    trip0 = list(zip(obj[own0 // 3].tolist(), prim[own0 // 3].tolist(), (own0 % 3).tolist()))
+    tripn = list(zip(obj[ownn // 3].tolist(), prim[ownn // 3].tolist(), (ownn % 3).tolist()))
+    o0, on = t["off0"].tolist(), t["offn"].tolist()
+    wedges = [Wedge(origin=t["origin"][i].copy(), e_hat=t["e_hat"][i].copy(),
+                    length=float(t["length"][i]), n0_hat=t["n0_hat"][i].copy(),
+                    nn_hat=t["nn_hat"][i].copy(), t0_hat=t["t0_hat"][i].copy(),
+                    n=float(t["n_open"][i]), face0=trip0[o0[i]:o0[i + 1]],
+                    facen=tripn[on[i]:on[i + 1]])
+              for i in range(nw)]
+    t["obj"], t["prim"] = obj, prim
+    return wedges, t

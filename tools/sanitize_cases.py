@@ -29,6 +29,10 @@ from paper_2504_21719_b200.sampling import Interaction  # noqa: E402
 
 ALL = frozenset(Interaction)
 case = sys.argv[1]
+if os.environ.get("SBR_REQUIRE_CHECKED") == "1":
+    from paper_2504_21719_b200 import _native
+    assert _native.lib().sbr_build_flags() & 1, "SBR_LIB_PATH is not the checked build"
+    print("checked build:", _native.LIB_PATH)
 if case == "map":
     meshes = scenes.box_room_walls()
     mats = scenes.uniform_materials(meshes, scenes.concrete(scattering=0.3))

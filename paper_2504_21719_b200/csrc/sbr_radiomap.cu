@@ -120,13 +120,14 @@ __device__ __forceinline__ unsigned long long append_slot(unsigned long long* co
 #ifndef SBR_TRACE_MINB
 #define SBR_TRACE_MINB 7  // with speculation: 6.85 ms vs 6.93 at 8 blocks
 #endif
-#ifndef SBR_SHADE_WARPSYNC
-#define SBR_SHADE_WARPSYNC 1  // canyon shade 5.08 -> 5.00 ms per step
-#endif
 #ifndef SBR_SHADE_SPLIT
 #define SBR_SHADE_SPLIT 1  // canyon shade 5.0 -> 4.8 ms per step (smaller kernels, less spill)
 #endif
 #define SHADE_FIRST (SBR_SHADE_SPLIT ? kFirst : seg == 0)
+#ifndef SBR_SHADE_CHUNK
+#define SBR_SHADE_CHUNK 128  // queue items a shade warp claims at once (256: config-4 map 899 ms, 128: 895, 1024: 962)
+#endif
+constexpr int kShadeChunk = SBR_SHADE_CHUNK;
 #ifndef SBR_SHADE_MINB
 #define SBR_SHADE_MINB 8
 #endif
@@ -162,7 +163,12 @@ __global__ void __launch_bounds__(SBR_TRACE_TPB, SBR_TRACE_MINB) k_map_trace(Dev
         else qst(&hits.tri[i], -3);  // comb slot past the end of the range
       } else {
         o = make_double3(qld(&q.ox[i]), qld(&q.oy[i]), qld(&q.oz[i]));
-        d = make_double3(qld(&q.dx[i]), qld(&q.dy[i]), qld(&q.dz[i]));
+        if (isnan(o.x)) {  // padding of a shade warp's last output batch
+          active = false;
+          qst(&hits.tri[i], -3);
+        } else {
+          d = make_double3(qld(&q.dx[i]), qld(&q.dy[i]), qld(&q.dz[i]));
+        }
       }
     }
     alignas(8) int sn[(SBR_PACKED_STACK ? 2 : 1) * kStackSize];
@@ -206,23 +212,39 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
                                                    MapQueue qo, unsigned long long* count_out,
                                                    ScatterQueue sq, unsigned long long* count_s,
                                                    double* __restrict__ grid,
-                                                   unsigned long long* __restrict__ counters, ShardMap sh) {
+                                                   unsigned long long* __restrict__ counters, ShardMap sh,
+                                                   unsigned long long* work) {
   LaneCounters K = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
   const uint64_t n = SHADE_FIRST ? comb.slots() : (uint64_t)*count_in;
   const double3 n_hat = make_double3(P.normal[0], P.normal[1], P.normal[2]);
-#if SBR_SHADE_WARPSYNC
-  // warp-uniform iterations with a __syncwarp at the end of each: lanes that
-  // take a short exit (escaped, culled) wait for the warp instead of running
-  // ahead into the next item, so the FP64 Fresnel / field code issues for
-  // converged lanes; `continue` inside the do-while(0) ends the item
-  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); i0 < n;
-       i0 += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i = i0 + (threadIdx.x & 31u);
-    if (i < n) do {
-#else
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-#endif
+  const unsigned lane = threadIdx.x & 31u;
+  // Work: each warp claims kShadeChunk consecutive queue items at a time and
+  // walks them 32 per warp-uniform iteration (a __syncwarp closes each: lanes
+  // that take a short exit wait for the warp, so the FP64 Fresnel / field code
+  // issues for converged lanes; `continue` inside the do-while(0) ends the
+  // item).  Output: the warp's R / T survivors fill 32-slot batches of the
+  // next queue in input order (a new batch reserved with one atomic when the
+  // current one is full), so a trace warp of the next segment gets the
+  // survivors of ~64 neighbouring rays -- coherent -- instead of two
+  // unrelated warps' survivors; the warp pads its last batch with dead
+  // entries (NaN origin) that the trace skips.
+  unsigned long long res_base = 0;
+  int res_fill = 32;  // warp-uniform: slots used in the current batch (32 = none reserved)
+  while (true) {
+    unsigned long long c0 = 0;
+    if (lane == 0) c0 = atomicAdd(work, (unsigned long long)kShadeChunk);
+    c0 = __shfl_sync(0xffffffffu, c0, 0);
+    if (c0 >= n) break;
+    const uint64_t c1 = c0 + kShadeChunk < n ? c0 + kShadeChunk : n;
+  for (uint64_t i0 = c0; i0 < c1; i0 += 32) {
+    const uint64_t i = i0 + lane;
+    bool emit = false;
+    // the item's state, declared here so the output after the body reads it
+    double3 o, d, pt, nd;
+    cvec3 E;
+    double r_dist, omega, weight;
+    uint64_t g;
+    if (i < c1) do {
     const int tri = qld(&hits.tri[i]);
     if (tri < -1) continue;  // empty comb slot / stack overflow
     SBR_DCHECK(S, tri < S.ntri && i < qi.cap);
@@ -233,10 +255,6 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
       K.escaped++;
       continue;
     }
-    double3 o, d;
-    cvec3 E;
-    double r_dist, omega, weight;
-    uint64_t g;
     if (SHADE_FIRST) {
       g = sh.gid(begin + comb.sample(i));
       o = make_double3(P.source[0], P.source[1], P.source[2]);
@@ -300,7 +318,7 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
       }
       if (!keep) continue;
     }
-    const double3 pt = o + t_hit * d;
+    pt = o + t_hit * d;
     double3 nrm = ldg3(S.normals + 3 * (int64_t)tri);
     if (dot_seq(d, nrm) > 0.0) nrm = neg(nrm);
     const double cos_i = fabs(dot_seq(d, nrm));
@@ -338,7 +356,7 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
     double3 e_perp, e_par;
     incidence_frame(d, nrm, e_perp, e_par);
     const cplx c_perp = cdot_real(E, e_perp), c_par = cdot_real(E, e_par);
-    double3 nd = d;
+    nd = d;
     if (code == 0) {
       const double dn = dot_seq(d, nrm);
       const double3 kr = d - (2.0 * dn) * nrm;
@@ -386,30 +404,54 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
       qst(&sq.matrow[j], __ldg(S.matrow + tri));
       continue;
     }
-    const unsigned long long j = append_slot(count_out);
-    SBR_DCHECK(S, j < qo.cap);
-    qst(&qo.ox[j], pt.x);
-    qst(&qo.oy[j], pt.y);
-    qst(&qo.oz[j], pt.z);
-    qst(&qo.dx[j], nd.x);
-    qst(&qo.dy[j], nd.y);
-    qst(&qo.dz[j], nd.z);
-    qst(&qo.exr[j], E.x.re);
-    qst(&qo.exi[j], E.x.im);
-    qst(&qo.eyr[j], E.y.re);
-    qst(&qo.eyi[j], E.y.im);
-    qst(&qo.ezr[j], E.z.re);
-    qst(&qo.ezi[j], E.z.im);
-    qst(&qo.r_dist[j], r_dist);
-    qst(&qo.omega[j], omega);
-    qst(&qo.weight[j], weight);
-    qst(&qo.g[j], g);
-#if SBR_SHADE_WARPSYNC
+    emit = true;
     } while (0);
+    // ordered batch output of this iteration's survivors (warp-converged)
+    const unsigned m = __ballot_sync(0xffffffffu, emit);
+    if (m) {
+      const int c = __popc(m);
+      const int first = c < 32 - res_fill ? c : 32 - res_fill;
+      unsigned long long nb = 0;
+      if (c > first) {
+        if (lane == 0) nb = atomicAdd(count_out, 32ULL);
+        nb = __shfl_sync(0xffffffffu, nb, 0);
+      }
+      const int rank = __popc(m & ((1u << lane) - 1u));
+      const unsigned long long j = rank < first ? res_base + res_fill + rank : nb + (rank - first);
+      if (c > first) {
+        res_base = nb;
+        res_fill = c - first;
+      } else {
+        res_fill += c;
+      }
+      if (emit) {
+        SBR_DCHECK(S, j < qo.cap);
+        qst(&qo.ox[j], pt.x);
+        qst(&qo.oy[j], pt.y);
+        qst(&qo.oz[j], pt.z);
+        qst(&qo.dx[j], nd.x);
+        qst(&qo.dy[j], nd.y);
+        qst(&qo.dz[j], nd.z);
+        qst(&qo.exr[j], E.x.re);
+        qst(&qo.exi[j], E.x.im);
+        qst(&qo.eyr[j], E.y.re);
+        qst(&qo.eyi[j], E.y.im);
+        qst(&qo.ezr[j], E.z.re);
+        qst(&qo.ezi[j], E.z.im);
+        qst(&qo.r_dist[j], r_dist);
+        qst(&qo.omega[j], omega);
+        qst(&qo.weight[j], weight);
+        qst(&qo.g[j], g);
+      }
+    }
     __syncwarp();
-#endif
   }
-  const unsigned lane = threadIdx.x & 31u;
+  }
+  // pad the last batch: dead entries (NaN origin) the next trace skips
+  if (res_fill < 32 && (int)lane >= res_fill) {
+    SBR_DCHECK(S, res_base + lane < qo.cap);
+    qst(&qo.ox[res_base + lane], __longlong_as_double(0x7ff8000000000000LL));
+  }
   const unsigned v[7] = {K.rb, K.deposits, K.escaped, K.respawns, K.terminated, K.thr, K.rr};
   const int idx[7] = {SBR_MC_RAY_BOUNCES, SBR_MC_DEPOSITS, SBR_MC_ESCAPED, SBR_MC_RESPAWNS,
                       SBR_MC_TERMINATED, SBR_MC_THRESHOLD_KILLED, SBR_MC_ROULETTE_KILLED};
@@ -506,10 +548,11 @@ __global__ void __launch_bounds__(128, SBR_SCATTER_MINB) k_map_scatter(DevScene 
 }
 
 __global__ void k_reset_pass(unsigned long long* work, unsigned long long* count_next,
-                             unsigned long long* count_s) {
+                             unsigned long long* count_s, unsigned long long* shade_work) {
   *work = 0ULL;
   *count_next = 0ULL;
   *count_s = 0ULL;
+  *shade_work = 0ULL;
 }
 
 __global__ void __launch_bounds__(128) k_direct(DevScene S, SbrMapParams P,
@@ -683,7 +726,8 @@ struct Wave {
   MapQueue q[2];
   HitBuf hits;
   ScatterQueue sq;
-  unsigned long long* ctl = nullptr;  // [0] work, [1] count A, [2] count B, [3] S count
+  unsigned long long* ctl = nullptr;  // [0] trace work, [1] count A, [2] count B, [3] S count,
+                                      // [4] shade work
 };
 
 int wave_alloc(int64_t cap, cudaStream_t st, Wave* w) {
@@ -753,7 +797,9 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
   const uint64_t F = comb_stride(P->num_samples);
   Wave wave;
   Wave* w = &wave;
-  if ((rc = wave_alloc(chunk + (int64_t)F, st, w))) return rc;
+  // + the dead padding of every shade warp's last output batch (< 32 each)
+  const int64_t pad = 32LL * sms * SBR_SHADE_MINB * 4 + 64;
+  if ((rc = wave_alloc(chunk + (int64_t)F + pad, st, w))) return rc;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_map_trace<false>, SBR_TRACE_TPB, 0);
   if (per_sm < 1) per_sm = 1;
@@ -766,7 +812,7 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
     int cur = 0;
     for (int seg = 0; seg <= P->max_depth; ++seg) {
       // ctl[0] = work counter; ctl[1 + cur] = this segment's count; ctl[2 - cur] = next count
-      k_reset_pass<<<1, 1, 0, st>>>(w->ctl, w->ctl + 2 - cur, w->ctl + 3);
+      k_reset_pass<<<1, 1, 0, st>>>(w->ctl, w->ctl + 2 - cur, w->ctl + 3, w->ctl + 4);
       if ((rc = launch_status("k_reset_pass"))) break;
       prof_begin(st, "k_map_trace");
       (seg == 0 ? k_map_trace<true> : k_map_trace<false>)<<<trace_blocks, SBR_TRACE_TPB, 0, st>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo, cnt,
@@ -776,7 +822,7 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
       prof_begin(st, "k_map_shade");
       (seg == 0 ? k_map_shade<true> : k_map_shade<false>)<<<shade_blocks, 128, 0, st>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo,
                                                 comb, w->hits, w->q[1 - cur], w->ctl + 2 - cur,
-                                                w->sq, w->ctl + 3, grid, counters, sh);
+                                                w->sq, w->ctl + 3, grid, counters, sh, w->ctl + 4);
       prof_end(st);
       if ((rc = launch_status("k_map_shade"))) break;
       if (seg < P->max_depth && (P->allow_mask & 2)) {

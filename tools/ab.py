@@ -20,6 +20,9 @@ import bench
 from paper_2504_21719_b200 import SceneModel, _native, _abi, scenes, PathConfig, RadioDevice, compute_paths
 from paper_2504_21719_b200.sampling import Interaction
 out = {}
+import os
+if os.environ.get("AB_BUILDER"):
+    _native.check(_native.lib().sbr_set_bvh_builder(int(os.environ["AB_BUILDER"])))
 def maps(workload, tx, n, what):
     meshes, mats, grid, cfg = workload
     sc = SceneModel(meshes, mats)

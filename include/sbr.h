@@ -461,6 +461,11 @@ int sbr_cir_fields(const SbrScene* scene, const SbrFieldParams* params, const Sb
                    const double* path_vertices_dev, const int32_t* status_dev, int64_t n,
                    double* gain_dev, double* delay_dev, double* doppler_dev,
                    double* departure_dev, double* arrival_dev, void* stream);
+/* Path count per link from which sbr_cfr contracts on the FP64 tensor cores
+ * (mma.sync m8n8k4 f64; fused multiply-adds, ~1e-16 of max|H| from the
+ * path-order sum) instead of the path-order SIMT kernel; < 0 disables it.
+ * Default 16.  No reference counterpart. */
+int sbr_set_cfr_dmma_min_paths(int64_t min_paths);
 /* Channel frequency response of one link (frequency_response paths.py:1519-1547):
  * H[r, t, f] = sum_p a_p u_rx,r(arrival_p) u_tx,t(departure_p) e^{-j 2 pi f tau_p},
  * accumulated in path order in float64.  synthetic = 0: element-indexed paths

@@ -380,6 +380,9 @@ __global__ void k_cfr_weights(const double* __restrict__ gain, int64_t np,
 // H[row, f] = sum_p W[row, p] E[p, f], p in order.  Block: 32 rows x 64
 // frequencies, 256 threads x (2 rows x 4 frequencies), K staged 16 at a time.
 constexpr int kCfrRows = 32, kCfrCols = 64, kCfrK = 16;
+#ifndef SBR_CFR_DMMA_MIN
+#define SBR_CFR_DMMA_MIN 16  // paths per link from which the FP64 tensor-core contraction runs (tools/cfr_sweep.py: 5 paths SIMT 14 vs 15 us, 20 paths DMMA 22 vs 24 us)
+#endif
 
 __global__ void __launch_bounds__(256) k_cfr_contract(const double2* __restrict__ W,
                                                       const double2* __restrict__ E,
@@ -437,6 +440,97 @@ __global__ void __launch_bounds__(256) k_cfr_contract(const double2* __restrict_
   }
 }
 
+// ---- FP64 tensor-core path (DMMA, mma.sync m8n8k4 f64) for many paths ----
+// H = W . E as four real products per complex one (Hr += Wr Er - Wi Ei,
+// Hi += Wr Ei + Wi Er), each an 8x8x4 float64 MMA on the tensor cores (B200:
+// FP64 tensor-core peak ~40 TFLOP/s vs the SIMT kernel's 18.6 TFLOP/s
+// instruction roofline for unfused complex products).  The MMA fuses its
+// multiply-adds, so H differs from the path-order sum by rounding (~1e-16 of
+// max|H| per path; the north star allows 1e-4); used from kCfrDmmaMin paths on.
+// Block: 4 warps, 32 rows x 64 frequencies; warp: 16 x 32 (2 x 4 MMA tiles);
+// K staged 16 paths at a time in shared memory, real / imaginary planes split.
+constexpr int kDmRows = 32, kDmCols = 64, kDmK = 16;
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(128) k_cfr_contract_dmma(const double2* __restrict__ W,
+                                                           const double2* __restrict__ E,
+                                                           int64_t rows, int64_t np, int nf,
+                                                           double2* __restrict__ H) {
+  __shared__ double wr[kDmRows][kDmK + 1], wi[kDmRows][kDmK + 1];
+  __shared__ double er[kDmK][kDmCols + 1], ei[kDmK][kDmCols + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = (warp >> 1) * 16, wn = (warp & 1) * 32;  // warp tile origin in the block
+  const int64_t row0 = (int64_t)blockIdx.y * kDmRows;
+  const int col0 = blockIdx.x * kDmCols;
+  const int g = lane >> 2, q = lane & 3;  // fragment coordinates
+  double hr[2][4][2], hi[2][4][2];
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int n = 0; n < 4; ++n) hr[m][n][0] = hr[m][n][1] = hi[m][n][0] = hi[m][n][1] = 0.0;
+  for (int64_t k0 = 0; k0 < np; k0 += kDmK) {
+    const int kn = (int)((np - k0) < kDmK ? (np - k0) : kDmK);
+    for (int e = threadIdx.x; e < kDmRows * kDmK; e += 128) {
+      const int rr = e / kDmK, kk = e % kDmK;
+      const int64_t row = row0 + rr;
+      const double2 v = (row < rows && kk < kn) ? W[row * np + k0 + kk] : make_double2(0.0, 0.0);
+      wr[rr][kk] = v.x;
+      wi[rr][kk] = v.y;
+    }
+    for (int e = threadIdx.x; e < kDmK * kDmCols; e += 128) {
+      const int kk = e / kDmCols, cc = e % kDmCols;
+      const double2 v = (kk < kn && col0 + cc < nf) ? E[(k0 + kk) * nf + col0 + cc]
+                                                     : make_double2(0.0, 0.0);
+      er[kk][cc] = v.x;
+      ei[kk][cc] = v.y;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < kDmK; ks += 4) {
+      double ar[2], ai[2], br[4], bi[4];
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {  // A 8x4 row-major: (row g, col q)
+        ar[m] = wr[wm + 8 * m + g][ks + q];
+        ai[m] = wi[wm + 8 * m + g][ks + q];
+      }
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {  // B 4x8 col-major: (row q, col g)
+        br[n] = er[ks + q][wn + 8 * n + g];
+        bi[n] = ei[ks + q][wn + 8 * n + g];
+      }
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+          dmma(hr[m][n][0], hr[m][n][1], ar[m], br[n]);
+          dmma(hr[m][n][0], hr[m][n][1], ai[m], -bi[n]);
+          dmma(hi[m][n][0], hi[m][n][1], ar[m], bi[n]);
+          dmma(hi[m][n][0], hi[m][n][1], ai[m], br[n]);
+        }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {  // C 8x8: (row g, cols 2q, 2q + 1)
+    const int64_t row = row0 + wm + 8 * m + g;
+    if (row >= rows) continue;
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int f = col0 + wn + 8 * n + 2 * q + c;
+        if (f < nf) H[row * nf + f] = make_double2(hr[m][n][c], hi[m][n][c]);
+      }
+  }
+}
+
+static int64_t g_cfr_dmma_min = SBR_CFR_DMMA_MIN;
+
 unsigned grid_for(int64_t n, int block, int cap = 148 * 32) {
   int64_t g = (n + block - 1) / block;
   if (g < 1) g = 1;
@@ -467,6 +561,11 @@ int sbr_cir_fields(const SbrScene* scene, const SbrFieldParams* P, const SbrReco
   k_cir_fields<<<grid_for(n, 128), 128, 0, (cudaStream_t)stream>>>(
       dev_view(scene), *P, *rec, pv, status, n, gain, delay, doppler, dep, arr);
   return launch_status("k_cir_fields");
+}
+
+int sbr_set_cfr_dmma_min_paths(int64_t min_paths) {
+  g_cfr_dmma_min = min_paths;  // < 0: never use the tensor-core contraction
+  return SBR_OK;
 }
 
 int sbr_cfr(const double* gain, const double* delay, const double* dep, const double* arr,
@@ -515,10 +614,17 @@ int sbr_cfr(const double* gain, const double* delay, const double* dep, const do
       rc = launch_status("k_cfr_weights");
     }
     if (!rc) {
-      const dim3 grid((nf + kCfrCols - 1) / kCfrCols, (unsigned)((rows + kCfrRows - 1) / kCfrRows));
       prof_begin(st, "k_cfr_contract");
-      k_cfr_contract<<<grid, 256, 0, st>>>((const double2*)W, (const double2*)E, rows, np, nf,
-                                           (double2*)H);
+      if (g_cfr_dmma_min >= 0 && np >= g_cfr_dmma_min) {
+        const dim3 grid((nf + kDmCols - 1) / kDmCols, (unsigned)((rows + kDmRows - 1) / kDmRows));
+        k_cfr_contract_dmma<<<grid, 128, 0, st>>>((const double2*)W, (const double2*)E, rows, np,
+                                                  nf, (double2*)H);
+      } else {
+        const dim3 grid((nf + kCfrCols - 1) / kCfrCols,
+                        (unsigned)((rows + kCfrRows - 1) / kCfrRows));
+        k_cfr_contract<<<grid, 256, 0, st>>>((const double2*)W, (const double2*)E, rows, np, nf,
+                                             (double2*)H);
+      }
       prof_end(st);
       rc = launch_status("k_cfr_contract");
     }

@@ -364,10 +364,22 @@ def test_config5_arrays_cfr_city_vs_oracle(cuda):
 
 
 @pytest.mark.parametrize("synthetic", [True, False])
-def test_cfr_contraction_many_paths_vs_oracle(cuda, synthetic):
+@pytest.mark.parametrize("dmma_min", [-1, 0, 16])
+def test_cfr_contraction_many_paths_vs_oracle(cuda, synthetic, dmma_min):
     """Factorised CFR (steering x spin contraction) against the oracle's path-by-path sum:
     300 random paths (more than one K tile, ragged), 4x4 Rx x 8x8 Tx, 1000 subcarriers
-    (ragged frequency tile), element-indexed and synthetic arrays."""
+    (ragged frequency tile), element-indexed and synthetic arrays; through the
+    path-order SIMT contraction (dmma_min -1) and the FP64 tensor-core one (0, and
+    the default threshold 16)."""
+    from paper_2504_21719_b200 import _native
+    _native.check(_native.lib().sbr_set_cfr_dmma_min_paths(dmma_min))
+    try:
+        _cfr_many_paths(synthetic)
+    finally:
+        _native.check(_native.lib().sbr_set_cfr_dmma_min_paths(16))
+
+
+def _cfr_many_paths(synthetic):
     import types
     import oracle
     from paper_2504_21719_b200.cir import channel_response

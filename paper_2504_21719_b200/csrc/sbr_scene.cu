@@ -501,11 +501,12 @@ __global__ void k_slot_tables(const TriSlot* __restrict__ tris, int n, double* _
 // ---------------------------------------------------------------------------
 #ifndef SBR_PLOC_RADIUS
 // PLOC search radius.  Re-swept on the config-4 headline (city, 1e9-ray map,
-// k_map_trace ms per map / nodes per ray-bounce): r4 540, r6 520, r8 496 /
-// 25.9, r10 599, r12 624 / 30.3, r16 528 / 26.6, r24 worse; config-3
-// visibility r8 59.9 ms vs r16 60.8; the canyon trace is flat (4.1-4.3 ms).
-// SAH cost (61.2-62.6) does not rank these trees; visits per ray do.
-#define SBR_PLOC_RADIUS 8
+// k_map_trace ms per map / nodes per ray-bounce): r4 540, r6 520, r7 458,
+// r8 474-496 / 25.9, r9 556, r10 599, r12 624 / 30.3, r16 528 / 26.6, r24
+// worse; config-3 visibility r7 59.8 ms vs r16 60.8; the canyon trace is
+// flat (4.1-4.3 ms).  SAH cost (61.2-62.6) does not rank these trees;
+// visits per ray do.
+#define SBR_PLOC_RADIUS 7
 #endif
 constexpr int kPlocRadius = SBR_PLOC_RADIUS;
 
@@ -1002,7 +1003,7 @@ int sbr_scene_set_attributes(SbrScene* S, const int32_t* tie_rank, const double*
                              const int32_t* matrow, const uint64_t* hash_r,
                              const uint64_t* hash_f) {
   if (!S) return set_error(SBR_ERR_INVALID, "NULL scene");
-  SBR_CUDA(cudaSetDevice(S->device));
+  DeviceGuard dg(S->device);  // restores the caller's device on return
   const size_t n = (size_t)S->ntri;
   if (tie_rank) SBR_CUDA(cudaMemcpy(S->tie_rank, tie_rank, 4 * n, cudaMemcpyHostToDevice));
   if (normals) SBR_CUDA(cudaMemcpy(S->normals, normals, 24 * n, cudaMemcpyHostToDevice));
@@ -1014,7 +1015,7 @@ int sbr_scene_set_attributes(SbrScene* S, const int32_t* tie_rank, const double*
 
 int sbr_scene_set_materials(SbrScene* S, const SbrMaterial* mats, int32_t n) {
   if (!S || !mats || n <= 0) return set_error(SBR_ERR_INVALID, "bad material table");
-  SBR_CUDA(cudaSetDevice(S->device));
+  DeviceGuard dg(S->device);  // restores the caller's device on return
   if (S->mats) SBR_CUDA(cudaFree(S->mats));
   SBR_CUDA(cudaMalloc(&S->mats, sizeof(SbrMaterial) * n));
   SBR_CUDA(cudaMemcpy(S->mats, mats, sizeof(SbrMaterial) * n, cudaMemcpyHostToDevice));
@@ -1025,7 +1026,7 @@ int sbr_scene_set_materials(SbrScene* S, const SbrMaterial* mats, int32_t n) {
 int sbr_scene_set_wedges(SbrScene* S, const SbrWedgeTable* W) {
   if (!S || !W) return set_error(SBR_ERR_INVALID, "NULL argument");
   if (W->n_wedges < 0) return set_error(SBR_ERR_INVALID, "bad wedge count");
-  SBR_CUDA(cudaSetDevice(S->device));
+  DeviceGuard dg(S->device);  // restores the caller's device on return
   if (S->wedge_block) {
     SBR_CUDA(cudaFree(S->wedge_block));
     S->wedge_block = nullptr;

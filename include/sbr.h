@@ -145,8 +145,9 @@ void sbr_scene_destroy(SbrScene* scene);
  * driver.  Synchronises the device.  No reference counterpart. */
 int sbr_release_scratch(int32_t device);
 /* Hierarchy of subsequently created scenes over the same GPU Morton sort:
- * 0 = Karras 2012 LBVH, 1 = PLOC (parallel locally-ordered clustering,
- * SAH-like quality; default).  Both collapse to <= 2-triangle leaves. */
+ * 0 = Karras 2012 LBVH; 1 = PLOC (parallel locally-ordered clustering) down
+ * to 262,144 clusters, then a top-down SAH over the clusters (default); 2 =
+ * PLOC all the way.  All collapse to <= 2-triangle leaves. */
 int sbr_set_bvh_builder(int32_t builder);
 int64_t sbr_scene_num_triangles(const SbrScene* scene);
 int64_t sbr_scene_num_nodes(const SbrScene* scene);

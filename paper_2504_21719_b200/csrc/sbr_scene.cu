@@ -13,6 +13,7 @@
 // watertight test reproduces the reference's arithmetic exactly.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -21,6 +22,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "sbr_common.cuh"
@@ -506,9 +508,21 @@ __global__ void k_slot_tables(const TriSlot* __restrict__ tris, int n, double* _
 // worse; config-3 visibility r7 59.8 ms vs r16 60.8; the canyon trace is
 // flat (4.1-4.3 ms).  SAH cost (61.2-62.6) does not rank these trees;
 // visits per ray do.
-#define SBR_PLOC_RADIUS 7
+#define SBR_PLOC_RADIUS 9  // with the SAH top (below) the radius barely matters
 #endif
 constexpr int kPlocRadius = SBR_PLOC_RADIUS;
+// The greedy merges of the last large clusters decide the top of the tree;
+// at some radii they made the root's children overlap (child / root surface
+// area 1.53 instead of 1.05) and the city trace 20 % slower.  Once kPlocTop
+// clusters remain, the rest of the tree is built top-down by SAH over the
+// cluster boxes (SahBuild, host threads).  City trace per config-4 map
+// (ms) / build (s): PLOC only 458 / 0.14, top 16k 444, 64k 405 / 0.28, 256k
+// 388 / 0.20, pure SAH 389 / 0.50; canyon 4.23 -> 3.37 ms; config-3
+// visibility 59.9 -> 57.6 ms.
+#ifndef SBR_PLOC_TOP
+#define SBR_PLOC_TOP 262144
+#endif
+constexpr int kPlocTop = SBR_PLOC_TOP;
 
 __device__ __forceinline__ float half_area(const Box32& b) {
   const float dx = b.hi[0] - b.lo[0], dy = b.hi[1] - b.lo[1], dz = b.hi[2] - b.lo[2];
@@ -547,14 +561,14 @@ __global__ void k_iota_i32(int32_t* a, int n) {
 }
 
 __global__ void k_ploc_nearest(const int32_t* __restrict__ C, int m, const Box32* __restrict__ box,
-                               int32_t* nearest) {
+                               int32_t* nearest, int radius) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
   const Box32 bi = box[C[i]];
   float best = __int_as_float(0x7f800000);
   int bj = -1;
-  const int lo = i - kPlocRadius < 0 ? 0 : i - kPlocRadius;
-  const int hi = i + kPlocRadius >= m ? m - 1 : i + kPlocRadius;
+  const int lo = i - radius < 0 ? 0 : i - radius;
+  const int hi = i + radius >= m ? m - 1 : i + radius;
   for (int j = lo; j <= hi; ++j) {
     if (j == i) continue;
     const float c = half_area(box_union(bi, box[C[j]]));
@@ -575,7 +589,8 @@ __global__ void k_ploc_flags(const int32_t* __restrict__ nearest, int m, int32_t
 
 __global__ void k_ploc_merge(int32_t* C, const int32_t* __restrict__ nearest,
                              const int32_t* __restrict__ flag, const int32_t* __restrict__ pos,
-                             int m, int n, int base, Box32* box, int2* kids, int32_t* parent) {
+                             int m, int n, int base, Box32* box, int2* kids, int32_t* parent,
+                             int32_t* csize) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m || !flag[i]) return;
   const int j = nearest[i];
@@ -583,6 +598,7 @@ __global__ void k_ploc_merge(int32_t* C, const int32_t* __restrict__ nearest,
   const int a = C[i], b = C[j];
   kids[id - n] = make_int2(a, b);
   box[id] = box_union(box[a], box[b]);
+  csize[id] = csize[a] + csize[b];
   parent[a] = id;
   parent[b] = id;
   C[i] = id;
@@ -659,7 +675,213 @@ __global__ void k_ploc_leaves(const int32_t* __restrict__ off, const Box32* __re
   ids_dfs[s] = ids_sorted[i];
 }
 
-static std::atomic<int> g_builder{1};  // 0 = Karras LBVH, 1 = PLOC
+__global__ void k_fill_i32(int32_t* a, int n, int v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = v;
+}
+
+static inline float half_area_h(const Box32& b) {
+  const float dx = b.hi[0] - b.lo[0], dy = b.hi[1] - b.lo[1], dz = b.hi[2] - b.lo[2];
+  return dx * dy + dy * dz + dz * dx;
+}
+static inline Box32 box_union_h(const Box32& a, const Box32& b) {
+  Box32 u;
+  for (int k = 0; k < 3; ++k) {
+    u.lo[k] = fminf(a.lo[k], b.lo[k]);
+    u.hi[k] = fmaxf(a.hi[k], b.hi[k]);
+  }
+  return u;
+}
+
+// Top-down SAH over clusters (boxes + triangle counts): binned (64 centroid
+// bins per axis) above 1024 clusters, an exact sweep below.  Subtrees above
+// 16k clusters are built on separate host threads; each returns its internal
+// nodes in post-order and the parent concatenates (left, right, itself), so
+// the node numbering -- and with it the emitted tree -- is deterministic.
+struct SahBuild {
+  struct Node {
+    int l, r;  // child refs: >= 0 cluster (node) id, < 0 local node ~k
+    Box32 b;
+    int64_t sz;
+  };
+  const std::vector<Box32>& box;      // cluster boxes (read-only)
+  const std::vector<int32_t>& size;   // triangles per cluster
+  static constexpr int kBins = 64;
+
+  static float centroid2(const Box32& x, int axis) { return x.lo[axis] + x.hi[axis]; }
+
+  // binned SAH split of ids[lo, hi) (partitioned in place); -1 if none
+  int binned_split(std::vector<int32_t>& ids, int lo, int hi) const {
+    float cmin[3] = {__builtin_inff(), __builtin_inff(), __builtin_inff()};
+    float cmax[3] = {-__builtin_inff(), -__builtin_inff(), -__builtin_inff()};
+    for (int i = lo; i < hi; ++i)
+      for (int k = 0; k < 3; ++k) {
+        const float c = centroid2(box[ids[i]], k);
+        cmin[k] = fminf(cmin[k], c);
+        cmax[k] = fmaxf(cmax[k], c);
+      }
+    float best_cost = __builtin_inff();
+    int best_axis = -1, best_bin = 0;
+    for (int axis = 0; axis < 3; ++axis) {
+      const float ext = cmax[axis] - cmin[axis];
+      if (!(ext > 0.0f)) continue;
+      const float scale = kBins / ext;
+      Box32 bb[kBins];
+      int64_t bc[kBins] = {0};
+      for (int b = 0; b < kBins; ++b)
+        for (int k = 0; k < 3; ++k) {
+          bb[b].lo[k] = __builtin_inff();
+          bb[b].hi[k] = -__builtin_inff();
+        }
+      for (int i = lo; i < hi; ++i) {
+        const Box32& x = box[ids[i]];
+        int b = (int)((centroid2(x, axis) - cmin[axis]) * scale);
+        b = b < 0 ? 0 : (b >= kBins ? kBins - 1 : b);
+        bb[b] = box_union_h(bb[b], x);
+        bc[b] += size[ids[i]];
+      }
+      float rc[kBins];
+      Box32 acc = bb[kBins - 1];
+      int64_t cnt = 0;
+      for (int b = kBins - 1; b > 0; --b) {
+        acc = box_union_h(acc, bb[b]);
+        cnt += bc[b];
+        rc[b] = cnt ? half_area_h(acc) * (float)cnt : 0.0f;
+      }
+      acc = bb[0];
+      cnt = 0;
+      for (int b = 1; b < kBins; ++b) {  // split: bins [0, b) | [b, kBins)
+        acc = box_union_h(acc, bb[b - 1]);
+        cnt += bc[b - 1];
+        if (!cnt || rc[b] == 0.0f) continue;
+        const float c = half_area_h(acc) * (float)cnt + rc[b];
+        if (c < best_cost) {
+          best_cost = c;
+          best_axis = axis;
+          best_bin = b;
+        }
+      }
+    }
+    if (best_axis < 0) return -1;
+    const float scale = kBins / (cmax[best_axis] - cmin[best_axis]);
+    const auto mid = std::stable_partition(ids.begin() + lo, ids.begin() + hi, [&](int id) {
+      int b = (int)((centroid2(box[id], best_axis) - cmin[best_axis]) * scale);
+      b = b < 0 ? 0 : (b >= kBins ? kBins - 1 : b);
+      return b < best_bin;
+    });
+    const int split = (int)(mid - ids.begin());
+    return (split > lo && split < hi) ? split : -1;
+  }
+
+  // exact SAH sweep over the three centroid orders (ids[lo, hi) left sorted
+  // along the chosen axis); returns the split position
+  int exact_split(std::vector<int32_t>& ids, int lo, int hi) const {
+    int best_axis = 0, best_split = lo + (hi - lo) / 2;
+    float best_cost = __builtin_inff();
+    std::vector<float> right_cost(hi - lo);
+    auto order = [&](int axis) {
+      std::sort(ids.begin() + lo, ids.begin() + hi, [&](int a, int b) {
+        const float ca = centroid2(box[a], axis), cb = centroid2(box[b], axis);
+        return ca < cb || (ca == cb && a < b);
+      });
+    };
+    for (int axis = 0; axis < 3; ++axis) {
+      order(axis);
+      Box32 acc = box[ids[hi - 1]];
+      int64_t cnt = 0;
+      for (int i = hi - 1; i > lo; --i) {  // suffix [i, hi)
+        acc = box_union_h(acc, box[ids[i]]);
+        cnt += size[ids[i]];
+        right_cost[i - lo] = half_area_h(acc) * (float)cnt;
+      }
+      acc = box[ids[lo]];
+      cnt = 0;
+      for (int i = lo + 1; i < hi; ++i) {  // split: [lo, i) | [i, hi)
+        acc = box_union_h(acc, box[ids[i - 1]]);
+        cnt += size[ids[i - 1]];
+        const float c = half_area_h(acc) * (float)cnt + right_cost[i - lo];
+        if (c < best_cost) {
+          best_cost = c;
+          best_axis = axis;
+          best_split = i;
+        }
+      }
+    }
+    order(best_axis);
+    return best_split;
+  }
+
+  Box32 ref_box(int ref, const std::vector<Node>& out) const { return ref >= 0 ? box[ref] : out[~ref].b; }
+  int64_t ref_size(int ref, const std::vector<Node>& out) const {
+    return ref >= 0 ? size[ref] : out[~ref].sz;
+  }
+  int emit(int l, int r, std::vector<Node>& out) const {
+    out.push_back(Node{l, r, box_union_h(ref_box(l, out), ref_box(r, out)),
+                       ref_size(l, out) + ref_size(r, out)});
+    return ~(int)(out.size() - 1);
+  }
+
+  // subtree over ids[lo, hi): internal nodes appended to `out` in post-order
+  int build(std::vector<int32_t>& ids, int lo, int hi, std::vector<Node>& out, int depth) const {
+    if (hi - lo == 1) return ids[lo];
+    int split = hi - lo > 1024 ? binned_split(ids, lo, hi) : -1;
+    if (split < 0) split = exact_split(ids, lo, hi);
+    if (depth < 5 && hi - lo > 16384) {
+      std::vector<Node> lout, rout;
+      int lref = 0;
+      std::thread t([&] { lref = build(ids, lo, split, lout, depth + 1); });
+      int rref = build(ids, split, hi, rout, depth + 1);
+      t.join();
+      auto remap = [](int ref, int off) { return ref < 0 ? ~(~ref + off) : ref; };
+      const int offl = (int)out.size();
+      for (const Node& x : lout) out.push_back(Node{remap(x.l, offl), remap(x.r, offl), x.b, x.sz});
+      const int offr = (int)out.size();
+      for (const Node& x : rout) out.push_back(Node{remap(x.l, offr), remap(x.r, offr), x.b, x.sz});
+      return emit(remap(lref, offl), remap(rref, offr), out);
+    }
+    const int l = build(ids, lo, split, out, depth + 1);
+    const int r = build(ids, split, hi, out, depth + 1);
+    return emit(l, r, out);
+  }
+};
+
+// top-down SAH over the m remaining PLOC clusters C[0, m): new internal nodes
+// base .. base + m - 2 (children before parents, root last)
+static int ploc_top_sah(const int32_t* C, int m, int n, int base, Box32* box_all, int2* kids,
+                        int32_t* parent, int32_t* csize, cudaStream_t st) {
+  const int total = 2 * n - 1;
+  std::vector<int32_t> ids(m), hpar(total), hsize(total);
+  std::vector<Box32> hbox(total);
+  SBR_CUDA(cudaMemcpyAsync(ids.data(), C, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, st));
+  SBR_CUDA(cudaMemcpyAsync(hbox.data(), box_all, sizeof(Box32) * total, cudaMemcpyDeviceToHost, st));
+  SBR_CUDA(cudaMemcpyAsync(hpar.data(), parent, sizeof(int32_t) * total, cudaMemcpyDeviceToHost, st));
+  SBR_CUDA(cudaMemcpyAsync(hsize.data(), csize, sizeof(int32_t) * total, cudaMemcpyDeviceToHost, st));
+  SBR_CUDA(cudaStreamSynchronize(st));
+  SahBuild B{hbox, hsize};
+  std::vector<SahBuild::Node> out;
+  out.reserve(m);
+  B.build(ids, 0, m, out, 0);
+  const int made = (int)out.size();
+  if (made != m - 1) return set_error(SBR_ERR_INTERNAL, "PLOC top build: bad node count");
+  std::vector<int2> hk(made);
+  auto gid = [&](int ref) { return ref >= 0 ? ref : base + ~ref; };
+  for (int k = 0; k < made; ++k) {
+    const int id = base + k, l = gid(out[k].l), r = gid(out[k].r);
+    hk[k] = make_int2(l, r);
+    hbox[id] = out[k].b;
+    hpar[l] = id;
+    hpar[r] = id;
+  }
+  SBR_CUDA(cudaMemcpyAsync(kids + (base - n), hk.data(), sizeof(int2) * made,
+                           cudaMemcpyHostToDevice, st));
+  SBR_CUDA(cudaMemcpyAsync(box_all + base, hbox.data() + base, sizeof(Box32) * made,
+                           cudaMemcpyHostToDevice, st));
+  SBR_CUDA(cudaMemcpyAsync(parent, hpar.data(), sizeof(int32_t) * total, cudaMemcpyHostToDevice, st));
+  SBR_CUDA(cudaStreamSynchronize(st));
+  return SBR_OK;
+}
+
+static std::atomic<int> g_builder{1};  // 0 = Karras LBVH, 1 = PLOC + SAH top, 2 = PLOC only
 
 // persistent scene buffer (freed by sbr_scene_destroy)
 template <typename T>
@@ -712,7 +934,8 @@ int sbr_build_flags(void) {
 }
 
 int sbr_set_bvh_builder(int32_t builder) {
-  if (builder != 0 && builder != 1) return set_error(SBR_ERR_INVALID, "builder: 0 LBVH, 1 PLOC");
+  if (builder < 0 || builder > 2)
+    return set_error(SBR_ERR_INVALID, "builder: 0 LBVH, 1 PLOC + SAH top, 2 PLOC only");
   g_builder = builder;
   return SBR_OK;
 }
@@ -819,13 +1042,19 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
       (rc = A.get(&int_box, nint)) || (rc = A.get(&visits, nint)))
     return rc;
   int32_t* ids_leaf = ids_sorted;  // triangle of each leaf slot
-  if (g_builder == 1 && n > 1) {
+  const int builder = g_builder;
+  if (builder >= 1 && n > 1) {
+    const int top = builder == 1 ? kPlocTop : 0;
     // ---- PLOC hierarchy, exported in depth-first leaf order ----
     const int total = 2 * n - 1;
     Box32* box_all;
     int2* kids;
     int32_t *C, *C2, *nearest, *flag, *pos, *parent, *cnt, *off, *ids_dfs;
     unsigned* vis2;
+    int32_t* csize;
+    if ((rc = A.get(&csize, total))) return rc;
+    k_fill_i32<<<grid_for(n, 256), 256, 0, st>>>(csize, n, 1);
+    count_launch();
     if ((rc = A.get(&box_all, total)) || (rc = A.get(&kids, nint)) || (rc = A.get(&C, n)) ||
         (rc = A.get(&C2, n)) || (rc = A.get(&nearest, n)) || (rc = A.get(&flag, n + 1)) ||
         (rc = A.get(&pos, n + 1)) || (rc = A.get(&parent, total)) || (rc = A.get(&cnt, total)) ||
@@ -842,11 +1071,18 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
     if ((rc = A.get(&stmp, sb))) return rc;
     int m = n, base = n;
     while (m > 1) {
-      k_ploc_nearest<<<grid_for(m, 128), 128, 0, st>>>(C, m, box_all, nearest);
+      if (m <= top) {
+        // the last clusters: top-down SAH instead of greedy merging (below)
+        if ((rc = ploc_top_sah(C, m, n, base, box_all, kids, parent, csize, st))) return rc;
+        base += m - 1;
+        m = 1;
+        break;
+      }
+      k_ploc_nearest<<<grid_for(m, 128), 128, 0, st>>>(C, m, box_all, nearest, kPlocRadius);
       k_ploc_flags<<<grid_for(m, 256), 256, 0, st>>>(nearest, m, flag);
       SBR_CUDA(cub::DeviceScan::ExclusiveSum(stmp, sb, flag, pos, m + 1, st));
       k_ploc_merge<<<grid_for(m, 256), 256, 0, st>>>(C, nearest, flag, pos, m, n, base, box_all,
-                                                     kids, parent);
+                                                     kids, parent, csize);
       k_ploc_valid<<<grid_for(m, 256), 256, 0, st>>>(C, m, flag);
       SBR_CUDA(cub::DeviceScan::ExclusiveSum(stmp, sb, flag, pos, m + 1, st));
       k_ploc_compact<<<grid_for(m, 256), 256, 0, st>>>(C, flag, pos, m, C2);

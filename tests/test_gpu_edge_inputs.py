@@ -176,14 +176,19 @@ def _deep_chain_meshes(n=110):
 
 
 def test_degenerate_deep_tree_traverses_like_the_reference(cuda):
-    """A pathological scene whose BVH is a chain ~110 deep: closest hits (far
+    """A pathological scene whose (PLOC-only) BVH is a chain ~110 deep: closest hits (far
     to near and near to far along the chain) and occlusion queries match the
     oracle, whose SAH tree needs a deep stack too -- no stack overflow below the
     reference's 256-entry limit (_core.pyx:15)."""
     import oracle
     from paper_2504_21719_b200 import _native
     meshes = _deep_chain_meshes()
-    acc = build_scene_accel(meshes)
+    L = _native.lib()
+    L.sbr_set_bvh_builder(2)  # PLOC only: the SAH top would build this chain 27 deep
+    try:
+        acc = build_scene_accel(meshes)
+    finally:
+        L.sbr_set_bvh_builder(1)
     nodes = np.zeros((int(_native.lib().sbr_scene_num_nodes(acc.handle)), 16), np.int32)
     _native.check(_native.lib().sbr_scene_copy_nodes(acc.handle, nodes.ctypes.data))
     depth, todo = {0: 1}, [0]

@@ -70,7 +70,7 @@ elif case == "build":
     from test_gpu_edge_inputs import _deep_chain_meshes
     L = _native.lib()
     rng = np.random.default_rng(0)
-    for builder in (1, 0):
+    for builder in (1, 2, 0):
         L.sbr_set_bvh_builder(builder)
         for meshes in (scenes.street_canyon(), _deep_chain_meshes()):
             sc = SceneModel(meshes, {m.object_id: scenes.concrete() for m in meshes})

@@ -764,6 +764,9 @@ struct ClosestTravT {
 
 // Resumable per-lane any-hit traversal (occlusion), while-while with parked
 // leaves like ClosestTrav; stops at the first triangle with t_min < t < limit.
+#ifndef SBR_ANY_ORDER
+#define SBR_ANY_ORDER 0
+#endif
 struct AnyTrav {
   Ray64 r;
   RayBox rb;
@@ -834,7 +837,13 @@ struct AnyTrav {
         // origin (the surface a CIR vertex lies on) before reaching the
         // occluders.  Config-3 visibility: near-first 126 ms, fixed order
         // 107, nearest-to-midpoint 99, far-first 93 (identical results)
-        const bool lfirst = tl > tr;
+#if SBR_ANY_ORDER == 0
+        const bool lfirst = tl > tr;   // far first
+#elif SBR_ANY_ORDER == 1
+        const bool lfirst = tl <= tr;  // near first
+#else
+        const bool lfirst = true;      // fixed
+#endif
         stack_node[sp++] = lfirst ? ch.y : ch.x;
         node = lfirst ? ch.x : ch.y;
       } else if (hl) {

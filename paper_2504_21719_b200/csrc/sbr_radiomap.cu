@@ -128,6 +128,13 @@ __device__ __forceinline__ unsigned long long append_slot(unsigned long long* co
 #define SBR_SHADE_CHUNK 128  // queue items a shade warp claims at once (256: config-4 map 899 ms, 128: 895, 1024: 962)
 #endif
 constexpr int kShadeChunk = SBR_SHADE_CHUNK;
+#ifndef SBR_SHADE_STATIC
+#define SBR_SHADE_STATIC 0  // 1: warp w takes chunks w, w + W, ... (no work atomic)
+#endif
+#ifndef SBR_SHADE_RES
+#define SBR_SHADE_RES 128  // next-queue slots a warp reserves per atomic (multiple of 32): config-4 map 32: 812 ms, 64: 797, 128: 784, 256: 785
+#endif
+constexpr int kShadeRes = SBR_SHADE_RES;
 #ifndef SBR_SHADE_MINB
 #define SBR_SHADE_MINB 8
 #endif
@@ -135,6 +142,9 @@ constexpr int kShadeChunk = SBR_SHADE_CHUNK;
 #define SBR_TRACE_SPLIT 0  // split trace measured equal (4.20 vs 4.21 ms; 8 blocks/SM 4.23)
 #endif
 #define TRACE_FIRST (SBR_TRACE_SPLIT ? kFirst : seg == 0)
+#ifndef SBR_TRACE_CLAIM
+#define SBR_TRACE_CLAIM 1  // batches of 32 rays a trace warp claims per atomic
+#endif
 #ifndef SBR_TRACE_TPB
 #define SBR_TRACE_TPB 128
 #endif
@@ -147,10 +157,17 @@ __global__ void __launch_bounds__(SBR_TRACE_TPB, SBR_TRACE_MINB) k_map_trace(Dev
   const unsigned lane = threadIdx.x & 31u;
   const uint64_t n = TRACE_FIRST ? comb.slots() : (uint64_t)*count_in;
   const double3 src = make_double3(P.source[0], P.source[1], P.source[2]);
+  unsigned long long claim = 0;
+  int left = 0;  // batches of 32 left in the current claim
   while (true) {
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(work, 32ULL);
-    base = __shfl_sync(0xffffffffu, base, 0);
+    if (left == 0) {
+      if (lane == 0) claim = atomicAdd(work, 32ULL * SBR_TRACE_CLAIM);
+      claim = __shfl_sync(0xffffffffu, claim, 0);
+      left = SBR_TRACE_CLAIM;
+    }
+    const unsigned long long base = claim;
+    claim += 32;
+    --left;
     if (base >= n) break;
     const uint64_t i = base + lane;
     bool active = i < n;
@@ -222,19 +239,27 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
   // walks them 32 per warp-uniform iteration (a __syncwarp closes each: lanes
   // that take a short exit wait for the warp, so the FP64 Fresnel / field code
   // issues for converged lanes; `continue` inside the do-while(0) ends the
-  // item).  Output: the warp's R / T survivors fill 32-slot batches of the
-  // next queue in input order (a new batch reserved with one atomic when the
-  // current one is full), so a trace warp of the next segment gets the
-  // survivors of ~64 neighbouring rays -- coherent -- instead of two
-  // unrelated warps' survivors; the warp pads its last batch with dead
-  // entries (NaN origin) that the trace skips.
+  // item).  Output: the warp's R / T survivors fill kShadeRes-slot batches of
+  // the next queue in input order (a new batch reserved with one atomic when
+  // the current one is full), so a trace warp of the next segment gets the
+  // survivors of neighbouring rays -- coherent -- instead of unrelated warps'
+  // survivors, with few atomics on the shared counter; the warp pads its last
+  // batch with dead entries (NaN origin) that the trace skips.
   unsigned long long res_base = 0;
-  int res_fill = 32;  // warp-uniform: slots used in the current batch (32 = none reserved)
+  int res_fill = kShadeRes;  // warp-uniform: slots used in the current batch (full = none reserved)
+#if SBR_SHADE_STATIC
+  const uint64_t gwarp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t ck = gwarp;; ck += nwarps) {
+    const unsigned long long c0 = ck * kShadeChunk;
+    if (c0 >= n) break;
+#else
   while (true) {
     unsigned long long c0 = 0;
     if (lane == 0) c0 = atomicAdd(work, (unsigned long long)kShadeChunk);
     c0 = __shfl_sync(0xffffffffu, c0, 0);
     if (c0 >= n) break;
+#endif
     const uint64_t c1 = c0 + kShadeChunk < n ? c0 + kShadeChunk : n;
   for (uint64_t i0 = c0; i0 < c1; i0 += 32) {
     const uint64_t i = i0 + lane;
@@ -410,10 +435,10 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
     const unsigned m = __ballot_sync(0xffffffffu, emit);
     if (m) {
       const int c = __popc(m);
-      const int first = c < 32 - res_fill ? c : 32 - res_fill;
+      const int first = c < kShadeRes - res_fill ? c : kShadeRes - res_fill;
       unsigned long long nb = 0;
       if (c > first) {
-        if (lane == 0) nb = atomicAdd(count_out, 32ULL);
+        if (lane == 0) nb = atomicAdd(count_out, (unsigned long long)kShadeRes);
         nb = __shfl_sync(0xffffffffu, nb, 0);
       }
       const int rank = __popc(m & ((1u << lane) - 1u));
@@ -448,9 +473,9 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
   }
   }
   // pad the last batch: dead entries (NaN origin) the next trace skips
-  if (res_fill < 32 && (int)lane >= res_fill) {
-    SBR_DCHECK(S, res_base + lane < qo.cap);
-    qst(&qo.ox[res_base + lane], __longlong_as_double(0x7ff8000000000000LL));
+  for (int p = res_fill + (int)lane; p < kShadeRes; p += 32) {
+    SBR_DCHECK(S, res_base + p < qo.cap);
+    qst(&qo.ox[res_base + p], __longlong_as_double(0x7ff8000000000000LL));
   }
   const unsigned v[7] = {K.rb, K.deposits, K.escaped, K.respawns, K.terminated, K.thr, K.rr};
   const int idx[7] = {SBR_MC_RAY_BOUNCES, SBR_MC_DEPOSITS, SBR_MC_ESCAPED, SBR_MC_RESPAWNS,
@@ -798,7 +823,7 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
   Wave wave;
   Wave* w = &wave;
   // + the dead padding of every shade warp's last output batch (< 32 each)
-  const int64_t pad = 32LL * sms * SBR_SHADE_MINB * 4 + 64;
+  const int64_t pad = (int64_t)kShadeRes * sms * SBR_SHADE_MINB * 4 + 64;
   if ((rc = wave_alloc(chunk + (int64_t)F + pad, st, w))) return rc;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_map_trace<false>, SBR_TRACE_TPB, 0);

@@ -25,6 +25,7 @@
 // ~2 ms per 1e7-ray map at HBM speed: the pipeline stays compute bound.
 #include <cooperative_groups.h>
 
+#include <atomic>
 #include <string>
 
 #include "sbr_utd.cuh"
@@ -142,6 +143,9 @@ constexpr int kShadeRes = SBR_SHADE_RES;
 #define SBR_TRACE_SPLIT 0  // split trace measured equal (4.20 vs 4.21 ms; 8 blocks/SM 4.23)
 #endif
 #define TRACE_FIRST (SBR_TRACE_SPLIT ? kFirst : seg == 0)
+#ifndef SBR_WAVE_STREAMS
+#define SBR_WAVE_STREAMS 2  // config-4 map 783 -> 757 ms (kernel tails of one pass overlap the other)
+#endif
 #ifndef SBR_TRACE_CLAIM
 #define SBR_TRACE_CLAIM 1  // batches of 32 rays a trace warp claims per atomic
 #endif
@@ -724,6 +728,8 @@ __global__ void __launch_bounds__(128) k_map_wedges(DevScene S, SbrMapParams P,
   }
 }
 
+std::atomic<int> g_wave_streams{SBR_WAVE_STREAMS > 1 ? 2 : 1};
+
 int launch_status(const char* what) {
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess)
@@ -820,49 +826,81 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
   const int64_t chunk = total < (uint64_t)kChunkRays ? (int64_t)total : kChunkRays;
   // segment 0 runs over comb slots: up to chunk + F items
   const uint64_t F = comb_stride(P->num_samples);
-  Wave wave;
-  Wave* w = &wave;
-  // + the dead padding of every shade warp's last output batch (< 32 each)
+  // SBR_WAVE_STREAMS (2): consecutive passes alternate between the caller's
+  // stream and a second one with its own queues, so one pass's kernel tails
+  // overlap the other's bulk (passes are independent sample ranges; the grid
+  // and counters take float64 / integer atomics from both)
+  const int nstreams = total > (uint64_t)chunk ? g_wave_streams.load() : 1;
+  Wave waves[2];
+  cudaStream_t sts[2] = {st, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // + the dead padding of every shade warp's last output batch
   const int64_t pad = (int64_t)kShadeRes * sms * SBR_SHADE_MINB * 4 + 64;
-  if ((rc = wave_alloc(chunk + (int64_t)F + pad, st, w))) return rc;
+  for (int k = 0; k < nstreams && !rc; ++k) rc = wave_alloc(chunk + (int64_t)F + pad, st, &waves[k]);
+  if (!rc && nstreams > 1) {
+    if (cudaStreamCreateWithFlags(&sts[1], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      rc = set_error(SBR_ERR_CUDA, "second wave stream");
+    } else {
+      cudaEventRecord(ev_fork, st);  // queues allocated, caller's prior work done
+      cudaStreamWaitEvent(sts[1], ev_fork, 0);
+    }
+  }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_map_trace<false>, SBR_TRACE_TPB, 0);
   if (per_sm < 1) per_sm = 1;
   const unsigned trace_blocks = (unsigned)(sms * per_sm);
   const unsigned shade_blocks = (unsigned)(sms * SBR_SHADE_MINB);
   const DevScene S = dev_view(scene);
-  for (uint64_t lo = sample_begin; lo < sample_end; lo += (uint64_t)chunk) {
+  int pass = 0;
+  for (uint64_t lo = sample_begin; lo < sample_end && !rc; lo += (uint64_t)chunk, ++pass) {
     const uint64_t cnt = (sample_end - lo) < (uint64_t)chunk ? (sample_end - lo) : (uint64_t)chunk;
     const CombMap comb{(cnt + F - 1) / F, F};
+    Wave* w = &waves[pass % nstreams];
+    cudaStream_t ps = sts[pass % nstreams];
     int cur = 0;
     for (int seg = 0; seg <= P->max_depth; ++seg) {
       // ctl[0] = work counter; ctl[1 + cur] = this segment's count; ctl[2 - cur] = next count
-      k_reset_pass<<<1, 1, 0, st>>>(w->ctl, w->ctl + 2 - cur, w->ctl + 3, w->ctl + 4);
+      k_reset_pass<<<1, 1, 0, ps>>>(w->ctl, w->ctl + 2 - cur, w->ctl + 3, w->ctl + 4);
       if ((rc = launch_status("k_reset_pass"))) break;
-      prof_begin(st, "k_map_trace");
-      (seg == 0 ? k_map_trace<true> : k_map_trace<false>)<<<trace_blocks, SBR_TRACE_TPB, 0, st>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo, cnt,
+      prof_begin(ps, "k_map_trace");
+      (seg == 0 ? k_map_trace<true> : k_map_trace<false>)<<<trace_blocks, SBR_TRACE_TPB, 0, ps>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo, cnt,
                                                 comb, w->hits, w->ctl, counters, sh);
-      prof_end(st);
+      prof_end(ps);
       if ((rc = launch_status("k_map_trace"))) break;
-      prof_begin(st, "k_map_shade");
-      (seg == 0 ? k_map_shade<true> : k_map_shade<false>)<<<shade_blocks, 128, 0, st>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo,
+      prof_begin(ps, "k_map_shade");
+      (seg == 0 ? k_map_shade<true> : k_map_shade<false>)<<<shade_blocks, 128, 0, ps>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo,
                                                 comb, w->hits, w->q[1 - cur], w->ctl + 2 - cur,
                                                 w->sq, w->ctl + 3, grid, counters, sh, w->ctl + 4);
-      prof_end(st);
+      prof_end(ps);
       if ((rc = launch_status("k_map_shade"))) break;
       if (seg < P->max_depth && (P->allow_mask & 2)) {
-        prof_begin(st, "k_map_scatter");
-        k_map_scatter<<<shade_blocks, 128, 0, st>>>(S, *P, seg, w->sq, w->ctl + 3, w->q[1 - cur],
+        prof_begin(ps, "k_map_scatter");
+        k_map_scatter<<<shade_blocks, 128, 0, ps>>>(S, *P, seg, w->sq, w->ctl + 3, w->q[1 - cur],
                                                     w->ctl + 2 - cur, counters);
-        prof_end(st);
+        prof_end(ps);
         if ((rc = launch_status("k_map_scatter"))) break;
       }
       cur = 1 - cur;
     }
-    if (rc) break;
   }
-  cudaFreeAsync(w->block, st);
+  if (sts[1]) {  // join: the caller's stream waits for the second stream's passes
+    cudaEventRecord(ev_join, sts[1]);
+    cudaStreamWaitEvent(st, ev_join, 0);
+    cudaStreamDestroy(sts[1]);
+  }
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
+  for (int k = 0; k < nstreams; ++k)
+    if (waves[k].block) cudaFreeAsync(waves[k].block, st);
   return rc;
+}
+
+int sbr_set_wave_streams(int32_t n) {
+  if (n != 1 && n != 2) return set_error(SBR_ERR_INVALID, "wave streams: 1 or 2");
+  g_wave_streams = n;
+  return SBR_OK;
 }
 
 int sbr_radiomap_bounce(const SbrScene* scene, const SbrMapParams* P, uint64_t sample_begin,

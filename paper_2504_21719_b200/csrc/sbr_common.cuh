@@ -477,15 +477,28 @@ __device__ __forceinline__ RayBox box_setup(double3 o, double3 d, float pad_floo
 }
 
 // entry distance of [lo,hi] or +inf when missed / beyond `bound`
+#ifndef SBR_BOX_FOLD
+#define SBR_BOX_FOLD 1  // config-4 map 758 -> 752 ms, config-3 visibility 57.5 -> 56.9 ms
+#endif
 __device__ __forceinline__ float box_enter(const RayBox& rb, float lox, float hix, float loy,
                                            float hiy, float loz, float hiz, float bound) {
   const float x0 = fmaf(lox, rb.ix, -rb.oxp), x1 = fmaf(hix, rb.ix, -rb.oxm);
   const float y0 = fmaf(loy, rb.iy, -rb.oyp), y1 = fmaf(hiy, rb.iy, -rb.oym);
   const float z0 = fmaf(loz, rb.iz, -rb.ozp), z1 = fmaf(hiz, rb.iz, -rb.ozm);
+#if SBR_BOX_FOLD
+  // max(tn, tlo) <= min(tf2, bound) is the same test (tlo <= t_min < bound
+  // always holds), with the entry clamped to tlo -- still a lower bound of
+  // any valid hit in the box, so ordering and stack culling stay exact
+  const float tn = fmaxf(fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fminf(z0, z1)), rb.tlo);
+  const float tf = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fmaxf(z0, z1));
+  const float tf2 = fminf(fmaf(0x1p-20f, fabsf(tf), tf), bound);
+  return tn <= tf2 ? tn : __int_as_float(0x7f800000);
+#else
   const float tn = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fminf(z0, z1));
   const float tf = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fmaxf(z0, z1));
   const float tf2 = fmaf(0x1p-20f, fabsf(tf), tf);
   return (tn <= tf2 && tf2 >= rb.tlo && tn <= bound) ? tn : __int_as_float(0x7f800000);
+#endif
 }
 
 // float upper bound of a float64 distance (for comparing fp32 entries)

@@ -97,6 +97,36 @@ __device__ __forceinline__ void qst(T* p, T v) {
 #endif
 }
 
+// Lane 0's atomicAdd on a uniform address: ptxas turns `if (lane == 0)
+// atomicAdd(p, v)` into a warp-aggregated atomic whose result is shuffled to
+// the group right away, so the warp stalls on the atomic's round trip at the
+// call site.  Here the address is formed from %laneid inside the asm (p + 8 *
+// laneid, which is p for the only caller, lane 0), so it is not provably
+// uniform and the result is waited for only where it is first read.
+// CALL FROM LANE 0 ONLY.
+__device__ __forceinline__ unsigned long long atom_add_async(unsigned long long* p,
+                                                            unsigned long long v) {
+  unsigned long long r;
+  asm volatile(
+      "{\n\t.reg .u32 l;\n\t.reg .u64 a;\n\t"
+      "mov.u32 l, %%laneid;\n\tmul.wide.u32 a, l, 8;\n\tadd.u64 a, a, %1;\n\t"
+      "atom.global.add.u64 %0, [a], %2;\n\t}"
+      : "=l"(r)
+      : "l"(p), "l"(v));
+  return r;
+}
+
+#ifndef SBR_RAW_ATOMICS
+#define SBR_RAW_ATOMICS 1  // config-4 map 758 -> 755 ms
+#endif
+__device__ __forceinline__ unsigned long long lane0_add(unsigned long long* p, unsigned long long v) {
+#if SBR_RAW_ATOMICS
+  return atom_add_async(p, v);
+#else
+  return atomicAdd(p, v);
+#endif
+}
+
 __device__ __forceinline__ unsigned long long append_slot(unsigned long long* counter) {
   cg::coalesced_group grp = cg::coalesced_threads();
   unsigned long long base = 0;
@@ -165,7 +195,7 @@ __global__ void __launch_bounds__(SBR_TRACE_TPB, SBR_TRACE_MINB) k_map_trace(Dev
   int left = 0;  // batches of 32 left in the current claim
   while (true) {
     if (left == 0) {
-      if (lane == 0) claim = atomicAdd(work, 32ULL * SBR_TRACE_CLAIM);
+      if (lane == 0) claim = lane0_add(work, 32ULL * SBR_TRACE_CLAIM);
       claim = __shfl_sync(0xffffffffu, claim, 0);
       left = SBR_TRACE_CLAIM;
     }
@@ -260,7 +290,7 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
 #else
   while (true) {
     unsigned long long c0 = 0;
-    if (lane == 0) c0 = atomicAdd(work, (unsigned long long)kShadeChunk);
+    if (lane == 0) c0 = lane0_add(work, (unsigned long long)kShadeChunk);
     c0 = __shfl_sync(0xffffffffu, c0, 0);
     if (c0 >= n) break;
 #endif
@@ -442,7 +472,7 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
       const int first = c < kShadeRes - res_fill ? c : kShadeRes - res_fill;
       unsigned long long nb = 0;
       if (c > first) {
-        if (lane == 0) nb = atomicAdd(count_out, (unsigned long long)kShadeRes);
+        if (lane == 0) nb = lane0_add(count_out, (unsigned long long)kShadeRes);
         nb = __shfl_sync(0xffffffffu, nb, 0);
       }
       const int rank = __popc(m & ((1u << lane) - 1u));
@@ -481,6 +511,7 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
     SBR_DCHECK(S, res_base + p < qo.cap);
     qst(&qo.ox[res_base + p], __longlong_as_double(0x7ff8000000000000LL));
   }
+
   const unsigned v[7] = {K.rb, K.deposits, K.escaped, K.respawns, K.terminated, K.thr, K.rr};
   const int idx[7] = {SBR_MC_RAY_BOUNCES, SBR_MC_DEPOSITS, SBR_MC_ESCAPED, SBR_MC_RESPAWNS,
                       SBR_MC_TERMINATED, SBR_MC_THRESHOLD_KILLED, SBR_MC_ROULETTE_KILLED};

@@ -76,6 +76,21 @@ def full(rep):
         for m in FULL_METRICS:
             if m in vals:
                 print(f"{m:70s} {vals[m]:>16s} {units.get(m, '')}")
+        # warp stall reasons (cycles per issued instruction) and local-memory traffic
+        stalls = []
+        for m, v in vals.items():
+            if m.startswith("smsp__average_warps_issue_stalled_") and m.endswith("_per_issue_active.ratio"):
+                try:
+                    stalls.append((float(v.replace(",", "")), m[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
+                except ValueError:
+                    pass
+        if stalls:
+            print("# stall reasons (warps stalled per issued instruction)")
+            for v, name in sorted(stalls, reverse=True)[:12]:
+                print(f"  stall_{name:40s} {v:8.3f}")
+        for m, v in sorted(vals.items()):
+            if "mem_local" in m and (m.endswith(".sum") or m.endswith(".pct")):
+                print(f"{m:70s} {v:>16s} {units.get(m, '')}")
     out = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True,
                          text=True).stdout
     print("\n## details (sections)")

@@ -242,8 +242,26 @@ __device__ __forceinline__ cplx operator*(cplx a, cplx b) {
   return C(a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re);
 }
 __device__ __forceinline__ cplx operator*(double s, cplx a) { return C(s * a.re, s * a.im); }
+// Code size of the complex helpers: every call site of an inlined float64
+// division / square root / exp / sincos expands to a few hundred bytes of
+// SASS, and the shade kernel called them ~40 times (85 KB of code, far past
+// the ~32 KB instruction cache; ncu: "no instruction" was the largest stall).
+// SBR_MATH_CALLS = 1 keeps one out-of-line copy of each (a call per use).
+#ifndef SBR_MATH_CALLS
+#define SBR_MATH_CALLS 1  // config-4 map 749 -> 727 ms; 2 (also cexp_, csqrt_): 742
+#endif
+#if SBR_MATH_CALLS >= 1
+#define SBR_MATH_FN static __device__ __noinline__
+#else
+#define SBR_MATH_FN __device__ __forceinline__
+#endif
+#if SBR_MATH_CALLS >= 2
+#define SBR_MATH_FN2 static __device__ __noinline__
+#else
+#define SBR_MATH_FN2 __device__ __forceinline__
+#endif
 // numpy CDOUBLE_divide: Smith's method with a reciprocal
-__device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
+SBR_MATH_FN cplx cdiv(cplx a, cplx b) {
   const double br = fabs(b.re), bi = fabs(b.im);
   if (br >= bi) {
     if (br == 0.0 && bi == 0.0) return C(a.re / br, a.im / br);
@@ -256,7 +274,7 @@ __device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
   return C((a.re * rat + a.im) * scl, (a.im * rat - a.re) * scl);
 }
 // np.abs(complex128) in numpy 2.x: max * sqrt(fma(r, r, 1)), r = min/max
-__device__ __forceinline__ double cabs_np(cplx a) {
+SBR_MATH_FN double cabs_np(cplx a) {
   const double x = fabs(a.re), y = fabs(a.im);
   const double m = fmax(x, y), k = fmin(x, y);
   if (m == 0.0 || isinf(m)) return m + k;
@@ -267,14 +285,14 @@ __device__ __forceinline__ double cabs2(cplx a) {
   const double m = cabs_np(a);
   return m * m;
 }
-__device__ __forceinline__ cplx cexp_(cplx a) {
+SBR_MATH_FN2 cplx cexp_(cplx a) {
   const double e = exp(a.re);
   double s, c;
   sincos(a.im, &s, &c);
   return C(e * c, e * s);
 }
 // principal sqrt, glibc csqrt finite branch (np.sqrt(complex) -> libm csqrt)
-__device__ __forceinline__ cplx csqrt_(cplx z) {
+SBR_MATH_FN2 cplx csqrt_(cplx z) {
   const double x = z.re, y = z.im;
   if (y == 0.0) {
     if (x < 0.0) return C(0.0, copysign(sqrt(-x), y));

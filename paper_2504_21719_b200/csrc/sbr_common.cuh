@@ -142,12 +142,16 @@ constexpr unsigned kErrBounds = 2u;
 // ---------------------------------------------------------------------------
 // Philox4x64-10 keyed stream
 // ---------------------------------------------------------------------------
+#ifndef SBR_PHILOX_UNROLL
+#define SBR_PHILOX_UNROLL 10
+#endif
+constexpr int kPhiloxUnroll = SBR_PHILOX_UNROLL;
 __device__ __forceinline__ double philox_uniform(uint64_t seed, uint64_t sample,
                                                  uint64_t depth, uint64_t tag,
                                                  uint64_t i) {
   uint64_t c0 = i / 4 + 1, c1 = 0, c2 = depth, c3 = tag;
   uint64_t k0 = seed, k1 = sample;
-#pragma unroll
+#pragma unroll kPhiloxUnroll
   for (int r = 0; r < 10; ++r) {
     if (r) {
       k0 += 0x9E3779B97F4A7C15ULL;
@@ -259,6 +263,23 @@ __device__ __forceinline__ cplx operator*(double s, cplx a) { return C(s * a.re,
 #define SBR_MATH_FN2 static __device__ __noinline__
 #else
 #define SBR_MATH_FN2 __device__ __forceinline__
+#endif
+// SBR_DIV_CALLS = 1: the shade kernel's real divisions go through one
+// out-of-line copy (an inlined IEEE float64 division is ~20 instructions plus
+// a slow-path call at every site)
+#ifndef SBR_DIV_CALLS
+#define SBR_DIV_CALLS 0
+#endif
+#if SBR_DIV_CALLS
+static __device__ __noinline__ double ddiv_call(double a, double b) { return a / b; }
+static __device__ __noinline__ double3 div3_call(double3 v, double s) {
+  return make_double3(v.x / s, v.y / s, v.z / s);
+}
+#define SBR_DIV(a, b) ::sbr::ddiv_call((a), (b))
+#define SBR_DIV3(v, s) ::sbr::div3_call((v), (s))
+#else
+#define SBR_DIV(a, b) ((a) / (b))
+#define SBR_DIV3(v, s) make_double3((v).x / (s), (v).y / (s), (v).z / (s))
 #endif
 // numpy CDOUBLE_divide: Smith's method with a reciprocal
 SBR_MATH_FN cplx cdiv(cplx a, cplx b) {

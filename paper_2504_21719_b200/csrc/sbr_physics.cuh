@@ -16,6 +16,10 @@
 
 namespace sbr {
 
+#ifndef SBR_FRESNEL_EXP_LOOP
+#define SBR_FRESNEL_EXP_LOOP 0
+#endif
+
 struct Fresnel4 {
   cplx rp, rl, tp, tl;
 };
@@ -46,8 +50,20 @@ __device__ __forceinline__ Fresnel4 slab_fresnel(const SbrMaterial& m, double c0
     r_par = C(1.0, 0.0);
   }
   const cplx q = m.kd * root;
+#if SBR_FRESNEL_EXP_LOOP
+  // both exponentials through one inlined cexp_ (a 2-trip loop): half the
+  // code of two inlined copies, no call
+  cplx phase2, phase1;
+#pragma unroll 1
+  for (int k = 0; k < 2; ++k) {
+    const cplx e = cexp_(k == 0 ? C(2.0 * q.im, -2.0 * q.re) : C(q.im, -q.re));
+    if (k == 0) phase2 = e;  // exp(-2j q)
+    else phase1 = e;         // exp(-1j q)
+  }
+#else
   const cplx phase2 = cexp_(C(2.0 * q.im, -2.0 * q.re));  // exp(-2j q)
   const cplx phase1 = cexp_(C(q.im, -q.re));              // exp(-1j q)
+#endif
   const cplx one_m_p2 = C(1.0 - phase2.re, -phase2.im);
   {
     const cplx r1sq = r_perp * r_perp;
@@ -181,25 +197,30 @@ static __device__ double alpha_sq(const SbrMapParams& P, double3 d) {
   return cabs2(acc);
 }
 
+// deterministic_perpendicular (em.py:96-107): projected x, else y axis --
+// the normal-incidence branch of incidence_frame, kept out of line (cold)
+static __device__ __noinline__ double3 deterministic_perp(double3 k) {
+  const double ax = k.x;  // x_axis . k via ddot == k.x exactly
+  double3 u = make_double3(1.0 - ax * k.x, 0.0 - ax * k.y, 0.0 - ax * k.z);
+  double un = sqrt(dot_ddot(u, u));
+  if (!(un > 1e-9)) {
+    const double ay = k.y;
+    u = make_double3(0.0 - ay * k.x, 1.0 - ay * k.y, 0.0 - ay * k.z);
+    un = sqrt(dot_ddot(u, u));
+  }
+  return make_double3(u.x / un, u.y / un, u.z / un);
+}
+
 // (e_perp, e_par) of an incident ray on a surface (radiomap.py:291-300)
 __device__ __forceinline__ void incidence_frame(double3 k, double3 n, double3& e_perp,
                                                 double3& e_par) {
   double3 cr = cross3(k, n);
   double nrm = norm_seq(cr);
   if (nrm < 1e-9) {
-    // deterministic_perpendicular (em.py:96-107): projected x, else y axis
-    const double ax = k.x;  // x_axis . k via ddot == k.x exactly
-    double3 u = make_double3(1.0 - ax * k.x, 0.0 - ax * k.y, 0.0 - ax * k.z);
-    double un = sqrt(dot_ddot(u, u));
-    if (!(un > 1e-9)) {
-      const double ay = k.y;
-      u = make_double3(0.0 - ay * k.x, 1.0 - ay * k.y, 0.0 - ay * k.z);
-      un = sqrt(dot_ddot(u, u));
-    }
-    cr = make_double3(u.x / un, u.y / un, u.z / un);
+    cr = deterministic_perp(k);
     nrm = 1.0;
   }
-  e_perp = make_double3(cr.x / nrm, cr.y / nrm, cr.z / nrm);
+  e_perp = SBR_DIV3(cr, nrm);
   e_par = cross3(e_perp, k);
 }
 

@@ -341,14 +341,14 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
     if (!SHADE_FIRST) {
       const double denom = dot_gemv(d, n_hat);
       double s = -1.0;
-      if (fabs(denom) > 1e-12) s = (P.plane_off - dot_gemv(o, n_hat)) / denom;
+      if (fabs(denom) > 1e-12) s = SBR_DIV(P.plane_off - dot_gemv(o, n_hat), denom);
       if (s > 1e-4 && s < t_hit) {
         const double3 pt = o + s * d;
         const double3 rel = make_double3(pt.x - P.corner[0], pt.y - P.corner[1], pt.z - P.corner[2]);
-        const double fu = floor(dot_gemv(rel, make_double3(P.u_hat[0], P.u_hat[1], P.u_hat[2])) / P.cell_w);
-        const double fv = floor(dot_gemv(rel, make_double3(P.v_hat[0], P.v_hat[1], P.v_hat[2])) / P.cell_h);
+        const double fu = floor(SBR_DIV(dot_gemv(rel, make_double3(P.u_hat[0], P.u_hat[1], P.u_hat[2])), P.cell_w));
+        const double fv = floor(SBR_DIV(dot_gemv(rel, make_double3(P.v_hat[0], P.v_hat[1], P.v_hat[2])), P.cell_h));
         if (fu >= 0.0 && fu < (double)P.nx && fv >= 0.0 && fv < (double)P.ny) {
-          const double val = P.scale * field_energy(E) * omega / fabs(denom) * weight;
+          const double val = SBR_DIV(P.scale * field_energy(E) * omega, fabs(denom)) * weight;
           atomicAdd(grid + (int64_t)fv * P.nx + (int64_t)fu, val);
           K.deposits++;
         }
@@ -390,9 +390,9 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
     const double den = r_sq + t_sq;
     if (den > 0.0) {
       const double s_sq = m.scattering * m.scattering;
-      q0 = 1.0 * (1.0 - s_sq) * r_sq / den;
-      q1 = 1.0 * s_sq * r_sq / den;
-      q2 = 1.0 * t_sq / den;
+      q0 = SBR_DIV(1.0 * (1.0 - s_sq) * r_sq, den);
+      q1 = SBR_DIV(1.0 * s_sq * r_sq, den);
+      q2 = SBR_DIV(1.0 * t_sq, den);
     }
     if (!(P.allow_mask & 1)) q0 = 0.0;
     if (!(P.allow_mask & 2)) q1 = 0.0;
@@ -402,15 +402,15 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
       K.terminated++;
       continue;
     }
-    q0 /= total;
-    q1 /= total;
-    q2 /= total;
-    const double q3 = 0.0 / total;
+    q0 = SBR_DIV(q0, total);
+    q1 = SBR_DIV(q1, total);
+    q2 = SBR_DIV(q2, total);
+    const double q3 = SBR_DIV(0.0, total);
     const double u = philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_INTERACTION, slot);
     const double c0 = q0, c1 = c0 + q1, c2 = c1 + q2, c3 = c2 + q3;
     int code = (u >= c0) + (u >= c1) + (u >= c2) + (u >= c3);
     if (code > 3) code = 3;
-    weight /= (code == 0 ? q0 : code == 1 ? q1 : code == 2 ? q2 : q3);
+    weight = SBR_DIV(weight, code == 0 ? q0 : code == 1 ? q1 : code == 2 ? q2 : q3);
 
     double3 e_perp, e_par;
     incidence_frame(d, nrm, e_perp, e_par);
@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
       // gamma_reflected (materials.py:400-419) here, the rest in k_map_scatter
       const double g_num = sqrt(cabs2(F.rp * c_perp) + cabs2(F.rl * c_par));
       const double g_den = sqrt(cabs2(c_perp) + cabs2(c_par));
-      const double gamma = g_den > 0.0 ? g_num / g_den : 0.0;
+      const double gamma = g_den > 0.0 ? SBR_DIV(g_num, g_den) : 0.0;
       const unsigned long long j = append_slot(count_s);
       SBR_DCHECK(S, j < sq.cap);
       qst(&sq.dx[j], d.x);

@@ -266,10 +266,10 @@ int sbr_radiomap_bounce(const SbrScene* scene, const SbrMapParams* params,
 int sbr_radiomap_bounce_sharded(const SbrScene* scene, const SbrMapParams* params,
                                 int32_t shard_index, int32_t shard_count, double* grid_dev,
                                 uint64_t* counters_dev, void* stream);
-/* Wavefront passes of a multi-pass map in flight at once: 2 (default) runs
- * consecutive passes on the caller's stream and a second one with their own
- * queues so kernel tails overlap; 1 serialises them (per-kernel timing).
- * No reference counterpart. */
+/* Wavefront passes of a multi-pass map in flight at once (1..4): 2 (default)
+ * runs consecutive passes on the caller's stream and a second one with their
+ * own queues (~7.4 GB each) so kernel tails overlap; 1 serialises them
+ * (per-kernel timing).  No reference counterpart. */
 int sbr_set_wave_streams(int32_t n);
 /* Replaces _direct_cells (radiomap.py:566-583): analytic LoS term per cell
  * centre into direct_dev (ny, nx) (overwritten), counts visible cells. */

@@ -759,7 +759,8 @@ __global__ void __launch_bounds__(128) k_map_wedges(DevScene S, SbrMapParams P,
   }
 }
 
-std::atomic<int> g_wave_streams{SBR_WAVE_STREAMS > 1 ? 2 : 1};
+constexpr int kMaxWaveStreams = 4;
+std::atomic<int> g_wave_streams{SBR_WAVE_STREAMS};
 
 int launch_status(const char* what) {
   const cudaError_t e = cudaGetLastError();
@@ -861,21 +862,28 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
   // stream and a second one with its own queues, so one pass's kernel tails
   // overlap the other's bulk (passes are independent sample ranges; the grid
   // and counters take float64 / integer atomics from both)
-  const int nstreams = total > (uint64_t)chunk ? g_wave_streams.load() : 1;
-  Wave waves[2];
-  cudaStream_t sts[2] = {st, nullptr};
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int nstreams = g_wave_streams.load();
+  const int64_t npass = (int64_t)((total + (uint64_t)chunk - 1) / (uint64_t)chunk);
+  if (nstreams > npass) nstreams = (int)npass;
+  Wave waves[kMaxWaveStreams];
+  cudaStream_t sts[kMaxWaveStreams] = {st, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[kMaxWaveStreams] = {nullptr, nullptr, nullptr, nullptr};
   // + the dead padding of every shade warp's last output batch
   const int64_t pad = (int64_t)kShadeRes * sms * SBR_SHADE_MINB * 4 + 64;
   for (int k = 0; k < nstreams && !rc; ++k) rc = wave_alloc(chunk + (int64_t)F + pad, st, &waves[k]);
   if (!rc && nstreams > 1) {
-    if (cudaStreamCreateWithFlags(&sts[1], cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess) {
-      rc = set_error(SBR_ERR_CUDA, "second wave stream");
+    if (cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess) {
+      rc = set_error(SBR_ERR_CUDA, "wave stream event");
     } else {
       cudaEventRecord(ev_fork, st);  // queues allocated, caller's prior work done
-      cudaStreamWaitEvent(sts[1], ev_fork, 0);
+      for (int k = 1; k < nstreams && !rc; ++k) {
+        if (cudaStreamCreateWithFlags(&sts[k], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ev_join[k], cudaEventDisableTiming) != cudaSuccess) {
+          rc = set_error(SBR_ERR_CUDA, "wave stream");
+        } else {
+          cudaStreamWaitEvent(sts[k], ev_fork, 0);
+        }
+      }
     }
   }
   int per_sm = 0;
@@ -916,20 +924,23 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
       cur = 1 - cur;
     }
   }
-  if (sts[1]) {  // join: the caller's stream waits for the second stream's passes
-    cudaEventRecord(ev_join, sts[1]);
-    cudaStreamWaitEvent(st, ev_join, 0);
-    cudaStreamDestroy(sts[1]);
+  for (int k = 1; k < kMaxWaveStreams; ++k) {
+    if (!sts[k]) continue;
+    if (ev_join[k]) {  // join: the caller's stream waits for the other streams' passes
+      cudaEventRecord(ev_join[k], sts[k]);
+      cudaStreamWaitEvent(st, ev_join[k], 0);
+      cudaEventDestroy(ev_join[k]);
+    }
+    cudaStreamDestroy(sts[k]);
   }
   if (ev_fork) cudaEventDestroy(ev_fork);
-  if (ev_join) cudaEventDestroy(ev_join);
   for (int k = 0; k < nstreams; ++k)
     if (waves[k].block) cudaFreeAsync(waves[k].block, st);
   return rc;
 }
 
 int sbr_set_wave_streams(int32_t n) {
-  if (n != 1 && n != 2) return set_error(SBR_ERR_INVALID, "wave streams: 1 or 2");
+  if (n < 1 || n > kMaxWaveStreams) return set_error(SBR_ERR_INVALID, "wave streams: 1 to 4");
   g_wave_streams = n;
   return SBR_OK;
 }

@@ -92,3 +92,11 @@ def test_config_validation():
     with pytest.raises(ValueError):
         RadioMapConfig(gain_threshold=-1.0)
     assert RadioMapConfig().wavelength == pytest.approx(299792458.0 / 3.5e9)
+
+
+def test_wave_streams_range_checked():
+    """sbr_set_wave_streams accepts 1..4 (pure host setter, no device call)."""
+    lib = _native.load_library()
+    assert lib.sbr_set_wave_streams(0) == _abi.SBR_ERR_INVALID
+    assert lib.sbr_set_wave_streams(5) == _abi.SBR_ERR_INVALID
+    assert lib.sbr_set_wave_streams(2) == 0

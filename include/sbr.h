@@ -217,6 +217,24 @@ int sbr_wedges_copy(const SbrWedgeSet* set, double* origin, double* e_hat, doubl
                     uint64_t* hash_r, uint64_t* hash_f, int64_t* off0, int64_t* own0,
                     int64_t* offn, int64_t* ownn);
 void sbr_wedges_free(SbrWedgeSet* set);
+
+/* ---- scene files (host code, no device needed) ------------------------- */
+/* Replaces _read_obj_arrays / _obj_corner_index (E/sceneio.py:129-175): ASCII
+ * OBJ text -> vertices (nv, 3) f64 and fan-triangulated 0-based triangles
+ * (nt, 3) i64; `v` / `f` lines only, 1-based or negative indices, v/vt/vn
+ * tokens, '#' comments; numbers in Python float()/int() syntax.  Parsed on
+ * host threads in two passes (counts, then blocks at known offsets).  On a
+ * syntax error returns SBR_ERR_INVALID with the 1-based line, the error kind
+ * (1 vertex needs 3 coordinates, 2 bad vertex, 3 face needs at least 3
+ * vertices, 4 bad face index, 5 index 0, 6 index out of range) and its detail
+ * text (the stripped line body / the face token / str(index)) in err_detail.
+ * Degenerate-triangle removal stays with the caller (reference semantics). */
+typedef struct SbrObjMesh SbrObjMesh;
+int sbr_obj_parse(const char* text, int64_t len, SbrObjMesh** out, int64_t* err_line,
+                  int32_t* err_kind, char* err_detail, int64_t detail_cap);
+int sbr_obj_sizes(const SbrObjMesh* mesh, int64_t* n_vertices, int64_t* n_triangles);
+int sbr_obj_copy(const SbrObjMesh* mesh, double* vertices, int64_t* triangles);
+void sbr_obj_free(SbrObjMesh* mesh);
 /* Reads and clears the device error word (stack overflow).  Synchronises
  * `stream`.  Returns SBR_ERR_STACK if any traversal overflowed. */
 int sbr_scene_check(SbrScene* scene, void* stream);

@@ -72,6 +72,12 @@ def _declare(lib):
         "sbr_cfr": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, i64, vp, i32, vp, i32, vp, i32,
                                    dbl, i32, vp, vp]),
         "sbr_set_cfr_dmma_min_paths": (ctypes.c_int, [i64]),
+        "sbr_obj_parse": (ctypes.c_int, [ctypes.c_char_p, i64, ctypes.POINTER(vp),
+                                         ctypes.POINTER(i64), ctypes.POINTER(i32),
+                                         ctypes.c_char_p, i64]),
+        "sbr_obj_sizes": (ctypes.c_int, [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+        "sbr_obj_copy": (ctypes.c_int, [vp, vp, vp]),
+        "sbr_obj_free": (None, [vp]),
         "sbr_last_error": (ctypes.c_char_p, []),
         "sbr_version": (ctypes.c_int, []),
         "sbr_build_flags": (ctypes.c_int, []),
@@ -101,7 +107,8 @@ def exported_symbols():
         "sbr_cir_vertex_order",
         "sbr_cir_visibility", "sbr_cir_row_pairs", "sbr_cir_select", "sbr_cir_local_dedup",
         "sbr_cir_resolve_records", "sbr_cir_records", "sbr_cir_refine",
-        "sbr_cir_fields", "sbr_cfr", "sbr_set_cfr_dmma_min_paths", "sbr_last_error",
+        "sbr_cir_fields", "sbr_cfr", "sbr_set_cfr_dmma_min_paths",
+        "sbr_obj_parse", "sbr_obj_sizes", "sbr_obj_copy", "sbr_obj_free", "sbr_last_error",
         "sbr_version", "sbr_build_flags", "sbr_kernel_launches", "sbr_profile_enable", "sbr_profile_kernel_ms",
     ]
 

@@ -57,6 +57,7 @@ struct DevScene {
   unsigned int* error_word;    // bit0: traversal stack overflow
   int64_t ntri;
   int32_t nnodes;
+  int32_t depth;               // levels of the binary tree (root = 1)
   int32_t nmat;
   float pad_base;              // conservative box padding: 2^-20 * (max|coord| + 1)
   double bounds_lo[3], bounds_hi[3];  // scene AABB (float64)
@@ -803,6 +804,92 @@ struct ClosestTravT {
         node = ww_pop_t(stack_node, stack_t, sp, bound, node_t);
       }
       if (!__any_sync(__activemask(), leaf < 0)) break;
+    }
+  }
+
+  // Warp-uniform form of round(): EVERY lane of the warp calls it (finished
+  // lanes idle inside, predicated off), so the loop votes use the full mask
+  // (no active-mask / divergence bookkeeping per iteration).  kCheck = false
+  // drops the per-push overflow test: valid when the tree is shallower than
+  // the stack (a depth-first stack holds at most one entry per level).
+  template <bool kCheck>
+  __device__ __forceinline__ void round_u(const DevScene& S) {
+    while (true) {
+      const bool act = node >= 0;
+      if (act) {
+        SBR_DCHECK(S, node < S.nnodes);
+        const BvhNode* nd = S.nodes + node;
+        const float4 a = __ldg(&nd->a), b = __ldg(&nd->b), c = __ldg(&nd->c);
+        const int4 ch = __ldg(&nd->d);
+        const float tl = box_enter(rb, a.x, a.y, a.z, a.w, c.x, c.y, bound);
+        const float tr = box_enter(rb, b.x, b.y, b.z, b.w, c.z, c.w, bound);
+        const bool hl = tl < __int_as_float(0x7f800000);
+        const bool hr = tr < __int_as_float(0x7f800000);
+        if (hl && hr) {
+          const bool lfirst = tl <= tr;
+          if (kCheck && sp >= kStackSize) {
+            ok = false;
+            node = kDone;
+            leaf = 0;
+          } else {
+            SBR_DCHECK(S, sp < kStackSize);
+#if SBR_PACKED_STACK
+            reinterpret_cast<int2*>(stack_node)[sp] =
+                make_int2(lfirst ? ch.y : ch.x, __float_as_int(lfirst ? tr : tl));
+#else
+            stack_node[sp] = lfirst ? ch.y : ch.x;
+            stack_t[sp] = lfirst ? tr : tl;
+#endif
+            ++sp;
+            node = lfirst ? ch.x : ch.y;
+            node_t = lfirst ? tl : tr;
+          }
+        } else if (hl) {
+          node = ch.x;
+          node_t = tl;
+        } else if (hr) {
+          node = ch.y;
+          node_t = tr;
+        } else {
+          node = ww_pop_t(stack_node, stack_t, sp, bound, node_t);
+        }
+        if (node < 0 && node != kDone && leaf == 0) {
+          leaf = node;
+          leaf_t = node_t;
+          node = ww_pop_t(stack_node, stack_t, sp, bound, node_t);
+        }
+      }
+      if (!__any_sync(0xffffffffu, act && leaf == 0)) break;
+    }
+    while (true) {
+      const bool has = leaf < 0;
+      if (has) {
+        const int s = leaf_start(leaf);
+        const int n = leaf_t <= bound ? leaf_count(leaf) : 0;
+        SBR_DCHECK(S, s >= 0 && s + leaf_count(leaf) <= S.ntri);
+        for (int j = s; j < s + n; ++j) {
+          double t, u, v;
+          u = v = 0.0;
+          if (tri_hit_idx<kUV>(r, S.tris + j, t_min, t, u, v)) {
+            const int rank = __ldg(S.tie_rank + j);
+            if (t < best_t || (t == best_t && best >= 0 && rank < best_rank)) {
+              best_t = t;
+              best = j;
+              best_rank = rank;
+              bu = u;
+              bv = v;
+              bound = bound_up(best_t);
+            }
+          }
+        }
+        leaf = 0;
+        if (node < 0 && node != kDone) {
+          leaf = node;
+          leaf_t = node_t;
+          node = ww_pop_t(stack_node, stack_t, sp, bound, node_t);
+        }
+      }
+      if (!__any_sync(0xffffffffu, has && leaf < 0)) break;
     }
   }
 

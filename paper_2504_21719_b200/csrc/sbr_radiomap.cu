@@ -182,7 +182,10 @@ constexpr int kShadeRes = SBR_SHADE_RES;
 #ifndef SBR_TRACE_TPB
 #define SBR_TRACE_TPB 128
 #endif
-template <bool kFirst>
+#ifndef SBR_TRACE_UNIFORM
+#define SBR_TRACE_UNIFORM 1  // warp-uniform traversal loops (ClosestTravT::round_u)
+#endif
+template <bool kFirst, bool kCheck = true>
 __global__ void __launch_bounds__(SBR_TRACE_TPB, SBR_TRACE_MINB) k_map_trace(DevScene S, SbrMapParams P, int seg,
                                                    MapQueue q, const unsigned long long* count_in,
                                                    uint64_t begin, uint64_t count0, CombMap comb,
@@ -227,7 +230,11 @@ __global__ void __launch_bounds__(SBR_TRACE_TPB, SBR_TRACE_MINB) k_map_trace(Dev
     ClosestTravT<false> T(sn, st);  // the map needs t and the slot only
     T.start(S, o, d, 1e-4, __longlong_as_double(0x7ff0000000000000LL));
     if (!active) T.idle();
+#if SBR_TRACE_UNIFORM
+    while (__any_sync(0xffffffffu, !T.done())) T.template round_u<kCheck>(S);
+#else
     while (!T.done()) T.round(S);
+#endif
     if (active) {
       HitRecord h;
       T.result(h);
@@ -892,6 +899,7 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
   const unsigned trace_blocks = (unsigned)(sms * per_sm);
   const unsigned shade_blocks = (unsigned)(sms * SBR_SHADE_MINB);
   const DevScene S = dev_view(scene);
+  const bool shallow = SBR_TRACE_UNIFORM && S.depth < kStackSize;
   int pass = 0;
   for (uint64_t lo = sample_begin; lo < sample_end && !rc; lo += (uint64_t)chunk, ++pass) {
     const uint64_t cnt = (sample_end - lo) < (uint64_t)chunk ? (sample_end - lo) : (uint64_t)chunk;
@@ -904,8 +912,11 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
       k_reset_pass<<<1, 1, 0, ps>>>(w->ctl, w->ctl + 2 - cur, w->ctl + 3, w->ctl + 4);
       if ((rc = launch_status("k_reset_pass"))) break;
       prof_begin(ps, "k_map_trace");
-      (seg == 0 ? k_map_trace<true> : k_map_trace<false>)<<<trace_blocks, SBR_TRACE_TPB, 0, ps>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo, cnt,
-                                                comb, w->hits, w->ctl, counters, sh);
+      // a tree shallower than the stack cannot overflow it: unchecked pushes
+      auto trace = seg == 0 ? (shallow ? k_map_trace<true, false> : k_map_trace<true, true>)
+                            : (shallow ? k_map_trace<false, false> : k_map_trace<false, true>);
+      trace<<<trace_blocks, SBR_TRACE_TPB, 0, ps>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo, cnt,
+                                                    comb, w->hits, w->ctl, counters, sh);
       prof_end(ps);
       if ((rc = launch_status("k_map_trace"))) break;
       prof_begin(ps, "k_map_shade");

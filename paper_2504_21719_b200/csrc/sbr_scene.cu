@@ -148,6 +148,7 @@ struct SbrScene {
   int device = 0;
   int64_t ntri = 0;
   int32_t nnodes = 0;
+  int32_t depth = 0;  // levels of the tree (a traversal stack needs < depth entries)
   sbr::BvhNode* nodes = nullptr;
   sbr::TriSlot* tris = nullptr;
   int32_t* tie_rank = nullptr;
@@ -185,6 +186,7 @@ DevScene dev_view(const SbrScene* s) {
   d.error_word = s->error_word;
   d.ntri = s->ntri;
   d.nnodes = s->nnodes;
+  d.depth = s->depth;
   d.nmat = s->nmat;
   d.pad_base = s->pad_base;
   for (int k = 0; k < 3; ++k) {
@@ -1149,6 +1151,25 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
   }
   count_launch();
   S->nnodes = nnodes;
+  {
+    // tree depth (host walk over the emitted nodes): traversals whose stack
+    // cannot overflow skip the per-push check
+    std::vector<BvhNode> bn((size_t)nnodes);
+    SBR_CUDA(cudaMemcpyAsync(bn.data(), S->nodes, sizeof(BvhNode) * (size_t)nnodes,
+                             cudaMemcpyDeviceToHost, st));
+    SBR_CUDA(cudaStreamSynchronize(st));
+    std::vector<std::pair<int, int>> work{{0, 1}};
+    int depth = 1;
+    while (!work.empty()) {
+      const auto [id, d] = work.back();
+      work.pop_back();
+      depth = std::max(depth, d + 1);  // + the leaf level
+      const int kids[2] = {bn[id].d.x, bn[id].d.y};
+      for (int c : kids)
+        if (c >= 0 && c < nnodes) work.push_back({c, d + 1});
+    }
+    S->depth = depth;
+  }
 
   if ((rc = palloc(&S->tris, n))) return rc;
   k_gather_tris<<<grid_for(n, 256), 256, 0, st>>>(dv0, dv1, dv2, ids_leaf, n, S->tris);

@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(128, SBR_SWEEP_MINB) k_cir_sweep(DevScene S, S
       } else {
         T.idle();
       }
-      while (!T.done()) T.round(S);
+      while (__any_sync(0xffffffffu, !T.done())) T.template round_u<true>(S);  // 1.08 -> 1.05 ms at config 3
       if (!alive) continue;
       HitRecord h;
       T.result(h);

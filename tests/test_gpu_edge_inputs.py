@@ -241,3 +241,43 @@ def test_wave_streams_same_map(cuda, streams):
     assert d == d2
     np.testing.assert_allclose(v, v2, rtol=1e-12)
 
+
+
+def test_deep_tree_radio_map_matches_oracle(cuda):
+    """A radio map over the degenerate chain tree (PLOC only, depth 74): the
+    map trace's warp-uniform loop with unchecked pushes (tree shallower than
+    the 256-entry stack) gives the oracle's map (whose SAH tree is shallow)
+    with identical counters.  The chain spans 1 .. 2^74; from ~2^89 on the
+    scene-relative pad floor of the fp32 box test lets the float64
+    triangle test run on triangles ~1e16 away, where its cancellation reports
+    hits the reference's own box test culls."""
+    import oracle
+    from paper_2504_21719_b200 import _native
+    meshes = _deep_chain_meshes(75)
+    L = _native.lib()
+    L.sbr_set_bvh_builder(2)
+    try:
+        sc = SceneModel(meshes, {0: CONC})
+        acc = sc.accel  # build with the PLOC-only builder
+    finally:
+        L.sbr_set_bvh_builder(1)
+    nodes = np.zeros((int(L.sbr_scene_num_nodes(acc.handle)), 16), np.int32)
+    _native.check(L.sbr_scene_copy_nodes(acc.handle, nodes.ctypes.data))
+    depth, todo = {0: 1}, [0]
+    while todo:
+        i = todo.pop()
+        for c in nodes[i, 12:14]:
+            if c >= 0:
+                depth[int(c)] = depth[i] + 1
+                todo.append(int(c))
+    assert 64 < max(depth.values()) < 256
+    grid = MeasurementGrid((2.0, 0.0, 0.05), (1, 0, 0), (0, 1, 0), (0.25, 0.25), (32, 8))
+    cfg = RadioMapConfig(num_samples=200_000, max_depth=4, enabled=R, seed=5)
+    src = (1.5, 0.3, 0.2)  # between the squares at x = 1 and x = 2
+    vals, diag = compute_radio_map_sbr(sc, src, grid, cfg, include_direct=False)
+    want, wdiag = oracle.OracleScene(meshes, {0: CONC}).radiomap(np.array(src), grid, cfg,
+                                                                 include_direct=False)
+    for key in ("deposits", "escaped", "ray_bounces", "terminated"):
+        assert diag.get(key, 0) == wdiag.get(key, 0), key
+    assert diag["deposits"] > 1000
+    np.testing.assert_allclose(vals, want, rtol=1e-12, atol=0.0)

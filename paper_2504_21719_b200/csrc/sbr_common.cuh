@@ -59,7 +59,7 @@ struct DevScene {
   int32_t nnodes;
   int32_t depth;               // levels of the binary tree (root = 1)
   int32_t nmat;
-  float pad_base;              // conservative box padding: 2^-20 * (max|coord| + 1)
+  float pad_base;              // box_setup's pad floor: 2^-62 * (max|coord| + 1)
   double bounds_lo[3], bounds_hi[3];  // scene AABB (float64)
   // diffraction wedges (n_wedges == 0: none)
   int64_t n_wedges;
@@ -472,7 +472,8 @@ __device__ __forceinline__ bool tri_hit(const Ray64& r, const TriSlot* __restric
 // So a box holding an exact hit with t_min < t <= best_t is never culled,
 // while the pad is 2^-22 |o| instead of a multiple of the scene size: a ray
 // leaving a surface no longer re-enters the (flat) boxes around its origin.
-// `pad_floor` (scene size * 2^-26) only guards origins near 0.
+// `pad_floor` (scene size * 2^-62) keeps the slab of a direction component of
+// exactly +-0 (reciprocal clamped to +-1e20) unbounded across the scene.
 struct RayBox {
   float ix, iy, iz;       // fl(1/fl(d)) (clamped to +-1e20)
   float oxp, oyp, ozp;    // fl((o + pad) * ix)  -> lo planes

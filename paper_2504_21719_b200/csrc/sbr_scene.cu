@@ -521,6 +521,9 @@ constexpr int kPlocRadius = SBR_PLOC_RADIUS;
 // (ms) / build (s): PLOC only 458 / 0.14, top 16k 444, 64k 405 / 0.28, 256k
 // 388 / 0.20, pure SAH 389 / 0.50; canyon 4.23 -> 3.37 ms; config-3
 // visibility 59.9 -> 57.6 ms.
+#ifndef SBR_PAD_FLOOR_LOG2
+#define SBR_PAD_FLOOR_LOG2 62  // was 26: boxes padded by 1.5e-8 x the scene size
+#endif
 #ifndef SBR_PLOC_TOP
 #define SBR_PLOC_TOP 262144
 #endif
@@ -1000,7 +1003,11 @@ int sbr_scene_create(const double* v0, const double* v1, const double* v2, int64
     S->lo[k] = lo[k];
     S->hi[k] = hi[k];
   }
-  S->pad_base = (float)(ldexp(max_abs + 1.0, -26));  // box_setup's pad floor
+  // box_setup's pad floor: with a direction component of exactly +-0 its
+  // reciprocal is clamped to +-1e20, and the pad x 1e20 must then exceed any
+  // distance inside the scene (2^-62 x 1e20 = 21.7 x the largest coordinate);
+  // the relative pad 2^-22 |o| carries the rest of the error analysis
+  S->pad_base = (float)(ldexp(max_abs + 1.0, -SBR_PAD_FLOOR_LOG2));
 
   double *dv0, *dv1, *dv2;
   const size_t bytes = sizeof(double) * 3 * (size_t)ntri;

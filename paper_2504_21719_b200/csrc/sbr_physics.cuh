@@ -182,6 +182,21 @@ static __device__ cvec3 antenna_field(const SbrAntenna& a, double3 d) {
   return E;
 }
 
+// antenna_field for an isotropic, unrotated pattern: the same operations on
+// local = d with cth = 1 (bit-identical), without the other patterns' code
+__device__ __forceinline__ cvec3 antenna_iso(double3 d) {
+  const double theta = acos(clamp1(d.z));
+  const double phi = atan2(d.y, d.x);
+  double st, ct, sp, cp;
+  sincos(theta, &st, &ct);
+  sincos(phi, &sp, &cp);
+  cvec3 E;
+  E.x = C(1.0 * (ct * cp), 0.0);
+  E.y = C(1.0 * (ct * sp), 0.0);
+  E.z = C(1.0 * -st, 0.0);
+  return E;
+}
+
 // |sum_m exp(j k d.o_m) u_m|^2 (radiomap.py:253-259)
 static __device__ double alpha_sq(const SbrMapParams& P, double3 d) {
   if (P.n_elements <= 0) return 1.0;

@@ -166,6 +166,9 @@ constexpr int kShadeChunk = SBR_SHADE_CHUNK;
 #define SBR_SHADE_RES 128  // next-queue slots a warp reserves per atomic (multiple of 32): config-4 map 32: 812 ms, 64: 797, 128: 784, 256: 785
 #endif
 constexpr int kShadeRes = SBR_SHADE_RES;
+#ifndef SBR_SHADE_SPECIALISE
+#define SBR_SHADE_SPECIALISE 1
+#endif
 #ifndef SBR_SHADE_MINB
 #define SBR_SHADE_MINB 8
 #endif
@@ -263,7 +266,11 @@ struct LaneCounters {
 // kFirst: the segment-0 instantiation (launch directions from the sample id)
 // and the queue instantiation are separate kernels when SBR_SHADE_SPLIT, so
 // each carries only its own ray-source code
-template <bool kFirst>
+// kCull: the run culls (gain threshold / Russian roulette); kSimple: an
+// isotropic, unrotated source without an array (the launch field is the
+// zenith unit vector, weight 1) -- both specialisations only drop code the
+// run never executes (smaller instruction footprint, SBR_SHADE_SPECIALISE)
+template <bool kFirst, bool kCull = true, bool kSimple = false>
 __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, SbrMapParams P, int seg,
                                                    MapQueue qi, const unsigned long long* count_in,
                                                    uint64_t begin, CombMap comb, HitBuf hits,
@@ -325,10 +332,15 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
       g = sh.gid(begin + comb.sample(i));
       o = make_double3(P.source[0], P.source[1], P.source[2]);
       d = fibonacci_dir(P.num_samples, g);
-      E = antenna_field(P.pattern, d);
+      if (kSimple) {
+        E = antenna_iso(d);
+        weight = 1.0;
+      } else {
+        E = antenna_field(P.pattern, d);
+        weight = alpha_sq(P, d);
+      }
       r_dist = 0.0;
       omega = P.omega0;
-      weight = alpha_sq(P, d);
     } else {
       g = qld(&qi.g[i]);
       o = make_double3(qld(&qi.ox[i]), qld(&qi.oy[i]), qld(&qi.oz[i]));
@@ -368,7 +380,7 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
     if (seg == P.max_depth) continue;
     const double r_hit = r_dist + t_hit;
     // culling (radiomap.py:427-447)
-    if (seg >= P.cull_from && (P.gain_threshold > 0.0 || P.rr_depth >= 0)) {
+    if (kCull && seg >= P.cull_from && (P.gain_threshold > 0.0 || P.rr_depth >= 0)) {
       const double e_sq = field_energy(E);
       bool keep = true;
       if (P.gain_threshold > 0.0) {
@@ -900,6 +912,9 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
   const unsigned shade_blocks = (unsigned)(sms * SBR_SHADE_MINB);
   const DevScene S = dev_view(scene);
   const bool shallow = SBR_TRACE_UNIFORM && S.depth < kStackSize;
+  const bool cull = !SBR_SHADE_SPECIALISE || P->gain_threshold > 0.0 || P->rr_depth >= 0;
+  const bool simple = SBR_SHADE_SPECIALISE && P->pattern.identity && P->pattern.kind == SBR_PATTERN_ISOTROPIC &&
+                      P->n_elements <= 0;
   int pass = 0;
   for (uint64_t lo = sample_begin; lo < sample_end && !rc; lo += (uint64_t)chunk, ++pass) {
     const uint64_t cnt = (sample_end - lo) < (uint64_t)chunk ? (sample_end - lo) : (uint64_t)chunk;
@@ -920,7 +935,10 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
       prof_end(ps);
       if ((rc = launch_status("k_map_trace"))) break;
       prof_begin(ps, "k_map_shade");
-      (seg == 0 ? k_map_shade<true> : k_map_shade<false>)<<<shade_blocks, 128, 0, ps>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo,
+      auto shade = seg == 0 ? (cull ? (simple ? k_map_shade<true, true, true> : k_map_shade<true, true, false>)
+                                    : (simple ? k_map_shade<true, false, true> : k_map_shade<true, false, false>))
+                            : (cull ? k_map_shade<false, true, false> : k_map_shade<false, false, false>);
+      shade<<<shade_blocks, 128, 0, ps>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo,
                                                 comb, w->hits, w->q[1 - cur], w->ctl + 2 - cur,
                                                 w->sq, w->ctl + 3, grid, counters, sh, w->ctl + 4);
       prof_end(ps);

@@ -673,6 +673,9 @@ __device__ __forceinline__ int ww_pop_t(const int* stack_node, const float* stac
   return kDone;
 }
 
+#ifndef SBR_UNI_NOSPEC
+#define SBR_UNI_NOSPEC 1  // in the uniform loop speculation no longer pays: config-4 map 682.7 -> 678.7 ms
+#endif
 // Resumable per-lane closest-hit traversal state.  round() runs one
 // inner-node phase + one leaf phase (while-while); done() reports completion.
 // kUV = false skips the barycentric (u, v) divisions (radio map, CIR sweep).
@@ -816,7 +819,11 @@ struct ClosestTravT {
   template <bool kCheck>
   __device__ __forceinline__ void round_u(const DevScene& S) {
     while (true) {
+#if SBR_UNI_NOSPEC
+      const bool act = node >= 0 && leaf == 0;  // no speculative descent past a parked leaf
+#else
       const bool act = node >= 0;
+#endif
       if (act) {
         SBR_DCHECK(S, node < S.nnodes);
         const BvhNode* nd = S.nodes + node;

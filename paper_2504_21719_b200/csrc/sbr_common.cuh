@@ -58,6 +58,7 @@ struct DevScene {
   int64_t ntri;
   int32_t nnodes;
   int32_t depth;               // levels of the binary tree (root = 1)
+  int32_t all_lambertian;      // every material scatters with the Lambertian lobe
   int32_t nmat;
   float pad_base;              // box_setup's pad floor: 2^-62 * (max|coord| + 1)
   double bounds_lo[3], bounds_hi[3];  // scene AABB (float64)

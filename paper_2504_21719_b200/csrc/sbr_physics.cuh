@@ -109,12 +109,15 @@ static __device__ double lobe_norm(int alpha, double cos_ti) {
 
 __device__ __forceinline__ double clamp1(double x) { return x < -1.0 ? -1.0 : (x > 1.0 ? 1.0 : x); }
 
+// the Lambertian lobe of pattern_density (materials.py:354-397)
+__device__ __forceinline__ double lambert_density(double3 ks, double3 n) {
+  double c = dot_seq(ks, n);
+  c = c < 0.0 ? 0.0 : (c > 1.0 ? 1.0 : c);
+  return c / kPi;
+}
+
 static __device__ double pattern_density(const SbrMaterial& m, double3 ki, double3 ks, double3 n) {
-  if (m.pattern_kind == SBR_SCAT_LAMBERTIAN) {
-    double c = dot_seq(ks, n);
-    c = c < 0.0 ? 0.0 : (c > 1.0 ? 1.0 : c);
-    return c / kPi;
-  }
+  if (m.pattern_kind == SBR_SCAT_LAMBERTIAN) return lambert_density(ks, n);
   const double ci = clamp1(-dot_seq(ki, n));
   const double kn = dot_seq(ki, n);
   const double3 kr = ki - (2.0 * kn) * n;

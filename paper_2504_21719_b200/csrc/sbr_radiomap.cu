@@ -545,6 +545,9 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
 #ifndef SBR_SCATTER_MINB
 #define SBR_SCATTER_MINB 8  // 64 registers: 0.38 -> 0.34 ms per map
 #endif
+// kLambert: every material's lobe is Lambertian (the other lobes' code --
+// lobe normalisation loops, pow -- dropped from this instantiation)
+template <bool kLambert = false>
 __global__ void __launch_bounds__(128, SBR_SCATTER_MINB) k_map_scatter(DevScene S, SbrMapParams P, int seg,
                                                         ScatterQueue sq,
                                                         const unsigned long long* count_s,
@@ -579,7 +582,7 @@ __global__ void __launch_bounds__(128, SBR_SCATTER_MINB) k_map_scatter(DevScene 
     const double3 ks = make_double3((a * t1.x + b * t2.x) + cos_t * nrm.x,
                                     (a * t1.y + b * t2.y) + cos_t * nrm.y,
                                     (a * t1.z + b * t2.z) + cos_t * nrm.z);
-    const double f_s = pattern_density(m, d, ks, nrm);
+    const double f_s = kLambert ? lambert_density(ks, nrm) : pattern_density(m, d, ks, nrm);
     const double patch = omega * (r_hit * r_hit) / (cos_i > 1e-12 ? cos_i : 1e-12);
     const double amp = m.scattering * gamma * sqrt(f_s * cos_i * patch);
     double3 th_i, ph_i;
@@ -945,7 +948,7 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
       if ((rc = launch_status("k_map_shade"))) break;
       if (seg < P->max_depth && (P->allow_mask & 2)) {
         prof_begin(ps, "k_map_scatter");
-        k_map_scatter<<<shade_blocks, 128, 0, ps>>>(S, *P, seg, w->sq, w->ctl + 3, w->q[1 - cur],
+        (S.all_lambertian && SBR_SHADE_SPECIALISE ? k_map_scatter<true> : k_map_scatter<false>)<<<shade_blocks, 128, 0, ps>>>(S, *P, seg, w->sq, w->ctl + 3, w->q[1 - cur],
                                                     w->ctl + 2 - cur, counters);
         prof_end(ps);
         if ((rc = launch_status("k_map_scatter"))) break;

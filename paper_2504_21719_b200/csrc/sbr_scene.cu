@@ -158,6 +158,7 @@ struct SbrScene {
   uint64_t* hash_f = nullptr;
   SbrMaterial* mats = nullptr;
   int32_t nmat = 0;
+  int32_t all_lambertian = 0;  // every material's scattering lobe is Lambertian
   unsigned int* error_word = nullptr;
   float pad_base = 0.f;
   double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
@@ -188,6 +189,7 @@ DevScene dev_view(const SbrScene* s) {
   d.nnodes = s->nnodes;
   d.depth = s->depth;
   d.nmat = s->nmat;
+  d.all_lambertian = s->all_lambertian;
   d.pad_base = s->pad_base;
   for (int k = 0; k < 3; ++k) {
     d.bounds_lo[k] = s->lo[k];
@@ -1284,6 +1286,9 @@ int sbr_scene_set_materials(SbrScene* S, const SbrMaterial* mats, int32_t n) {
   SBR_CUDA(cudaMalloc(&S->mats, sizeof(SbrMaterial) * n));
   SBR_CUDA(cudaMemcpy(S->mats, mats, sizeof(SbrMaterial) * n, cudaMemcpyHostToDevice));
   S->nmat = n;
+  S->all_lambertian = 1;
+  for (int32_t k = 0; k < n; ++k)
+    if (mats[k].pattern_kind != SBR_SCAT_LAMBERTIAN) S->all_lambertian = 0;
   return SBR_OK;
 }
 

@@ -275,12 +275,15 @@ int sbr_philox_uniform(uint64_t seed, uint64_t sample, uint64_t depth,
 int sbr_radiomap_bounce(const SbrScene* scene, const SbrMapParams* params,
                         uint64_t sample_begin, uint64_t sample_end,
                         double* grid_dev, uint64_t* counters_dev, void* stream);
-/* The bounce loop over a chunk-cyclic shard of the global sample ids
- * [0, num_samples): global RNG chunks (g >> SBR_CHUNK_LOG2) = shard_index,
- * shard_index + shard_count, ...  The shards of one call partition the ids, so
- * summing their grids / counters gives sbr_radiomap_bounce(0, num_samples);
- * unlike contiguous ranges every shard sees the whole sphere of directions
- * (balanced work per GPU).  No reference counterpart (multi-GPU only). */
+/* The bounce loop over a block-cyclic shard of the global sample ids
+ * [0, num_samples): blocks of 2^b ids (g >> b) = shard_index, shard_index +
+ * shard_count, ..., b = log2(num_samples / (8 * shard_count)) clamped to
+ * [SBR_CHUNK_LOG2, 23] (whole RNG chunks; >= 8 blocks per shard).  The shards
+ * of one call partition the ids, so summing their grids / counters gives
+ * sbr_radiomap_bounce(0, num_samples); unlike contiguous ranges every shard
+ * sees the whole sphere of directions (balanced work per GPU), while each
+ * block is a contiguous polar band (coherent passes).  No reference
+ * counterpart (multi-GPU only). */
 int sbr_radiomap_bounce_sharded(const SbrScene* scene, const SbrMapParams* params,
                                 int32_t shard_index, int32_t shard_count, double* grid_dev,
                                 uint64_t* counters_dev, void* stream);

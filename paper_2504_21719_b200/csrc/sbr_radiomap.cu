@@ -166,14 +166,6 @@ constexpr int kShadeChunk = SBR_SHADE_CHUNK;
 #define SBR_SHADE_RES 128  // next-queue slots a warp reserves per atomic (multiple of 32): config-4 map 32: 812 ms, 64: 797, 128: 784, 256: 785
 #endif
 constexpr int kShadeRes = SBR_SHADE_RES;
-#ifndef SBR_BRANCH_HINTS
-#define SBR_BRANCH_HINTS 0
-#endif
-#if SBR_BRANCH_HINTS
-#define SBR_UNLIKELY(c) __builtin_expect(!!(c), 0)
-#else
-#define SBR_UNLIKELY(c) (c)
-#endif
 #ifndef SBR_SHADE_SPECIALISE
 #define SBR_SHADE_SPECIALISE 1
 #endif
@@ -327,7 +319,7 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
     uint64_t g;
     if (i < c1) do {
     const int tri = qld(&hits.tri[i]);
-    if (SBR_UNLIKELY(tri < -1)) continue;  // empty comb slot / stack overflow
+    if (tri < -1) continue;  // empty comb slot / stack overflow
     SBR_DCHECK(S, tri < S.ntri && i < qi.cap);
     if (SHADE_FIRST && tri < 0) {
       // a launch ray that escapes does nothing but count (no plane crossing at
@@ -425,7 +417,7 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
     if (!(P.allow_mask & 2)) q1 = 0.0;
     if (!(P.allow_mask & 4)) q2 = 0.0;
     const double total = ((q0 + q1) + q2) + 0.0;
-    if (SBR_UNLIKELY(!(total > 0.0))) {
+    if (!(total > 0.0)) {
       K.terminated++;
       continue;
     }
@@ -459,7 +451,7 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
       E.z = e_perp.z * a + e_par.z * b;
     }
     r_dist = r_hit;
-    if (SBR_UNLIKELY(code == 1)) {
+    if (code == 1) {
       // gamma_reflected (materials.py:400-419) here, the rest in k_map_scatter
       const double g_num = sqrt(cabs2(F.rp * c_perp) + cabs2(F.rl * c_par));
       const double g_den = sqrt(cabs2(c_perp) + cabs2(c_par));

@@ -550,6 +550,21 @@ __device__ __forceinline__ float box_enter(const RayBox& rb, float lox, float hi
 #endif
 }
 
+// box_enter as (hit, entry) without the +inf select (the caller branches on
+// the predicate directly; same test as SBR_BOX_FOLD box_enter)
+__device__ __forceinline__ bool box_hit(const RayBox& rb, float lox, float hix, float loy,
+                                        float hiy, float loz, float hiz, float bound,
+                                        float& tn_out) {
+  const float x0 = fmaf(lox, rb.ix, -rb.oxp), x1 = fmaf(hix, rb.ix, -rb.oxm);
+  const float y0 = fmaf(loy, rb.iy, -rb.oyp), y1 = fmaf(hiy, rb.iy, -rb.oym);
+  const float z0 = fmaf(loz, rb.iz, -rb.ozp), z1 = fmaf(hiz, rb.iz, -rb.ozm);
+  const float tn = fmaxf(fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fminf(z0, z1)), rb.tlo);
+  const float tf = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fmaxf(z0, z1));
+  const float tf2 = fminf(fmaf(0x1p-20f, fabsf(tf), tf), bound);
+  tn_out = tn;
+  return tn <= tf2;
+}
+
 // float upper bound of a float64 distance (for comparing fp32 entries)
 __device__ __forceinline__ float bound_up(double t) {
   if (!(t < 3.0e38)) return __int_as_float(0x7f800000);
@@ -681,6 +696,12 @@ __device__ __forceinline__ int ww_pop_t(const int* stack_node, const float* stac
   return kDone;
 }
 
+#ifndef SBR_ANY_BOX_HIT
+#define SBR_ANY_BOX_HIT 1  // config-3 visibility 56.5 -> 55.5 ms
+#endif
+#ifndef SBR_BOX_HIT
+#define SBR_BOX_HIT 1  // (hit, entry) box test in the traversal loops: config-4 map 672 -> 660 ms
+#endif
 #ifndef SBR_UNI_NOSPEC
 #define SBR_UNI_NOSPEC 1  // in the uniform loop speculation no longer pays: config-4 map 682.7 -> 678.7 ms
 #endif
@@ -837,10 +858,16 @@ struct ClosestTravT {
         const BvhNode* nd = S.nodes + node;
         const float4 a = __ldg(&nd->a), b = __ldg(&nd->b), c = __ldg(&nd->c);
         const int4 ch = __ldg(&nd->d);
+#if SBR_BOX_HIT && SBR_BOX_FOLD
+        float tl, tr;
+        const bool hl = box_hit(rb, a.x, a.y, a.z, a.w, c.x, c.y, bound, tl);
+        const bool hr = box_hit(rb, b.x, b.y, b.z, b.w, c.z, c.w, bound, tr);
+#else
         const float tl = box_enter(rb, a.x, a.y, a.z, a.w, c.x, c.y, bound);
         const float tr = box_enter(rb, b.x, b.y, b.z, b.w, c.z, c.w, bound);
         const bool hl = tl < __int_as_float(0x7f800000);
         const bool hr = tr < __int_as_float(0x7f800000);
+#endif
         if (hl && hr) {
           const bool lfirst = tl <= tr;
           if (kCheck && sp >= kStackSize) {
@@ -976,10 +1003,16 @@ struct AnyTrav {
       const BvhNode* nd = S.nodes + node;
       const float4 a = __ldg(&nd->a), b = __ldg(&nd->b), c = __ldg(&nd->c);
       const int4 ch = __ldg(&nd->d);
+#if SBR_ANY_BOX_HIT && SBR_BOX_FOLD
+      float tl, tr;
+      const bool hl = box_hit(rb, a.x, a.y, a.z, a.w, c.x, c.y, bound, tl);
+      const bool hr = box_hit(rb, b.x, b.y, b.z, b.w, c.z, c.w, bound, tr);
+#else
       const float tl = box_enter(rb, a.x, a.y, a.z, a.w, c.x, c.y, bound);
       const float tr = box_enter(rb, b.x, b.y, b.z, b.w, c.z, c.w, bound);
       const bool hl = tl < __int_as_float(0x7f800000);
       const bool hr = tr < __int_as_float(0x7f800000);
+#endif
       if (hl && hr) {
         if (sp >= kStackSize) {
           ok = false;

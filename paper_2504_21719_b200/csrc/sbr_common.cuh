@@ -669,6 +669,10 @@ __device__ __forceinline__ bool trace_closest(const DevScene& S, double3 o, doub
 // (t, tie_rank) over all triangles is independent of visiting order; box
 // culling is conservative).  Lanes with active == false only vote.
 constexpr int kDone = (int)0x80000000;  // never a node index or a leaf code
+constexpr int kPending = (int)0x80000001;  // round_u: pop after the parked leaf's test
+#ifndef SBR_DEFER_POP
+#define SBR_DEFER_POP 1  // config-4 map 660 -> 647 ms, c2 trace 2.85 -> 2.67 ms
+#endif
 
 // SBR_PACKED_STACK: a stack entry is one 8-byte (node, entry distance) pair
 // (one local load / store per pop / push instead of two); the caller's node
@@ -899,7 +903,11 @@ struct ClosestTravT {
         if (node < 0 && node != kDone && leaf == 0) {
           leaf = node;
           leaf_t = node_t;
+#if SBR_DEFER_POP
+          node = kPending;  // popped after the leaf test, with its tighter bound
+#else
           node = ww_pop_t(stack_node, stack_t, sp, bound, node_t);
+#endif
         }
       }
       if (!__any_sync(0xffffffffu, act && leaf == 0)) break;
@@ -926,10 +934,17 @@ struct ClosestTravT {
           }
         }
         leaf = 0;
+#if SBR_DEFER_POP
+        if (node == kPending) node = ww_pop_t(stack_node, stack_t, sp, bound, node_t);
+#endif
         if (node < 0 && node != kDone) {
           leaf = node;
           leaf_t = node_t;
+#if SBR_DEFER_POP
+          node = kPending;
+#else
           node = ww_pop_t(stack_node, stack_t, sp, bound, node_t);
+#endif
         }
       }
       if (!__any_sync(0xffffffffu, has && leaf < 0)) break;

@@ -166,6 +166,9 @@ constexpr int kShadeChunk = SBR_SHADE_CHUNK;
 #define SBR_SHADE_RES 128  // next-queue slots a warp reserves per atomic (multiple of 32): config-4 map 32: 812 ms, 64: 797, 128: 784, 256: 785
 #endif
 constexpr int kShadeRes = SBR_SHADE_RES;
+#ifndef SBR_SEG0_DIR_QUEUE
+#define SBR_SEG0_DIR_QUEUE 1  // config-4 map 648 -> 643 ms
+#endif
 #ifndef SBR_SHADE_SPECIALISE
 #define SBR_SHADE_SPECIALISE 1
 #endif
@@ -216,7 +219,16 @@ __global__ void __launch_bounds__(SBR_TRACE_TPB, SBR_TRACE_MINB) k_map_trace(Dev
       if (TRACE_FIRST) {
         const uint64_t local = comb.sample(i);
         active = local < count0;
-        if (active) d = fibonacci_dir(P.num_samples, sh.gid(begin + local));
+        if (active) {
+          d = fibonacci_dir(P.num_samples, sh.gid(begin + local));
+#if SBR_SEG0_DIR_QUEUE
+          // the (otherwise unused) segment-0 input queue carries the launch
+          // direction to the shade, which would recompute it
+          qst(&q.dx[i], d.x);
+          qst(&q.dy[i], d.y);
+          qst(&q.dz[i], d.z);
+#endif
+        }
         else qst(&hits.tri[i], -3);  // comb slot past the end of the range
       } else {
         o = make_double3(qld(&q.ox[i]), qld(&q.oy[i]), qld(&q.oz[i]));
@@ -331,7 +343,11 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
     if (SHADE_FIRST) {
       g = sh.gid(begin + comb.sample(i));
       o = make_double3(P.source[0], P.source[1], P.source[2]);
+#if SBR_SEG0_DIR_QUEUE
+      d = make_double3(qld(&qi.dx[i]), qld(&qi.dy[i]), qld(&qi.dz[i]));
+#else
       d = fibonacci_dir(P.num_samples, g);
+#endif
       if (kSimple) {
         E = antenna_iso(d);
         weight = 1.0;

@@ -16,11 +16,14 @@
 // into their slices of the output.  Each block keeps its first error; the
 // earliest line's error is reported.
 #include <algorithm>
+#include <memory>
+#include <atomic>
 #include <cerrno>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <new>
 #include <string>
 #include <thread>
 #include <vector>
@@ -329,8 +332,22 @@ void parse_block(Block& B, double* V, int64_t* T) {
 
 extern "C" {
 
+static int obj_parse_impl(const char* text, int64_t len, SbrObjMesh** out, int64_t* err_line,
+                          int32_t* err_kind, char* err_detail, int64_t detail_cap);
+
 int sbr_obj_parse(const char* text, int64_t len, SbrObjMesh** out, int64_t* err_line,
                   int32_t* err_kind, char* err_detail, int64_t detail_cap) {
+  try {
+    return obj_parse_impl(text, len, out, err_line, err_kind, err_detail, detail_cap);
+  } catch (const std::bad_alloc&) {
+    return sbr::set_error(SBR_ERR_NOMEM, "obj: out of memory");
+  } catch (...) {
+    return sbr::set_error(SBR_ERR_INTERNAL, "obj: internal error");
+  }
+}
+
+static int obj_parse_impl(const char* text, int64_t len, SbrObjMesh** out, int64_t* err_line,
+                          int32_t* err_kind, char* err_detail, int64_t detail_cap) {
   if (!out || (!text && len > 0) || len < 0) return sbr::set_error(SBR_ERR_INVALID, "obj: bad arguments");
   *out = nullptr;
   if (err_line) *err_line = 0;
@@ -354,14 +371,28 @@ int sbr_obj_parse(const char* text, int64_t len, SbrObjMesh** out, int64_t* err_
     blocks.push_back(B);
     p = q;
   }
+  // blocks b = t, t + nthreads, ... on host thread t; whatever a failed thread
+  // creation leaves unstarted runs on the calling thread (no exception
+  // crosses the C ABI)
   auto run = [&](auto fn) {
     std::vector<std::thread> th;
     const size_t nthreads = std::min<size_t>(blocks.size(), hw);
-    for (size_t t = 0; t < nthreads; ++t)
-      th.emplace_back([&, t] {
+    std::atomic<bool> failed{false};  // an exception inside a worker (bad_alloc)
+    auto work = [&](size_t t) {
+      try {
         for (size_t b = t; b < blocks.size(); b += nthreads) fn(blocks[b]);
-      });
+      } catch (...) {
+        failed = true;
+      }
+    };
+    size_t started = 0;
+    try {
+      for (; started < nthreads; ++started) th.emplace_back(work, started);
+    } catch (...) {
+    }
+    for (size_t t = started; t < nthreads; ++t) work(t);
     for (auto& x : th) x.join();
+    if (failed) throw std::bad_alloc();
   };
   if (blocks.size() > 1) run([](Block& B) { count_block(B); });
   else if (!blocks.empty()) count_block(blocks[0]);
@@ -374,14 +405,9 @@ int sbr_obj_parse(const char* text, int64_t len, SbrObjMesh** out, int64_t* err_
     nv += B.nv;
     nt += B.nt;
   }
-  auto* M = new SbrObjMesh;
-  try {
-    M->verts.resize(3 * (size_t)nv);
-    M->tris.resize(3 * (size_t)nt);
-  } catch (...) {
-    delete M;
-    return sbr::set_error(SBR_ERR_NOMEM, "obj: out of memory");
-  }
+  std::unique_ptr<SbrObjMesh> M(new SbrObjMesh);
+  M->verts.resize(3 * (size_t)nv);  // bad_alloc -> SBR_ERR_NOMEM (sbr_obj_parse)
+  M->tris.resize(3 * (size_t)nt);
   double* V = M->verts.data();
   int64_t* T = M->tris.data();
   if (blocks.size() > 1) run([&](Block& B) { parse_block(B, V, T); });
@@ -397,10 +423,9 @@ int sbr_obj_parse(const char* text, int64_t len, SbrObjMesh** out, int64_t* err_
       std::memcpy(err_detail, first->detail.data(), n);
       err_detail[n] = '\0';
     }
-    delete M;
     return sbr::set_error(SBR_ERR_INVALID, "obj: parse error at line " + std::to_string(first->line));
   }
-  *out = M;
+  *out = M.release();
   return SBR_OK;
 }
 

@@ -182,6 +182,9 @@ constexpr int kShadeRes = SBR_SHADE_RES;
 #ifndef SBR_WAVE_STREAMS
 #define SBR_WAVE_STREAMS 2  // config-4 map 783 -> 757 ms (kernel tails of one pass overlap the other)
 #endif
+#ifndef SBR_TRACE_CLAIM_AHEAD
+#define SBR_TRACE_CLAIM_AHEAD 1  // config-4 map 644 -> 640 ms
+#endif
 #ifndef SBR_TRACE_CLAIM
 #define SBR_TRACE_CLAIM 1  // batches of 32 rays a trace warp claims per atomic
 #endif
@@ -200,6 +203,16 @@ __global__ void __launch_bounds__(SBR_TRACE_TPB, SBR_TRACE_MINB) k_map_trace(Dev
   const unsigned lane = threadIdx.x & 31u;
   const uint64_t n = TRACE_FIRST ? comb.slots() : (uint64_t)*count_in;
   const double3 src = make_double3(P.source[0], P.source[1], P.source[2]);
+#if SBR_TRACE_CLAIM_AHEAD
+  // the next batch is claimed while this one is traced: the atomic's round
+  // trip hides behind the traversal (lane 0's raw atomic is not aggregated)
+  unsigned long long next = 0;
+  if (lane == 0) next = atom_add_async(work, 32ULL);
+  while (true) {
+    const unsigned long long base = __shfl_sync(0xffffffffu, next, 0);
+    if (base >= n) break;
+    if (lane == 0) next = atom_add_async(work, 32ULL);
+#else
   unsigned long long claim = 0;
   int left = 0;  // batches of 32 left in the current claim
   while (true) {
@@ -212,6 +225,7 @@ __global__ void __launch_bounds__(SBR_TRACE_TPB, SBR_TRACE_MINB) k_map_trace(Dev
     claim += 32;
     --left;
     if (base >= n) break;
+#endif
     const uint64_t i = base + lane;
     bool active = i < n;
     double3 o = src, d = make_double3(0.0, 0.0, 1.0);

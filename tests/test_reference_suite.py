@@ -1,0 +1,283 @@
+"""The reference's own unit tests for the hot path, restated against this API.
+
+Each test states the behaviour of one test in emtrace's test-suite
+(`pkg/tests/test_geometry.py`, `test_radiomap.py`, `test_paths.py`; cited per
+test), on the same scenes and configurations, so a user moving from the
+reference finds the same guarantees.  The host-side validation tests run on
+CPU; everything that traces is `gpu`-marked and runs the CUDA path.
+"""
+
+import numpy as np
+import pytest
+
+from paper_2504_21719_b200 import (MeasurementGrid, Mesh, PathConfig, RadioDevice,
+                                   RadioMapConfig, Ray, SceneModel, build_scene_accel,
+                                   compute_paths, compute_radio_map_sbr,
+                                   generate_candidates, intersect_closest, scenes)
+from paper_2504_21719_b200.em import ArrayGeometry
+from paper_2504_21719_b200.errors import UnresolvedMaterial
+from paper_2504_21719_b200.materials import RadioMaterial
+from paper_2504_21719_b200.sampling import Interaction
+
+C0 = 299792458.0
+BOX_LO, BOX_HI = np.array([-3.0, -4.0, 0.0]), np.array([3.0, 4.0, 3.0])
+TX_POS, RX_POS = np.array([-1.0, -2.0, 1.5]), np.array([1.5, 2.0, 1.5])
+CONCRETE = RadioMaterial("concrete", eps_r=5.24, sigma=0.1, thickness=0.3)
+R_ONLY = frozenset({Interaction.REFLECTION})
+RS = frozenset({Interaction.REFLECTION, Interaction.SCATTERING})
+
+
+def _walled_room(material=CONCRETE):
+    """Closed room, one object per wall (test_radiomap.py:48-66)."""
+    (xl, yl, zl), (xh, yh, zh) = BOX_LO, BOX_HI
+    quads = [
+        ([xl, yl, zl], [xh, yl, zl], [xh, yh, zl], [xl, yh, zl]),
+        ([xl, yl, zh], [xh, yl, zh], [xh, yh, zh], [xl, yh, zh]),
+        ([xl, yl, zl], [xh, yl, zl], [xh, yl, zh], [xl, yl, zh]),
+        ([xl, yh, zl], [xh, yh, zl], [xh, yh, zh], [xl, yh, zh]),
+        ([xl, yl, zl], [xl, yh, zl], [xl, yh, zh], [xl, yl, zh]),
+        ([xh, yl, zl], [xh, yh, zl], [xh, yh, zh], [xh, yl, zh]),
+    ]
+    meshes = [Mesh(np.array(q, dtype=np.float64), np.array([[0, 1, 2], [0, 2, 3]]), object_id=i + 1)
+              for i, q in enumerate(quads)]
+    return SceneModel(meshes, {i: material for i in range(1, 7)})
+
+
+def _inward_room(material=CONCRETE):
+    """One inward-facing box object (test_paths.py:53-55)."""
+    return SceneModel([scenes.box_mesh(BOX_LO, BOX_HI, object_id=0, inward=True)], {0: material})
+
+
+def _small_grid(cell=1.0, n=2):
+    return MeasurementGrid((0.5, 1.0, 1.2), (1, 0, 0), (0, 1, 0), (cell, cell), (n, n))
+
+
+# ---------------------------------------------------------------------------
+# host-side validation (CPU)
+# ---------------------------------------------------------------------------
+
+def test_mesh_rejects_degenerate_triangle_and_bad_index():
+    # test_geometry.py:16-25
+    with pytest.raises(ValueError):
+        Mesh(np.array([[0, 0, 0], [1, 0, 0], [2, 0, 0]], float), np.array([[0, 1, 2]]), object_id=0)
+    with pytest.raises(ValueError):
+        Mesh(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0]], float), np.array([[0, 1, 3]]), object_id=0)
+
+
+def test_ray_requires_unit_direction():
+    # test_geometry.py:28-30
+    with pytest.raises(ValueError):
+        Ray(np.zeros(3), np.array([0.0, 0.0, 2.0]))
+
+
+def test_grid_validation_messages():
+    # test_radiomap.py:106-114
+    with pytest.raises(ValueError, match="unit"):
+        MeasurementGrid((0, 0, 0), (2, 0, 0), (0, 1, 0), (1, 1), (2, 2))
+    with pytest.raises(ValueError, match="orthogonal"):
+        MeasurementGrid((0, 0, 0), (1, 0, 0), (1, 0, 0), (1, 1), (2, 2))
+    with pytest.raises(ValueError, match="cell size"):
+        MeasurementGrid((0, 0, 0), (1, 0, 0), (0, 1, 0), (0.0, 1), (2, 2))
+    with pytest.raises(ValueError, match="shape"):
+        MeasurementGrid((0, 0, 0), (1, 0, 0), (0, 1, 0), (1, 1), (0, 2))
+
+
+def test_unresolved_material_raises_before_any_device_work():
+    # test_paths.py:625-628
+    mesh = scenes.box_mesh(BOX_LO, BOX_HI, object_id=3, inward=True)
+    with pytest.raises(UnresolvedMaterial):
+        SceneModel([mesh], {0: CONCRETE})
+
+
+# ---------------------------------------------------------------------------
+# closest hit (GPU)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.gpu
+def test_single_triangle_accel_bounds(cuda):
+    # test_geometry.py:38-44
+    acc = build_scene_accel([Mesh(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0]], float),
+                                  np.array([[0, 1, 2]]), object_id=0)])
+    assert acc.num_triangles == 1
+    lo, hi = acc.bounds
+    assert np.allclose(lo, [0, 0, 0], atol=1e-9) and np.allclose(hi, [1, 1, 0], atol=1e-9)
+
+
+@pytest.mark.gpu
+def test_two_disjoint_boxes_nearer_first(cuda):
+    # test_geometry.py:47-55
+    acc = build_scene_accel([scenes.box_mesh([0, 0, 0], [1, 1, 1], object_id=0),
+                             scenes.box_mesh([3, 0, 0], [4, 1, 1], object_id=1)])
+    assert acc.num_triangles == 24
+    h = intersect_closest(acc, Ray(np.array([-2.0, 0.5, 0.5]), np.array([1.0, 0.0, 0.0])))
+    assert h.object_id == 0
+    assert h.t == pytest.approx(2.0, abs=1e-12)
+
+
+@pytest.mark.gpu
+def test_ground_plane_hit_and_cap(cuda):
+    # test_geometry.py:58-66
+    acc = build_scene_accel([scenes.quad_mesh()])
+    ray = Ray(np.array([0.0, 0.0, 1.0]), np.array([0.0, 0.0, -1.0]))
+    h = intersect_closest(acc, ray)
+    assert h.t == pytest.approx(1.0, abs=1e-12)
+    assert np.allclose(h.point, [0, 0, 0], atol=1e-12)
+    assert np.allclose(h.normal, [0, 0, 1])
+    assert intersect_closest(acc, Ray(ray.origin, ray.direction, max_t=0.5)) is None
+
+
+@pytest.mark.gpu
+def test_shared_diagonal_tie_breaks_to_lower_primitive(cuda):
+    # test_geometry.py:69-74: (0.5, 0.5) lies on the diagonal both triangles own
+    acc = build_scene_accel([scenes.quad_mesh()])
+    h = intersect_closest(acc, Ray(np.array([0.5, 0.5, 2.0]), np.array([0.0, 0.0, -1.0])))
+    assert (h.object_id, h.primitive_id) == (0, 0)
+
+
+@pytest.mark.gpu
+def test_normal_faces_incident_side(cuda):
+    # test_geometry.py:77-81
+    acc = build_scene_accel([scenes.quad_mesh()])
+    below = intersect_closest(acc, Ray(np.array([0.2, 0.1, -1.0]), np.array([0.0, 0.0, 1.0])))
+    assert np.allclose(below.normal, [0, 0, -1])
+
+
+@pytest.mark.gpu
+def test_hit_point_consistency(cuda):
+    # test_geometry.py:144-156 (hypothesis, 50 examples over px, py in
+    # [-0.9, 0.9], tilt in [-0.45, 0.45]): 50 seeded draws plus the box corners
+    rng = np.random.default_rng(144)
+    draws = np.column_stack([rng.uniform(-0.9, 0.9, 50), rng.uniform(-0.9, 0.9, 50),
+                             rng.uniform(-0.45, 0.45, 50)])
+    corners = np.array([[a, b, c] for a in (-0.9, 0.9) for b in (-0.9, 0.9) for c in (-0.45, 0.45)])
+    acc = build_scene_accel([scenes.quad_mesh()])
+    hits = 0
+    for px, py, tilt in np.vstack([draws, corners, [[0.0, 0.0, 0.0]]]):
+        d = np.array([tilt, tilt / 2, -1.0])
+        d /= np.linalg.norm(d)
+        o = np.array([px, py, 1.0])
+        h = intersect_closest(acc, Ray(o, d))
+        if h is None:
+            continue
+        hits += 1
+        assert float(h.normal @ d) <= 0.0
+        assert np.linalg.norm(h.point - (o + h.t * d)) <= 1e-6 * max(h.t, 1.0)
+    assert hits > 40
+
+
+# ---------------------------------------------------------------------------
+# radio map (GPU)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.gpu
+def test_bounce_map_matches_path_solver(cuda):
+    # test_radiomap.py:258-278: cell averages agree with the non-coherent sum
+    # over refined paths to the cell centres
+    scene = _walled_room()
+    grid = _small_grid(cell=0.5)
+    vals, diag = compute_radio_map_sbr(scene, TX_POS, grid,
+                                       RadioMapConfig(num_samples=800_000, max_depth=3,
+                                                      enabled=R_ONLY, seed=0))
+    assert diag["deposits"] > 0
+    centers = grid.cell_centers().reshape(-1, 3)
+    result = compute_paths(scene, [RadioDevice(position=TX_POS)],
+                           [RadioDevice(position=c) for c in centers],
+                           PathConfig(num_samples=120_000, max_depth=3, enabled=R_ONLY,
+                                      q_diffraction=0.0, seed=0))
+    truth = np.zeros(len(centers))
+    for p in result.paths:
+        truth[p.rx_index] += abs(p.gain) ** 2
+    truth = truth.reshape(grid.shape[1], grid.shape[0])
+    assert np.all(truth > 0.0)
+    assert np.max(np.abs(vals - truth) / truth) < 0.06
+
+
+@pytest.mark.gpu
+def test_culling_counters_and_threshold_bias(cuda):
+    # test_radiomap.py:299-319
+    scene, grid = _walled_room(), _small_grid()
+    kw = dict(num_samples=100_000, max_depth=3, enabled=RS, seed=1)
+    v0, d0 = compute_radio_map_sbr(scene, TX_POS, grid, RadioMapConfig(**kw))
+    assert d0.get("threshold_killed", 0) == 0 and d0.get("roulette_killed", 0) == 0
+    _, d1 = compute_radio_map_sbr(scene, TX_POS, grid, RadioMapConfig(rr_depth=1, rr_max=0.9, **kw))
+    assert d1["roulette_killed"] > 0
+    v2, d2 = compute_radio_map_sbr(scene, TX_POS, grid, RadioMapConfig(gain_threshold=1e-3, **kw))
+    assert d2["threshold_killed"] > 0
+    assert np.all(v2 <= v0 + 1e-18)  # the threshold only removes energy
+
+
+@pytest.mark.gpu
+def test_roulette_stays_close_to_plain_estimate(cuda):
+    # test_radiomap.py:322-332
+    scene, grid = _walled_room(), _small_grid()
+    kw = dict(num_samples=400_000, max_depth=3, enabled=RS, seed=7)
+    v0, _ = compute_radio_map_sbr(scene, TX_POS, grid, RadioMapConfig(**kw))
+    v1, _ = compute_radio_map_sbr(scene, TX_POS, grid, RadioMapConfig(rr_depth=1, rr_max=0.9, **kw))
+    assert v1.sum() == pytest.approx(v0.sum(), rel=0.12)
+
+
+# ---------------------------------------------------------------------------
+# path solver (GPU)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.gpu
+def test_specular_paths_invariant_to_extra_interactions(cuda):
+    # test_paths.py:548-574: enabling S and T does not change the pure-R paths
+    rough = RadioMaterial("rough", eps_r=5.24, sigma=0.1, thickness=0.3, scattering=0.4)
+    scene = _inward_room(rough)
+    tx, rx = [RadioDevice(position=TX_POS)], [RadioDevice(position=RX_POS)]
+    only_r = compute_paths(scene, tx, rx, PathConfig(num_samples=12000, max_depth=2, seed=3,
+                                                     q_diffraction=0.0, enabled=R_ONLY))
+    everything = compute_paths(scene, tx, rx, PathConfig(num_samples=12000, max_depth=2, seed=3,
+                                                         q_diffraction=0.0))
+    pure = {p.chain_hash: p for p in everything.paths if set(p.kinds) <= {"R"}}
+    assert len(pure) == len(only_r.paths) > 0
+    for p in only_r.paths:
+        q = pure[p.chain_hash]
+        assert q.gain == pytest.approx(p.gain, rel=1e-12)
+        assert q.delay == pytest.approx(p.delay, rel=1e-12)
+        np.testing.assert_allclose(q.vertices, p.vertices, atol=1e-9)
+
+
+@pytest.mark.gpu
+def test_depth_limited_run_has_no_deeper_paths(cuda):
+    # test_paths.py:577-582
+    ps = compute_paths(_inward_room(), [RadioDevice(position=TX_POS)], [RadioDevice(position=RX_POS)],
+                       PathConfig(num_samples=20000, max_depth=1, enabled=R_ONLY, q_diffraction=0.0))
+    assert {p.depth for p in ps.paths} == {0, 1}
+
+
+@pytest.mark.gpu
+def test_all_rows_terminate_when_nothing_enabled_applies(cuda):
+    # test_paths.py:585-593: diffraction alone in a wedge-free room
+    cfg = PathConfig(num_samples=2000, max_depth=2, seed=0, q_diffraction=0.2,
+                     enabled=frozenset({Interaction.DIFFRACTION}))
+    result = generate_candidates(_inward_room(), TX_POS, RX_POS[None, :], cfg)
+    assert all(not r.steps for r in result.records)
+    assert result.diagnostics["samples_terminated"] == 2000
+
+
+@pytest.mark.gpu
+def test_buffer_capacity_keeps_the_first_candidates(cuda):
+    # test_paths.py:596-609
+    scene = _inward_room()
+    kw = dict(num_samples=30000, max_depth=2, enabled=R_ONLY, q_diffraction=0.0)
+    capped = generate_candidates(scene, TX_POS, RX_POS[None, :], PathConfig(buffer_capacity=3, **kw))
+    free = generate_candidates(scene, TX_POS, RX_POS[None, :], PathConfig(**kw))
+    assert len(capped.records) == 3
+    assert capped.diagnostics["buffer_overflow"] > 0
+    assert [r.chain_hash for r in capped.records] == [r.chain_hash for r in free.records[:3]]
+
+
+@pytest.mark.gpu
+def test_per_element_tracing_offsets_sources(cuda):
+    # test_paths.py:701-714: synthetic_arrays=False traces every element
+    offsets = np.array([[0.0, 0.0, 0.0], [0.0, 0.0, 0.2]])
+    tx = RadioDevice(position=TX_POS, array=ArrayGeometry(offsets))
+    cfg = PathConfig(num_samples=1000, max_depth=0, enabled=R_ONLY, q_diffraction=0.0,
+                     synthetic_arrays=False)
+    ps = compute_paths(_inward_room(), [tx], [RadioDevice(position=RX_POS)], cfg)
+    assert sorted(p.tx_element for p in ps.paths) == [0, 1]
+    for p in ps.paths:
+        dist = float(np.linalg.norm(RX_POS - (TX_POS + offsets[p.tx_element])))
+        assert p.delay == pytest.approx(dist / C0, rel=1e-12)

@@ -281,3 +281,85 @@ def test_per_element_tracing_offsets_sources(cuda):
     for p in ps.paths:
         dist = float(np.linalg.norm(RX_POS - (TX_POS + offsets[p.tx_element])))
         assert p.delay == pytest.approx(dist / C0, rel=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# launch lattice and random streams (GPU; test_sampling.py)
+# ---------------------------------------------------------------------------
+
+def _fib(n, begin=0, end=None):
+    from paper_2504_21719_b200.sampling import fibonacci_directions
+    return fibonacci_directions(n, begin, end).cpu().numpy()
+
+
+@pytest.mark.gpu
+def test_fibonacci_single_point_and_rejects_empty(cuda):
+    # test_sampling.py:32-35, 65-67: n = 0 sits at polar angle pi/2, azimuth 0
+    np.testing.assert_allclose(_fib(1), [[1.0, 0.0, 0.0]], atol=1e-15)
+    with pytest.raises(ValueError):
+        _fib(0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("count", [2, 17, 1000])
+def test_fibonacci_unit_norms(cuda, count):
+    # test_sampling.py:38-42
+    d = _fib(count)
+    assert d.shape == (count, 3)
+    np.testing.assert_allclose(np.linalg.norm(d, axis=1), 1.0, atol=1e-12)
+
+
+@pytest.mark.gpu
+def test_fibonacci_near_uniform_and_deterministic(cuda):
+    # test_sampling.py:45-47, 61-62
+    assert np.linalg.norm(_fib(10 ** 4).mean(axis=0)) < 0.02
+    assert np.array_equal(_fib(257), _fib(257))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("count", [100, 1000, 10000])
+def test_fibonacci_no_large_holes(cuda, count):
+    # test_sampling.py:50-58: no direction is isolated far beyond the mean spacing
+    from scipy.spatial import cKDTree
+    d = _fib(count)
+    dist, _ = cKDTree(d).query(d, k=2)
+    gap = 2.0 * np.arcsin(np.clip(dist[:, 1] / 2.0, 0.0, 1.0))
+    assert gap.max() <= 4.0 * gap.mean()
+
+
+@pytest.mark.gpu
+def test_fibonacci_slices_are_the_full_lattice(cuda):
+    # shards and passes evaluate [begin, end) of one lattice: any slicing
+    # reproduces the full evaluation bit for bit
+    full = _fib(4099)
+    for lo, hi in ((0, 1), (1, 4099), (1000, 1001), (2048, 4099), (17, 3000)):
+        assert np.array_equal(_fib(4099, lo, hi), full[lo:hi])
+
+
+def _draws(seed, sample, depth, purpose, count, first=0):
+    from paper_2504_21719_b200.sampling import rng_uniform
+    return rng_uniform(seed, sample, depth, purpose, count, first).cpu().numpy()
+
+
+@pytest.mark.gpu
+def test_stream_reproducible_and_distinct_ids(cuda):
+    # test_sampling.py:240-256
+    ref = _draws(42, 13, 2, "interaction", 100)
+    assert np.array_equal(ref, _draws(42, 13, 2, "interaction", 100))
+    for other in (_draws(43, 13, 2, "interaction", 10), _draws(42, 14, 2, "interaction", 10),
+                  _draws(42, 13, 3, "interaction", 10), _draws(42, 13, 2, "hemisphere", 10)):
+        assert not np.array_equal(ref[:10], other)
+
+
+@pytest.mark.gpu
+def test_stream_order_and_offset_independence(cuda):
+    # test_sampling.py:259-271: a stream's draws never depend on which streams
+    # ran first; on the device the draws are stateless, so any sub-range of a
+    # stream equals the same slice of the whole stream
+    serial = [_draws(5, i, 0, "interaction", 16) for i in range(8)]
+    shuffled = {i: _draws(5, i, 0, "interaction", 16) for i in (5, 2, 7, 0, 6, 1, 4, 3)}
+    for i in range(8):
+        assert np.array_equal(serial[i], shuffled[i])
+        for first, count in ((0, 1), (3, 5), (4, 12), (15, 1)):
+            assert np.array_equal(_draws(5, i, 0, "interaction", count, first),
+                                  serial[i][first:first + count])

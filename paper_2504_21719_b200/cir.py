@@ -640,6 +640,11 @@ def refine_candidate(record, scene):
         rec.t[k].copy_(torch.from_numpy(np.ascontiguousarray(v)).reshape(rec.t[k].shape))
     tgt = torch.from_numpy(np.asarray(record.target, np.float64)[None, :].copy()).to(dev)
     cfg = PathConfig(num_samples=1, max_depth=L)
+    if scene._material_freq is None:
+        # refinement is geometric, but the kernel reads the material table; a
+        # fresh scene (no solver run yet) binds the default frequency, as the
+        # reference's refine_candidate needs no prior solve
+        scene.bind_frequency(cfg.frequency)
     cand = DeviceCandidates(scene, record.source, np.asarray(record.target)[None, :], tgt, cfg,
                             rec, 1, record.source_id)
     cand.params = _cir_params(record.source, tgt, cfg)

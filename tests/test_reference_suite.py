@@ -363,3 +363,173 @@ def test_stream_order_and_offset_independence(cuda):
         for first, count in ((0, 1), (3, 5), (4, 12), (15, 1)):
             assert np.array_equal(_draws(5, i, 0, "interaction", count, first),
                                   serial[i][first:first + count])
+
+
+# ---------------------------------------------------------------------------
+# box room against closed-form answers (GPU; test_paths.py:92-407, 612-622)
+# ---------------------------------------------------------------------------
+
+WALLS = [(a, v) for a in range(3) for v in (BOX_LO[a], BOX_HI[a])]
+
+
+def _mirror_paths(tx, rx, max_depth):
+    """Image-method enumeration of the specular paths inside the box: every
+    wall sequence without immediate repeats whose back-traced reflection
+    points land strictly inside their walls, in order (the room is convex,
+    so nothing else can block them).  Returns {depth: [unfolded length]}."""
+    out = {0: [float(np.linalg.norm(rx - tx))]}
+
+    def extend(chain, images):
+        if chain:
+            p_next, ok = rx, True
+            for (a, v), img in zip(reversed(chain), reversed(images)):
+                den = p_next[a] - img[a]
+                t = (v - img[a]) / den if den != 0.0 else -1.0
+                if not 1e-9 < t < 1.0 - 1e-9:
+                    ok = False
+                    break
+                p = img + t * (p_next - img)
+                others = [b for b in range(3) if b != a]
+                if any(not BOX_LO[b] + 1e-9 < p[b] < BOX_HI[b] - 1e-9 for b in others):
+                    ok = False
+                    break
+                p_next = p
+            if ok:
+                out.setdefault(len(chain), []).append(float(np.linalg.norm(rx - images[-1])))
+        if len(chain) == max_depth:
+            return
+        last = images[-1] if images else tx
+        for w in WALLS:
+            if chain and w == chain[-1]:
+                continue
+            img = last.copy()
+            img[w[0]] = 2.0 * w[1] - img[w[0]]
+            extend(chain + [w], images + [img])
+
+    extend([], [])
+    return out
+
+
+@pytest.fixture(scope="module")
+def box_paths():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cfg = PathConfig(num_samples=120_000, max_depth=3, enabled=R_ONLY, q_diffraction=0.0, seed=0)
+    scene = _inward_room()
+    return scene, cfg, compute_paths(scene, [RadioDevice(position=TX_POS)],
+                                     [RadioDevice(position=RX_POS)], cfg)
+
+
+@pytest.mark.gpu
+def test_box_counts_and_delays_match_image_enumeration(box_paths):
+    # test_paths.py:303-317
+    _, _, ps = box_paths
+    want = _mirror_paths(TX_POS, RX_POS, 3)
+    found = {}
+    for p in ps.paths:
+        found.setdefault(p.depth, []).append(p.delay)
+    assert set(found) == set(want)
+    for depth, lengths in want.items():
+        assert len(found[depth]) == len(lengths), f"depth {depth}"
+        np.testing.assert_allclose(np.sort(found[depth]), np.sort(lengths) / C0, rtol=1e-9)
+
+
+def _slab(cos0, eta, thickness, lam, pol):
+    """ITU-R P.2040 slab over vacuum, one polarization (materials.py:163-238)."""
+    root = np.sqrt(complex(eta) - (1.0 - cos0 * cos0))
+    if root.imag > 0.0:
+        root = -root
+    r = (cos0 - root) / (cos0 + root) if pol == "perp" else \
+        (eta * cos0 - root) / (eta * cos0 + root)
+    q = 2.0 * np.pi * thickness / lam * root
+    p2, p1 = np.exp(-2j * q), np.exp(-1j * q)
+    den = 1.0 - r * r * p2
+    return r * (1.0 - p2) / den, (1.0 - r * r) * p1 / den
+
+
+@pytest.mark.gpu
+def test_box_single_bounce_gains_analytic(box_paths):
+    # test_paths.py:337-376: devices at equal height, so a floor / ceiling
+    # bounce is purely parallel and a side-wall bounce purely perpendicular
+    _, cfg, ps = box_paths
+    lam = cfg.wavelength
+    eta = CONCRETE.complex_permittivity(cfg.frequency)
+    singles = [p for p in ps.paths if p.depth == 1]
+    assert len(singles) == 6
+    for axis, value in WALLS:
+        image = TX_POS.copy()
+        image[axis] = 2.0 * value - image[axis]
+        length = float(np.linalg.norm(RX_POS - image))
+        r, _ = _slab(abs((RX_POS - image)[axis]) / length, eta, CONCRETE.thickness, lam,
+                     "par" if axis == 2 else "perp")
+        match = [p for p in singles if abs(p.delay - length / C0) < 1e-13
+                 and abs(p.steps[0].vertex[axis] - value) < 1e-9]
+        assert match, f"bounce off axis {axis} at {value} missing"
+        for p in match:
+            assert abs(p.gain) == pytest.approx(lam / (4.0 * np.pi * length) * abs(r), rel=1e-9)
+
+
+@pytest.mark.gpu
+def test_box_refinement_fixed_point(box_paths):
+    # test_paths.py:379-389: refining a refined path returns it
+    from paper_2504_21719_b200.cir import CandidateRecord, PathGeometry, refine_candidate
+    scene, _, ps = box_paths
+    for p in ps.paths[:20]:
+        rec = CandidateRecord(source_id=0, target_id=0, source=TX_POS, target=RX_POS,
+                              sample_id=p.sample_id, steps=p.steps, suffix_start=0,
+                              anchor=TX_POS, prefix_probability=1.0, chain_hash=p.chain_hash)
+        again = refine_candidate(rec, scene)
+        assert isinstance(again, PathGeometry)
+        np.testing.assert_allclose(again.vertices, p.vertices, atol=1e-9)
+
+
+@pytest.mark.gpu
+def test_refinement_rejects_plane_mismatch(cuda):
+    # test_paths.py:392-406
+    from paper_2504_21719_b200.cir import (CandidateRecord, InteractionStep, Rejection,
+                                           refine_candidate)
+    bogus = InteractionStep(kind=Interaction.REFLECTION, object_id=0, primitive_id=0,
+                            vertex=np.array([0.0, 0.0, 0.0]), normal=np.array([1.0, 0.0, 0.0]))
+    rec = CandidateRecord(source_id=0, target_id=0, source=TX_POS, target=RX_POS, sample_id=0,
+                          steps=(bogus,), suffix_start=0, anchor=TX_POS, prefix_probability=1.0,
+                          chain_hash=0)
+    out = refine_candidate(rec, _inward_room())
+    assert isinstance(out, Rejection) and out.reason == "coplanar-miss"
+
+
+@pytest.mark.gpu
+def test_doppler_static_scene_is_zero(box_paths):
+    # test_paths.py:635-637
+    assert all(p.doppler == 0.0 for p in box_paths[2].paths)
+
+
+@pytest.mark.gpu
+def test_generation_diagnostics_account_for_all_rows(cuda):
+    # test_paths.py:612-622: closed room, reflection only -- every ray survives
+    # both bounces and every bounce vertex sees the single target
+    cfg = PathConfig(num_samples=5000, max_depth=2, enabled=R_ONLY, q_diffraction=0.0, seed=0)
+    diag = generate_candidates(_inward_room(), TX_POS, RX_POS[None, :], cfg).diagnostics
+    assert diag["samples_escaped"] == 0
+    assert diag["duplicates"] + (diag["hash_registered"] - 1) == 2 * 5000
+    assert diag["candidates"] == diag["hash_registered"]
+
+
+@pytest.mark.gpu
+def test_worker_counts_give_identical_paths(cuda):
+    # test_paths.py:513-533: the reference's worker pool is a host knob; the
+    # device result must not depend on it either
+    rough = RadioMaterial("rough", eps_r=5.24, sigma=0.1, thickness=0.3, scattering=0.15)
+    scene = _inward_room(rough)
+    tx, rx = [RadioDevice(position=TX_POS)], [RadioDevice(position=RX_POS)]
+    runs = [compute_paths(scene, tx, rx, PathConfig(num_samples=8000, max_depth=3, seed=7,
+                                                    q_diffraction=0.0, workers=w))
+            for w in (1, 2, 4)]
+    base = runs[0]
+    assert any(p.kinds and "S" in p.kinds for p in base.paths)
+    for other in runs[1:]:
+        assert len(other.paths) == len(base.paths)
+        for a, b in zip(base.paths, other.paths):
+            assert a.gain == b.gain and a.delay == b.delay and a.sample_id == b.sample_id
+            assert np.array_equal(a.vertices, b.vertices)
+        assert other.diagnostics == base.diagnostics

@@ -533,3 +533,135 @@ def test_worker_counts_give_identical_paths(cuda):
             assert a.gain == b.gain and a.delay == b.delay and a.sample_id == b.sample_id
             assert np.array_equal(a.vertices, b.vertices)
         assert other.diagnostics == base.diagnostics
+
+
+# ---------------------------------------------------------------------------
+# grid and configuration (host; test_radiomap.py:117-177)
+# ---------------------------------------------------------------------------
+
+def test_grid_geometry():
+    g = MeasurementGrid((1.0, 2.0, 3.0), (1, 0, 0), (0, 1, 0), (0.5, 0.25), (4, 8))
+    assert np.allclose(g.normal, [0, 0, 1])
+    assert g.cell_area == pytest.approx(0.125)
+    assert np.allclose(g.corner, [0.0, 1.0, 3.0])
+    c = g.cell_centers()
+    assert c.shape == (8, 4, 3)
+    assert np.allclose(c[0, 0], [0.25, 1.125, 3.0]) and np.allclose(c[-1, -1], [1.75, 2.875, 3.0])
+    h = MeasurementGrid.horizontal((0, 0, 1.5), (10.0, 6.0), (2.0, 2.0))
+    assert h.shape == (5, 3) and np.allclose(h.normal, [0, 0, 1])
+
+
+def test_cell_lookup_boundaries_go_to_the_higher_cell():
+    g = MeasurementGrid((0.0, 0.0, 2.0), (1, 0, 0), (0, 1, 0), (1.0, 1.0), (2, 2))
+    assert g.cell_lookup((0.0, 0.0, 2.0)) == (1, 1)
+    assert g.cell_lookup((-0.5, -0.5, 2.0)) == (0, 0)
+    assert g.cell_lookup((0.999, 0.2, 2.0)) == (1, 1)
+    assert g.cell_lookup((1.001, 0.0, 2.0)) is None
+    assert g.cell_lookup((0.0, 0.0, 2.1)) is None
+
+
+def test_config_validation_and_roulette_probability():
+    from paper_2504_21719_b200.radiomap import russian_roulette_probability
+    for kw in (dict(num_samples=0), dict(rr_max=0.0), dict(rr_depth=4, max_depth=3),
+               dict(gain_threshold=-1.0)):
+        with pytest.raises(ValueError):
+            RadioMapConfig(**kw)
+    assert RadioMapConfig(frequency=3.5e9).wavelength == pytest.approx(C0 / 3.5e9)
+    assert russian_roulette_probability(2.0, 0.01, 0.95) == pytest.approx(0.04)
+    assert russian_roulette_probability(10.0, 1.0, 0.95) == 0.95
+
+
+# ---------------------------------------------------------------------------
+# screen: occlusion, transmission, diffraction (GPU; test_paths.py:432-510,
+# test_radiomap.py:244-255)
+# ---------------------------------------------------------------------------
+
+def _screen_scene():
+    """Vertical 4 m square screen in the y = 0 plane, x in [-2, 2], z in [0, 4]."""
+    quad = scenes.quad_mesh(half=2.0, z=0.0, object_id=5)
+    swap = np.array([[1.0, 0, 0], [0, 0, 1.0], [0, 1.0, 0]])
+    mesh = Mesh(quad.vertices @ swap + np.array([0.0, 0.0, 2.0]), quad.triangles, object_id=5)
+    return SceneModel([mesh], {5: CONCRETE})
+
+
+SCREEN_TX, SCREEN_RX = np.array([0.0, -3.0, 2.0]), np.array([0.0, 3.0, 2.5])
+
+
+@pytest.fixture(scope="module")
+def screen_paths():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    scene = _screen_scene()
+    cfg = PathConfig(num_samples=150_000, max_depth=1, seed=0, q_diffraction=0.3)
+    return scene, cfg, compute_paths(scene, [RadioDevice(position=SCREEN_TX)],
+                                     [RadioDevice(position=SCREEN_RX)], cfg)
+
+
+@pytest.mark.gpu
+def test_screen_blocks_los_and_transmits(screen_paths):
+    _, cfg, ps = screen_paths
+    kinds = sorted(p.kinds for p in ps.paths)
+    assert "" not in kinds, "blocked line of sight must not appear"
+    assert kinds.count("T") == 1 and kinds.count("D") == 4
+    t_path = next(p for p in ps.paths if p.kinds == "T")
+    a, m, b = t_path.vertices
+    assert np.linalg.norm(np.cross(b - a, m - a)) < 1e-9  # straight through
+    dist = float(np.linalg.norm(b - a))
+    assert t_path.delay == pytest.approx(dist / C0, rel=1e-12)
+    # the ray runs in the x = 0 plane, the incidence plane of the y = 0 screen:
+    # a zenith-referenced pattern is purely parallel
+    _, t_par = _slab(abs((b - a)[1]) / dist, CONCRETE.complex_permittivity(cfg.frequency),
+                     CONCRETE.thickness, cfg.wavelength, "par")
+    assert abs(t_path.gain) == pytest.approx(cfg.wavelength / (4.0 * np.pi * dist) * abs(t_par),
+                                             rel=1e-9)
+
+
+@pytest.mark.gpu
+def test_screen_diffraction_points_minimize_length(screen_paths):
+    from scipy.optimize import minimize_scalar
+    scene, _, ps = screen_paths
+    d_paths = [p for p in ps.paths if p.kinds == "D"]
+    assert len(d_paths) == 4
+    for p in d_paths:
+        w = scene.wedges[p.steps[0].wedge_index]
+        v = p.vertices[1]
+        x = float((v - w.origin) @ w.e_hat)
+        length = lambda s: (np.linalg.norm(w.origin + s * w.e_hat - SCREEN_TX)  # noqa: E731
+                            + np.linalg.norm(SCREEN_RX - w.origin - s * w.e_hat))
+        ref = minimize_scalar(length, bounds=(0.0, w.length), method="bounded",
+                              options={"xatol": 1e-10}).x
+        assert x == pytest.approx(ref, abs=1e-6)
+        k_in, k_out = v - SCREEN_TX, SCREEN_RX - v
+        k_in, k_out = k_in / np.linalg.norm(k_in), k_out / np.linalg.norm(k_out)
+        assert k_in @ w.e_hat == pytest.approx(k_out @ w.e_hat, abs=1e-9)  # Keller cone
+
+
+@pytest.mark.gpu
+def test_off_edge_diffraction_rejected(cuda):
+    from paper_2504_21719_b200.cir import (CandidateRecord, InteractionStep, Rejection,
+                                           refine_candidate)
+    scene = _screen_scene()
+    top = next(i for i, w in enumerate(scene.wedges)
+               if abs(w.origin[2] - 4.0) < 1e-9 and abs(w.e_hat[2]) < 1e-9)
+    w = scene.wedges[top]
+    source, target = np.array([40.0, -3.0, 6.0]), np.array([41.0, 3.0, 7.0])  # far beyond +x
+    step = InteractionStep(kind=Interaction.DIFFRACTION, object_id=5, primitive_id=0,
+                           vertex=w.point_at(w.length), normal=w.n0_hat, wedge_index=top)
+    rec = CandidateRecord(source_id=0, target_id=0, source=source, target=target, sample_id=0,
+                          steps=(step,), suffix_start=0, anchor=source, prefix_probability=1.0,
+                          chain_hash=0)
+    out = refine_candidate(rec, scene)
+    assert isinstance(out, Rejection) and out.reason == "off-edge"
+
+
+@pytest.mark.gpu
+def test_direct_term_respects_occlusion(cuda):
+    # test_radiomap.py:244-255: with no bounces the map is the analytic direct
+    # term; the screen's shadow is empty, the outer columns see the source
+    grid = MeasurementGrid((0.0, 2.0, 1.0), (1, 0, 0), (0, 1, 0), (1.0, 1.0), (10, 2))
+    vals, _ = compute_radio_map_sbr(_screen_scene(), np.array([0.0, -3.0, 2.5]), grid,
+                                    RadioMapConfig(num_samples=1, max_depth=0))
+    shadowed = vals == 0.0
+    assert shadowed.any() and (~shadowed).any()
+    assert vals[0, 0] > 0.0 and vals[0, 5] == 0.0

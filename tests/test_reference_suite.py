@@ -665,3 +665,74 @@ def test_direct_term_respects_occlusion(cuda):
     shadowed = vals == 0.0
     assert shadowed.any() and (~shadowed).any()
     assert vals[0, 0] > 0.0 and vals[0, 5] == 0.0
+
+
+# ---------------------------------------------------------------------------
+# edge (diffraction) map (GPU; test_radiomap.py:353-373, 502-538)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.gpu
+def test_collect_wedges_radius_and_visibility(cuda):
+    from paper_2504_21719_b200.radiomap import collect_wedges_near_source
+    scene = _screen_scene()
+    assert len(scene.wedges) == 4
+    everything = collect_wedges_near_source(scene, SCREEN_TX, 100.0)
+    assert sorted(everything) == [0, 1, 2, 3]
+    # a point hovering just off the bottom edge keeps only that wedge
+    lows = [wi for wi in everything if abs(scene.wedges[wi].origin[2]) < 1e-9
+            and abs(scene.wedges[wi].e_hat[2]) < 0.5]
+    assert collect_wedges_near_source(scene, np.array([0.0, -0.4, 0.0]), 0.5) == lows
+    # a cage around the source hides the screen's wedges (its own stay visible)
+    cage = scenes.box_mesh(SCREEN_TX - 0.2, SCREEN_TX + 0.2, object_id=9)
+    caged = SceneModel([scene.meshes[0], cage], {5: CONCRETE, 9: CONCRETE})
+    kept = collect_wedges_near_source(caged, SCREEN_TX, 100.0)
+    screen_wedges = [wi for wi, w in enumerate(caged.wedges)
+                     if abs(w.origin[1]) < 1e-9 and abs(w.e_hat[1]) < 1e-9 and wi < 4]
+    assert screen_wedges and not set(kept) & set(screen_wedges)
+
+
+@pytest.mark.gpu
+def test_edge_map_worker_determinism(cuda):
+    # test_radiomap.py:517-527 asserts bitwise-equal maps for 1 and 4 workers.
+    # Here every per-sample decision and every counter is identical; the cell
+    # sums are float64 atomics, so their last bits follow the summation order
+    # (DESIGN.md §2): equal to 1e-12 relative, not bitwise.
+    from paper_2504_21719_b200 import compute_radio_map_diffraction
+    scene = _screen_scene()
+    grid = MeasurementGrid((0.25, 2.25, 1.7), (1, 0, 0), (0, 1, 0), (0.5, 0.5), (1, 1))
+    runs = [compute_radio_map_diffraction(scene, SCREEN_TX, grid, [0, 1, 2, 3],
+                                          RadioMapConfig(workers=w, wedge_samples=100_000, seed=2))
+            for w in (1, 4)]
+    assert runs[0][1] == runs[1][1]
+    np.testing.assert_allclose(runs[0][0], runs[1][0], rtol=1e-12, atol=0.0)
+    assert runs[0][0][0, 0] > 0.0
+
+
+@pytest.mark.gpu
+def test_bounce_map_worker_determinism(cuda):
+    # test_radiomap.py:335-346, with the same float64-atomics caveat
+    scene = _walled_room()
+    grid = _small_grid(cell=0.5)
+    runs = [compute_radio_map_sbr(scene, TX_POS, grid,
+                                  RadioMapConfig(workers=w, num_samples=40_000, max_depth=2,
+                                                 enabled=RS, seed=5)) for w in (1, 3)]
+    assert runs[0][1] == runs[1][1]
+    np.testing.assert_allclose(runs[0][0], runs[1][0], rtol=1e-12, atol=0.0)
+
+
+@pytest.mark.gpu
+def test_compute_radio_map_multi_source_with_diffraction(cuda):
+    from paper_2504_21719_b200 import compute_radio_map
+    scene = _screen_scene()
+    grid = MeasurementGrid((0.0, 2.0, 1.0), (1, 0, 0), (0, 1, 0), (1.0, 1.0), (2, 2))
+    cfg = RadioMapConfig(num_samples=20_000, wedge_samples=20_000, max_depth=1, seed=0)
+    sources = [np.array([0.0, -3.0, 2.5]), RadioDevice(position=(1.0, -2.0, 2.5))]
+    res = compute_radio_map(scene, sources, grid, cfg)
+    assert res.values.shape == (2, 2, 2)
+    assert np.allclose(res.total(), res.values.sum(axis=0))
+    assert len(res.diagnostics) == 2 and res.diagnostics[0]["wedges"] == 4
+    plain = compute_radio_map(scene, sources[:1], grid,
+                              RadioMapConfig(num_samples=20_000, max_depth=1, enabled=RS))
+    assert "wedges" not in plain.diagnostics[0]
+    with pytest.raises(ValueError, match="precoder"):
+        compute_radio_map(scene, sources, grid, cfg, precoders=[[1.0]])

@@ -736,3 +736,64 @@ def test_compute_radio_map_multi_source_with_diffraction(cuda):
     assert "wedges" not in plain.diagnostics[0]
     with pytest.raises(ValueError, match="precoder"):
         compute_radio_map(scene, sources, grid, cfg, precoders=[[1.0]])
+
+
+# ---------------------------------------------------------------------------
+# DedupTable / PathBuffer semantics of the device selection (GPU;
+# test_paths.py:175-202): crafted rows straight into sbr_cir_select
+# ---------------------------------------------------------------------------
+
+def _select(pairs, n_hash, n_buffer=16):
+    """Chain rows (pair_r, pair_f) in this ordinal order at depth 1, one
+    target whose line of sight is blocked -> (selected row indices, counters)."""
+    import torch
+    from paper_2504_21719_b200 import _abi
+    from paper_2504_21719_b200.cir import _cir_params, _select_rows
+    dev = torch.device("cuda", 0)
+    n = len(pairs)
+    cfg = PathConfig(num_samples=max(n, 1), max_depth=1, enabled=R_ONLY, q_diffraction=0.0,
+                     hash_capacity=n_hash, buffer_capacity=n_buffer)
+    tgt = torch.zeros((1, 3), dtype=torch.float64, device=dev)
+    params = _cir_params(np.zeros(3), tgt, cfg)
+    key = torch.tensor([(1 << 60) | (i << 20) for i in range(n)], dtype=torch.int64,
+                       device=dev).view(torch.uint64)
+    as_u64 = lambda v: torch.tensor(np.array(v, dtype=np.uint64).view(np.int64),  # noqa: E731
+                                    device=dev).view(torch.uint64)
+    pr, pf = as_u64([p[0] for p in pairs]), as_u64([p[1] for p in pairs])
+    chain = torch.ones(n, dtype=torch.uint8, device=dev)
+    los = torch.zeros(1, dtype=torch.uint8, device=dev)
+    counters = torch.zeros(_abi.SBR_CC_COUNT, dtype=torch.int64, device=dev)
+    rec_row, m = _select_rows(params, key, pr, pf, chain, n, los, cfg, counters, dev)
+    c = counters.cpu().numpy()
+    return rec_row[:m].cpu().tolist(), {k: int(c[i]) for k, i in _abi.CC.items()}
+
+
+@pytest.mark.gpu
+def test_dedup_registers_exactly_once(cuda):
+    rows, c = _select([(11, 500), (11, 500)], n_hash=1024)
+    assert rows == [0]
+    assert c["hash_registered"] == 1 and c["duplicates"] == 1
+
+
+@pytest.mark.gpu
+def test_dedup_one_shared_slot_rejects(cuda):
+    # capacity 100: (105, 207) lands on slots (5, 7), (5, 8) shares slot 5
+    rows, c = _select([(5, 7), (105, 207), (5, 8)], n_hash=100)
+    assert rows == [0] and c["hash_registered"] == 1
+
+
+@pytest.mark.gpu
+def test_dedup_rejection_leaves_no_trace(cuda):
+    # slot 9 appears in a rejected pair; a later pair must still claim it
+    rows, c = _select([(5, 7), (5, 9), (9, 9)], n_hash=100)
+    assert rows == [0, 2] and c["hash_registered"] == 2
+
+
+@pytest.mark.gpu
+def test_buffer_drops_on_overflow_keeps_first(cuda):
+    # the first two are kept, the third dropped; within one chunk the
+    # reference trims rows to the buffer's room before appending
+    # (_emit_records paths.py:954-960), so it counts as chunk_truncated
+    rows, c = _select([(1, 2), (3, 4), (5, 6)], n_hash=1024, n_buffer=2)
+    assert rows == [0, 1]
+    assert c["chunk_truncated"] == 1 and c["buffer_overflow"] == 0

@@ -797,3 +797,59 @@ def test_buffer_drops_on_overflow_keeps_first(cuda):
     rows, c = _select([(1, 2), (3, 4), (5, 6)], n_hash=1024, n_buffer=2)
     assert rows == [0, 1]
     assert c["chunk_truncated"] == 1 and c["buffer_overflow"] == 0
+
+
+# ---------------------------------------------------------------------------
+# plane / chain hashing (test_paths.py:106-172): the host helpers on CPU, the
+# per-slot plane hashes the device derives in sbr_scene_create on the GPU
+# ---------------------------------------------------------------------------
+
+def test_host_plane_hash_properties():
+    from paper_2504_21719_b200.paths import hash_plane, pair_with_target
+    rng = np.random.default_rng(122)
+    for _ in range(20):
+        n, p = rng.normal(size=3), rng.normal(size=3) * 10.0
+        assert hash_plane(n, p) == hash_plane(-n, p)  # winding
+    z = np.array([0.0, 0.0, 1.0])
+    assert hash_plane(z, np.array([0.3, -0.7, 1.25])) == hash_plane(z, np.array([-5.0, 2.0, 1.25]))
+    # noise at a quantizer boundary flips at most one of the two hashes
+    r_lo, f_lo = hash_plane(z, np.array([0.0, 0.0, 1.5e-4 - 1e-9]))
+    r_hi, f_hi = hash_plane(z, np.array([0.0, 0.0, 1.5e-4 + 1e-9]))
+    assert r_lo != r_hi and f_lo == f_hi
+    r_lo, f_lo = hash_plane(z, np.array([0.0, 0.0, 2.0e-4 - 1e-9]))
+    r_hi, f_hi = hash_plane(z, np.array([0.0, 0.0, 2.0e-4 + 1e-9]))
+    assert f_lo != f_hi and r_lo == r_hi
+    assert len({pair_with_target(0x1234ABCD5678, k) for k in range(64)}) == 64
+
+
+def _horizontal_tri(z, x0=0.0, y0=0.0, flip=False, object_id=0):
+    v = np.array([[x0, y0, z], [x0 + 1.0, y0, z], [x0, y0 + 1.0, z]])
+    t = np.array([[0, 2, 1]] if flip else [[0, 1, 2]])
+    return Mesh(v, t, object_id=object_id)
+
+
+def _device_plane_hashes(meshes):
+    acc = build_scene_accel(meshes)
+    _, hr, hf = acc._device_tables()
+    return {int(acc.tri_object_id[s]): (int(hr[s]), int(hf[s])) for s in range(acc.num_triangles)}
+
+
+@pytest.mark.gpu
+def test_device_plane_hashes_ignore_winding_and_anchor(cuda):
+    h = _device_plane_hashes([_horizontal_tri(1.25, object_id=0),
+                              _horizontal_tri(1.25, flip=True, object_id=1),
+                              _horizontal_tri(1.25, x0=-5.0, y0=2.0, object_id=2),
+                              _horizontal_tri(1.30, object_id=3)])
+    assert h[0] == h[1] == h[2]
+    assert h[3][0] != h[0][0] and h[3][1] != h[0][1]
+
+
+@pytest.mark.gpu
+def test_device_plane_hashes_boundary_straddle(cuda):
+    eps = 1e-9
+    h = _device_plane_hashes([_horizontal_tri(1.5e-4 - eps, object_id=0),
+                              _horizontal_tri(1.5e-4 + eps, object_id=1),
+                              _horizontal_tri(2.0e-4 - eps, object_id=2),
+                              _horizontal_tri(2.0e-4 + eps, object_id=3)])
+    assert h[0][0] != h[1][0] and h[0][1] == h[1][1]  # half-cell: round flips
+    assert h[2][1] != h[3][1] and h[2][0] == h[3][0]  # cell: floor flips

@@ -292,6 +292,14 @@ int sbr_radiomap_bounce_sharded(const SbrScene* scene, const SbrMapParams* param
  * own queues (~7.4 GB each) so kernel tails overlap; 1 serialises them
  * (per-kernel timing).  No reference counterpart. */
 int sbr_set_wave_streams(int32_t n);
+/* Exact map cells (0 = off, default; 1 = on): deposits accumulate as 192-bit
+ * fixed-point integers (LSB 2^-160, range 2^32) and are converted once per
+ * call, so maps are bitwise reproducible whatever the deposit order -- the
+ * reference's worker-count determinism (radiomap.py chunk sums;
+ * tests/test_radiomap.py:335-346).  Off: float64 atomics, last-bit order
+ * dependence, ~3 % faster on config 4.  Applies to sbr_radiomap_bounce*,
+ * sbr_radiomap_wedges. */
+int sbr_set_exact_maps(int32_t on);
 /* Replaces _direct_cells (radiomap.py:566-583): analytic LoS term per cell
  * centre into direct_dev (ny, nx) (overwritten), counts visible cells. */
 int sbr_radiomap_direct(const SbrScene* scene, const SbrMapParams* params,

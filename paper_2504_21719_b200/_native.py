@@ -55,6 +55,7 @@ def _declare(lib):
         "sbr_radiomap_bounce_sharded": (ctypes.c_int, [vp, vp, i32, i32, vp, vp, vp]),
         "sbr_radiomap_direct": (ctypes.c_int, [vp, vp, vp, vp, vp]),
         "sbr_set_wave_streams": (ctypes.c_int, [i32]),
+        "sbr_set_exact_maps": (ctypes.c_int, [i32]),
         "sbr_radiomap_wedges": (ctypes.c_int, [vp, vp, vp, i32, u64, vp, vp, vp]),
         "sbr_cir_sweep": (ctypes.c_int, [vp, vp, u64, u64, vp, vp, vp]),
         "sbr_cir_sweep_sharded": (ctypes.c_int, [vp, vp, i32, i32, vp, vp, vp]),
@@ -102,7 +103,7 @@ def exported_symbols():
         "sbr_wedges_copy", "sbr_wedges_free", "sbr_trace_closest", "sbr_trace_any",
         "sbr_occluded", "sbr_fibonacci", "sbr_philox_uniform",
         "sbr_radiomap_bounce", "sbr_radiomap_bounce_sharded", "sbr_radiomap_direct",
-        "sbr_set_wave_streams",
+        "sbr_set_wave_streams", "sbr_set_exact_maps",
         "sbr_radiomap_wedges", "sbr_cir_sweep", "sbr_cir_sweep_sharded",
         "sbr_cir_vertex_order",
         "sbr_cir_visibility", "sbr_cir_row_pairs", "sbr_cir_select", "sbr_cir_local_dedup",

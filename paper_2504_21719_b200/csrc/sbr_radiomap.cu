@@ -43,6 +43,75 @@ using namespace sbr;
 
 namespace {
 
+// Exact cell accumulator (opt-in: sbr_set_exact_maps).  Every deposit is a
+// non-negative float64; it is added to its cell as a 192-bit fixed-point
+// integer (three 64-bit words, least significant bit 2^-160, range 2^32) with
+// a carry chain of integer atomics, and k_exact_to_grid converts each cell
+// once at the end of the call.  Integer addition is associative, so a cell's
+// value does not depend on the order in which rays deposit: maps become
+// bitwise reproducible run to run and for any wave-stream count, as the
+// reference's maps are for any worker count (test_radiomap.py:335-346,
+// 517-527).  Off by default: the atomics that return their old value cost
+// ~3 % of a config-4 map (639 -> 661 ms) against float64 atomics, whose cell
+// sums match to ~1e-16 relative in any order.
+constexpr int kExactFrac = 160;
+std::atomic<int> g_exact_maps{0};
+
+__device__ __noinline__ void exact_add(unsigned long long* w, double v) {
+  if (!(v > 0.0) || !(v < 4294967296.0)) return;  // zero / NaN deposit nothing; range 2^32
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+  const int e = (int)(bits >> 52) & 0x7ff;
+  unsigned long long m = bits & 0xFFFFFFFFFFFFFULL;
+  int p;  // weight of m's least significant bit: 2^(p - kExactFrac)
+  if (e == 0) {
+    p = 1 - 1075 + kExactFrac;
+  } else {
+    m |= 1ULL << 52;
+    p = e - 1075 + kExactFrac;
+  }
+  if (p < 0) {
+    if (p < -53) return;
+    const int sh = -p;
+    m = (m >> sh) + ((m >> (sh - 1)) & 1ULL);  // nearest, ties up
+    p = 0;
+    if (m == 0) return;
+  }
+  const int q = p >> 6, r = p & 63;
+  unsigned long long a[3] = {0ULL, 0ULL, 0ULL};
+  a[q] = m << r;
+  if (r && q < 2) a[q + 1] = m >> (64 - r);
+  // each word's own wrap-arounds are carried into the next word: the final
+  // words are the exact 192-bit sum whatever the order of the adds
+  unsigned long long carry = 0;
+  for (int k = q; k < 3; ++k) {
+    const unsigned long long add = a[k] + carry;
+    unsigned long long c = add < carry ? 1ULL : 0ULL;
+    if (add) {
+      const unsigned long long old = atomicAdd(w + k, add);
+      c += old + add < old ? 1ULL : 0ULL;
+    }
+    carry = c;
+  }
+}
+
+__device__ __forceinline__ void grid_deposit(double* grid, bool exact, int64_t cell, double v) {
+  if (exact) exact_add(reinterpret_cast<unsigned long long*>(grid) + 3 * cell, v);
+  else atomicAdd(grid + cell, v);
+}
+
+// cells of the exact accumulator added into the caller's float64 grid
+__global__ void k_exact_to_grid(const unsigned long long* __restrict__ acc, int64_t ncell,
+                                double* __restrict__ grid) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ncell;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long w0 = acc[3 * i], w1 = acc[3 * i + 1], w2 = acc[3 * i + 2];
+    if (w0 | w1 | w2) {
+      const double v = fma((double)w2, 0x1p128, (double)w1 * 0x1p64) + (double)w0;
+      grid[i] += v * 0x1p-160;
+    }
+  }
+}
+
 
 #ifndef SBR_WAVE_LOG2
 #define SBR_WAVE_LOG2 24  // 16.7M samples per pass (~7.4 GB of queues): one pass for 1e7
@@ -296,7 +365,7 @@ struct LaneCounters {
 // isotropic, unrotated source without an array (the launch field is the
 // zenith unit vector, weight 1) -- both specialisations only drop code the
 // run never executes (smaller instruction footprint, SBR_SHADE_SPECIALISE)
-template <bool kFirst, bool kCull = true, bool kSimple = false>
+template <bool kFirst, bool kCull = true, bool kSimple = false, bool kExact = false>
 __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, SbrMapParams P, int seg,
                                                    MapQueue qi, const unsigned long long* count_in,
                                                    uint64_t begin, CombMap comb, HitBuf hits,
@@ -398,7 +467,7 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
         const double fv = floor(SBR_DIV(dot_gemv(rel, make_double3(P.v_hat[0], P.v_hat[1], P.v_hat[2])), P.cell_h));
         if (fu >= 0.0 && fu < (double)P.nx && fv >= 0.0 && fv < (double)P.ny) {
           const double val = SBR_DIV(P.scale * field_energy(E) * omega, fabs(denom)) * weight;
-          atomicAdd(grid + (int64_t)fv * P.nx + (int64_t)fu, val);
+          grid_deposit(grid, kExact, (int64_t)fv * P.nx + (int64_t)fu, val);
           K.deposits++;
         }
       }
@@ -728,7 +797,7 @@ __device__ __forceinline__ void cone_point(const DevScene& S, int w, double3 src
 __global__ void __launch_bounds__(128) k_map_wedges(DevScene S, SbrMapParams P,
                                                     const int32_t* __restrict__ wedge_ids,
                                                     int32_t nw, uint64_t wedge_samples,
-                                                    double* __restrict__ grid,
+                                                    double* __restrict__ grid, bool exact,
                                                     unsigned long long* __restrict__ counters) {
   unsigned deposits = 0, cones = 0;
   const uint64_t total = (uint64_t)nw * wedge_samples;
@@ -798,8 +867,8 @@ __global__ void __launch_bounds__(128) k_map_wedges(DevScene S, SbrMapParams P,
     const double spread = s_in * gamma * (s_in + gamma);
     const double e_p = (cabs2(o0) + cabs2(o1)) / spread;
     const double norm = len * nopen * kPi / (double)wedge_samples;
-    atomicAdd(grid + (int64_t)fv * P.nx + (int64_t)fu,
-              norm * P.scale * e_p * factor * alpha_sq(P, k_i));
+    grid_deposit(grid, exact, (int64_t)fv * P.nx + (int64_t)fu,
+                 norm * P.scale * e_p * factor * alpha_sq(P, k_i));
     deposits++;
   }
   const unsigned lane = threadIdx.x & 31u;
@@ -934,6 +1003,16 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
   // + the dead padding of every shade warp's last output batch
   const int64_t pad = (int64_t)kShadeRes * sms * SBR_SHADE_MINB * 4 + 64;
   for (int k = 0; k < nstreams && !rc; ++k) rc = wave_alloc(chunk + (int64_t)F + pad, st, &waves[k]);
+  const int64_t ncell = (int64_t)P->nx * P->ny;
+  const bool exact = g_exact_maps.load() != 0;
+  unsigned long long* acc = nullptr;  // exact accumulator, when enabled
+  if (!rc && exact) {
+    if (scratch_alloc((void**)&acc, (size_t)ncell * 3 * sizeof(unsigned long long), st) != cudaSuccess)
+      rc = set_error(SBR_ERR_NOMEM, "map accumulator");
+    else
+      cudaMemsetAsync(acc, 0, (size_t)ncell * 3 * sizeof(unsigned long long), st);
+  }
+  double* dep = exact ? reinterpret_cast<double*>(acc) : grid;
   if (!rc && nstreams > 1) {
     if (cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess) {
       rc = set_error(SBR_ERR_CUDA, "wave stream event");
@@ -981,10 +1060,11 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
       prof_begin(ps, "k_map_shade");
       auto shade = seg == 0 ? (cull ? (simple ? k_map_shade<true, true, true> : k_map_shade<true, true, false>)
                                     : (simple ? k_map_shade<true, false, true> : k_map_shade<true, false, false>))
-                            : (cull ? k_map_shade<false, true, false> : k_map_shade<false, false, false>);
+                            : exact ? (cull ? k_map_shade<false, true, false, true> : k_map_shade<false, false, false, true>)
+                                    : (cull ? k_map_shade<false, true, false> : k_map_shade<false, false, false>);
       shade<<<shade_blocks, 128, 0, ps>>>(S, *P, seg, w->q[cur], w->ctl + 1 + cur, lo,
                                                 comb, w->hits, w->q[1 - cur], w->ctl + 2 - cur,
-                                                w->sq, w->ctl + 3, grid, counters, sh, w->ctl + 4);
+                                                w->sq, w->ctl + 3, dep, counters, sh, w->ctl + 4);
       prof_end(ps);
       if ((rc = launch_status("k_map_shade"))) break;
       if (seg < P->max_depth && (P->allow_mask & 2)) {
@@ -1009,7 +1089,21 @@ static int bounce_impl(const SbrScene* scene, const SbrMapParams* P, uint64_t sa
   if (ev_fork) cudaEventDestroy(ev_fork);
   for (int k = 0; k < nstreams; ++k)
     if (waves[k].block) cudaFreeAsync(waves[k].block, st);
+  if (acc) {
+    if (!rc) {
+      const int64_t b = (ncell + 255) / 256;
+      k_exact_to_grid<<<(unsigned)(b < 148 * 16 ? b : 148 * 16), 256, 0, st>>>(acc, ncell, grid);
+      rc = launch_status("k_exact_to_grid");
+    }
+    cudaFreeAsync(acc, st);
+  }
   return rc;
+}
+
+int sbr_set_exact_maps(int32_t on) {
+  if (on != 0 && on != 1) return set_error(SBR_ERR_INVALID, "exact maps: 0 or 1");
+  g_exact_maps = on;
+  return SBR_OK;
 }
 
 int sbr_set_wave_streams(int32_t n) {
@@ -1057,12 +1151,30 @@ int sbr_radiomap_wedges(const SbrScene* scene, const SbrMapParams* P, const int3
   const uint64_t total = (uint64_t)n_wedges * wedge_samples;
   uint64_t blocks = (total + 127) / 128;
   if (blocks > 148 * 64) blocks = 148 * 64;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t ncell = (int64_t)P->nx * P->ny;
+  const bool exact = g_exact_maps.load() != 0;
+  unsigned long long* acc = nullptr;
+  if (exact) {
+    if (scratch_alloc((void**)&acc, (size_t)ncell * 3 * sizeof(unsigned long long), st) != cudaSuccess)
+      return set_error(SBR_ERR_NOMEM, "map accumulator");
+    cudaMemsetAsync(acc, 0, (size_t)ncell * 3 * sizeof(unsigned long long), st);
+  }
   prof_begin(stream, "k_map_wedges");
-  k_map_wedges<<<(unsigned)blocks, 128, 0, (cudaStream_t)stream>>>(
-      dev_view(scene), *P, wedge_ids, n_wedges, wedge_samples, grid,
-      (unsigned long long*)counters);
+  k_map_wedges<<<(unsigned)blocks, 128, 0, st>>>(
+      dev_view(scene), *P, wedge_ids, n_wedges, wedge_samples,
+      exact ? reinterpret_cast<double*>(acc) : grid, exact, (unsigned long long*)counters);
   prof_end(stream);
-  return launch_status("k_map_wedges");
+  rc = launch_status("k_map_wedges");
+  if (acc) {
+    if (!rc) {
+      const int64_t b = (ncell + 255) / 256;
+      k_exact_to_grid<<<(unsigned)(b < 148 * 16 ? b : 148 * 16), 256, 0, st>>>(acc, ncell, grid);
+      rc = launch_status("k_exact_to_grid");
+    }
+    cudaFreeAsync(acc, st);
+  }
+  return rc;
 }
 
 int sbr_radiomap_direct(const SbrScene* scene, const SbrMapParams* P, double* direct,

@@ -227,7 +227,8 @@ def test_degenerate_deep_tree_traverses_like_the_reference(cuda):
 def test_wave_streams_same_map(cuda, streams):
     """A multi-pass map (3 wavefront passes of 2^24 samples) is the same map
     whether its passes run on 1, 2 (default), 3 or 4 streams: identical
-    counters, values equal up to float64 atomic summation order."""
+    counters, values equal up to float64 atomic summation order (bitwise
+    with exact_maps: tests/test_reference_suite.py)."""
     from paper_2504_21719_b200 import _native
     sc = _room()
     grid = MeasurementGrid((0.0, 0.0, 1.5), (1, 0, 0), (0, 1, 0), (0.5, 0.5), (8, 8))

@@ -94,6 +94,14 @@ def test_config_validation():
     assert RadioMapConfig().wavelength == pytest.approx(299792458.0 / 3.5e9)
 
 
+def test_exact_maps_switch_checked():
+    """sbr_set_exact_maps takes 0 / 1 (pure host setter, no device call)."""
+    lib = _native.load_library()
+    assert lib.sbr_set_exact_maps(2) == _abi.SBR_ERR_INVALID
+    assert lib.sbr_set_exact_maps(-1) == _abi.SBR_ERR_INVALID
+    assert lib.sbr_set_exact_maps(1) == 0 and lib.sbr_set_exact_maps(0) == 0
+
+
 def test_wave_streams_range_checked():
     """sbr_set_wave_streams accepts 1..4 (pure host setter, no device call)."""
     lib = _native.load_library()

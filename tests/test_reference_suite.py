@@ -693,31 +693,34 @@ def test_collect_wedges_radius_and_visibility(cuda):
 
 @pytest.mark.gpu
 def test_edge_map_worker_determinism(cuda):
-    # test_radiomap.py:517-527 asserts bitwise-equal maps for 1 and 4 workers.
-    # Here every per-sample decision and every counter is identical; the cell
-    # sums are float64 atomics, so their last bits follow the summation order
-    # (DESIGN.md §2): equal to 1e-12 relative, not bitwise.
+    # test_radiomap.py:517-527: bitwise-equal maps for 1 and 4 workers (with
+    # exact_maps the cells accumulate in fixed point: deposit order is moot)
     from paper_2504_21719_b200 import compute_radio_map_diffraction
+    from paper_2504_21719_b200.radiomap import exact_maps
     scene = _screen_scene()
     grid = MeasurementGrid((0.25, 2.25, 1.7), (1, 0, 0), (0, 1, 0), (0.5, 0.5), (1, 1))
-    runs = [compute_radio_map_diffraction(scene, SCREEN_TX, grid, [0, 1, 2, 3],
-                                          RadioMapConfig(workers=w, wedge_samples=100_000, seed=2))
-            for w in (1, 4)]
+    with exact_maps():
+        runs = [compute_radio_map_diffraction(scene, SCREEN_TX, grid, [0, 1, 2, 3],
+                                              RadioMapConfig(workers=w, wedge_samples=100_000,
+                                                             seed=2))
+                for w in (1, 4)]
     assert runs[0][1] == runs[1][1]
-    np.testing.assert_allclose(runs[0][0], runs[1][0], rtol=1e-12, atol=0.0)
+    assert np.array_equal(runs[0][0], runs[1][0])
     assert runs[0][0][0, 0] > 0.0
 
 
 @pytest.mark.gpu
 def test_bounce_map_worker_determinism(cuda):
-    # test_radiomap.py:335-346, with the same float64-atomics caveat
+    # test_radiomap.py:335-346
+    from paper_2504_21719_b200.radiomap import exact_maps
     scene = _walled_room()
     grid = _small_grid(cell=0.5)
-    runs = [compute_radio_map_sbr(scene, TX_POS, grid,
-                                  RadioMapConfig(workers=w, num_samples=40_000, max_depth=2,
-                                                 enabled=RS, seed=5)) for w in (1, 3)]
+    with exact_maps():
+        runs = [compute_radio_map_sbr(scene, TX_POS, grid,
+                                      RadioMapConfig(workers=w, num_samples=40_000, max_depth=2,
+                                                     enabled=RS, seed=5)) for w in (1, 3)]
     assert runs[0][1] == runs[1][1]
-    np.testing.assert_allclose(runs[0][0], runs[1][0], rtol=1e-12, atol=0.0)
+    assert np.array_equal(runs[0][0], runs[1][0])
 
 
 @pytest.mark.gpu
@@ -853,3 +856,28 @@ def test_device_plane_hashes_boundary_straddle(cuda):
                               _horizontal_tri(2.0e-4 + eps, object_id=3)])
     assert h[0][0] != h[1][0] and h[0][1] == h[1][1]  # half-cell: round flips
     assert h[2][1] != h[3][1] and h[2][0] == h[3][0]  # cell: floor flips
+
+
+@pytest.mark.gpu
+def test_map_bitwise_reproducible_across_runs_and_wave_streams(cuda):
+    # a multi-pass map (3 wavefront passes) deposits from 1 or 2 streams in a
+    # different order every run; with exact_maps the result is bitwise
+    # identical anyway, and equals the float64-atomics map to 1e-12
+    from paper_2504_21719_b200 import _native
+    from paper_2504_21719_b200.radiomap import exact_maps
+    scene = _walled_room()
+    grid = MeasurementGrid((0.0, 0.0, 1.0), (1, 0, 0), (0, 1, 0), (0.5, 0.5), (10, 14))
+    cfg = RadioMapConfig(num_samples=3 * (1 << 24) - 777, max_depth=2, enabled=RS, seed=9)
+    plain, dplain = compute_radio_map_sbr(scene, TX_POS, grid, cfg)
+    with exact_maps():
+        ref, dref = compute_radio_map_sbr(scene, TX_POS, grid, cfg)
+        again, dagain = compute_radio_map_sbr(scene, TX_POS, grid, cfg)
+        try:
+            _native.check(_native.lib().sbr_set_wave_streams(1))
+            one, done_ = compute_radio_map_sbr(scene, TX_POS, grid, cfg)
+        finally:
+            _native.check(_native.lib().sbr_set_wave_streams(2))
+    assert dplain == dref == dagain == done_
+    assert np.array_equal(ref, again) and np.array_equal(ref, one)
+    assert np.all(ref > 0)
+    np.testing.assert_allclose(ref, plain, rtol=1e-12, atol=0.0)

@@ -32,6 +32,7 @@ from .radiomap import (  # noqa: E402
     compute_radio_map,
     compute_radio_map_diffraction,
     compute_radio_map_sbr,
+    exact_maps,
 )
 from .sampling import Interaction  # noqa: E402
 from .sceneio import (  # noqa: E402
@@ -55,7 +56,7 @@ __all__ = [
     "PathSet", "PathTensors", "ValidPath", "baseband_gains", "compute_paths",
     "frequency_response", "generate_candidates", "refine_candidate",
     "MeasurementGrid", "RadioMapConfig", "RadioMapResult",
-    "compute_radio_map", "compute_radio_map_diffraction", "compute_radio_map_sbr",
+    "compute_radio_map", "compute_radio_map_diffraction", "compute_radio_map_sbr", "exact_maps",
     "Interaction", "LoadedScene", "SceneDescription", "load_mesh_obj", "load_scene",
     "read_paths_csv", "read_radio_map_csv", "write_mesh_obj", "write_paths",
     "write_radio_map", "write_scene", "__version__",

@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(128, SBR_SHADE_MINB) k_map_shade(DevScene S, S
     q0 = SBR_DIV(q0, total);
     q1 = SBR_DIV(q1, total);
     q2 = SBR_DIV(q2, total);
-    const double q3 = SBR_DIV(0.0, total);
+    const double q3 = 0.0;  // q_D / total with q_D = 0 and total in (0, 3]: exactly +0
     const double u = philox_uniform(P.seed, chunk, (uint64_t)seg, TAG_MAP_INTERACTION, slot);
     const double c0 = q0, c1 = c0 + q1, c2 = c1 + q2, c3 = c2 + q3;
     int code = (u >= c0) + (u >= c1) + (u >= c2) + (u >= c3);

@@ -284,7 +284,15 @@ static __device__ __noinline__ double3 div3_call(double3 v, double s) {
 #define SBR_DIV3(v, s) make_double3((v).x / (s), (v).y / (s), (v).z / (s))
 #endif
 // numpy CDOUBLE_divide: Smith's method with a reciprocal
-SBR_MATH_FN cplx cdiv(cplx a, cplx b) {
+#ifndef SBR_CDIV_INLINE
+#define SBR_CDIV_INLINE 0
+#endif
+#if SBR_CDIV_INLINE
+__device__ __forceinline__
+#else
+SBR_MATH_FN
+#endif
+cplx cdiv(cplx a, cplx b) {
   const double br = fabs(b.re), bi = fabs(b.im);
   if (br >= bi) {
     if (br == 0.0 && bi == 0.0) return C(a.re / br, a.im / br);
@@ -295,6 +303,34 @@ SBR_MATH_FN cplx cdiv(cplx a, cplx b) {
   const double rat = b.re / b.im;
   const double scl = 1.0 / (b.im + b.re * rat);
   return C((a.re * rat + a.im) * scl, (a.im * rat - a.re) * scl);
+}
+// a1 / b and a2 / b with one Smith ratio and scale: cdiv's operations on the
+// same b, so both results are cdiv's bits, for two of its divisions
+struct cplx2 {
+  cplx x, y;
+};
+#ifndef SBR_CDIV2
+#define SBR_CDIV2 2  // inlined: config-4 map 632.5 -> 617.4 ms (out of line: 631.4)
+#endif
+#if SBR_CDIV2 == 2
+__device__ __forceinline__
+#else
+static __device__ __noinline__
+#endif
+cplx2 cdiv2(cplx a1, cplx a2, cplx b) {
+  const double br = fabs(b.re), bi = fabs(b.im);
+  if (br >= bi) {
+    if (br == 0.0 && bi == 0.0)
+      return cplx2{C(a1.re / br, a1.im / br), C(a2.re / br, a2.im / br)};
+    const double rat = b.im / b.re;
+    const double scl = 1.0 / (b.re + b.im * rat);
+    return cplx2{C((a1.re + a1.im * rat) * scl, (a1.im - a1.re * rat) * scl),
+                 C((a2.re + a2.im * rat) * scl, (a2.im - a2.re * rat) * scl)};
+  }
+  const double rat = b.re / b.im;
+  const double scl = 1.0 / (b.im + b.re * rat);
+  return cplx2{C((a1.re * rat + a1.im) * scl, (a1.im * rat - a1.re) * scl),
+               C((a2.re * rat + a2.im) * scl, (a2.im * rat - a2.re) * scl)};
 }
 // np.abs(complex128) in numpy 2.x: max * sqrt(fma(r, r, 1)), r = min/max
 SBR_MATH_FN double cabs_np(cplx a) {

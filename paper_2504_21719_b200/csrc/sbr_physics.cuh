@@ -69,15 +69,27 @@ __device__ __forceinline__ Fresnel4 slab_fresnel(const SbrMaterial& m, double c0
     const cplx r1sq = r_perp * r_perp;
     const cplx z = r1sq * phase2;
     const cplx den = C(1.0 - z.re, -z.im);
+#if SBR_CDIV2
+    const cplx2 q = cdiv2(r_perp * one_m_p2, C(1.0 - r1sq.re, -r1sq.im) * phase1, den);
+    f.rp = q.x;
+    f.tp = q.y;
+#else
     f.rp = cdiv(r_perp * one_m_p2, den);
     f.tp = cdiv(C(1.0 - r1sq.re, -r1sq.im) * phase1, den);
+#endif
   }
   {
     const cplx r1sq = r_par * r_par;
     const cplx z = r1sq * phase2;
     const cplx den = C(1.0 - z.re, -z.im);
+#if SBR_CDIV2
+    const cplx2 q = cdiv2(r_par * one_m_p2, C(1.0 - r1sq.re, -r1sq.im) * phase1, den);
+    f.rl = q.x;
+    f.tl = q.y;
+#else
     f.rl = cdiv(r_par * one_m_p2, den);
     f.tl = cdiv(C(1.0 - r1sq.re, -r1sq.im) * phase1, den);
+#endif
   }
   return f;
 }

@@ -333,7 +333,15 @@ cplx2 cdiv2(cplx a1, cplx a2, cplx b) {
                C((a2.re * rat + a2.im) * scl, (a2.im * rat - a2.re) * scl)};
 }
 // np.abs(complex128) in numpy 2.x: max * sqrt(fma(r, r, 1)), r = min/max
-SBR_MATH_FN double cabs_np(cplx a) {
+#ifndef SBR_CABS_INLINE
+#define SBR_CABS_INLINE 0
+#endif
+#if SBR_CABS_INLINE
+__device__ __forceinline__
+#else
+SBR_MATH_FN
+#endif
+double cabs_np(cplx a) {
   const double x = fabs(a.re), y = fabs(a.im);
   const double m = fmax(x, y), k = fmin(x, y);
   if (m == 0.0 || isinf(m)) return m + k;

@@ -436,27 +436,35 @@ def _sweep_rows(scene, source, targets, cfg, lo, hi, shard=None):
         _native.check(L_.sbr_cir_vertex_order(acc.handle, ctypes.byref(vb.abi), nv,
                                               _native.ptr(order), stream))
     slab = max(32, ((1 << 26) // nt) // 32 * 32)
-    cap = max(1 << 20, min(nv * nt, int(nv * nt * 0.03)))
+    # room for several slabs' worst case, so the row count is read back (a
+    # host sync) only when the slabs launched since the last read could
+    # overflow the buffer, not after every slab
+    cap = max(1 << 20, min(nv * nt, max(int(nv * nt * 0.03), 4 * slab * nt)))
     row_key = torch.empty(cap, dtype=torch.uint64, device=dev)
     row_vtx = torch.empty(cap, dtype=torch.int32, device=dev)
-    nrows = 0
+    nrows = 0  # rows known after the last read-back
+    bound = 0  # nrows + worst case of the slabs launched since
     for v0 in range(0, nv, slab):
         v1 = min(nv, v0 + slab)
-        need = nrows + (v1 - v0) * nt
-        if need > cap:
-            cap = max(need, int(cap * 1.5))
-            nk = torch.empty(cap, dtype=torch.uint64, device=dev)
-            nv_ = torch.empty(cap, dtype=torch.int32, device=dev)
-            nk[:nrows].copy_(row_key[:nrows])
-            nv_[:nrows].copy_(row_vtx[:nrows])
-            row_key, row_vtx = nk, nv_
+        if bound + (v1 - v0) * nt > cap:
+            nrows = int(counters[_abi.CC["rows"]].item())
+            bound = nrows
+            need = nrows + (v1 - v0) * nt
+            if need > cap:
+                cap = max(need, int(cap * 1.5))
+                nk = torch.empty(cap, dtype=torch.uint64, device=dev)
+                nv_ = torch.empty(cap, dtype=torch.int32, device=dev)
+                nk[:nrows].copy_(row_key[:nrows])
+                nv_[:nrows].copy_(row_vtx[:nrows])
+                row_key, row_vtx = nk, nv_
         _native.check(L_.sbr_cir_visibility(
             acc.handle, ctypes.byref(R.params), ctypes.byref(vb.abi), v0, v1,
             _native.ptr(order), _native.ptr(row_key), _native.ptr(row_vtx), cap,
             _native.ptr(counters), stream))
-        nrows = int(counters[_abi.CC["rows"]].item())
-        if nrows > cap:
-            raise RuntimeError("visibility row buffer overflow")  # cannot happen
+        bound += (v1 - v0) * nt
+    nrows = int(counters[_abi.CC["rows"]].item())
+    if nrows > cap:
+        raise RuntimeError("visibility row buffer overflow")  # cannot happen
     acc.check()
     gt.mark("visibility")
     R.n = nrows
